@@ -1,0 +1,163 @@
+/*
+ * fl_b200.h -- C ABI of the B200-native factorized-learning hot path.
+ *
+ * This is the drop-in boundary that replaces the reference's operator surface
+ * (`pkg/src/factorlearn/ops.py:147-328`, class TargetHandle) and its trainers
+ * (`pkg/src/factorlearn/trainers.py:138-331`).  The host side
+ * (`paper_2502_01985_b200/ops.py`, `trainers.py`) binds these entry points
+ * with ctypes; INTEGRATION.md shows the binding a reference maintainer would
+ * add to `factorlearn`.
+ *
+ * Conventions
+ *  - Every function returns an int status: FL_OK (0) or one of FL_ERR_*,
+ *    which the host maps to the reference's exception classes.  The message
+ *    of the last failure on the calling thread is `fl_last_error()`.
+ *  - Table buffers are library-owned device memory.  Operand / output
+ *    pointers are caller-owned; a pointer may be host or device memory
+ *    (UVA, copied with cudaMemcpyDefault) unless it says "device".
+ *  - All work is ordered on the caller's stream (`void* stream` is a
+ *    cudaStream_t; NULL = legacy default stream).  Functions that return
+ *    host scalars synchronise that stream.
+ *  - Values are stored as fp32; every reduction over target rows is carried
+ *    in fp64 (SURVEY.md §7 "fp32 parity at 1e-4").
+ */
+#ifndef FL_B200_H
+#define FL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_OK 0
+#define FL_ERR_SHAPE 1      /* reference sparse.py:39 ShapeError        */
+#define FL_ERR_OP 2         /* reference ops.py:33 OpError              */
+#define FL_ERR_METADATA 3   /* reference metadata.py:53 MetadataError   */
+#define FL_ERR_CONFIG 4     /* reference trainers.py:32 ConfigError     */
+#define FL_ERR_DIVERGENCE 5 /* reference trainers.py:36 DivergenceError */
+#define FL_ERR_CUDA 6       /* CUDA runtime failure                     */
+#define FL_ERR_ARG 7        /* invalid argument / state                 */
+
+/* elementwise function ids (reference sparse.py:300-307 ELEMENTWISE_FUNCS) */
+#define FL_EW_SCALE 0
+#define FL_EW_DIVIDE 1
+#define FL_EW_SQUARE 2
+#define FL_EW_ABS 3
+#define FL_EW_EXPM1 4
+#define FL_EW_LOGISTIC_CENTERED 5
+
+/* models (reference trainers.py:310-315 TRAINER_FUNCS) */
+#define FL_MODEL_LINREG 0
+#define FL_MODEL_LOGREG 1
+
+typedef struct fl_table fl_table;
+typedef struct fl_glm fl_glm;
+typedef struct fl_kmeans fl_kmeans;
+typedef struct fl_gnmf fl_gnmf;
+
+const char* fl_last_error(void);
+int fl_version(void);
+/* device properties used by the host for grid sizing and reporting */
+int fl_device_info(int device, int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor);
+
+/* ---- table lifecycle: replaces TargetHandle.factorized (ops.py:164-169) and
+ *      _build_selectors (ops.py:55-74) ---------------------------------- */
+int fl_table_create(int device, int64_t r_T, int32_t c_T, fl_table** out);
+/* Add source k (in order).  values: r_k x c_k row-major fp32 (host or device).
+ * ind_sel: r_T int32 source row per target row, -1 = no match (ops.py:58-61).
+ * col_map: c_k int32 target column of each source column (map_sel_t,
+ * ops.py:67-72), host memory. */
+int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* values,
+                        const int32_t* ind_sel, const int32_t* col_map);
+/* Build the device layout: classify sources, derive the device row order
+ * (stable sort by the largest gathered source's FK) and inverse CSRs. */
+int fl_table_finalize(fl_table* t, void* stream);
+int fl_table_destroy(fl_table* t);
+int fl_table_shape(const fl_table* t, int64_t* r_T, int32_t* c_T, int32_t* n_sources);
+/* stream_cols = real columns in the streamed block; n_gather = gathered
+ * sources; sort_source = user index of the sort source (-1 = none) */
+int fl_table_layout(const fl_table* t, int32_t* stream_cols, int32_t* stream_pitch,
+                    int32_t* n_gather, int32_t* sort_source, int64_t* device_bytes);
+/* Device-derived selectors of source k in TARGET-row terms, for bit-exact
+ * comparison with the reference's _build_selectors (ops.py:55-74).
+ * ind_sel: r_T; group_indptr: r_k+1; group_rows: nnz(I_k).  Host or device
+ * outputs.  Stream (injective) sources report ind_sel only (group_* NULL ok). */
+int fl_table_selectors(fl_table* t, int32_t k, int32_t* ind_sel, int64_t* group_indptr,
+                       int32_t* group_rows, void* stream);
+/* device row order: perm[p] = target row of device row p (r_T entries) */
+int fl_table_perm(fl_table* t, int32_t* perm, void* stream);
+
+/* ---- operators: TargetHandle.{lmm,transpose_lmm,rmm,row_sum,col_sum,
+ *      elementwise,materialize_target} (ops.py:206-328) ---------------- */
+/* out (r_T x c_x fp32) = T x, x: c_T x c_x fp32 row-major (ops.py:219-235) */
+int fl_lmm(fl_table* t, const float* x, int32_t c_x, float* out, void* stream);
+/* out (c_T x c_y fp64) = T^T y, y: r_T x c_y fp32 (ops.py:255-271) */
+int fl_tlmm(fl_table* t, const float* y, int32_t c_y, double* out, void* stream);
+/* out (r_x x c_T fp64) = x T, x: r_x x r_T fp32 (ops.py:237-253) */
+int fl_rmm(fl_table* t, const float* x, int32_t r_x, double* out, void* stream);
+/* out (r_T fp32) = row sums (ops.py:297-311) */
+int fl_row_sum(fl_table* t, float* out, void* stream);
+/* out (c_T fp64) = column sums (ops.py:313-328) */
+int fl_col_sum(fl_table* t, double* out, void* stream);
+/* new table with f applied to every stored source value, sharing the
+ * metadata (ops.py:273-295; f(0) = 0 for every registered f) */
+int fl_elementwise(fl_table* t, int32_t func, double scalar, fl_table** out, void* stream);
+/* dense target (r_T x c_T fp32, target row order): the join
+ * (metadata.py:215-225, ops.py:206-217); values are copies (bit-exact) */
+int fl_materialize(fl_table* t, float* out, void* stream);
+/* rows[n] target rows of T gathered into out (n x c_T fp32, exact copies);
+ * the K-means seeding step (trainers.py:213-218 fetches them via rmm) */
+int fl_target_rows(fl_table* t, const int64_t* rows, int32_t n, float* out, void* stream);
+/* crossprod T^T T (c_T x c_T fp64) -- named in the north star; the reference
+ * has no operator for it (its composition is transpose_lmm(lmm(I))) */
+int fl_crossprod(fl_table* t, double* out, void* stream);
+
+/* ---- fused GD for linear / logistic regression (trainers.py:138-195) -----
+ * One session = device-resident w (fp64 master), labels in device order and
+ * a per-iteration pipeline of three kernels: [update + dim q = S_d w_d] ->
+ * [fact-row pass: gather + residual/sigmoid + S^T r partials + I_sort^T
+ * segmented sums] -> [dim S_d^T bins + final fixed-order reduction].
+ * y: r_T values in TARGET order: fp32 for linreg, uint8 0/1 for logreg. */
+int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rate,
+                  fl_glm** out, void* stream);
+/* one iteration's partial (local) gradient + loss into the reduce buffer */
+int fl_glm_partial(fl_glm* s, void* stream);
+/* device pointer + length (c_T + 1 doubles: gradient then loss) of the buffer
+ * a multi-GPU caller all-reduces between fl_glm_partial and the next step */
+int fl_glm_reduce_buffer(fl_glm* s, double** buf, int32_t* len);
+/* apply the pending update (w -= lr * grad; loss_history[it] = loss) */
+int fl_glm_update(fl_glm* s, void* stream);
+/* single-GPU convenience: iterations x (partial, update), CUDA-graph replayed */
+int fl_glm_run(fl_glm* s, int32_t iterations, void* stream);
+/* copy out w (c_T fp64) and the first n losses (fp64); host or device */
+int fl_glm_result(fl_glm* s, double* w, double* loss, int32_t n, int32_t* n_done, void* stream);
+int fl_glm_destroy(fl_glm* s);
+
+/* ---- fused K-means (trainers.py:198-246) ---------------------------------
+ * centroids0: k x c_T fp64 initial centroids (host or device). */
+int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans** out,
+                     void* stream);
+int fl_kmeans_partial(fl_kmeans* s, int32_t write_assign, void* stream);
+int fl_kmeans_reduce_buffer(fl_kmeans* s, double** buf, int32_t* len);
+int fl_kmeans_update(fl_kmeans* s, void* stream);
+int fl_kmeans_run(fl_kmeans* s, int32_t iterations, void* stream);
+/* centroids k x c_T fp64, assignments r_T int32 (target order), losses */
+int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* loss,
+                     int32_t n, int32_t* n_done, void* stream);
+int fl_kmeans_destroy(fl_kmeans* s);
+
+/* ---- Gaussian NMF, multiplicative updates (trainers.py:256-307) ----------
+ * w0: r_T x rank fp64 (target order), h0: rank x c_T fp64. */
+int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0,
+                   double t_sq, fl_gnmf** out, void* stream);
+int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream);
+int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n,
+                   int32_t* n_done, void* stream);
+int fl_gnmf_destroy(fl_gnmf* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FL_B200_H */

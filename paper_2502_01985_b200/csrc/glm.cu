@@ -1,0 +1,908 @@
+// Fused gradient descent for linear / logistic regression over a factorized
+// table (reference trainers.py:138-195 on top of ops.py:219-271).
+//
+// One GD iteration = three kernels (plus one all-reduce between K3 and the
+// update when the fact rows are sharded over several GPUs):
+//
+//  K1 k_glm_dim_q     q_d[j]   = S_d[j,:] . w_d            (S_d streamed once)
+//  K2 k_glm_fact      per device row p (one pass over F, TMA-staged tiles):
+//                       z  = F[p,:] . w_F + sum_d q_d[fk_d[p]]
+//                       r  = z - y (linreg) | sigmoid(z) - y (logreg)
+//                       loss partial, grad_F partial += r F[p,:]
+//                       bins_sort[fk_sort[p]] += r  (contiguous segmented sum;
+//                       rows are in FK order, so no atomics)
+//                       resid[p] = r  (only if an unsorted gathered source exists)
+//  K3 k_glm_dim_t     grad_d = S_d^T bins_d (S_d streamed again), then the last
+//                     CTA reduces all per-CTA fp64 partials in a fixed order
+//                     and (single GPU) applies w <- w - lr grad.
+//
+// Algorithmic HBM bytes per iteration:
+//   4 r_T pf + 4 r_T n_gather + b_y r_T + sum_d 2 * 4 r_d pitch_d (+ 4 r_T if resid)
+#include <algorithm>
+
+#include "internal.h"
+
+namespace flb {
+
+struct CarryRec {
+  int head_key;   // key of the CTA's first segment if it began before the CTA range
+  int tail_key;   // key of the CTA's last segment if it began inside and continues
+  int through;    // the whole CTA range is one segment that continues past its end
+  int pad;
+  double head_val;
+  double tail_val;
+};
+
+struct GlmState {
+  int it;          // iterations whose update has been applied
+  int done_fact;   // last-block-done counters
+  int done_dim;
+  int pad;
+};
+
+struct GlmFactArgs {
+  const float* F;
+  int pf, c4;
+  const void* y;
+  int64_t r_T, ntiles;
+  int ng, sort_g;
+  const int32_t* fk[MAX_GATHER];
+  const float* q[MAX_GATHER];
+  float* bins;
+  float* resid;
+  const float* wF;
+  double* part;          // gridDim.x x (pf + 1)
+  CarryRec* carry;       // gridDim.x
+  GlmState* state;
+  uint32_t stage_bytes, off_fk, off_y;
+  int nst;
+};
+
+struct DimArgs {
+  int ng;
+  const float* S[MAX_GATHER];
+  int pitch[MAX_GATHER];
+  int64_t rows[MAX_GATHER];
+  int nblk[MAX_GATHER];          // CTAs used for source d (<= gridDim.x)
+  const float* w[MAX_GATHER];    // fp32 w_d (pitch entries)
+  float* q[MAX_GATHER];          // K1 output
+  // K3 inputs
+  const float* bins[MAX_GATHER]; // sorted source: bins; else null
+  const int64_t* grp_ptr[MAX_GATHER];
+  const int32_t* grp_rows[MAX_GATHER];
+  const float* resid;
+  double* part[MAX_GATHER];      // nblk x pitch
+  uint32_t stage_bytes;
+  int nst;
+};
+
+struct UpdateArgs {
+  int c_T, pf, ng;
+  double lr;
+  const int32_t* f_tcol;
+  const int32_t* d_tcol[MAX_GATHER];
+  int pitch[MAX_GATHER];
+  float* wF;
+  float* wd[MAX_GATHER];
+  double* w64;
+  double* red;        // c_T + 1
+  double* loss_hist;
+  int loss_cap;
+  GlmState* state;
+  // reduction inputs (K3 last block)
+  const double* part_fact;
+  int nblk_fact;
+  const double* part_dim[MAX_GATHER];
+  int nblk_dim[MAX_GATHER];
+};
+
+__device__ __forceinline__ float softplus(float x) {
+  // log(1 + e^x), stable
+  return x > 0.f ? x + log1pf(expf(-x)) : log1pf(expf(x));
+}
+
+// -log(clip(p, 1e-12, 1 - 1e-12)) saturates at this value (trainers.py:185-186)
+__device__ __constant__ float kLogClip = 27.631021115928547f;
+
+// ---------------------------------------------------------------------------
+// K1: q_d = S_d w_d, thread per row from TMA-staged tiles
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_glm_dim_q(DimArgs a) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t bar[4];
+  __shared__ float4 w4[64];
+  const int d = blockIdx.y;
+  if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
+  const int tid = threadIdx.x;
+  const int pitch = a.pitch[d], c4 = pitch / 4;
+  const int64_t rows = a.rows[d];
+  const int64_t ntiles = ceil_div(rows, TILE);
+  const int nb = a.nblk[d];
+  const int64_t base = ntiles / nb, rem = ntiles % nb;
+  const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
+  const int64_t cnt = base + (blockIdx.x < rem ? 1 : 0);
+  const uint32_t tile_bytes = TILE * pitch * 4;
+  for (int j = tid; j < c4; j += NTHREADS) w4[j] = reinterpret_cast<const float4*>(a.w[d])[j];
+  if (tid == 0) {
+    for (int s = 0; s < a.nst; s++) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < a.nst && s < cnt; s++) {
+      mbar_arrive_expect_tx(&bar[s], tile_bytes);
+      bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + s) * TILE * (int64_t)pitch, tile_bytes,
+               &bar[s]);
+    }
+  }
+  for (int64_t i = 0; i < cnt; i++) {
+    const int s = (int)(i % a.nst);
+    mbar_wait(&bar[s], (uint32_t)((i / a.nst) & 1));
+    const float4* tile = reinterpret_cast<const float4*>(smem + s * a.stage_bytes);
+    float z = 0.f;
+    for (int j = 0; j < c4; j++) {
+      float4 v = tile[tid * c4 + j];
+      float4 w = w4[j];
+      z = fmaf(v.x, w.x, z);
+      z = fmaf(v.y, w.y, z);
+      z = fmaf(v.z, w.z, z);
+      z = fmaf(v.w, w.w, z);
+    }
+    int64_t row = (t0 + i) * TILE + tid;
+    if (row < rows) a.q[d][row] = z;
+    __syncthreads();
+    if (tid == 0 && i + a.nst < cnt) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bar[s], tile_bytes);
+      bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + i + a.nst) * TILE * (int64_t)pitch,
+               tile_bytes, &bar[s]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: the fact-row pass
+// ---------------------------------------------------------------------------
+template <int MODEL>
+__global__ void __launch_bounds__(NTHREADS, 2) k_glm_fact(GlmFactArgs a) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t bar[4];
+  __shared__ float4 w4[64];
+  __shared__ float r_s[TILE];
+  __shared__ int key_first[8], key_last[8];
+  __shared__ float v_last[8];
+  __shared__ int run_key[2];
+  __shared__ float run_val[2];
+  __shared__ int head_key_s, head_open_s, head_rec_key;
+  __shared__ float head_rec_val;
+  __shared__ double red_s[NTHREADS];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c4 = a.c4;
+  const int64_t G = gridDim.x;
+  const int64_t base = a.ntiles / G, rem = a.ntiles % G;
+  const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
+  const int64_t cnt = base + (blockIdx.x < rem ? 1 : 0);
+  const int64_t R0 = t0 * TILE, R1 = min64((t0 + cnt) * TILE, a.r_T);
+  const uint32_t f_bytes = TILE * c4 * 16;
+  const uint32_t y_bytes = MODEL == 1 ? TILE : TILE * 4;
+  const bool has_sort = a.sort_g >= 0;
+  const int32_t* fks = has_sort ? a.fk[a.sort_g] : nullptr;
+  uint32_t tx_bytes = f_bytes + y_bytes + (has_sort ? TILE * 4 : 0);
+
+  for (int j = tid; j < c4; j += NTHREADS) w4[j] = reinterpret_cast<const float4*>(a.wF)[j];
+  if (tid == 0) {
+    for (int s = 0; s < a.nst; s++) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    run_key[0] = run_key[1] = -1;
+    run_val[0] = run_val[1] = 0.f;
+    int hk = -1;
+    if (has_sort && cnt > 0 && R0 > 0 && R0 < a.r_T) {
+      int k0 = fks[R0];
+      if (k0 >= 0 && fks[R0 - 1] == k0) hk = k0;
+    }
+    head_key_s = hk;
+    head_open_s = hk >= 0;
+    head_rec_key = -1;
+    head_rec_val = 0.f;
+  }
+  __syncthreads();
+
+  auto issue = [&](int s, int64_t tile) {
+    char* st = smem + s * a.stage_bytes;
+    mbar_arrive_expect_tx(&bar[s], tx_bytes);
+    bulk_g2s(st, a.F + tile * TILE * (int64_t)a.pf, f_bytes, &bar[s]);
+    bulk_g2s(st + a.off_y, reinterpret_cast<const char*>(a.y) + tile * (int64_t)y_bytes, y_bytes,
+             &bar[s]);
+    if (has_sort) bulk_g2s(st + a.off_fk, fks + tile * TILE, TILE * 4, &bar[s]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < a.nst && s < cnt; s++) issue(s, t0 + s);
+
+  // phase-B mapping: thread -> (float4 column j, row group g)
+  const int Gr = NTHREADS / c4;
+  const bool pb = tid < Gr * c4;
+  const int pj = tid % c4, pg = tid / c4;
+  double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, lossd = 0;
+  const int head_key = head_key_s;
+
+  for (int64_t i = 0; i < cnt; i++) {
+    const int s = (int)(i % a.nst);
+    const int cur = (int)(i & 1), prev = cur ^ 1;
+    mbar_wait(&bar[s], (uint32_t)((i / a.nst) & 1));
+    const char* st = smem + s * a.stage_bytes;
+    const float4* Ft = reinterpret_cast<const float4*>(st);
+    const int64_t p = (t0 + i) * TILE + tid;
+    const bool valid = p < a.r_T;
+    // ---- phase A: z, residual, loss
+    float z = 0.f;
+    for (int j = 0; j < c4; j++) {
+      float4 v = Ft[tid * c4 + j];
+      float4 w = w4[j];
+      z = fmaf(v.x, w.x, z);
+      z = fmaf(v.y, w.y, z);
+      z = fmaf(v.z, w.z, z);
+      z = fmaf(v.w, w.w, z);
+    }
+    int key = -1;
+    if (has_sort) key = reinterpret_cast<const int32_t*>(st + a.off_fk)[tid];
+    for (int d = 0; d < a.ng; d++) {
+      int32_t fk = (d == a.sort_g) ? key : a.fk[d][p];
+      if (fk >= 0) z += __ldg(a.q[d] + fk);
+    }
+    float r, l;
+    if (MODEL == 0) {
+      float yv = reinterpret_cast<const float*>(st + a.off_y)[tid];
+      r = z - yv;
+      l = 0.5f * r * r;
+    } else {
+      float yv = (float)reinterpret_cast<const uint8_t*>(st + a.off_y)[tid];
+      float pr = 1.f / (1.f + expf(-z));
+      r = pr - yv;
+      // -(y log p + (1-y) log(1-p)) with the reference's clip
+      l = yv != 0.f ? fminf(softplus(-z), kLogClip) : fminf(softplus(z), kLogClip);
+    }
+    if (!valid) {
+      r = 0.f;
+      l = 0.f;
+      key = -1;
+    }
+    r_s[tid] = r;
+    lossd += (double)l;
+    if (a.resid) a.resid[p] = r;
+    // ---- segmented sum of r by sorted key (warp scan)
+    float v = r;
+    if (has_sort) {
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        float vu = __shfl_up_sync(0xffffffffu, v, off);
+        int ku = __shfl_up_sync(0xffffffffu, key, off);
+        if (lane >= off && ku == key) v += vu;
+      }
+      if (lane == 0) key_first[warp] = key;
+      if (lane == 31) {
+        key_last[warp] = key;
+        v_last[warp] = v;
+      }
+    }
+    __syncthreads();
+    // ---- segment ends: resolve carries and emit
+    if (has_sort) {
+      // the previous tile's last segment is complete unless row 0 continues it
+      if (tid == 0) {
+        int pk = run_key[prev];
+        if (pk >= 0 && pk != key) {
+          if (head_open_s && pk == head_key) {
+            head_rec_key = pk;
+            head_rec_val = run_val[prev];
+            head_open_s = 0;
+          } else {
+            a.bins[pk] = run_val[prev];
+          }
+        }
+      }
+      int kn = __shfl_down_sync(0xffffffffu, key, 1);
+      // a segment ends where the next ROW's key differs: for lane 31 that is
+      // lane 0 of the next warp; row 255 closes the tile (running carry)
+      if (lane == 31) kn = warp < NTHREADS / 32 - 1 ? key_first[warp + 1] : ~key;
+      bool end = kn != key;
+      if (end && key >= 0) {
+        float total = v;
+        if (key_first[warp] == key) {
+          bool reached_start = true;
+          for (int w2 = warp - 1; w2 >= 0; w2--) {
+            if (key_last[w2] != key) {
+              reached_start = false;
+              break;
+            }
+            total += v_last[w2];
+            if (key_first[w2] != key) {
+              reached_start = false;
+              break;
+            }
+          }
+          if (reached_start && run_key[prev] == key) total += run_val[prev];
+        }
+        if (tid == NTHREADS - 1) {
+          run_key[cur] = key;
+          run_val[cur] = total;
+        } else if (head_open_s && key == head_key) {
+          head_rec_key = key;
+          head_rec_val = total;
+          head_open_s = 0;
+        } else {
+          a.bins[key] = total;
+        }
+      } else if (tid == NTHREADS - 1) {
+        run_key[cur] = -1;
+        run_val[cur] = 0.f;
+      }
+    }
+    // ---- phase B: grad_F += r * F rows (column-parallel, float4)
+    if (pb) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int row = pg; row < TILE; row += Gr) {
+        float rr = r_s[row];
+        float4 v4 = Ft[row * c4 + pj];
+        acc.x = fmaf(rr, v4.x, acc.x);
+        acc.y = fmaf(rr, v4.y, acc.y);
+        acc.z = fmaf(rr, v4.z, acc.z);
+        acc.w = fmaf(rr, v4.w, acc.w);
+      }
+      acc0 += acc.x;
+      acc1 += acc.y;
+      acc2 += acc.z;
+      acc3 += acc.w;
+    }
+    __syncthreads();
+    if (tid == 0 && i + a.nst < cnt) {
+      fence_proxy_async();
+      issue(s, t0 + i + a.nst);
+    }
+  }
+
+  // ---- CTA end: final running segment -> carry record
+  __syncthreads();
+  if (tid == 0 && has_sort) {
+    CarryRec c;
+    c.head_key = -1;
+    c.tail_key = -1;
+    c.through = 0;
+    c.pad = 0;
+    c.head_val = 0.0;
+    c.tail_val = 0.0;
+    if (cnt > 0) {
+      const int last = (int)((cnt - 1) & 1);
+      int K = run_key[last];
+      float V = run_val[last];
+      if (K >= 0) {
+        bool cont = R1 < a.r_T && fks[R1] == K;
+        if (head_open_s && K == head_key) {
+          head_rec_key = K;
+          head_rec_val = V;
+          head_open_s = 0;
+          c.through = cont ? 1 : 0;
+        } else if (cont) {
+          c.tail_key = K;
+          c.tail_val = (double)V;
+        } else {
+          a.bins[K] = V;
+        }
+      }
+      c.head_key = head_rec_key;
+      c.head_val = (double)head_rec_val;
+    }
+    a.carry[blockIdx.x] = c;
+  }
+  // ---- CTA partials (fixed-order reductions)
+  double* red = red_s;
+  const int pfc = c4 * 4;
+  double* out = a.part + blockIdx.x * (int64_t)(pfc + 1);
+  // gradient: sum over groups for each of the pfc columns
+  for (int comp = 0; comp < 4; comp++) {
+    double val = comp == 0 ? acc0 : comp == 1 ? acc1 : comp == 2 ? acc2 : acc3;
+    __syncthreads();
+    red[tid] = pb ? val : 0.0;
+    __syncthreads();
+    if (tid < c4) {
+      double sum = 0.0;
+      for (int g = 0; g < Gr; g++) sum += red[g * c4 + tid];
+      out[tid * 4 + comp] = sum;
+    }
+  }
+  // loss
+  double ls = warp_sum(lossd);
+  __syncthreads();
+  if (lane == 0) red[warp] = ls;
+  __syncthreads();
+  if (tid == 0) {
+    double sum = 0.0;
+    for (int w2 = 0; w2 < NTHREADS / 32; w2++) sum += red[w2];
+    out[pfc] = sum;
+  }
+  // ---- last CTA: stitch the segments that span CTAs (fixed order)
+  __threadfence();
+  __syncthreads();
+  __shared__ int is_last;
+  if (tid == 0) is_last = atomicAdd(&a.state->done_fact, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (has_sort) {
+    volatile CarryRec* cr = a.carry;
+    for (int c = tid; c < (int)gridDim.x; c += NTHREADS) {
+      int K = cr[c].tail_key;
+      if (K < 0) continue;
+      double total = cr[c].tail_val;
+      for (int c2 = c + 1; c2 < (int)gridDim.x; c2++) {
+        if (cr[c2].head_key != K) break;
+        total += cr[c2].head_val;
+        if (!cr[c2].through) break;
+      }
+      a.bins[K] = (float)total;
+    }
+  }
+  if (tid == 0) a.state->done_fact = 0;
+}
+
+// ---------------------------------------------------------------------------
+// update: w <- w - lr * red; loss_hist[it] = red[c_T]; refresh fp32 copies
+// ---------------------------------------------------------------------------
+__device__ void glm_apply_update(const UpdateArgs& u) {
+  const int tid = threadIdx.x;
+  const int it = u.state->it;
+  if (tid == 0 && it < u.loss_cap) u.loss_hist[it] = u.red[u.c_T];
+  for (int c = tid; c < u.c_T; c += blockDim.x) u.w64[c] -= u.lr * u.red[c];
+  __syncthreads();
+  for (int j = tid; j < u.pf; j += blockDim.x) {
+    int tc = u.f_tcol[j];
+    u.wF[j] = tc >= 0 ? (float)u.w64[tc] : 0.f;
+  }
+  for (int d = 0; d < u.ng; d++)
+    for (int c = tid; c < u.pitch[d]; c += blockDim.x) {
+      int tc = u.d_tcol[d][c];
+      u.wd[d][c] = tc >= 0 ? (float)u.w64[tc] : 0.f;
+    }
+  if (tid == 0) u.state->it = it + 1;
+}
+
+__device__ void glm_reduce_all(const UpdateArgs& u) {
+  const int tid = threadIdx.x;
+  for (int c = tid; c <= u.c_T; c += blockDim.x) u.red[c] = 0.0;
+  __syncthreads();
+  const int pf1 = u.pf + 1;
+  for (int j = tid; j < pf1; j += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < u.nblk_fact; b++) s += u.part_fact[(int64_t)b * pf1 + j];
+    if (j == u.pf) u.red[u.c_T] = s;
+    else if (u.f_tcol[j] >= 0) u.red[u.f_tcol[j]] = s;
+  }
+  for (int d = 0; d < u.ng; d++) {
+    for (int c = tid; c < u.pitch[d]; c += blockDim.x) {
+      int tc = u.d_tcol[d][c];
+      if (tc < 0) continue;
+      double s = 0.0;
+      for (int b = 0; b < u.nblk_dim[d]; b++) s += u.part_dim[d][(int64_t)b * u.pitch[d] + c];
+      u.red[tc] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// K3: grad_d = S_d^T bins_d, then last CTA reduces (and optionally updates)
+__global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u, int fuse_update) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t bar[4];
+  __shared__ float b_s[TILE];
+  __shared__ double red[NTHREADS];
+  const int d = blockIdx.y;
+  const int tid = threadIdx.x;
+  const bool active = d < a.ng && (int)blockIdx.x < a.nblk[d];
+  if (active) {
+    const int pitch = a.pitch[d], c4 = pitch / 4;
+    const int64_t rows = a.rows[d];
+    const int64_t ntiles = ceil_div(rows, TILE);
+    const int nb = a.nblk[d];
+    const int64_t base = ntiles / nb, rem = ntiles % nb;
+    const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
+    const int64_t cnt = base + (blockIdx.x < rem ? 1 : 0);
+    const uint32_t tile_bytes = TILE * pitch * 4;
+    if (tid == 0) {
+      for (int s = 0; s < a.nst; s++) mbar_init(&bar[s], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int s = 0; s < a.nst && s < cnt; s++) {
+        mbar_arrive_expect_tx(&bar[s], tile_bytes);
+        bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + s) * TILE * (int64_t)pitch, tile_bytes,
+                 &bar[s]);
+      }
+    const int Gr = NTHREADS / c4;
+    const bool pb = tid < Gr * c4;
+    const int pj = tid % c4, pg = tid / c4;
+    double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    for (int64_t i = 0; i < cnt; i++) {
+      const int s = (int)(i % a.nst);
+      int64_t row = (t0 + i) * TILE + tid;
+      float b = 0.f;
+      if (row < rows) {
+        if (a.bins[d]) {
+          b = a.bins[d][row];
+        } else {
+          int64_t m0 = a.grp_ptr[d][row], m1 = a.grp_ptr[d][row + 1];
+          for (int64_t m = m0; m < m1; m++) b += a.resid[a.grp_rows[d][m]];
+        }
+      }
+      b_s[tid] = b;
+      mbar_wait(&bar[s], (uint32_t)((i / a.nst) & 1));
+      __syncthreads();
+      const float4* tile = reinterpret_cast<const float4*>(smem + s * a.stage_bytes);
+      if (pb) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r2 = pg; r2 < TILE; r2 += Gr) {
+          float bb = b_s[r2];
+          float4 v4 = tile[r2 * c4 + pj];
+          acc.x = fmaf(bb, v4.x, acc.x);
+          acc.y = fmaf(bb, v4.y, acc.y);
+          acc.z = fmaf(bb, v4.z, acc.z);
+          acc.w = fmaf(bb, v4.w, acc.w);
+        }
+        acc0 += acc.x;
+        acc1 += acc.y;
+        acc2 += acc.z;
+        acc3 += acc.w;
+      }
+      __syncthreads();
+      if (tid == 0 && i + a.nst < cnt) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[s], tile_bytes);
+        bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + i + a.nst) * TILE * (int64_t)pitch,
+                 tile_bytes, &bar[s]);
+      }
+    }
+    double* out = a.part[d] + blockIdx.x * (int64_t)pitch;
+    for (int comp = 0; comp < 4; comp++) {
+      double val = comp == 0 ? acc0 : comp == 1 ? acc1 : comp == 2 ? acc2 : acc3;
+      __syncthreads();
+      red[tid] = pb ? val : 0.0;
+      __syncthreads();
+      if (tid < c4) {
+        double sum = 0.0;
+        for (int g = 0; g < Gr; g++) sum += red[g * c4 + tid];
+        out[tid * 4 + comp] = sum;
+      }
+    }
+  }
+  // last-block-done over the whole grid
+  __threadfence();
+  __syncthreads();
+  __shared__ int is_last;
+  if (tid == 0)
+    is_last = atomicAdd(&u.state->done_dim, 1) == (int)(gridDim.x * gridDim.y) - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  glm_reduce_all(u);
+  if (fuse_update) glm_apply_update(u);
+  if (tid == 0) u.state->done_dim = 0;
+}
+
+__global__ void k_glm_update(UpdateArgs u) { glm_apply_update(u); }
+
+}  // namespace flb
+
+using namespace flb;
+
+struct fl_glm {
+  fl_table* t = nullptr;
+  int model = 0;
+  double lr = 0;
+  int nblk_fact = 0;
+  int nst_fact = 0;
+  uint32_t stage_fact = 0, off_fk = 0, off_y = 0;
+  size_t smem_fact = 0;
+  int nst_dim = 0;
+  uint32_t stage_dim = 0;
+  size_t smem_dim = 0;
+  int dim_grid_x = 0;
+  DevBuf y, wF, wd, w64, q, bins, resid, part_fact, part_dim, carry, red, loss_hist, state;
+  GlmFactArgs fa{};
+  DimArgs da{};
+  UpdateArgs ua{};
+  int loss_cap = 1 << 16;
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int bins_rows = 0;
+};
+
+namespace flb {
+
+static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
+  fl_table* t = s->t;
+  if (s->bins_rows > 0) FL_CUDA(cudaMemsetAsync(s->bins.p, 0, (size_t)s->bins_rows * 4, st));
+  if (s->da.ng > 0) {
+    dim3 grid(s->dim_grid_x, s->da.ng);
+    k_glm_dim_q<<<grid, NTHREADS, s->smem_dim, st>>>(s->da);
+    FL_CHECK_LAUNCH();
+  }
+  if (s->model == FL_MODEL_LINREG)
+    k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
+  else
+    k_glm_fact<1><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
+  FL_CHECK_LAUNCH();
+  dim3 grid3(std::max(1, s->dim_grid_x), std::max(1, s->da.ng));
+  k_glm_dim_t<<<grid3, NTHREADS, s->smem_dim, st>>>(s->da, s->ua, fuse_update ? 1 : 0);
+  FL_CHECK_LAUNCH();
+  (void)t;
+  return FL_OK;
+}
+
+}  // namespace flb
+
+extern "C" {
+
+int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rate, fl_glm** out,
+                  void* stream) {
+  if (!t || !t->finalized || !y || !out) {
+    set_error("fl_glm_create: bad arguments");
+    return FL_ERR_ARG;
+  }
+  if (model != FL_MODEL_LINREG && model != FL_MODEL_LOGREG) {
+    set_error("unknown model id %d", model);
+    return FL_ERR_CONFIG;
+  }
+  if (!(learning_rate > 0.0)) {
+    set_error("learning_rate must be > 0");
+    return FL_ERR_CONFIG;
+  }
+  if ((int)t->g.size() > MAX_GATHER || t->pf > 252) {
+    set_error("fused GLM supports <= %d gathered sources and <= 252 streamed columns", MAX_GATHER);
+    return FL_ERR_OP;
+  }
+  FL_CUDA(cudaSetDevice(t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* s = new fl_glm();
+  std::unique_ptr<fl_glm> guard(s);
+  s->t = t;
+  s->model = model;
+  s->lr = learning_rate;
+  int rc;
+  const int64_t r_pad = t->r_pad;
+  const int ng = (int)t->g.size();
+  // labels in device order
+  const int yb = model == FL_MODEL_LOGREG ? 1 : 4;
+  if ((rc = s->y.alloc((size_t)r_pad * yb + 16))) return rc;
+  {
+    void* ydev = nullptr;
+    FL_CUDA(cudaMallocAsync(&ydev, (size_t)t->r_T * yb + 16, st));
+    FL_CUDA(cudaMemcpyAsync(ydev, y, (size_t)t->r_T * yb, cudaMemcpyDefault, st));
+    rc = launch_gather_rows_to_device_order(t, ydev, s->y.p, yb, st);
+    if (rc) return rc;
+    FL_CUDA(cudaFreeAsync(ydev, st));
+  }
+  // parameters
+  if ((rc = s->w64.alloc((size_t)t->c_T * 8))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->w64.p, 0, (size_t)t->c_T * 8, st));
+  if ((rc = s->wF.alloc((size_t)t->pf * 4))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->wF.p, 0, (size_t)t->pf * 4, st));
+  size_t wd_total = 0, q_total = 0;
+  for (auto& g : t->g) {
+    wd_total += g.pitch;
+    q_total += round_up(g.rows, 4);
+  }
+  if ((rc = s->wd.alloc(wd_total * 4 + 16))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->wd.p, 0, wd_total * 4 + 16, st));
+  if ((rc = s->q.alloc(q_total * 4 + 16))) return rc;
+  bool any_unsorted = false;
+  for (auto& g : t->g) any_unsorted |= !g.sorted;
+  if (t->sort_g >= 0) {
+    s->bins_rows = (int)t->g[t->sort_g].rows;
+    if ((rc = s->bins.alloc((size_t)s->bins_rows * 4 + 16))) return rc;
+  }
+  if (any_unsorted) {
+    if ((rc = s->resid.alloc((size_t)r_pad * 4))) return rc;
+  }
+  // fact-pass geometry
+  const int c4 = t->pf / 4;
+  s->off_y = (uint32_t)(TILE * t->pf * 4);
+  s->off_fk = s->off_y + (uint32_t)round_up(TILE * yb, 128);
+  s->stage_fact = (uint32_t)round_up(s->off_fk + (t->sort_g >= 0 ? TILE * 4 : 0), 128);
+  s->nst_fact = s->stage_fact <= 24 * 1024 ? 4 : (s->stage_fact <= 36 * 1024 ? 3 : 2);
+  s->smem_fact = (size_t)s->nst_fact * s->stage_fact;
+  if (s->smem_fact > 200 * 1024) {
+    set_error("fused GLM: streamed block too wide (%d columns)", t->nf);
+    return FL_ERR_OP;
+  }
+  auto kf = model == FL_MODEL_LINREG ? (const void*)k_glm_fact<0> : (const void*)k_glm_fact<1>;
+  FL_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_fact));
+  int occ = 1;
+  FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, NTHREADS, s->smem_fact));
+  occ = std::max(1, std::min(occ, 2));
+  const int64_t ntiles = r_pad / TILE;
+  s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)t->sm_count * occ));
+  if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (t->pf + 1) * 8))) return rc;
+  if ((rc = s->carry.alloc((size_t)s->nblk_fact * sizeof(CarryRec)))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->carry.p, 0xff, (size_t)s->nblk_fact * sizeof(CarryRec), st));
+  if ((rc = s->state.alloc(sizeof(GlmState)))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->state.p, 0, sizeof(GlmState), st));
+  if ((rc = s->red.alloc((size_t)(t->c_T + 1) * 8))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->red.p, 0, (size_t)(t->c_T + 1) * 8, st));
+  if ((rc = s->loss_hist.alloc((size_t)s->loss_cap * 8))) return rc;
+
+  GlmFactArgs& fa = s->fa;
+  fa.F = t->F->as<float>();
+  fa.pf = t->pf;
+  fa.c4 = c4;
+  fa.y = s->y.p;
+  fa.r_T = t->r_T;
+  fa.ntiles = ntiles;
+  fa.ng = ng;
+  fa.sort_g = t->sort_g;
+  {
+    size_t qo = 0;
+    for (int d = 0; d < ng; d++) {
+      fa.fk[d] = t->g[d].fk->as<int32_t>();
+      fa.q[d] = s->q.as<float>() + qo;
+      qo += round_up(t->g[d].rows, 4);
+    }
+  }
+  fa.bins = t->sort_g >= 0 ? s->bins.as<float>() : nullptr;
+  fa.resid = any_unsorted ? s->resid.as<float>() : nullptr;
+  fa.wF = s->wF.as<float>();
+  fa.part = s->part_fact.as<double>();
+  fa.carry = s->carry.as<CarryRec>();
+  fa.state = s->state.as<GlmState>();
+  fa.stage_bytes = s->stage_fact;
+  fa.off_fk = s->off_fk;
+  fa.off_y = s->off_y;
+  fa.nst = s->nst_fact;
+
+  // dim geometry
+  DimArgs& da = s->da;
+  da.ng = ng;
+  int max_pitch = 4;
+  for (auto& g : t->g) max_pitch = std::max(max_pitch, g.pitch);
+  s->stage_dim = (uint32_t)(TILE * max_pitch * 4);
+  s->nst_dim = s->stage_dim <= 24 * 1024 ? 4 : (s->stage_dim <= 48 * 1024 ? 3 : 2);
+  s->smem_dim = (size_t)s->nst_dim * s->stage_dim;
+  if (s->smem_dim > 200 * 1024) {
+    set_error("fused GLM: gathered source too wide");
+    return FL_ERR_OP;
+  }
+  FL_CUDA(cudaFuncSetAttribute(k_glm_dim_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->smem_dim));
+  FL_CUDA(cudaFuncSetAttribute(k_glm_dim_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->smem_dim));
+  int occd = 1;
+  FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, k_glm_dim_t, NTHREADS, s->smem_dim));
+  occd = std::max(1, occd);
+  da.stage_bytes = s->stage_dim;
+  da.nst = s->nst_dim;
+  size_t part_dim_total = 0;
+  s->dim_grid_x = 1;
+  for (int d = 0; d < ng; d++) {
+    const GatherSrc& g = t->g[d];
+    int64_t tiles = ceil_div(g.rows, TILE);
+    // share the SMs between sources in proportion to their bytes
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)t->sm_count * occd));
+    da.nblk[d] = nb;
+    s->dim_grid_x = std::max(s->dim_grid_x, nb);
+    part_dim_total += (size_t)nb * g.pitch;
+  }
+  if ((rc = s->part_dim.alloc(part_dim_total * 8 + 16))) return rc;
+  {
+    size_t wo = 0, po = 0;
+    for (int d = 0; d < ng; d++) {
+      const GatherSrc& g = t->g[d];
+      da.S[d] = g.S->as<float>();
+      da.pitch[d] = g.pitch;
+      da.rows[d] = g.rows;
+      da.w[d] = s->wd.as<float>() + wo;
+      da.q[d] = const_cast<float*>(fa.q[d]);
+      da.bins[d] = g.sorted ? fa.bins : nullptr;
+      da.grp_ptr[d] = g.grp_ptr->as<int64_t>();
+      da.grp_rows[d] = g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr;
+      da.part[d] = s->part_dim.as<double>() + po;
+      wo += g.pitch;
+      po += (size_t)da.nblk[d] * g.pitch;
+    }
+    da.resid = fa.resid;
+  }
+  UpdateArgs& ua = s->ua;
+  ua.c_T = t->c_T;
+  ua.pf = t->pf;
+  ua.ng = ng;
+  ua.lr = learning_rate;
+  ua.f_tcol = t->d_f_tcol->as<int32_t>();
+  ua.wF = s->wF.as<float>();
+  ua.w64 = s->w64.as<double>();
+  ua.red = s->red.as<double>();
+  ua.loss_hist = s->loss_hist.as<double>();
+  ua.loss_cap = s->loss_cap;
+  ua.state = s->state.as<GlmState>();
+  ua.part_fact = s->part_fact.as<double>();
+  ua.nblk_fact = s->nblk_fact;
+  for (int d = 0; d < ng; d++) {
+    ua.d_tcol[d] = t->g[d].d_tcol->as<int32_t>();
+    ua.pitch[d] = t->g[d].pitch;
+    ua.wd[d] = const_cast<float*>(da.w[d]);
+    ua.part_dim[d] = da.part[d];
+    ua.nblk_dim[d] = da.nblk[d];
+  }
+  FL_CUDA(cudaStreamSynchronize(st));
+  *out = guard.release();
+  return FL_OK;
+}
+
+int fl_glm_partial(fl_glm* s, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  return glm_launch_iteration(s, (cudaStream_t)stream, false);
+}
+
+int fl_glm_reduce_buffer(fl_glm* s, double** buf, int32_t* len) {
+  if (!s || !buf || !len) return FL_ERR_ARG;
+  *buf = s->red.as<double>();
+  *len = s->t->c_T + 1;
+  return FL_OK;
+}
+
+int fl_glm_update(fl_glm* s, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  k_glm_update<<<1, NTHREADS, 0, (cudaStream_t)stream>>>(s->ua);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
+  if (!s || iterations < 1) {
+    set_error("iterations must be >= 1");
+    return FL_ERR_CONFIG;
+  }
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!s->graph) {
+    if (!s->cap_stream) FL_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = glm_launch_iteration(s, s->cap_stream, true);
+    cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
+    if (rc) return rc;
+    FL_CUDA(e);
+    FL_CUDA(cudaGraphInstantiate(&s->graph, g, 0));
+    FL_CUDA(cudaGraphDestroy(g));
+  }
+  for (int i = 0; i < iterations; i++) FL_CUDA(cudaGraphLaunch(s->graph, st));
+  return FL_OK;
+}
+
+int fl_glm_result(fl_glm* s, double* w, double* loss, int32_t n, int32_t* n_done, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  GlmState h{};
+  FL_CUDA(cudaMemcpyAsync(&h, s->state.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (w) FL_CUDA(cudaMemcpyAsync(w, s->w64.p, (size_t)s->t->c_T * 8, cudaMemcpyDefault, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  int nd = std::min(h.it, s->loss_cap);
+  if (n_done) *n_done = nd;
+  if (loss && n > 0) {
+    int m = std::min(n, nd);
+    if (m > 0) FL_CUDA(cudaMemcpyAsync(loss, s->loss_hist.p, (size_t)m * 8, cudaMemcpyDefault, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+  }
+  return FL_OK;
+}
+
+int fl_glm_destroy(fl_glm* s) {
+  if (!s) return FL_OK;
+  cudaSetDevice(s->t->device);
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  delete s;
+  return FL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+// Internal types shared by the fl_b200 translation units.
+//
+// Device layout of a factorized table T = sum_k I_k S_k M_k^T (see DESIGN.md
+// "Data layout in HBM"):
+//
+//  * Target rows live on the device in a permuted "device order" p -> perm[p]
+//    chosen so that the foreign key of the largest gathered source (the "sort
+//    source") is non-decreasing.  I_sort^T then becomes a contiguous segmented
+//    reduction inside the streaming pass.  Only summation order changes.
+//  * Every source whose indicator is injective (fanout <= 1; the fact table,
+//    union blocks) is expanded into ONE dense row-major fp32 "stream block"
+//    F[r_pad x pf] in device order (zero rows where the source has no match).
+//    Its columns carry their target column (f_tcol); M_k is column addressing.
+//  * Every other source ("gathered", the dimension tables) stays compact:
+//    S_d[r_d x pitch] fp32, plus fk_d[r_pad] int32 in device order (-1 = no
+//    match) and, for unsorted sources, the inverse CSR of I_d (grp_ptr,
+//    grp_rows in device rows, members in ascending TARGET row = the
+//    reference's group order, ops.py:62-66).
+//  * Row pitches are padded to an odd number of float4 so a thread-per-row
+//    read of a TMA-staged tile from shared memory is bank-conflict free.
+//  * All row arrays are padded to a multiple of TILE rows so every TMA bulk
+//    copy moves whole, 16-byte aligned tiles.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/fl_b200.h"
+
+namespace flb {
+
+constexpr int TILE = 256;          // rows per streamed tile (= threads per CTA)
+constexpr int NTHREADS = 256;
+constexpr int MAX_GATHER = 8;      // gathered sources handled by the fused kernels
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define FL_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e__ = (call);                                                \
+    if (e__ != cudaSuccess) return ::flb::cuda_fail(e__, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define FL_CHECK_LAUNCH() FL_CUDA(cudaGetLastError())
+
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// pitch (floats) for c columns: multiple of 4, odd number of float4
+inline int pitch_for(int c) {
+  int c4 = (c + 3) / 4;
+  if (c4 < 1) c4 = 1;
+  if ((c4 & 1) == 0) c4 += 1;
+  return 4 * c4;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf();
+  int alloc(size_t n);
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct GatherSrc {
+  int src_index = -1;        // position among the user's sources
+  int64_t rows = 0;          // r_d
+  int cols = 0;              // c_d
+  int pitch = 0;             // floats
+  std::shared_ptr<DevBuf> S; // rows_pad x pitch fp32 (values; replaced by elementwise)
+  std::vector<int32_t> tcol; // pitch entries (host), -1 = padding column
+  std::shared_ptr<DevBuf> d_tcol;
+  std::shared_ptr<DevBuf> fk;        // r_pad int32 device order
+  bool sorted = false;
+  int64_t n_neg = 0;                 // rows with fk = -1 (sorted source: at the front)
+  std::shared_ptr<DevBuf> grp_ptr;   // (rows+1) int64
+  std::shared_ptr<DevBuf> grp_rows;  // matched int32 device rows (unsorted only)
+  int64_t matched = 0;
+};
+
+struct SrcInfo {
+  bool stream = false;
+  int gidx = -1;       // index into gathers (if gathered)
+  int f_off = 0;       // column offset inside F (if stream)
+  int64_t rows = 0;
+  int cols = 0;
+};
+
+struct Staged {            // source data between add_source and finalize
+  int64_t rows = 0;
+  int cols = 0;
+  std::shared_ptr<DevBuf> vals;     // rows x cols fp32 (compact)
+  std::shared_ptr<DevBuf> ind_sel;  // r_T int32 (target order)
+  std::vector<int32_t> col_map;     // cols target columns
+};
+
+struct Workspace {
+  DevBuf a, b, c, d, e;      // generic scratch, grown on demand
+  DevBuf counter;            // last-block-done counters (zeroed)
+  int grow(DevBuf& buf, size_t bytes);
+};
+
+}  // namespace flb
+
+struct fl_table {
+  int device = 0;
+  int sm_count = 148;
+  int64_t r_T = 0;
+  int c_T = 0;
+  int64_t r_pad = 0;
+  bool finalized = false;
+  std::vector<flb::Staged> staged;
+  std::vector<flb::SrcInfo> src;
+  // stream block
+  int pf = 0;                        // pitch of F in floats (0 = no stream source)
+  int nf = 0;                        // real F columns
+  std::shared_ptr<flb::DevBuf> F;    // r_pad x pf
+  std::vector<int32_t> f_tcol;       // pf entries
+  std::shared_ptr<flb::DevBuf> d_f_tcol;
+  std::vector<flb::GatherSrc> g;
+  int sort_g = -1;                   // gather index of the sort source
+  std::shared_ptr<flb::DevBuf> perm;   // r_pad int32 device row -> target row (-1 pad)
+  std::shared_ptr<flb::DevBuf> iperm;  // r_T int32 target row -> device row
+  flb::Workspace ws;
+};
+
+namespace flb {
+// table.cu
+int table_upload_tcols(fl_table* t);
+// ops.cu helpers used by trainers
+int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target,
+                                       void* dst_dev, int elem_bytes, cudaStream_t s);
+int device_sm_count(int device);
+}  // namespace flb
+
+namespace flb {
+// host-or-device operand / output staging (UVA)
+template <class T>
+inline int to_device(const T* p, size_t n, cudaStream_t s, T** dev, bool* owned) {
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e == cudaSuccess && (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged)) {
+    *dev = const_cast<T*>(p);
+    *owned = false;
+    return FL_OK;
+  }
+  cudaGetLastError();
+  FL_CUDA(cudaMallocAsync((void**)dev, n * sizeof(T) + 16, s));
+  FL_CUDA(cudaMemcpyAsync(*dev, p, n * sizeof(T), cudaMemcpyDefault, s));
+  *owned = true;
+  return FL_OK;
+}
+
+template <class T>
+inline int out_buffer(T* p, size_t n, cudaStream_t s, T** dev, bool* owned) {
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e == cudaSuccess && (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged)) {
+    *dev = p;
+    *owned = false;
+    return FL_OK;
+  }
+  cudaGetLastError();
+  FL_CUDA(cudaMallocAsync((void**)dev, n * sizeof(T) + 16, s));
+  *owned = true;
+  return FL_OK;
+}
+
+template <class T>
+inline int finish_out(T* user, T* dev, bool owned, size_t n, cudaStream_t s) {
+  if (owned) {
+    FL_CUDA(cudaMemcpyAsync(user, dev, n * sizeof(T), cudaMemcpyDefault, s));
+    FL_CUDA(cudaFreeAsync(dev, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+  }
+  return FL_OK;
+}
+
+}  // namespace flb
+
+// ---------------------------------------------------------------------------
+// Device helpers (PTX wrappers for TMA bulk copies and mbarriers).
+// ---------------------------------------------------------------------------
+#ifdef __CUDACC__
+namespace flb {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// TMA 1-D bulk copy global -> shared, completion signalled on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace flb
+#endif

@@ -1,0 +1,413 @@
+// Generic factorized operators behind TargetHandle (ops.py:219-328).
+//
+//   lmm   T x   = F x_F  +  sum_d gather(fk_d, S_d x_d)        (ops.py:227-233)
+//   tlmm  T^T y = F^T y' +  sum_d S_d^T (I_d^T y')             (ops.py:264-269)
+//   rmm   x T   = (T^T x^T)^T  (strided view, ops.py:243-251)
+//
+// y' is y read in device row order.  Per-row dot products run in fp32;
+// every reduction over rows is carried in fp64 with a fixed-order final
+// reduction (deterministic, independent of scheduling).  These kernels serve
+// the op-level API; the trainers use the fused kernels in glm.cu / kmeans.cu.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace flb {
+
+constexpr int CX_CHUNK = 32;   // output columns per launch chunk (lmm)
+
+struct GatherSet {
+  const float* q[MAX_GATHER];
+  const int32_t* fk[MAX_GATHER];
+  int n;
+};
+
+static inline unsigned gridn(int64_t n, int b = 256) { return (unsigned)ceil_div(n, b); }
+
+// q[j, col] = sum_c S[j, c] * x[tcol[c], col0 + col]
+__global__ void k_dim_q(const float* __restrict__ S, int pitch, int cols, int64_t rows,
+                        const int32_t* __restrict__ tcol, const float* __restrict__ x, int c_x,
+                        int col0, int ncol, float* __restrict__ q) {
+  extern __shared__ float xs[];  // cols x ncol
+  for (int i = threadIdx.x; i < cols * ncol; i += blockDim.x) {
+    int c = i / ncol, col = i - c * ncol;
+    xs[i] = x[(int64_t)tcol[c] * c_x + col0 + col];
+  }
+  __syncthreads();
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * ncol) return;
+  int64_t j = idx / ncol;
+  int col = (int)(idx - j * ncol);
+  const float* r = S + j * pitch;
+  float acc = 0.f;
+  for (int c = 0; c < cols; c++) acc = fmaf(r[c], xs[c * ncol + col], acc);
+  q[j * ncol + col] = acc;
+}
+
+// out[perm[p], col0+col] = F[p,:] . xF[:, col] + sum_d q_d[fk_d[p], col]
+__global__ void k_lmm_main(const float* __restrict__ F, int pf, const int32_t* __restrict__ ftcol,
+                           const float* __restrict__ x, int c_x, int col0, int ncol,
+                           GatherSet gs, const int32_t* __restrict__ perm, int64_t r_T,
+                           float* __restrict__ out) {
+  extern __shared__ float xf[];  // pf x ncol
+  for (int i = threadIdx.x; i < pf * ncol; i += blockDim.x) {
+    int j = i / ncol, col = i - j * ncol;
+    int tc = ftcol[j];
+    xf[i] = tc >= 0 ? x[(int64_t)tc * c_x + col0 + col] : 0.f;
+  }
+  __syncthreads();
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= r_T * ncol) return;
+  int64_t p = idx / ncol;
+  int col = (int)(idx - p * ncol);
+  float acc = 0.f;
+  if (pf > 0) {
+    const float* r = F + p * pf;
+    for (int j = 0; j < pf; j++) acc = fmaf(r[j], xf[j * ncol + col], acc);
+  }
+  for (int d = 0; d < gs.n; d++) {
+    int32_t fk = gs.fk[d][p];
+    if (fk >= 0) acc += gs.q[d][(int64_t)fk * ncol + col];
+  }
+  out[(int64_t)perm[p] * c_x + col0 + col] = acc;
+}
+
+// Strided fp32 operand view: element (target row t, col) at base[t*sr + col*sc]
+struct YView {
+  const float* base;
+  int64_t sr, sc;
+  __device__ float at(int64_t t, int col) const { return base[t * sr + (int64_t)col * sc]; }
+};
+
+// Per-block partial of A^T Y over a contiguous row range, A = row-major
+// (pitch) fp32 rows; Y rows either from a device-ordered fp64 buffer (bins)
+// or from the strided target-order view through perm.  Partials are fp64:
+// part[block][j * cy + col].
+template <bool BINS>
+__global__ void k_tmm_partial(const float* __restrict__ A, int pitch, int acols, int64_t rows,
+                              YView yv, const int32_t* __restrict__ perm,
+                              const double* __restrict__ bins, int cy, int64_t rows_per_block,
+                              double* __restrict__ part) {
+  extern __shared__ double acc[];  // acols * cy
+  constexpr int RC = 32;
+  __shared__ float as_[RC * 80];
+  __shared__ double ys[RC * 32];
+  const int npair = acols * cy;
+  for (int i = threadIdx.x; i < npair; i += blockDim.x) acc[i] = 0.0;
+  int64_t r0 = blockIdx.x * rows_per_block;
+  int64_t r1 = min(rows, r0 + rows_per_block);
+  // process in chunks of RC rows; columns of A in chunks of 80, y cols in chunks of 32
+  for (int64_t rb = r0; rb < r1; rb += RC) {
+    int nr = (int)min64(RC, r1 - rb);
+    for (int a0 = 0; a0 < acols; a0 += 80) {
+      int na = min(80, acols - a0);
+      for (int y0 = 0; y0 < cy; y0 += 32) {
+        int ny = min(32, cy - y0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nr * na; i += blockDim.x) {
+          int r = i / na, c = i - r * na;
+          as_[r * 80 + c] = A[(rb + r) * pitch + a0 + c];
+        }
+        for (int i = threadIdx.x; i < nr * ny; i += blockDim.x) {
+          int r = i / ny, c = i - r * ny;
+          double v;
+          if (BINS) v = bins[(rb + r) * cy + y0 + c];
+          else v = (double)yv.at(perm[rb + r], y0 + c);
+          ys[r * 32 + c] = v;
+        }
+        __syncthreads();
+        for (int pr = threadIdx.x; pr < na * ny; pr += blockDim.x) {
+          int a = pr / ny, c = pr - a * ny;
+          double s = 0.0;
+          for (int r = 0; r < nr; r++) s = fma((double)as_[r * 80 + a], ys[r * 32 + c], s);
+          acc[(a0 + a) * cy + y0 + c] += s;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npair; i += blockDim.x)
+    part[(int64_t)blockIdx.x * npair + i] = acc[i];
+}
+
+// bins[j, col] = sum over members m of group j (ascending target row) of y'(m, col)
+__global__ void k_group_bins(const int64_t* __restrict__ grp_ptr, const int32_t* __restrict__ grp_rows,
+                             bool sorted, int64_t n_neg, int64_t rows, YView yv,
+                             const int32_t* __restrict__ perm, int cy, double* __restrict__ bins) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * cy) return;
+  int64_t j = idx / cy;
+  int col = (int)(idx - j * cy);
+  int64_t m0 = grp_ptr[j], m1 = grp_ptr[j + 1];
+  double s = 0.0;
+  for (int64_t m = m0; m < m1; m++) {
+    int64_t p = sorted ? n_neg + m : (int64_t)grp_rows[m];
+    s += (double)yv.at(perm[p], col);
+  }
+  bins[idx] = s;
+}
+
+// out[tcol[a] * os_t + col * os_c] += sum_b part[b][a*cy + col]  (fixed order)
+__global__ void k_reduce_partials(const double* __restrict__ part, int nblocks, int acols,
+                                  int cy, const int32_t* __restrict__ tcol, double* __restrict__ out,
+                                  int64_t os_t, int64_t os_c) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int npair = acols * cy;
+  if (i >= npair) return;
+  int a = i / cy, col = i - a * cy;
+  int tc = tcol[a];
+  if (tc < 0) return;
+  double s = 0.0;
+  for (int b = 0; b < nblocks; b++) s += part[(int64_t)b * npair + i];
+  out[tc * os_t + col * os_c] += s;
+}
+
+__global__ void k_fill(float* p, int64_t n, float v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_gather_dev_order(const char* __restrict__ src, char* __restrict__ dst,
+                                   const int32_t* __restrict__ perm, int64_t r_pad, int eb) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= r_pad) return;
+  int32_t t = perm[p];
+  for (int b = 0; b < eb; b++) dst[p * eb + b] = t >= 0 ? src[(int64_t)t * eb + b] : 0;
+}
+
+int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target, void* dst_dev,
+                                       int elem_bytes, cudaStream_t s) {
+  k_gather_dev_order<<<gridn(t->r_pad), 256, 0, s>>>((const char*)src_target, (char*)dst_dev,
+                                                     t->perm->as<int32_t>(), t->r_pad, elem_bytes);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+// ---------------------------------------------------------------------------
+static int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s) {
+  if ((int)t->g.size() > MAX_GATHER) {
+    set_error("lmm: at most %d gathered sources supported", MAX_GATHER);
+    return FL_ERR_OP;
+  }
+  for (int col0 = 0; col0 < c_x; col0 += CX_CHUNK) {
+    int ncol = std::min(CX_CHUNK, c_x - col0);
+    GatherSet gs{};
+    gs.n = (int)t->g.size();
+    std::vector<float*> qs;
+    for (int d = 0; d < gs.n; d++) {
+      const GatherSrc& g = t->g[d];
+      float* q = nullptr;
+      FL_CUDA(cudaMallocAsync((void**)&q, g.rows * ncol * 4 + 16, s));
+      qs.push_back(q);
+      size_t sm = (size_t)g.cols * ncol * 4;
+      k_dim_q<<<gridn(g.rows * ncol), 256, sm, s>>>(g.S->as<float>(), g.pitch, g.cols, g.rows,
+                                                    g.d_tcol->as<int32_t>(), x_dev, c_x, col0,
+                                                    ncol, q);
+      FL_CHECK_LAUNCH();
+      gs.q[d] = q;
+      gs.fk[d] = g.fk->as<int32_t>();
+    }
+    size_t sm = (size_t)t->pf * ncol * 4;
+    k_lmm_main<<<gridn(t->r_T * ncol), 256, sm, s>>>(
+        t->F ? t->F->as<float>() : nullptr, t->pf, t->pf ? t->d_f_tcol->as<int32_t>() : nullptr,
+        x_dev, c_x, col0, ncol, gs, t->perm->as<int32_t>(), t->r_T, out_dev);
+    FL_CHECK_LAUNCH();
+    for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
+  }
+  return FL_OK;
+}
+
+// generic T^T y with strided y view and strided fp64 output
+static int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
+                   cudaStream_t s) {
+  const int sms = t->sm_count;
+  auto launch_tmm = [&](const float* A, int pitch, int acols, int64_t rows, const double* bins,
+                        const int32_t* tcol) -> int {
+    if (rows <= 0 || acols <= 0) return FL_OK;
+    int64_t nb = std::min<int64_t>(std::max<int64_t>(1, ceil_div(rows, 2048)), 4 * sms);
+    int64_t rpb = round_up(ceil_div(rows, nb), 32);
+    nb = ceil_div(rows, rpb);
+    int npair = acols * cy;
+    double* part = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
+    size_t sm = (size_t)npair * 8;
+    if (sm > 200 * 1024) {
+      set_error("tlmm: %d x %d output too wide for one pass", acols, cy);
+      return FL_ERR_OP;
+    }
+    if (bins) {
+      FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+      k_tmm_partial<true><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv, nullptr, bins,
+                                                        cy, rpb, part);
+    } else {
+      FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_tmm_partial<false><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv,
+                                                         t->perm->as<int32_t>(), nullptr, cy, rpb,
+                                                         part);
+    }
+    FL_CHECK_LAUNCH();
+    k_reduce_partials<<<gridn(npair), 256, 0, s>>>(part, (int)nb, acols, cy, tcol, out, os_t, os_c);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaFreeAsync(part, s));
+    return FL_OK;
+  };
+  int rc;
+  if (t->pf > 0) {
+    rc = launch_tmm(t->F->as<float>(), t->pf, t->pf, t->r_T, nullptr, t->d_f_tcol->as<int32_t>());
+    if (rc) return rc;
+  }
+  for (auto& g : t->g) {
+    double* bins = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&bins, g.rows * cy * 8 + 16, s));
+    k_group_bins<<<gridn(g.rows * cy), 256, 0, s>>>(
+        g.grp_ptr->as<int64_t>(), g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr, g.sorted,
+        g.n_neg, g.rows, yv, t->perm->as<int32_t>(), cy, bins);
+    FL_CHECK_LAUNCH();
+    rc = launch_tmm(g.S->as<float>(), g.pitch, g.cols, g.rows, bins, g.d_tcol->as<int32_t>());
+    if (rc) return rc;
+    FL_CUDA(cudaFreeAsync(bins, s));
+  }
+  return FL_OK;
+}
+
+}  // namespace flb
+
+using namespace flb;
+
+#define FL_REQUIRE_TABLE(t)                                  \
+  do {                                                       \
+    if (!(t) || !(t)->finalized) {                           \
+      set_error("table is null or not finalized");           \
+      return FL_ERR_ARG;                                     \
+    }                                                        \
+    FL_CUDA(cudaSetDevice((t)->device));                     \
+  } while (0)
+
+extern "C" {
+
+int fl_lmm(fl_table* t, const float* x, int32_t c_x, float* out, void* stream) {
+  FL_REQUIRE_TABLE(t);
+  if (c_x < 1 || !x || !out) {
+    set_error("lmm: bad operand");
+    return FL_ERR_SHAPE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  float *xd, *od;
+  bool xo, oo;
+  int rc = to_device(x, (size_t)t->c_T * c_x, s, &xd, &xo);
+  if (rc) return rc;
+  rc = out_buffer(out, (size_t)t->r_T * c_x, s, &od, &oo);
+  if (rc) return rc;
+  rc = do_lmm(t, xd, c_x, od, s);
+  if (rc) return rc;
+  if (xo) FL_CUDA(cudaFreeAsync(xd, s));
+  return finish_out(out, od, oo, (size_t)t->r_T * c_x, s);
+}
+
+int fl_tlmm(fl_table* t, const float* y, int32_t c_y, double* out, void* stream) {
+  FL_REQUIRE_TABLE(t);
+  if (c_y < 1 || !y || !out) {
+    set_error("transpose_lmm: bad operand");
+    return FL_ERR_SHAPE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  float* yd;
+  double* od;
+  bool yo, oo;
+  int rc = to_device(y, (size_t)t->r_T * c_y, s, &yd, &yo);
+  if (rc) return rc;
+  rc = out_buffer(out, (size_t)t->c_T * c_y, s, &od, &oo);
+  if (rc) return rc;
+  FL_CUDA(cudaMemsetAsync(od, 0, (size_t)t->c_T * c_y * 8, s));
+  rc = do_tlmm(t, YView{yd, c_y, 1}, c_y, od, c_y, 1, s);
+  if (rc) return rc;
+  if (yo) FL_CUDA(cudaFreeAsync(yd, s));
+  return finish_out(out, od, oo, (size_t)t->c_T * c_y, s);
+}
+
+int fl_rmm(fl_table* t, const float* x, int32_t r_x, double* out, void* stream) {
+  FL_REQUIRE_TABLE(t);
+  if (r_x < 1 || !x || !out) {
+    set_error("rmm: bad operand");
+    return FL_ERR_SHAPE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  float* xd;
+  double* od;
+  bool xo, oo;
+  int rc = to_device(x, (size_t)r_x * t->r_T, s, &xd, &xo);
+  if (rc) return rc;
+  rc = out_buffer(out, (size_t)r_x * t->c_T, s, &od, &oo);
+  if (rc) return rc;
+  FL_CUDA(cudaMemsetAsync(od, 0, (size_t)r_x * t->c_T * 8, s));
+  // y'(target row, col) = x[col, target row]; out[col, tcol]
+  rc = do_tlmm(t, YView{xd, 1, t->r_T}, r_x, od, 1, t->c_T, s);
+  if (rc) return rc;
+  if (xo) FL_CUDA(cudaFreeAsync(xd, s));
+  return finish_out(out, od, oo, (size_t)r_x * t->c_T, s);
+}
+
+int fl_row_sum(fl_table* t, float* out, void* stream) {
+  FL_REQUIRE_TABLE(t);
+  cudaStream_t s = (cudaStream_t)stream;
+  float* ones;
+  FL_CUDA(cudaMallocAsync((void**)&ones, t->c_T * 4 + 16, s));
+  k_fill<<<gridn(t->c_T), 256, 0, s>>>(ones, t->c_T, 1.0f);
+  FL_CHECK_LAUNCH();
+  float* od;
+  bool oo;
+  int rc = out_buffer(out, (size_t)t->r_T, s, &od, &oo);
+  if (rc) return rc;
+  rc = do_lmm(t, ones, 1, od, s);
+  if (rc) return rc;
+  FL_CUDA(cudaFreeAsync(ones, s));
+  return finish_out(out, od, oo, (size_t)t->r_T, s);
+}
+
+int fl_col_sum(fl_table* t, double* out, void* stream) {
+  FL_REQUIRE_TABLE(t);
+  cudaStream_t s = (cudaStream_t)stream;
+  float* ones;
+  FL_CUDA(cudaMallocAsync((void**)&ones, t->r_T * 4 + 16, s));
+  k_fill<<<gridn(t->r_T), 256, 0, s>>>(ones, t->r_T, 1.0f);
+  FL_CHECK_LAUNCH();
+  double* od;
+  bool oo;
+  int rc = out_buffer(out, (size_t)t->c_T, s, &od, &oo);
+  if (rc) return rc;
+  FL_CUDA(cudaMemsetAsync(od, 0, (size_t)t->c_T * 8, s));
+  rc = do_tlmm(t, YView{ones, 1, 0}, 1, od, 1, 0, s);
+  if (rc) return rc;
+  FL_CUDA(cudaFreeAsync(ones, s));
+  return finish_out(out, od, oo, (size_t)t->c_T, s);
+}
+
+int fl_crossprod(fl_table* t, double* out, void* stream) {
+  FL_REQUIRE_TABLE(t);
+  cudaStream_t s = (cudaStream_t)stream;
+  // T^T T: materialize in row panels and reuse the strided tlmm (panel of
+  // target columns as y).  O(r_T c_T^2) -- a reference-free extra operator.
+  const int64_t r_T = t->r_T;
+  const int c_T = t->c_T;
+  float* mat;
+  FL_CUDA(cudaMallocAsync((void**)&mat, (size_t)r_T * c_T * 4 + 16, s));
+  int rc = fl_materialize(t, mat, stream);
+  if (rc) return rc;
+  double* od;
+  bool oo;
+  rc = out_buffer(out, (size_t)c_T * c_T, s, &od, &oo);
+  if (rc) return rc;
+  FL_CUDA(cudaMemsetAsync(od, 0, (size_t)c_T * c_T * 8, s));
+  for (int c0 = 0; c0 < c_T; c0 += 32) {
+    int nc = std::min(32, c_T - c0);
+    // y'(t, col) = mat[t, c0 + col]; out[tc, c0 + col]
+    rc = do_tlmm(t, YView{mat + c0, c_T, 1}, nc, od + c0, c_T, 1, s);
+    if (rc) return rc;
+  }
+  FL_CUDA(cudaFreeAsync(mat, s));
+  return finish_out(out, od, oo, (size_t)c_T * c_T, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+"""GPU parity: the B200 operators vs the reference's golden vectors and the
+CPU oracle.  Integer / index work and the join are compared bit-exactly;
+floating point at the north-star tolerance (fp32 storage, fp64 reductions)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_names, load_golden, star_table
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5   # operator outputs: fp32 values, fp64 reductions
+
+
+def rel(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def fl():
+    import paper_2502_01985_b200 as fl
+    return fl
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_materialize_bit_exact(fl, name):
+    g = load_golden(name)
+    h = fl.TargetHandle.factorized(g.ft)
+    got = h.materialize_dense()
+    assert got.dtype == np.float32
+    assert np.array_equal(got.astype(np.float64), g["materialized"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_selectors_bit_exact(fl, name):
+    """Device-derived selectors (perm, stable sort, scan) == the reference's
+    `_build_selectors` output (ops.py:55-74)."""
+    g = load_golden(name)
+    h = fl.TargetHandle.factorized(g.ft)
+    sels = h.selectors
+    for k, s in enumerate(sels):
+        assert np.array_equal(s.ind_sel, g[f"ind_sel{k}"])
+        assert np.array_equal(s.group_indptr, g[f"group_indptr{k}"])
+        assert np.array_equal(s.group_rows, g[f"group_rows{k}"])
+        assert np.array_equal(s.map_sel, g[f"map_sel{k}"])
+        assert np.array_equal(s.map_sel_t, g[f"map_sel_t{k}"])
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if n != "clusters"])
+def test_operators_match_reference(fl, name):
+    g = load_golden(name)
+    h = fl.TargetHandle.factorized(g.ft)
+    x = fl.SparseMatrix.from_dense(g["op_x"])
+    w = fl.SparseMatrix.from_dense(g["op_w"])
+    y = fl.SparseMatrix.from_dense(g["op_y"])
+    assert rel(h.lmm(x).to_dense(), g["lmm"]) < RTOL
+    assert rel(h.rmm(w).to_dense(), g["rmm"]) < RTOL
+    assert rel(h.transpose_lmm(y).to_dense(), g["tlmm"]) < RTOL
+    assert rel(h.row_sum().to_dense(), g["row_sum"]) < RTOL
+    assert rel(h.col_sum().to_dense(), g["col_sum"]) < RTOL
+    sq = h.elementwise("square").materialize_target().to_dense()
+    assert rel(sq, g["sq_materialized"]) < 1e-7
+    assert rel(h.elementwise("abs").lmm(x).to_dense(), g["abs_lmm"]) < RTOL
+
+
+def test_spec_examples(fl):
+    """test_factorized_ops.py:87-138: lmm(I)=T, rmm(I)=T, rmm(e_i)=row i,
+    lmm(1)=rowSum, rmm(1)=colSum, tlmm(I)=T^T."""
+    g = load_golden("two_source")
+    ref = g["materialized"]
+    h = fl.TargetHandle.factorized(g.ft)
+    eye = fl.SparseMatrix.identity(4)
+    assert np.array_equal(h.lmm(eye).to_dense(), ref)
+    assert np.array_equal(h.rmm(eye).to_dense(), ref)
+    assert np.array_equal(h.transpose_lmm(eye).to_dense(), ref.T)
+    for i in range(4):
+        e = fl.SparseMatrix.from_coo(1, 4, [0], [i], [1.0])
+        assert np.array_equal(h.rmm(e).to_dense(), ref[i:i + 1])
+    ones = fl.SparseMatrix.from_dense(np.ones((4, 1)))
+    assert np.allclose(h.lmm(ones).to_dense(), h.row_sum().to_dense())
+    ones_r = fl.SparseMatrix.from_dense(np.ones((1, 4)))
+    assert np.allclose(h.rmm(ones_r).to_dense(), h.col_sum().to_dense())
+
+
+def test_outer_padding_row_is_zero(fl):
+    g = load_golden("outer")
+    h = fl.TargetHandle.factorized(g.ft)
+    rs = h.row_sum().to_dense()
+    assert rs[4, 0] == 0.0
+
+
+def test_materialized_handle_matches(fl):
+    g = load_golden("star3")
+    tmat = fl.SparseMatrix.from_dense(g["materialized"])
+    mh = fl.TargetHandle.materialized(tmat)
+    assert mh.path == "materialized"
+    x = g["op_x"]
+    assert rel(mh.lmm(x), g["lmm"]) < RTOL
+    assert rel(mh.transpose_lmm(g["op_y"]), g["tlmm"]) < RTOL
+    assert rel(mh.rmm(g["op_w"]), g["rmm"]) < RTOL
+
+
+def test_crossprod(fl):
+    g = load_golden("star3")
+    h = fl.TargetHandle.factorized(g.ft)
+    td = g["materialized"]
+    assert rel(h.crossprod(), td.T @ td) < RTOL
+
+
+def test_shape_errors(fl):
+    g = load_golden("two_source")
+    h = fl.TargetHandle.factorized(g.ft)
+    with pytest.raises(fl.ShapeError):
+        h.lmm(np.ones((5, 2)))
+    with pytest.raises(fl.ShapeError):
+        h.rmm(np.ones((2, 5)))
+    with pytest.raises(fl.ShapeError):
+        h.transpose_lmm(np.ones((3, 2)))
+    with pytest.raises(fl.OpError, match="materialization"):
+        h.elementwise("logistic")
+
+
+def test_invalid_metadata_rejected(fl):
+    from paper_2502_01985_b200.metadata import MetadataError
+    s1 = fl.SparseMatrix.from_dense([[1.0, 2.0]])
+    s2 = fl.SparseMatrix.from_dense([[3.0, 4.0]])
+    m1 = fl.MappingMatrix(fl.SparseMatrix.from_dense([[1, 0], [0, 1], [0, 0]]))
+    m2 = fl.MappingMatrix(fl.SparseMatrix.from_dense([[0, 0], [1, 0], [0, 1]]))
+    i = fl.IndicatorMatrix(fl.SparseMatrix.from_dense([[1.0]]))
+    bad = fl.FactorizedTable([s1, s2], [m1, m2], [i, i], "inner", 1, 3)
+    with pytest.raises(MetadataError):
+        fl.TargetHandle.factorized(bad)
+
+
+@pytest.mark.parametrize("dims,sort_fk", [([(1000, 13)], False), ([(700, 9), (60, 5)], False),
+                                          ([(50, 7)], True), ([(3, 4), (997, 6)], False)])
+def test_random_star_vs_oracle(fl, dims, sort_fk):
+    """Larger random star schemas (several tiles and CTAs, segments crossing
+    tiles and CTAs) vs the oracle."""
+    ft = star_table(5, 150_000, dims, 21, sort_fk=sort_fk)
+    tab = oracle.OracleTable.from_ft(ft)
+    h = fl.TargetHandle.factorized(ft)
+    rng = np.random.default_rng(0)
+    x = rng.random((ft.c_T, 3)).astype(np.float32)
+    y = rng.random((ft.r_T, 2)).astype(np.float32)
+    w = rng.random((2, ft.r_T)).astype(np.float32)
+    assert rel(h.lmm(x), oracle.lmm(tab, x)) < RTOL
+    assert rel(h.transpose_lmm(y), oracle.transpose_lmm(tab, y)) < RTOL
+    assert rel(h.rmm(w), oracle.rmm(tab, w)) < RTOL
+    assert np.array_equal(h.materialize_dense().astype(np.float64), oracle.materialize(tab))

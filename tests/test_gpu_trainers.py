@@ -1,0 +1,117 @@
+"""GPU parity of the fused trainers vs the reference's golden runs and the
+CPU oracle.  Tolerance (north star): 1e-4 relative on weights, losses and
+centroids; K-means assignments identical on well-separated data."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import reference_trainers as rt
+from conftest import golden_names, load_golden, star_table
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def max_rel(a, b, floor=1e-12):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    scale = max(np.max(np.abs(b)), floor)
+    return float(np.max(np.abs(a - b)) / scale)
+
+
+@pytest.fixture(scope="module")
+def fl():
+    import paper_2502_01985_b200 as fl
+    return fl
+
+
+def _cases(models):
+    out = []
+    for name in golden_names():
+        g = load_golden(name)
+        for m in g.meta.get("trainers", {}):
+            if m in models:
+                out.append((name, m))
+    return out
+
+
+@pytest.mark.parametrize("name,model", _cases(("linreg", "logreg")))
+def test_glm_matches_reference(fl, name, model):
+    g = load_golden(name)
+    m = g.meta["trainers"][model]
+    h = fl.TargetHandle.factorized(g.ft)
+    y = g["y_lin"] if model == "linreg" else g["y_log"]
+    cfg = fl.TrainConfig(iterations=m["iterations"], learning_rate=m["learning_rate"],
+                         k_clusters=m["k_clusters"], rank=m["rank"], seed=m["seed"])
+    res = fl.train(model, h, cfg, fl.SparseMatrix.from_dense(y))
+    assert len(res.loss_history) == m["iterations"]
+    assert max_rel(res.loss_history, g[f"{model}_loss"]) < TOL
+    assert max_rel(res.parameters["w"], g[f"{model}_w"]) < TOL
+
+
+@pytest.mark.parametrize("model", ["linreg", "logreg"])
+@pytest.mark.parametrize("dims", [[(2000, 17)], [(900, 11), (40, 3)], [(30000, 6)]])
+def test_glm_random_star_vs_oracle(fl, model, dims):
+    ft = star_table(11, 120_000, dims, 20)
+    tab = oracle.OracleTable.from_ft(ft)
+    rng = np.random.default_rng(3)
+    if model == "linreg":
+        y = rng.random(ft.r_T).astype(np.float32).astype(np.float64)
+    else:
+        y = rng.integers(0, 2, ft.r_T).astype(np.float64)
+    lr = rt.safe_learning_rate(tab)
+    want = rt.train(model, tab, iterations=8, learning_rate=lr, y=y)
+    h = fl.TargetHandle.factorized(ft)
+    res = fl.train(model, h, fl.TrainConfig(iterations=8, learning_rate=lr), y.reshape(-1, 1))
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+    assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
+
+
+def test_glm_deterministic(fl):
+    ft = star_table(12, 90_000, [(500, 9)], 12)
+    y = np.random.default_rng(1).random((ft.r_T, 1))
+    h = fl.TargetHandle.factorized(ft)
+    cfg = fl.TrainConfig(iterations=5, learning_rate=1e-6)
+    a = fl.train("linreg", h, cfg, y)
+    b = fl.train("linreg", h, cfg, y)
+    assert np.array_equal(a.parameters["w"], b.parameters["w"])
+    assert a.loss_history == b.loss_history
+
+
+def test_first_loss_and_one_step(fl):
+    """test_trainers.py:112-119, :151-160: loss_0 = 1/2||y||^2; one step from
+    w0 = 0 lands at lr T^T y."""
+    g = load_golden("two_source")
+    h = fl.TargetHandle.factorized(g.ft)
+    y = np.random.default_rng(4).standard_normal((4, 1))
+    res = fl.train("linreg", h, fl.TrainConfig(iterations=1, learning_rate=1e-3), y)
+    assert res.loss_history[0] == pytest.approx(0.5 * float((y ** 2).sum()), rel=1e-6)
+    want = 1e-3 * (g["materialized"].T @ y)
+    assert max_rel(res.parameters["w"], want) < 1e-6
+
+
+def test_divergence_raises(fl):
+    g = load_golden("two_source")
+    h = fl.TargetHandle.factorized(g.ft)
+    y = np.random.default_rng(5).standard_normal((4, 1))
+    with pytest.raises(fl.DivergenceError) as exc:
+        fl.train("linreg", h, fl.TrainConfig(iterations=200, learning_rate=1e3), y)
+    assert exc.value.iteration > 0
+
+
+def test_logreg_label_check(fl):
+    g = load_golden("two_source")
+    h = fl.TargetHandle.factorized(g.ft)
+    with pytest.raises(fl.ConfigError, match="0/1"):
+        fl.train("logreg", h, fl.TrainConfig(), np.array([[2.0], [0.0], [1.0], [0.0]]))
+
+
+def test_materialized_path_agrees(fl):
+    g = load_golden("star")
+    m = g.meta["trainers"]["linreg"]
+    cfg = fl.TrainConfig(iterations=m["iterations"], learning_rate=m["learning_rate"])
+    mh = fl.TargetHandle.materialized(fl.SparseMatrix.from_dense(g["materialized"]))
+    res = fl.train("linreg", mh, cfg, g["y_lin"])
+    assert max_rel(res.loss_history, g["linreg_loss"]) < TOL
