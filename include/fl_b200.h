@@ -66,7 +66,8 @@ int fl_device_info(int device, int* sm_count, int64_t* l2_bytes, int* cc_major, 
  *      _build_selectors (ops.py:55-74) ---------------------------------- */
 int fl_table_create(int device, int64_t r_T, int32_t c_T, fl_table** out);
 /* Add source k (in order).  values: r_k x c_k row-major fp32 (host or device).
- * ind_sel: r_T int32 source row per target row, -1 = no match (ops.py:58-61).
+ * ind_sel: r_T int32 source row per target row, -1 = no match (ops.py:58-61);
+ * NULL = identity indicator (requires r_k == r_T: the fact table of a star).
  * col_map: c_k int32 target column of each source column (map_sel_t,
  * ops.py:67-72), host memory. */
 int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* values,
@@ -131,6 +132,10 @@ int fl_glm_reduce_buffer(fl_glm* s, double** buf, int32_t* len);
 int fl_glm_update(fl_glm* s, void* stream);
 /* single-GPU convenience: iterations x (partial, update), CUDA-graph replayed */
 int fl_glm_run(fl_glm* s, int32_t iterations, void* stream);
+/* measurement hook: run `iters` iterations launching K1 / K2 / K3 separately
+ * with CUDA events between them on `stream`; ms_out[3] = mean ms per kernel
+ * (K1 includes the bins memset).  Advances the model like fl_glm_run. */
+int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream);
 /* copy out w (c_T fp64) and the first n losses (fp64); host or device */
 int fl_glm_result(fl_glm* s, double* w, double* loss, int32_t n, int32_t* n_done, void* stream);
 int fl_glm_destroy(fl_glm* s);

@@ -90,7 +90,10 @@ def _group_sum(ind_sel, n_groups, x):
     """I_k^T x: ascending-member grouped sum (`_kernels.py:252-288`)."""
     out = np.zeros((n_groups, x.shape[1]))
     ok = ind_sel >= 0
-    np.add.at(out, ind_sel[ok], x[ok])
+    idx = ind_sel[ok]
+    xs = x[ok]
+    for c in range(x.shape[1]):
+        out[:, c] = np.bincount(idx, weights=xs[:, c], minlength=n_groups)
     return out
 
 

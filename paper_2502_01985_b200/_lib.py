@@ -70,6 +70,7 @@ SIGNATURES = {
     "fl_glm_reduce_buffer": [_P, C.POINTER(C.c_void_p), C.POINTER(_I32)],
     "fl_glm_update": [_P, _P],
     "fl_glm_run": [_P, _I32, _P],
+    "fl_glm_kernel_times": [_P, _I32, _P, _P],
     "fl_glm_result": [_P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_glm_destroy": [_P],
     "fl_kmeans_create": [_P, _I32, _P, _PP, _P],

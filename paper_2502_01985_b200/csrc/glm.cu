@@ -878,6 +878,44 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
   return FL_OK;
 }
 
+int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
+  if (!s || iters < 1 || !ms_out) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[4];
+  for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
+  float acc[3] = {0.f, 0.f, 0.f};
+  for (int i = 0; i < iters; i++) {
+    FL_CUDA(cudaEventRecord(ev[0], st));
+    if (s->bins_rows > 0) FL_CUDA(cudaMemsetAsync(s->bins.p, 0, (size_t)s->bins_rows * 4, st));
+    if (s->da.ng > 0) {
+      dim3 grid(s->dim_grid_x, s->da.ng);
+      k_glm_dim_q<<<grid, NTHREADS, s->smem_dim, st>>>(s->da);
+      FL_CHECK_LAUNCH();
+    }
+    FL_CUDA(cudaEventRecord(ev[1], st));
+    if (s->model == FL_MODEL_LINREG)
+      k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
+    else
+      k_glm_fact<1><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord(ev[2], st));
+    dim3 grid3(std::max(1, s->dim_grid_x), std::max(1, s->da.ng));
+    k_glm_dim_t<<<grid3, NTHREADS, s->smem_dim, st>>>(s->da, s->ua, 1);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord(ev[3], st));
+    FL_CUDA(cudaEventSynchronize(ev[3]));
+    for (int k = 0; k < 3; k++) {
+      float ms = 0.f;
+      FL_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      acc[k] += ms;
+    }
+  }
+  for (int k = 0; k < 3; k++) ms_out[k] = acc[k] / iters;
+  for (auto& e : ev) cudaEventDestroy(e);
+  return FL_OK;
+}
+
 int fl_glm_result(fl_glm* s, double* w, double* loss, int32_t n, int32_t* n_done, void* stream) {
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));

@@ -313,7 +313,7 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     set_error("fl_table_add_source: table is finalized or null");
     return FL_ERR_ARG;
   }
-  if (r_k < 1 || c_k < 1 || !values || !ind_sel || !col_map) {
+  if (r_k < 1 || c_k < 1 || !values || !col_map || (!ind_sel && r_k != t->r_T)) {
     set_error("fl_table_add_source: invalid source %lld x %d", (long long)r_k, c_k);
     return FL_ERR_ARG;
   }
@@ -335,7 +335,13 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
   st.ind_sel = make_buf((size_t)t->r_T * 4, &rc);
   if (rc) return rc;
   FL_CUDA(cudaMemcpy(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault));
-  FL_CUDA(cudaMemcpy(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault));
+  if (ind_sel) {
+    FL_CUDA(cudaMemcpy(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault));
+  } else {  // identity indicator (the fact table of a star schema)
+    k_iota_perm<<<grid_for(t->r_T), 256>>>(st.ind_sel->as<int32_t>(), t->r_T, t->r_T);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaDeviceSynchronize());
+  }
   t->staged.push_back(std::move(st));
   return FL_OK;
 }

@@ -94,7 +94,9 @@ def upload_arrays(sources, ind_sels, col_maps, r_T: int, c_T: int, *,
         else:
             keep = np.ascontiguousarray(vals, dtype=np.float32)
             v_ptr, (r_k, c_k) = keep.ctypes.data, keep.shape
-        if _is_torch(sel):
+        if sel is None:           # identity indicator (r_k == r_T)
+            s_keep, s_ptr = None, 0
+        elif _is_torch(sel):
             s_keep, s_ptr = sel, sel.data_ptr()
         else:
             s_keep = np.ascontiguousarray(sel, dtype=np.int32)

@@ -180,6 +180,14 @@ class GlmSession:
         _lib.call("fl_glm_reduce_buffer", self.ptr, C.byref(buf), C.byref(n))
         return buf.value, n.value
 
+    def kernel_times(self, iters: int, stream=None) -> list[float]:
+        """Mean ms of [dim q, fact pass, dim t + update] over `iters` iterations
+        (CUDA events between the kernels, recorded by the library)."""
+        out = (C.c_float * 3)()
+        _lib.call("fl_glm_kernel_times", self.ptr, int(iters), out,
+                  stream if stream is not None else C.c_void_p(0))
+        return [float(v) for v in out]
+
     def result(self, n: int):
         w = np.empty(self.c_T, dtype=np.float64)
         loss = np.empty(max(n, 1), dtype=np.float64)
