@@ -19,6 +19,7 @@
 // Algorithmic HBM bytes per iteration:
 //   4 r_T pf + 4 r_T n_gather + b_y r_T + sum_d 2 * 4 r_d pitch_d (+ 4 r_T if resid)
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -445,6 +446,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_glm_fact(GlmFactArgs a) {
   if (tid == 0) a.state->done_fact = 0;
 }
 
+#include "glm_fact_warp.cuh"
+
 // ---------------------------------------------------------------------------
 // update: w <- w - lr * red; loss_hist[it] = red[c_T]; refresh fp32 copies
 // ---------------------------------------------------------------------------
@@ -592,6 +595,34 @@ __global__ void k_glm_update(UpdateArgs u) { glm_apply_update(u); }
 
 }  // namespace flb
 
+namespace flb {
+template <int MODEL, int C4>
+static void launch_fw(const GlmFactWArgs& a, int grid, size_t smem, cudaStream_t st) {
+  constexpr int RPL = C4 <= 7 ? 2 : 1;
+  k_glm_fact_w<MODEL, C4, RPL><<<grid, FW_WARPS * 32, smem, st>>>(a);
+}
+template <int MODEL, int C4>
+static const void* fw_ptr() {
+  constexpr int RPL = C4 <= 7 ? 2 : 1;
+  return (const void*)k_glm_fact_w<MODEL, C4, RPL>;
+}
+#define FW_CASES(M, X) \
+  X(M, 1) X(M, 3) X(M, 5) X(M, 7) X(M, 9) X(M, 11) X(M, 13) X(M, 15) X(M, 17) X(M, 19)
+static bool fw_supported(int c4) { return c4 >= 1 && c4 <= 19 && (c4 & 1); }
+static const void* fw_kernel(int model, int c4) {
+#define FW_PTR(M, C) if (c4 == C) return fw_ptr<M, C>();
+  if (model == 0) { FW_CASES(0, FW_PTR) } else { FW_CASES(1, FW_PTR) }
+#undef FW_PTR
+  return nullptr;
+}
+static void fw_launch(int model, int c4, const GlmFactWArgs& a, int grid, size_t smem,
+                      cudaStream_t st) {
+#define FW_LAUNCH(M, C) if (c4 == C) { launch_fw<M, C>(a, grid, smem, st); return; }
+  if (model == 0) { FW_CASES(0, FW_LAUNCH) } else { FW_CASES(1, FW_LAUNCH) }
+#undef FW_LAUNCH
+}
+}  // namespace flb
+
 using namespace flb;
 
 struct fl_glm {
@@ -607,6 +638,7 @@ struct fl_glm {
   size_t smem_dim = 0;
   int dim_grid_x = 0;
   DevBuf y, wF, wd, w64, q, bins, resid, part_fact, part_dim, carry, red, loss_hist, state;
+  DevBuf fw_carry, fw_part;
   GlmFactArgs fa{};
   DimArgs da{};
   UpdateArgs ua{};
@@ -614,6 +646,10 @@ struct fl_glm {
   cudaGraphExec_t graph = nullptr;
   cudaStream_t cap_stream = nullptr;
   int bins_rows = 0;
+  bool use_fw = false;
+  GlmFactWArgs fw{};
+  int nblk_fw = 0;
+  size_t smem_fw = 0;
 };
 
 namespace flb {
@@ -626,7 +662,9 @@ static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
     k_glm_dim_q<<<grid, NTHREADS, s->smem_dim, st>>>(s->da);
     FL_CHECK_LAUNCH();
   }
-  if (s->model == FL_MODEL_LINREG)
+  if (s->use_fw)
+    fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st);
+  else if (s->model == FL_MODEL_LINREG)
     k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
   else
     k_glm_fact<1><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
@@ -758,6 +796,49 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
   fa.off_y = s->off_y;
   fa.nst = s->nst_fact;
 
+  // per-warp-pipeline fact pass (preferred when the stream width is templated)
+  if (fw_supported(c4) && !getenv("FL_GLM_CTA_TILES")) {
+    const int rpl = c4 <= 7 ? 2 : 1;
+    const int rw = 32 * rpl;
+    GlmFactWArgs& fw = s->fw;
+    fw.F = fa.F;
+    fw.pf = t->pf;
+    fw.y = fa.y;
+    fw.r_T = t->r_T;
+    fw.nunits = r_pad / rw;
+    fw.ng = fa.ng;
+    fw.sort_g = fa.sort_g;
+    for (int d = 0; d < ng; d++) {
+      fw.fk[d] = fa.fk[d];
+      fw.q[d] = fa.q[d];
+    }
+    fw.bins = fa.bins;
+    fw.resid = fa.resid;
+    fw.wF = fa.wF;
+    fw.state = fa.state;
+    fw.off_y = (uint32_t)round_up((int64_t)rw * t->pf * 4, 16);
+    fw.off_fk = fw.off_y + (uint32_t)round_up((int64_t)rw * yb, 16);
+    fw.stage_bytes = (uint32_t)round_up(fw.off_fk + (t->sort_g >= 0 ? rw * 4 : 0), 128);
+    int nst = (int)((200 * 1024) / ((size_t)FW_WARPS * fw.stage_bytes));
+    fw.nst = std::max(2, std::min(4, nst));
+    s->smem_fw = (size_t)FW_WARPS * fw.nst * fw.stage_bytes;
+    if (s->smem_fw <= 220 * 1024) {
+      const void* kfw = fw_kernel(model, c4);
+      FL_CUDA(cudaFuncSetAttribute(kfw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)s->smem_fw));
+      int occw = 1;
+      FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occw, kfw, FW_WARPS * 32, s->smem_fw));
+      occw = std::max(1, occw);
+      int64_t want = ceil_div(fw.nunits, FW_WARPS);
+      s->nblk_fw = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)t->sm_count * occw));
+      if ((rc = s->fw_carry.alloc((size_t)s->nblk_fw * FW_WARPS * sizeof(WarpCarry)))) return rc;
+      if ((rc = s->fw_part.alloc((size_t)s->nblk_fw * (t->pf + 1) * 8))) return rc;
+      fw.carry = s->fw_carry.as<WarpCarry>();
+      fw.part = s->fw_part.as<double>();
+      s->use_fw = true;
+    }
+  }
+
   // dim geometry
   DimArgs& da = s->da;
   da.ng = ng;
@@ -821,8 +902,8 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
   ua.loss_hist = s->loss_hist.as<double>();
   ua.loss_cap = s->loss_cap;
   ua.state = s->state.as<GlmState>();
-  ua.part_fact = s->part_fact.as<double>();
-  ua.nblk_fact = s->nblk_fact;
+  ua.part_fact = s->use_fw ? s->fw_part.as<double>() : s->part_fact.as<double>();
+  ua.nblk_fact = s->use_fw ? s->nblk_fw : s->nblk_fact;
   for (int d = 0; d < ng; d++) {
     ua.d_tcol[d] = t->g[d].d_tcol->as<int32_t>();
     ua.pitch[d] = t->g[d].pitch;
@@ -894,7 +975,9 @@ int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[1], st));
-    if (s->model == FL_MODEL_LINREG)
+    if (s->use_fw)
+      fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st);
+    else if (s->model == FL_MODEL_LINREG)
       k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
     else
       k_glm_fact<1><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);

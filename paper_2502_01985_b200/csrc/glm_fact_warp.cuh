@@ -1,0 +1,299 @@
+// K2 v2: the fact-row pass with one independent TMA pipeline PER WARP.
+//
+// Why: the CTA-tile version (k_glm_fact) was latency-bound (ncu r01: 25%
+// occupancy, two __syncthreads per 256-row tile, ~490 warp instructions per
+// 32 rows, DRAM at 38% of peak although traffic == algorithmic bytes).
+// Here each warp owns a contiguous range of device rows and streams it through
+// its own NST-stage ring of TMA bulk copies (lane 0 issues, all lanes wait on
+// the stage mbarrier) -- no block-level synchronisation in the main loop, so
+// warps drift and hide each other's latency.  A row lives in registers
+// (C4 float4, compile-time), each lane owns RPL rows per stage (ILP), and the
+// I_sort^T segmented sum is a warp scan with a register-carried running
+// segment; segments that cross warp ranges are stitched in a fixed order by
+// the last CTA (deterministic).
+#pragma once
+// (included inside namespace flb by glm.cu)
+
+constexpr int FW_WARPS = 8;        // warps per CTA
+constexpr int FW_FLUSH = 16;       // stages between fp32 -> fp64 flushes
+
+struct WarpCarry {
+  int head_key, tail_key, through, pad;
+  double head_val, tail_val;
+};
+
+struct GlmFactWArgs {
+  const float* F;
+  int pf;
+  const void* y;
+  int64_t r_T, nunits;       // nunits = r_pad / RW
+  int ng, sort_g;
+  const int32_t* fk[MAX_GATHER];
+  const float* q[MAX_GATHER];
+  float* bins;
+  float* resid;
+  const float* wF;
+  double* part;              // gridDim.x x (pf + 1)
+  WarpCarry* carry;          // gridDim.x * FW_WARPS
+  GlmState* state;
+  uint32_t stage_bytes, off_y, off_fk;
+  int nst;
+};
+
+template <int MODEL, int C4, int RPL>
+__global__ void __launch_bounds__(FW_WARPS * 32, 1) k_glm_fact_w(GlmFactWArgs a) {
+  constexpr int RW = 32 * RPL;               // rows per warp stage
+  constexpr bool W_REG = C4 <= 9;            // w in registers (else smem broadcast)
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t bar[FW_WARPS][4];
+  __shared__ double gsum[FW_WARPS][C4 * 4];
+  __shared__ double lsum[FW_WARPS];
+  __shared__ float4 w_s[C4];
+  __shared__ int is_last;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * FW_WARPS + warp;
+  const int64_t NW = (int64_t)gridDim.x * FW_WARPS;
+  const int64_t base = a.nunits / NW, rem = a.nunits % NW;
+  const int64_t u0 = gw * base + min64(gw, rem);
+  const int64_t cnt = base + (gw < rem ? 1 : 0);
+  const int64_t W0 = u0 * RW;
+  const int64_t W1 = min64((u0 + cnt) * RW, a.r_T);
+  const bool has_sort = a.sort_g >= 0;
+  const int32_t* fks = has_sort ? a.fk[a.sort_g] : nullptr;
+  constexpr uint32_t F_BYTES = RW * C4 * 16;
+  constexpr uint32_t Y_BYTES = MODEL == 1 ? RW : RW * 4;
+  const uint32_t tx = F_BYTES + Y_BYTES + (has_sort ? RW * 4 : 0);
+  char* wsm = smem + (size_t)warp * a.nst * a.stage_bytes;
+  uint64_t* wbar = bar[warp];
+
+  for (int j = threadIdx.x; j < C4; j += blockDim.x)
+    w_s[j] = reinterpret_cast<const float4*>(a.wF)[j];
+  for (int j = lane; j < C4 * 4; j += 32) gsum[warp][j] = 0.0;
+  if (lane == 0) {
+    lsum[warp] = 0.0;
+    for (int s = 0; s < a.nst; s++) mbar_init(&wbar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  float4 w[W_REG ? C4 : 1];
+  if (W_REG) {
+#pragma unroll
+    for (int j = 0; j < C4; j++) w[j] = w_s[j];
+  }
+
+  auto issue = [&](int s, int64_t unit) {
+    char* st = wsm + (size_t)s * a.stage_bytes;
+    mbar_arrive_expect_tx(&wbar[s], tx);
+    bulk_g2s(st, a.F + unit * RW * (int64_t)a.pf, F_BYTES, &wbar[s]);
+    bulk_g2s(st + a.off_y, reinterpret_cast<const char*>(a.y) + unit * (int64_t)Y_BYTES, Y_BYTES,
+             &wbar[s]);
+    if (has_sort) bulk_g2s(st + a.off_fk, fks + unit * RW, RW * 4, &wbar[s]);
+  };
+  if (lane == 0)
+    for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
+
+  // the warp's first segment may have begun before W0
+  int head_key = -1;
+  if (has_sort && cnt > 0 && W0 > 0 && W0 < a.r_T) {
+    int k0 = fks[W0];
+    if (k0 >= 0 && fks[W0 - 1] == k0) head_key = k0;
+  }
+  bool head_open = head_key >= 0;
+  float head_val = 0.f;
+  int ck = -1;          // running segment key (warp uniform)
+  float cv = 0.f;       // running segment partial
+
+  float4 acc[C4];
+#pragma unroll
+  for (int j = 0; j < C4; j++) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float lacc = 0.f;
+
+  auto flush = [&]() {
+#pragma unroll
+    for (int j = 0; j < C4; j++) {
+      float v4[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        float v = v4[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) gsum[warp][j * 4 + c] += (double)v;
+      }
+      acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float v = lacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) lsum[warp] += (double)v;
+    lacc = 0.f;
+  };
+
+  for (int64_t i = 0; i < cnt; i++) {
+    const int s = (int)(i % a.nst);
+    mbar_wait(&wbar[s], (uint32_t)((i / a.nst) & 1));
+    const char* st = wsm + (size_t)s * a.stage_bytes;
+    const float4* Ft = reinterpret_cast<const float4*>(st);
+    const int64_t unit_row0 = (u0 + i) * RW;
+#pragma unroll
+    for (int h = 0; h < RPL; h++) {
+      const int lr = h * 32 + lane;
+      const int64_t p = unit_row0 + lr;
+      const bool valid = p < a.r_T;
+      int key = has_sort ? reinterpret_cast<const int32_t*>(st + a.off_fk)[lr] : -1;
+      // issue the gathers first so their latency overlaps the dot product
+      float gq = 0.f;
+      for (int d = 0; d < a.ng; d++) {
+        int32_t fk = (d == a.sort_g) ? key : a.fk[d][p];
+        if (fk >= 0) gq += __ldg(a.q[d] + fk);
+      }
+      float4 x[C4];
+#pragma unroll
+      for (int j = 0; j < C4; j++) x[j] = Ft[lr * C4 + j];
+      float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < C4; j++) {
+        float4 wj = W_REG ? w[j] : w_s[j];
+        z0 = fmaf(x[j].x, wj.x, z0);
+        z1 = fmaf(x[j].y, wj.y, z1);
+        z0 = fmaf(x[j].z, wj.z, z0);
+        z1 = fmaf(x[j].w, wj.w, z1);
+      }
+      float z = z0 + z1 + gq;
+      float r, l;
+      if (MODEL == 0) {
+        float yv = reinterpret_cast<const float*>(st + a.off_y)[lr];
+        r = z - yv;
+        l = 0.5f * r * r;
+      } else {
+        float yv = (float)reinterpret_cast<const uint8_t*>(st + a.off_y)[lr];
+        float e = __expf(-fabsf(z));                 // in (0, 1]
+        float sp = log1pf(e);                        // softplus(-|z|)
+        float pr = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+        r = pr - yv;
+        // -log(p) = softplus(-z), -log(1-p) = softplus(z); clip at 1e-12
+        float lp = z >= 0.f ? sp : sp - z;           // softplus(-z)
+        float lq = z >= 0.f ? sp + z : sp;           // softplus(z)
+        l = yv != 0.f ? fminf(lp, kLogClip) : fminf(lq, kLogClip);
+      }
+      if (!valid) {
+        r = 0.f;
+        l = 0.f;
+        key = -1;
+      }
+      lacc += l;
+#pragma unroll
+      for (int j = 0; j < C4; j++) {
+        acc[j].x = fmaf(r, x[j].x, acc[j].x);
+        acc[j].y = fmaf(r, x[j].y, acc[j].y);
+        acc[j].z = fmaf(r, x[j].z, acc[j].z);
+        acc[j].w = fmaf(r, x[j].w, acc[j].w);
+      }
+      if (a.resid) a.resid[p] = r;
+      if (has_sort) {
+        // segmented inclusive scan over the 32 rows of this sub-tile
+        float v = r;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          float vu = __shfl_up_sync(0xffffffffu, v, off);
+          int ku = __shfl_up_sync(0xffffffffu, key, off);
+          if (lane >= off && ku == key) v += vu;
+        }
+        // rows continuing the running segment (keys are non-decreasing)
+        if (key >= 0 && key == ck) v += cv;
+        const int k0 = __shfl_sync(0xffffffffu, key, 0);
+        if (ck >= 0 && k0 != ck) {              // running segment is complete
+          if (head_open && ck == head_key) {
+            head_val = cv;
+            head_open = false;
+          } else if (lane == 0) {
+            a.bins[ck] = cv;
+          }
+        }
+        const int kn = __shfl_down_sync(0xffffffffu, key, 1);
+        const bool end = lane < 31 && key >= 0 && kn != key;
+        const bool eh = end && head_open && key == head_key;
+        const unsigned bm = __ballot_sync(0xffffffffu, eh);
+        if (bm) {
+          head_val = __shfl_sync(0xffffffffu, v, __ffs(bm) - 1);
+          head_open = false;
+        }
+        if (end && !eh) a.bins[key] = v;
+        ck = __shfl_sync(0xffffffffu, key, 31);
+        cv = __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && i + a.nst < cnt) {
+      fence_proxy_async();
+      issue(s, u0 + i + a.nst);
+    }
+    if ((i % FW_FLUSH) == FW_FLUSH - 1) flush();
+  }
+  flush();
+
+  // warp range end: running segment -> carry record
+  if (has_sort) {
+    WarpCarry c;
+    c.head_key = -1;
+    c.tail_key = -1;
+    c.through = 0;
+    c.pad = 0;
+    c.head_val = 0.0;
+    c.tail_val = 0.0;
+    if (cnt > 0) {
+      if (ck >= 0) {
+        const bool cont = W1 < a.r_T && fks[W1] == ck;
+        if (head_open && ck == head_key) {
+          head_val = cv;
+          head_open = false;
+          c.head_key = ck;
+          c.through = cont ? 1 : 0;
+        } else if (cont) {
+          c.tail_key = ck;
+          c.tail_val = (double)cv;
+        } else if (lane == 0) {
+          a.bins[ck] = cv;
+        }
+      }
+      if (!head_open && head_key >= 0) {
+        c.head_key = head_key;
+        c.head_val = (double)head_val;
+      }
+    }
+    if (lane == 0) a.carry[gw] = c;
+  }
+  __syncthreads();
+  // CTA partials in fixed warp order
+  double* out = a.part + (int64_t)blockIdx.x * (C4 * 4 + 1);
+  for (int t = threadIdx.x; t <= C4 * 4; t += blockDim.x) {
+    double sum = 0.0;
+    if (t < C4 * 4)
+      for (int w2 = 0; w2 < FW_WARPS; w2++) sum += gsum[w2][t];
+    else
+      for (int w2 = 0; w2 < FW_WARPS; w2++) sum += lsum[w2];
+    out[t] = sum;
+  }
+  // last CTA stitches the segments that span warp ranges (fixed order)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(&a.state->done_fact, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (has_sort) {
+    volatile WarpCarry* cr = a.carry;
+    for (int64_t c = threadIdx.x; c < NW; c += blockDim.x) {
+      int K = cr[c].tail_key;
+      if (K < 0) continue;
+      double total = cr[c].tail_val;
+      for (int64_t c2 = c + 1; c2 < NW; c2++) {
+        if (cr[c2].head_key != K) break;
+        total += cr[c2].head_val;
+        if (!cr[c2].through) break;
+      }
+      a.bins[K] = (float)total;
+    }
+  }
+  if (threadIdx.x == 0) a.state->done_fact = 0;
+}
