@@ -819,7 +819,9 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     fw.off_y = (uint32_t)round_up((int64_t)rw * t->pf * 4, 16);
     fw.off_fk = fw.off_y + (uint32_t)round_up((int64_t)rw * yb, 16);
     fw.stage_bytes = (uint32_t)round_up(fw.off_fk + (t->sort_g >= 0 ? rw * 4 : 0), 128);
-    int nst = (int)((200 * 1024) / ((size_t)FW_WARPS * fw.stage_bytes));
+    const size_t budget = fw_min_blocks(c4) == 2 ? 100 * 1024 : 200 * 1024;
+    int nst = (int)(budget / ((size_t)FW_WARPS * fw.stage_bytes));
+    if (const char* e = getenv("FL_GLM_NST")) nst = atoi(e);
     fw.nst = std::max(2, std::min(4, nst));
     s->smem_fw = (size_t)FW_WARPS * fw.nst * fw.stage_bytes;
     if (s->smem_fw <= 220 * 1024) {

@@ -22,6 +22,7 @@
 //    copy moves whole, 16-byte aligned tiles.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -132,6 +133,11 @@ struct fl_table {
 };
 
 namespace flb {
+// tma.cu: 2-D fp32 TMA tensor map over a row-major [rows x cols] array with
+// `row_bytes` pitch; box = box_rows x box_cols (columns past `cols` are
+// zero-filled by the TMA unit).  swizzle_bytes in {0, 32, 64, 128}.
+int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                 uint64_t row_bytes, uint32_t box_rows, uint32_t box_cols, int swizzle_bytes);
 // table.cu
 int table_upload_tcols(fl_table* t);
 // ops.cu helpers used by trainers
@@ -239,6 +245,45 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// TMA 2-D tile load (tensor map in param / const space), coordinates
+// {column, row}; out-of-range elements are zero-filled.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int col, int row,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA 2-D tile store shared -> global (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int col, int row,
+                                             const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::
+                   "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups still READ their shared source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// 4 fp32 8x4 matrices -> the m16n8k8 tf32 A fragment (rows 0-7 / 8-15,
+// cols 0-3 / 4-7); lane l supplies the address of row (l & 15) at column
+// offset (l >> 4) * 4.  Rows must be 16-byte aligned.
+__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                        const void* row_ptr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_u32(row_ptr)));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -1,0 +1,911 @@
+// Fused Lloyd K-means over a factorized table (reference trainers.py:198-246,
+// built on ops.py:219-271).
+//
+// The reference computes D = rowSum(T^2) 1^T - 2 T C^T + 1 ||c||^2^T with a
+// full lmm, takes a row argmin (ties -> lowest index) and re-estimates
+// C <- (A^T T) / (A^T 1) with a transpose_lmm of the one-hot matrix A.  Here
+// one iteration is three kernels (plus the all-reduce of `red` between K3 and
+// the update when fact rows are sharded across GPUs):
+//
+//  K1 k_km_dim_e   E_d[r, j] = ||S_d[r,:] - C_j[cols of d]||^2 for every
+//                  dimension row (row r_d = the all-zero "no match" row),
+//                  direct differences in fp32; zero the I_d^T A counters.
+//  K2 k_km_fact    one pass over the fact rows (per-warp TMA pipelines):
+//                    z    = F[p,:] C_F^T          (3xTF32 mma.sync)
+//                    dist = ||c_F||^2 - 2 z + sum_d E_d[fk_d[p], :]
+//                    a    = argmin_j dist (ties -> lowest j)
+//                    loss += ||F[p,:] - C_F[a]||^2 + sum_d E_d[fk_d[p], a]
+//                    sums_F[a,:] += F[p,:], count[a] += 1   (3xTF32 mma:
+//                                    one-hot^T x [F | 1])
+//                    cnt_d[fk_d[p], a] += 1      (I_d^T A: integer atomics,
+//                                    warp-aggregated -- exact, order-free)
+//  K3 k_km_dim_sums  sums_d = cnt_d^T S_d (fp64 per-CTA partials), then the
+//                  last CTA reduces every partial in a fixed order into `red`
+//                  and (single GPU) applies C <- sums / counts (empty clusters
+//                  keep their centroid).
+//
+// Why the row term ||F||^2 never appears: it is constant per row (argmin) and
+// the loss is taken from direct differences, which avoids the fp32
+// cancellation of the expanded form on tight clusters.
+#include <algorithm>
+#include <cstdlib>
+
+#include "internal.h"
+#include "mma_tf32.cuh"
+
+namespace flb {
+
+constexpr int KM_WARPS = 8;
+constexpr int KM_FLUSH = 16;   // stages between fp32 -> fp64 flushes (<= 512 rows)
+#define kInf __int_as_float(0x7f800000)
+
+struct KmState {
+  int it;
+  int done_dim;
+  int pad[2];
+};
+
+struct KmFactArgs {
+  const float* F;
+  int pf, c_T, k;
+  int64_t r_T, nunits;           // units of 32 device rows
+  int ng, sort_g;
+  const int32_t* fk[MAX_GATHER];
+  const float* E[MAX_GATHER];    // (r_d + 1) x KP
+  int32_t* cnt[MAX_GATHER];      // r_d x KP
+  int64_t rows[MAX_GATHER];
+  const float* C32;              // k x c_T
+  const int32_t* f_tcol;         // pf
+  int32_t* assign;               // r_pad device order, or null
+  double* part;                  // gridDim.x x (KP * SC + 1)
+  uint32_t stage_bytes;          // 32 x FP fp32 TMA tile | 32 int32 sort-source FK
+  int nst;
+};
+
+struct KmDimArgs {
+  int ng, k, KP, c_T;
+  const float* S[MAX_GATHER];
+  int pitch[MAX_GATHER];
+  int cols[MAX_GATHER];
+  int64_t rows[MAX_GATHER];
+  int nblk[MAX_GATHER];
+  const int32_t* tcol[MAX_GATHER];
+  float* E[MAX_GATHER];
+  int32_t* cnt[MAX_GATHER];
+  double* part[MAX_GATHER];      // nblk x (KP * cols)
+  const float* C32;
+};
+
+struct KmUpdateArgs {
+  int c_T, k, KP, SC, pf, ng;
+  const int32_t* f_tcol;
+  const int32_t* d_tcol[MAX_GATHER];
+  int d_cols[MAX_GATHER];
+  const double* part_fact;
+  int nblk_fact;
+  const double* part_dim[MAX_GATHER];
+  int nblk_dim[MAX_GATHER];
+  double* red;                   // k*c_T sums | k counts | loss
+  double* C64;
+  float* C32;
+  double* loss_hist;
+  int loss_cap;
+  KmState* state;
+};
+
+// ---------------------------------------------------------------------------
+// K1: E_d and counter reset
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_km_dim_e(KmDimArgs a) {
+  const int d = blockIdx.y;
+  if (d >= a.ng) return;
+  const int KP = a.KP;
+  const int64_t rows = a.rows[d];
+  const int cols = a.cols[d], pitch = a.pitch[d];
+  extern __shared__ float cs[];  // KP x cols centroid slice
+  for (int i = threadIdx.x; i < KP * cols; i += blockDim.x) {
+    int j = i / cols, c = i - j * cols;
+    cs[i] = j < a.k ? a.C32[(int64_t)j * a.c_T + a.tcol[d][c]] : 0.f;
+  }
+  __syncthreads();
+  const int64_t total = (rows + 1) * KP;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / KP;
+    const int j = (int)(idx - r * KP);
+    float e = 0.f;
+    if (j < a.k) {
+      const float* srow = a.S[d] + r * pitch;
+      const float* crow = cs + j * cols;
+      if (r < rows) {
+        for (int c = 0; c < cols; c++) {
+          float df = srow[c] - crow[c];
+          e = fmaf(df, df, e);
+        }
+      } else {
+        for (int c = 0; c < cols; c++) e = fmaf(crow[c], crow[c], e);
+      }
+    }
+    a.E[d][idx] = e;
+    if (r < rows) a.cnt[d][idx] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: the fact-row pass
+// ---------------------------------------------------------------------------
+template <int NT, int KC>
+__global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
+    k_km_fact(const __grid_constant__ CUtensorMap tmF, KmFactArgs a) {
+  constexpr int KP = NT * 8;          // padded cluster count
+  constexpr int MT = (NT + 1) / 2;    // 16-cluster tiles of the one-hot operand
+  constexpr int SC = KC * 8;          // MMA columns of F (count column = pf < SC)
+  constexpr int FP = SC + 4;          // smem F row pitch (TMA box width, zero-filled)
+  constexpr int CFP = SC + 4;         // fp32 centroid row pitch in smem
+  constexpr int ZP = KP + 4;          // per-warp distance transpose pitch
+  extern __shared__ __align__(128) char smem[];
+  __shared__ uint64_t bar[KM_WARPS][4];
+  __shared__ double lsum[KM_WARPS];
+
+  uint2* bfrag = reinterpret_cast<uint2*>(smem);                       // KC*NT*32
+  float* cf = reinterpret_cast<float*>(bfrag + KC * NT * 32);          // KP x CFP
+  float* cn = cf + KP * CFP;                                           // KP (+4)
+  double* acc64 = reinterpret_cast<double*>(cn + KP + 4);              // warps x MT*16*SC
+  float* zs_all = reinterpret_cast<float*>(acc64 + KM_WARPS * MT * 16 * SC);  // warps x 32*ZP
+  char* stages = smem + round_up((int64_t)(reinterpret_cast<char*>(zs_all + KM_WARPS * 32 * ZP) -
+                                           smem), 128);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int pf = a.pf, k = a.k;
+
+  // centroid fact slice (zero past pf and past k), tf32 B fragments, norms
+  for (int i = threadIdx.x; i < KP * CFP; i += blockDim.x) {
+    int j = i / CFP, c = i - j * CFP;
+    float v = 0.f;
+    if (j < k && c < pf) {
+      int tc = a.f_tcol[c];
+      if (tc >= 0) v = a.C32[(int64_t)j * a.c_T + tc];
+    }
+    cf[i] = v;
+  }
+  double* wacc = acc64 + warp * (MT * 16 * SC);
+  for (int i = lane; i < MT * 16 * SC; i += 32) wacc[i] = 0.0;
+  if (lane == 0) {
+    lsum[warp] = 0.0;
+    for (int s = 0; s < a.nst; s++) mbar_init(&bar[warp][s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < KC * NT * 32; i += blockDim.x) {
+    int l = i & 31, kn = i >> 5;
+    int kc = kn / NT, n = kn - kc * NT;
+    int gg = l >> 2, tt = l & 3;
+    bfrag[i] = make_uint2(tf32_bits(cf[(n * 8 + gg) * CFP + kc * 8 + tt]),
+                          tf32_bits(cf[(n * 8 + gg) * CFP + kc * 8 + tt + 4]));
+  }
+  for (int j = threadIdx.x; j < KP; j += blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < SC; c++) s = fmaf(cf[j * CFP + c], cf[j * CFP + c], s);
+    cn[j] = j < k ? s : kInf;
+  }
+  __syncthreads();
+  float cn_max = 0.f;
+  for (int j = 0; j < k; j++) cn_max = fmaxf(cn_max, cn[j]);
+
+  // this warp's contiguous range of 32-row units
+  const int64_t gw = (int64_t)blockIdx.x * KM_WARPS + warp;
+  const int64_t NW = (int64_t)gridDim.x * KM_WARPS;
+  const int64_t base = a.nunits / NW, rem = a.nunits % NW;
+  const int64_t u0 = gw * base + min64(gw, rem);
+  const int64_t cnt = base + (gw < rem ? 1 : 0);
+  const bool has_sort = a.sort_g >= 0;
+  constexpr uint32_t F_BYTES = 32u * FP * 4u;
+  const uint32_t tx = F_BYTES + (has_sort ? 128u : 0u);
+  char* wsm = stages + (size_t)warp * a.nst * a.stage_bytes;
+  float* zs = zs_all + warp * 32 * ZP;
+  uint64_t* wbar = bar[warp];
+  auto issue = [&](int s, int64_t unit) {
+    char* st = wsm + (size_t)s * a.stage_bytes;
+    mbar_arrive_expect_tx(&wbar[s], tx);
+    tma_load_2d(st, &tmF, 0, (int)(unit * 32), &wbar[s]);
+    if (has_sort) bulk_g2s(st + F_BYTES, a.fk[a.sort_g] + unit * 32, 128, &wbar[s]);
+  };
+  if (lane == 0)
+    for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
+
+  float sacc[MT][KC][4];
+#pragma unroll
+  for (int m = 0; m < MT; m++)
+#pragma unroll
+    for (int c = 0; c < KC; c++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) sacc[m][c][e] = 0.f;
+  float lacc = 0.f;
+
+  auto flush = [&]() {
+#pragma unroll
+    for (int m = 0; m < MT; m++)
+#pragma unroll
+      for (int c = 0; c < KC; c++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          int row = m * 16 + g + (e >> 1) * 8, col = c * 8 + 2 * t + (e & 1);
+          wacc[row * SC + col] += (double)sacc[m][c][e];
+          sacc[m][c][e] = 0.f;
+        }
+    float v = lacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) lsum[warp] += (double)v;
+    lacc = 0.f;
+  };
+
+  for (int64_t i = 0; i < cnt; i++) {
+    const int s = (int)(i % a.nst);
+    mbar_wait(&wbar[s], (uint32_t)((i / a.nst) & 1));
+    float* Fs = reinterpret_cast<float*>(wsm + (size_t)s * a.stage_bytes);
+    const int32_t* fks_s = reinterpret_cast<const int32_t*>(wsm + (size_t)s * a.stage_bytes + F_BYTES);
+    const int64_t p0 = (u0 + i) * 32;
+    const bool valid = p0 + lane < a.r_T;
+
+    // ---- screen: z = F C_F^T on the tensor cores (1xTF32, operands straight
+    // from the TMA tile via ldmatrix)
+    float z[2][NT][4];
+#pragma unroll
+    for (int m = 0; m < 2; m++)
+#pragma unroll
+      for (int n = 0; n < NT; n++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) z[m][n][e] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < KC; kc++) {
+      uint2 bf[NT];
+#pragma unroll
+      for (int n = 0; n < NT; n++) bf[n] = bfrag[(kc * NT + n) * 32 + lane];
+#pragma unroll
+      for (int m = 0; m < 2; m++) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(a0, a1, a2, a3, Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
+#pragma unroll
+        for (int n = 0; n < NT; n++) mma_tf32(z[m][n], a0, a1, a2, a3, bf[n].x, bf[n].y);
+      }
+    }
+    // transpose to lane-per-row through the warp's smem scratch
+#pragma unroll
+    for (int m = 0; m < 2; m++)
+#pragma unroll
+      for (int n = 0; n < NT; n++) {
+        *reinterpret_cast<float2*>(zs + (m * 16 + g) * ZP + n * 8 + 2 * t) =
+            make_float2(z[m][n][0], z[m][n][1]);
+        *reinterpret_cast<float2*>(zs + (m * 16 + g + 8) * ZP + n * 8 + 2 * t) =
+            make_float2(z[m][n][2], z[m][n][3]);
+      }
+    // count column of [F | 1] (read by the sums MMA below)
+    Fs[lane * FP + pf] = 1.f;
+    __syncwarp();
+    float dv[KP];
+#pragma unroll
+    for (int q = 0; q < KP / 4; q++) {
+      float4 zz = *reinterpret_cast<const float4*>(zs + lane * ZP + q * 4);
+      dv[q * 4 + 0] = fmaf(-2.f, zz.x, cn[q * 4 + 0]);
+      dv[q * 4 + 1] = fmaf(-2.f, zz.y, cn[q * 4 + 1]);
+      dv[q * 4 + 2] = fmaf(-2.f, zz.z, cn[q * 4 + 2]);
+      dv[q * 4 + 3] = fmaf(-2.f, zz.w, cn[q * 4 + 3]);
+    }
+    int fkl[MAX_GATHER];
+#pragma unroll
+    for (int d = 0; d < MAX_GATHER; d++) {
+      if (d >= a.ng) break;
+      const int f = (d == a.sort_g) ? fks_s[lane] : a.fk[d][p0 + lane];
+      fkl[d] = f;
+      const float4* er = reinterpret_cast<const float4*>(a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP);
+#pragma unroll
+      for (int q = 0; q < KP / 4; q++) {
+        float4 ev = er[q];
+        dv[q * 4 + 0] += ev.x;
+        dv[q * 4 + 1] += ev.y;
+        dv[q * 4 + 2] += ev.z;
+        dv[q * 4 + 3] += ev.w;
+      }
+    }
+    // best / runner-up (ties -> lowest index)
+    float v1 = dv[0];
+    int al = 0;
+#pragma unroll
+    for (int j = 1; j < KP; j++)
+      if (dv[j] < v1) {
+        v1 = dv[j];
+        al = j;
+      }
+    float v2 = kInf;
+#pragma unroll
+    for (int j = 0; j < KP; j++)
+      if (j != al) v2 = fminf(v2, dv[j]);
+    const float4* fr = reinterpret_cast<const float4*>(Fs + lane * FP);
+    // ---- certify: keep the screened winner unless the runner-up lies within
+    // the screen's error bound; near-ties are re-decided from direct fp32
+    // differences (the reference orders them in fp64)
+    if (valid) {
+      float xn = 0.f;
+      for (int c4 = 0; c4 < pf / 4; c4++) {
+        float4 x = fr[c4];
+        xn = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, xn))));
+      }
+      const float tol = 3.2e-3f * (xn + cn_max) + 2e-5f * (fabsf(v1) + fabsf(v2));
+      if (!(v2 - v1 > tol)) {
+        uint32_t cand = 0;   // clusters that can still win
+#pragma unroll
+        for (int j = 0; j < KP; j++)
+          if (dv[j] - v1 <= tol) cand |= 1u << j;
+        float bd = kInf;
+        int bj = 0;
+        while (cand) {
+          const int j = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const float4* cr = reinterpret_cast<const float4*>(cf + j * CFP);
+          float dj = 0.f;
+          for (int c4 = 0; c4 < pf / 4; c4++) {
+            float4 x = fr[c4], c = cr[c4];
+            float d0 = x.x - c.x, d1 = x.y - c.y, d2 = x.z - c.z, d3 = x.w - c.w;
+            dj = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, dj))));
+          }
+#pragma unroll
+          for (int d = 0; d < MAX_GATHER; d++) {
+            if (d >= a.ng) break;
+            dj += a.E[d][(fkl[d] >= 0 ? (int64_t)fkl[d] : a.rows[d]) * KP + j];
+          }
+          if (dj < bd) {
+            bd = dj;
+            bj = j;
+          }
+        }
+        al = bj;
+      }
+    } else {
+      al = -1;
+    }
+    // ---- loss (direct differences), I_d^T A counters, assignments
+    if (valid) {
+      const float4* cr = reinterpret_cast<const float4*>(cf + al * CFP);
+      float l = 0.f;
+      for (int c4 = 0; c4 < pf / 4; c4++) {
+        float4 x = fr[c4], c = cr[c4];
+        float d0 = x.x - c.x, d1 = x.y - c.y, d2 = x.z - c.z, d3 = x.w - c.w;
+        l = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, l))));
+      }
+      lacc += l;
+    }
+#pragma unroll
+    for (int d = 0; d < MAX_GATHER; d++) {
+      if (d >= a.ng) break;
+      const int f = fkl[d];
+      if (valid) lacc += a.E[d][(f >= 0 ? (int64_t)f : a.rows[d]) * KP + al];
+      const int key = (valid && f >= 0) ? f * KP + al : -1 - lane;
+      const unsigned mask = __match_any_sync(0xffffffffu, key);
+      if (key >= 0 && (__ffs(mask) - 1) == lane) atomicAdd(&a.cnt[d][key], __popc(mask));
+    }
+    if (a.assign && valid) a.assign[p0 + lane] = al;
+    // ---- sums_F | counts = one-hot^T [F | 1]: 2-term tf32 split of F (hi =
+    // truncated mantissa, lo = exact remainder), one-hot exact
+#pragma unroll
+    for (int kb = 0; kb < 4; kb++) {
+      const int rr0 = kb * 8 + t, rr1 = rr0 + 4;
+      const int ar0 = __shfl_sync(0xffffffffu, al, rr0);
+      const int ar1 = __shfl_sync(0xffffffffu, al, rr1);
+      uint32_t oh[MT][4];
+#pragma unroll
+      for (int m = 0; m < MT; m++) {
+        const int j0 = m * 16 + g, j1 = j0 + 8;
+        oh[m][0] = ar0 == j0 ? kTf32One : 0u;
+        oh[m][1] = ar0 == j1 ? kTf32One : 0u;
+        oh[m][2] = ar1 == j0 ? kTf32One : 0u;
+        oh[m][3] = ar1 == j1 ? kTf32One : 0u;
+      }
+#pragma unroll
+      for (int c = 0; c < KC; c++) {
+        const float b0 = Fs[rr0 * FP + c * 8 + g];
+        const float b1 = Fs[rr1 * FP + c * 8 + g];
+        const uint32_t h0 = __float_as_uint(b0) & 0xffffe000u;
+        const uint32_t h1 = __float_as_uint(b1) & 0xffffe000u;
+        const uint32_t l0 = __float_as_uint(b0 - __uint_as_float(h0));
+        const uint32_t l1 = __float_as_uint(b1 - __uint_as_float(h1));
+#pragma unroll
+        for (int m = 0; m < MT; m++) {
+          mma_tf32(sacc[m][c], oh[m][0], oh[m][1], oh[m][2], oh[m][3], h0, h1);
+          mma_tf32(sacc[m][c], oh[m][0], oh[m][1], oh[m][2], oh[m][3], l0, l1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && i + a.nst < cnt) {
+      fence_proxy_async();
+      issue(s, u0 + i + a.nst);
+    }
+    if ((i % KM_FLUSH) == KM_FLUSH - 1) flush();
+  }
+  flush();
+  __syncthreads();
+  // CTA partial in fixed warp order: [KP x SC] sums (count at column pf) | loss
+  double* out = a.part + (int64_t)blockIdx.x * (KP * SC + 1);
+  for (int i = threadIdx.x; i < KP * SC; i += blockDim.x) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < KM_WARPS; w2++) s += acc64[w2 * (MT * 16 * SC) + i];
+    out[i] = s;
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < KM_WARPS; w2++) s += lsum[w2];
+    out[KP * SC] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: sums_d = cnt_d^T S_d, then fixed-order reduction (+ update)
+// ---------------------------------------------------------------------------
+__device__ void km_apply_update(const KmUpdateArgs& u) {
+  const int tid = threadIdx.x;
+  const int it = u.state->it;
+  const double* cnt = u.red + (int64_t)u.k * u.c_T;
+  if (tid == 0 && it < u.loss_cap) u.loss_hist[it] = u.red[(int64_t)u.k * u.c_T + u.k];
+  for (int i = tid; i < u.k * u.c_T; i += blockDim.x) {
+    int j = i / u.c_T;
+    double n = cnt[j];
+    if (n > 0.0) u.C64[i] = u.red[i] / n;
+    u.C32[i] = (float)u.C64[i];
+  }
+  __syncthreads();
+  if (tid == 0) u.state->it = it + 1;
+}
+
+__device__ void km_reduce_all(const KmUpdateArgs& u) {
+  const int tid = threadIdx.x;
+  const int n_red = u.k * u.c_T + u.k + 1;
+  for (int i = tid; i < n_red; i += blockDim.x) u.red[i] = 0.0;
+  __syncthreads();
+  const int stride = u.KP * u.SC + 1;
+  // fact sums (+ count column pf, + loss)
+  for (int i = tid; i < u.k * u.SC; i += blockDim.x) {
+    int j = i / u.SC, c = i - j * u.SC;
+    if (c > u.pf) continue;
+    int tc = c < u.pf ? u.f_tcol[c] : -2;
+    if (tc == -1) continue;
+    double s = 0.0;
+    for (int b = 0; b < u.nblk_fact; b++) s += u.part_fact[(int64_t)b * stride + j * u.SC + c];
+    if (c == u.pf) u.red[(int64_t)u.k * u.c_T + j] = s;
+    else u.red[(int64_t)j * u.c_T + tc] = s;
+  }
+  if (tid == 0) {
+    double s = 0.0;
+    for (int b = 0; b < u.nblk_fact; b++) s += u.part_fact[(int64_t)b * stride + u.KP * u.SC];
+    u.red[(int64_t)u.k * u.c_T + u.k] = s;
+  }
+  for (int d = 0; d < u.ng; d++) {
+    const int cols = u.d_cols[d];
+    const int st = u.KP * cols;
+    for (int i = tid; i < u.k * cols; i += blockDim.x) {
+      int j = i / cols, c = i - j * cols;
+      double s = 0.0;
+      for (int b = 0; b < u.nblk_dim[d]; b++) s += u.part_dim[d][(int64_t)b * st + i];
+      u.red[(int64_t)j * u.c_T + u.d_tcol[d][c]] = s;
+    }
+  }
+  __syncthreads();
+}
+
+constexpr int KMD_ROWS = 32;
+
+__global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a, KmUpdateArgs u,
+                                                     int fuse_update, int* done) {
+  extern __shared__ __align__(16) char smem_d[];
+  const int d = blockIdx.y;
+  const bool active = d < a.ng && (int)blockIdx.x < a.nblk[d];
+  if (active) {
+    const int KP = a.KP, cols = a.cols[d], pitch = a.pitch[d];
+    const int64_t rows = a.rows[d];
+    const int nb = a.nblk[d];
+    const int64_t rpb = ceil_div(ceil_div(rows, nb), KMD_ROWS) * KMD_ROWS;
+    const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
+    float* ss = reinterpret_cast<float*>(smem_d);            // KMD_ROWS x cols
+    float* cs = ss + KMD_ROWS * cols;                          // KMD_ROWS x KP
+    double* acc = reinterpret_cast<double*>(cs + KMD_ROWS * KP + 2);  // KP x cols
+    const int npair = KP * cols;
+    for (int i = threadIdx.x; i < npair; i += blockDim.x) acc[i] = 0.0;
+    for (int64_t rb = r0; rb < r1; rb += KMD_ROWS) {
+      const int nr = (int)min64(KMD_ROWS, r1 - rb);
+      __syncthreads();
+      for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
+        int r = i / cols, c = i - r * cols;
+        ss[i] = a.S[d][(rb + r) * pitch + c];
+      }
+      for (int i = threadIdx.x; i < nr * KP; i += blockDim.x)
+        cs[i] = (float)a.cnt[d][rb * KP + i];
+      __syncthreads();
+      for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+        int j = pr / cols, c = pr - j * cols;
+        double sd = 0.0;
+        for (int r = 0; r < nr; r++) sd = fma((double)cs[r * KP + j], (double)ss[r * cols + c], sd);
+        acc[pr] += sd;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < npair; i += blockDim.x)
+      a.part[d][(int64_t)blockIdx.x * npair + i] = acc[i];
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int is_last;
+  if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == (int)(gridDim.x * gridDim.y) - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  km_reduce_all(u);
+  if (fuse_update) km_apply_update(u);
+  if (threadIdx.x == 0) *done = 0;
+}
+
+__global__ void k_km_update(KmUpdateArgs u) { km_apply_update(u); }
+
+__global__ void k_km_assign_to_target(const int32_t* __restrict__ a_dev,
+                                      const int32_t* __restrict__ perm, int64_t r_T,
+                                      int32_t* __restrict__ out) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < r_T) out[perm[p]] = a_dev[p];
+}
+
+// instantiation table: NT in {1,2,4} (k <= 8/16/32), KC in {1,2,3,4,6,8,12,16}
+#define KM_KC_CASES(X, NT) X(NT, 1) X(NT, 2) X(NT, 3) X(NT, 4) X(NT, 6) X(NT, 8) X(NT, 12) X(NT, 16)
+static int km_kc_for(int pf) {
+  const int need = pf / 8 + 1;  // pf == 4 (mod 8): KC*8 > pf leaves the count column
+  const int opts[] = {1, 2, 3, 4, 6, 8, 12, 16};
+  for (int v : opts)
+    if (v >= need) return v;
+  return -1;
+}
+static int km_nt_for(int k) { return k <= 8 ? 1 : k <= 16 ? 2 : k <= 32 ? 4 : -1; }
+static const void* km_fact_ptr(int nt, int kc) {
+#define KM_PTR(NT_, KC_) if (nt == NT_ && kc == KC_) return (const void*)k_km_fact<NT_, KC_>;
+  KM_KC_CASES(KM_PTR, 1) KM_KC_CASES(KM_PTR, 2) KM_KC_CASES(KM_PTR, 4)
+#undef KM_PTR
+  return nullptr;
+}
+static void km_fact_launch(int nt, int kc, const CUtensorMap& tm, const KmFactArgs& a, int grid,
+                           size_t smem, cudaStream_t st) {
+#define KM_LAUNCH(NT_, KC_) \
+  if (nt == NT_ && kc == KC_) { k_km_fact<NT_, KC_><<<grid, KM_WARPS * 32, smem, st>>>(tm, a); return; }
+  KM_KC_CASES(KM_LAUNCH, 1) KM_KC_CASES(KM_LAUNCH, 2) KM_KC_CASES(KM_LAUNCH, 4)
+#undef KM_LAUNCH
+}
+
+}  // namespace flb
+
+using namespace flb;
+
+struct fl_kmeans {
+  CUtensorMap tmF;               // F as [r_pad x pf] fp32, box 32 x (8 KC + 4)
+  fl_table* t = nullptr;
+  int k = 0, KP = 0, NT = 0, KC = 0, SC = 0;
+  KmFactArgs fa{};
+  KmDimArgs da{};
+  KmUpdateArgs ua{};
+  int nblk_fact = 0;
+  size_t smem_fact = 0, smem_e = 0, smem_sum = 0;
+  int grid_e = 1, grid_sum = 1;
+  DevBuf C64, C32, E, cnt, part_fact, part_dim, red, loss_hist, state, assign, done;
+  int loss_cap = 1 << 16;
+  cudaGraphExec_t graph = nullptr, graph_assign = nullptr;
+  cudaStream_t cap_stream = nullptr;
+};
+
+namespace flb {
+
+static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
+                               bool write_assign) {
+  if (s->da.ng > 0) {
+    dim3 ge(s->grid_e, s->da.ng);
+    k_km_dim_e<<<ge, 256, s->smem_e, st>>>(s->da);
+    FL_CHECK_LAUNCH();
+  }
+  KmFactArgs fa = s->fa;
+  fa.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
+  km_fact_launch(s->NT, s->KC, s->tmF, fa, s->nblk_fact, s->smem_fact, st);
+  FL_CHECK_LAUNCH();
+  dim3 gs(std::max(1, s->grid_sum), std::max(1, s->da.ng));
+  k_km_dim_sums<<<gs, 256, s->smem_sum, st>>>(s->da, s->ua, fuse_update ? 1 : 0,
+                                              s->done.as<int>());
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+static int km_graph(fl_kmeans* s, bool write_assign, cudaGraphExec_t* out) {
+  if (*out) return FL_OK;
+  if (!s->cap_stream) FL_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = km_launch_iteration(s, s->cap_stream, true, write_assign);
+  cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
+  if (rc) return rc;
+  FL_CUDA(e);
+  FL_CUDA(cudaGraphInstantiate(out, g, 0));
+  FL_CUDA(cudaGraphDestroy(g));
+  return FL_OK;
+}
+
+}  // namespace flb
+
+extern "C" {
+
+int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans** out,
+                     void* stream) {
+  if (!t || !t->finalized || !centroids0 || !out) {
+    set_error("fl_kmeans_create: bad arguments");
+    return FL_ERR_ARG;
+  }
+  if (k < 1 || k > t->r_T) {
+    set_error("k_clusters = %d exceeds row count %lld", k, (long long)t->r_T);
+    return FL_ERR_CONFIG;
+  }
+  const int NT = km_nt_for(k), KC = km_kc_for(t->pf);
+  if (NT < 0 || KC < 0 || (int)t->g.size() > MAX_GATHER) {
+    set_error("fused K-means supports k <= 32, <= 124 streamed columns and <= %d gathered "
+              "sources (k=%d, streamed pitch=%d)", MAX_GATHER, k, t->pf);
+    return FL_ERR_OP;
+  }
+  for (auto& g : t->g)
+    if ((g.rows + 1) * (int64_t)(NT * 8) >= INT32_MAX) {
+      set_error("fused K-means: dimension source with %lld rows is too large", (long long)g.rows);
+      return FL_ERR_OP;
+    }
+  FL_CUDA(cudaSetDevice(t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* s = new fl_kmeans();
+  std::unique_ptr<fl_kmeans> guard(s);
+  s->t = t;
+  s->k = k;
+  s->NT = NT;
+  s->KP = NT * 8;
+  s->KC = KC;
+  s->SC = KC * 8;
+  const int KP = s->KP, SC = s->SC, MT = (NT + 1) / 2;
+  const int ng = (int)t->g.size();
+  const int c_T = t->c_T;
+  int rc;
+  if ((rc = s->C64.alloc((size_t)k * c_T * 8))) return rc;
+  if ((rc = s->C32.alloc((size_t)k * c_T * 4))) return rc;
+  FL_CUDA(cudaMemcpyAsync(s->C64.p, centroids0, (size_t)k * c_T * 8, cudaMemcpyDefault, st));
+  {
+    std::vector<double> h((size_t)k * c_T);
+    FL_CUDA(cudaMemcpyAsync(h.data(), s->C64.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    std::vector<float> f(h.size());
+    for (size_t i = 0; i < h.size(); i++) f[i] = (float)h[i];
+    FL_CUDA(cudaMemcpy(s->C32.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+  }
+  size_t e_total = 0, c_total = 0;
+  for (auto& g : t->g) {
+    e_total += (size_t)(g.rows + 1) * KP;
+    c_total += (size_t)g.rows * KP;
+  }
+  if ((rc = s->E.alloc(e_total * 4 + 16))) return rc;
+  if ((rc = s->cnt.alloc(c_total * 4 + 16))) return rc;
+  if ((rc = s->red.alloc(((size_t)k * c_T + k + 1) * 8))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->red.p, 0, ((size_t)k * c_T + k + 1) * 8, st));
+  if ((rc = s->loss_hist.alloc((size_t)s->loss_cap * 8))) return rc;
+  if ((rc = s->state.alloc(sizeof(KmState)))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->state.p, 0, sizeof(KmState), st));
+  if ((rc = s->done.alloc(16))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->done.p, 0, 16, st));
+  if ((rc = s->assign.alloc((size_t)t->r_pad * 4))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->assign.p, 0, (size_t)t->r_pad * 4, st));
+
+  // ---- fact pass geometry
+  KmFactArgs& fa = s->fa;
+  fa.F = t->F->as<float>();
+  fa.pf = t->pf;
+  fa.c_T = c_T;
+  fa.k = k;
+  fa.r_T = t->r_T;
+  fa.nunits = t->r_pad / 32;
+  fa.ng = ng;
+  fa.sort_g = t->sort_g;
+  {
+    size_t eo = 0, co = 0;
+    for (int d = 0; d < ng; d++) {
+      fa.fk[d] = t->g[d].fk->as<int32_t>();
+      fa.E[d] = s->E.as<float>() + eo;
+      fa.cnt[d] = s->cnt.as<int32_t>() + co;
+      fa.rows[d] = t->g[d].rows;
+      eo += (size_t)(t->g[d].rows + 1) * KP;
+      co += (size_t)t->g[d].rows * KP;
+    }
+  }
+  fa.C32 = s->C32.as<float>();
+  fa.f_tcol = t->d_f_tcol->as<int32_t>();
+  fa.assign = nullptr;
+  const int FP = SC + 4, ZP = KP + 4;
+  fa.stage_bytes = (uint32_t)round_up(32 * FP * 4 + 128, 128);
+  if ((rc = make_tmap_2d(&s->tmF, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
+                         (uint64_t)t->pf * 4, 32, (uint32_t)FP, 0)))
+    return rc;
+  const size_t fixed = (size_t)KC * NT * 32 * 8 + (size_t)KP * (SC + 4) * 4 + (KP + 4) * 4 +
+                       (size_t)KM_WARPS * MT * 16 * SC * 8 + (size_t)KM_WARPS * 32 * ZP * 4;
+  const size_t fixed_al = round_up((int64_t)fixed, 128);
+  // two CTAs (16 warps) per SM when the tile fits in half the shared memory
+  const bool two = NT <= 2 && KC <= 4 && fixed_al + (size_t)KM_WARPS * 2 * fa.stage_bytes <= 110 * 1024;
+  const size_t budget = two ? 110 * 1024 : 220 * 1024;
+  int nst = (int)((budget - std::min(budget, fixed_al)) / ((size_t)KM_WARPS * fa.stage_bytes));
+  if (const char* e = getenv("FL_KM_NST")) nst = atoi(e);
+  nst = std::max(2, std::min(4, nst));
+  fa.nst = nst;
+  s->smem_fact = fixed_al + (size_t)KM_WARPS * nst * fa.stage_bytes;
+  if (s->smem_fact > 225 * 1024) {
+    set_error("fused K-means: shared memory budget exceeded (%zu bytes)", s->smem_fact);
+    return FL_ERR_OP;
+  }
+  // the stage area starts right after the fixed area (kernel computes the
+  // same offsets); pad the fixed area so stages stay 128-byte aligned
+  const void* kf = km_fact_ptr(NT, KC);
+  FL_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->smem_fact));
+  int occ = 1;
+  FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, KM_WARPS * 32, s->smem_fact));
+  occ = std::max(1, occ);
+  s->nblk_fact = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(fa.nunits, KM_WARPS), (int64_t)t->sm_count * occ));
+  if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (KP * SC + 1) * 8))) return rc;
+  fa.part = s->part_fact.as<double>();
+
+  // ---- dimension kernels
+  KmDimArgs& da = s->da;
+  da.ng = ng;
+  da.k = k;
+  da.KP = KP;
+  da.c_T = c_T;
+  da.C32 = s->C32.as<float>();
+  int max_cols = 1;
+  int64_t max_rows = 1;
+  size_t part_total = 0;
+  s->grid_sum = 1;
+  for (int d = 0; d < ng; d++) {
+    const GatherSrc& g = t->g[d];
+    da.S[d] = g.S->as<float>();
+    da.pitch[d] = g.pitch;
+    da.cols[d] = g.cols;
+    da.rows[d] = g.rows;
+    da.tcol[d] = g.d_tcol->as<int32_t>();
+    da.E[d] = const_cast<float*>(fa.E[d]);
+    da.cnt[d] = fa.cnt[d];
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 256),
+                                                         (int64_t)t->sm_count * 2));
+    da.nblk[d] = nb;
+    s->grid_sum = std::max(s->grid_sum, nb);
+    max_cols = std::max(max_cols, g.cols);
+    max_rows = std::max(max_rows, g.rows + 1);
+    part_total += (size_t)nb * KP * g.cols;
+  }
+  if ((rc = s->part_dim.alloc(part_total * 8 + 16))) return rc;
+  {
+    size_t po = 0;
+    for (int d = 0; d < ng; d++) {
+      da.part[d] = s->part_dim.as<double>() + po;
+      po += (size_t)da.nblk[d] * KP * t->g[d].cols;
+    }
+  }
+  s->smem_e = (size_t)KP * max_cols * 4;
+  s->grid_e = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows * KP, 256),
+                                                          (int64_t)t->sm_count * 8));
+  s->smem_sum = (size_t)KMD_ROWS * max_cols * 4 + (size_t)KMD_ROWS * KP * 4 + 16 +
+                (size_t)KP * max_cols * 8;
+  if (s->smem_e > 200 * 1024 || s->smem_sum > 200 * 1024) {
+    set_error("fused K-means: dimension source too wide");
+    return FL_ERR_OP;
+  }
+  FL_CUDA(cudaFuncSetAttribute(k_km_dim_e, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(s->smem_e, 16)));
+  FL_CUDA(cudaFuncSetAttribute(k_km_dim_sums, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->smem_sum));
+
+  KmUpdateArgs& ua = s->ua;
+  ua.c_T = c_T;
+  ua.k = k;
+  ua.KP = KP;
+  ua.SC = SC;
+  ua.pf = t->pf;
+  ua.ng = ng;
+  ua.f_tcol = t->d_f_tcol->as<int32_t>();
+  for (int d = 0; d < ng; d++) {
+    ua.d_tcol[d] = t->g[d].d_tcol->as<int32_t>();
+    ua.d_cols[d] = t->g[d].cols;
+    ua.part_dim[d] = da.part[d];
+    ua.nblk_dim[d] = da.nblk[d];
+  }
+  ua.part_fact = s->part_fact.as<double>();
+  ua.nblk_fact = s->nblk_fact;
+  ua.red = s->red.as<double>();
+  ua.C64 = s->C64.as<double>();
+  ua.C32 = s->C32.as<float>();
+  ua.loss_hist = s->loss_hist.as<double>();
+  ua.loss_cap = s->loss_cap;
+  ua.state = s->state.as<KmState>();
+  FL_CUDA(cudaStreamSynchronize(st));
+  *out = guard.release();
+  return FL_OK;
+}
+
+int fl_kmeans_partial(fl_kmeans* s, int32_t write_assign, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  return km_launch_iteration(s, (cudaStream_t)stream, false, write_assign != 0);
+}
+
+int fl_kmeans_reduce_buffer(fl_kmeans* s, double** buf, int32_t* len) {
+  if (!s || !buf || !len) return FL_ERR_ARG;
+  *buf = s->red.as<double>();
+  *len = s->k * s->t->c_T + s->k + 1;
+  return FL_OK;
+}
+
+int fl_kmeans_update(fl_kmeans* s, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  k_km_update<<<1, 256, 0, (cudaStream_t)stream>>>(s->ua);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+int fl_kmeans_run(fl_kmeans* s, int32_t iterations, void* stream) {
+  if (!s || iterations < 1) {
+    set_error("iterations must be >= 1");
+    return FL_ERR_CONFIG;
+  }
+  FL_CUDA(cudaSetDevice(s->t->device));
+  int rc = km_graph(s, false, &s->graph);
+  if (rc) return rc;
+  rc = km_graph(s, true, &s->graph_assign);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i + 1 < iterations; i++) FL_CUDA(cudaGraphLaunch(s->graph, st));
+  FL_CUDA(cudaGraphLaunch(s->graph_assign, st));
+  return FL_OK;
+}
+
+int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* loss, int32_t n,
+                     int32_t* n_done, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  KmState h{};
+  FL_CUDA(cudaMemcpyAsync(&h, s->state.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (centroids)
+    FL_CUDA(cudaMemcpyAsync(centroids, s->C64.p, (size_t)s->k * s->t->c_T * 8, cudaMemcpyDefault,
+                            st));
+  if (assign) {
+    int32_t* tmp = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&tmp, (size_t)s->t->r_T * 4 + 16, st));
+    k_km_assign_to_target<<<(unsigned)ceil_div(s->t->r_T, 256), 256, 0, st>>>(
+        s->assign.as<int32_t>(), s->t->perm->as<int32_t>(), s->t->r_T, tmp);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaMemcpyAsync(assign, tmp, (size_t)s->t->r_T * 4, cudaMemcpyDefault, st));
+    FL_CUDA(cudaFreeAsync(tmp, st));
+  }
+  FL_CUDA(cudaStreamSynchronize(st));
+  int nd = std::min(h.it, s->loss_cap);
+  if (n_done) *n_done = nd;
+  if (loss && n > 0) {
+    int m = std::min(n, nd);
+    if (m > 0) FL_CUDA(cudaMemcpy(loss, s->loss_hist.p, (size_t)m * 8, cudaMemcpyDefault));
+  }
+  return FL_OK;
+}
+
+int fl_kmeans_destroy(fl_kmeans* s) {
+  if (!s) return FL_OK;
+  cudaSetDevice(s->t->device);
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  if (s->graph_assign) cudaGraphExecDestroy(s->graph_assign);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  delete s;
+  return FL_OK;
+}
+
+}  // extern "C"

@@ -115,3 +115,105 @@ def test_materialized_path_agrees(fl):
     mh = fl.TargetHandle.materialized(fl.SparseMatrix.from_dense(g["materialized"]))
     res = fl.train("linreg", mh, cfg, g["y_lin"])
     assert max_rel(res.loss_history, g["linreg_loss"]) < TOL
+
+
+# ---------------------------------------------------------------------------
+# K-means (trainers.py:198-246)
+# ---------------------------------------------------------------------------
+def _cfg(fl, m):
+    return fl.TrainConfig(iterations=m["iterations"], learning_rate=m["learning_rate"],
+                          k_clusters=m["k_clusters"], rank=m["rank"], seed=m["seed"])
+
+
+@pytest.mark.parametrize("name,model", _cases(("kmeans",)))
+def test_kmeans_matches_reference(fl, name, model):
+    g = load_golden(name)
+    m = g.meta["trainers"]["kmeans"]
+    res = fl.train("kmeans", fl.TargetHandle.factorized(g.ft), _cfg(fl, m))
+    assert len(res.loss_history) == m["iterations"]
+    assert np.array_equal(res.parameters["assignments"], g["kmeans_assignments"])
+    assert max_rel(res.loss_history, g["kmeans_loss"]) < TOL
+    assert max_rel(res.parameters["centroids"], g["kmeans_centroids"]) < TOL
+
+
+def planted_star(seed, r_fact, dims, c_fact, k, noise=0.01):
+    """Star schema with planted, well-separated clusters: every dimension row
+    and every fact row carries a cluster label; a fact row only references
+    dimension rows of its own cluster, so T's rows cluster cleanly."""
+    from paper_2502_01985_b200.metadata import FactorizedTable, block_mapping, fk_indicator
+    from paper_2502_01985_b200.sparse import SparseMatrix
+    rng = np.random.default_rng(seed)
+    lab = rng.integers(0, k, r_fact)
+    c_t = c_fact + sum(c for _, c in dims)
+    cen = rng.random((k, c_fact))
+    fact = (cen[lab] + noise * rng.standard_normal((r_fact, c_fact))).astype(np.float32)
+    srcs = [SparseMatrix.from_dense(fact.astype(np.float64))]
+    maps = [block_mapping(c_t, c_fact, 0)]
+    inds = [fk_indicator(r_fact, r_fact, np.arange(r_fact))]
+    off = c_fact
+    for r_d, c_d in dims:
+        dlab = np.arange(r_d) % k
+        dcen = rng.random((k, c_d))
+        dim = (dcen[dlab] + noise * rng.standard_normal((r_d, c_d))).astype(np.float32)
+        # fact row i -> a random dim row with the same label
+        fk = np.empty(r_fact, dtype=np.int64)
+        for j in range(k):
+            rows = np.nonzero(dlab == j)[0]
+            mine = np.nonzero(lab == j)[0]
+            fk[mine] = rows[rng.integers(0, rows.size, mine.size)]
+        srcs.append(SparseMatrix.from_dense(dim.astype(np.float64)))
+        maps.append(block_mapping(c_t, c_d, off))
+        inds.append(fk_indicator(r_fact, r_d, fk))
+        off += c_d
+    return FactorizedTable(srcs, maps, inds, "inner", r_fact, c_t)
+
+
+@pytest.mark.parametrize("k,dims,c_fact", [(16, [(3000, 30), (200, 5)], 20),
+                                           (4, [(500, 9)], 12),
+                                           (24, [(4000, 7)], 5)])
+def test_kmeans_planted_star_vs_oracle(fl, k, dims, c_fact):
+    ft = planted_star(21, 60_000, dims, c_fact, k)
+    tab = oracle.OracleTable.from_ft(ft)
+    want = rt.kmeans(tab, 6, k, 3)
+    res = fl.train("kmeans", fl.TargetHandle.factorized(ft),
+                   fl.TrainConfig(iterations=6, k_clusters=k, seed=3))
+    assert np.array_equal(res.parameters["assignments"], want["parameters"]["assignments"])
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+    assert max_rel(res.parameters["centroids"], want["parameters"]["centroids"]) < TOL
+
+
+def test_kmeans_tie_and_empty_cluster(fl):
+    """test_trainers.py:261-270: [[0],[0],[10]], k=3 -> [0, 0, 2], loss 0 and
+    the empty cluster keeps its centroid."""
+    from paper_2502_01985_b200.metadata import FactorizedTable, block_mapping, fk_indicator
+    s = fl.SparseMatrix.from_dense([[0.0], [0.0], [10.0]])
+    ft = FactorizedTable([s], [block_mapping(1, 1, 0)], [fk_indicator(3, 3, [0, 1, 2])],
+                         "inner", 3, 1)
+    res = fl.train("kmeans", fl.TargetHandle.factorized(ft),
+                   fl.TrainConfig(iterations=3, k_clusters=3, seed=0))
+    assert list(res.parameters["assignments"]) == [0, 0, 2]
+    assert res.parameters["centroids"][1, 0] == 0.0
+    assert res.loss_history[-1] == 0.0
+
+
+def test_kmeans_k1_is_global_mean(fl):
+    """test_trainers.py:272-277."""
+    g = load_golden("star")
+    res = fl.train("kmeans", fl.TargetHandle.factorized(g.ft),
+                   fl.TrainConfig(iterations=2, k_clusters=1))
+    want = g["materialized"].mean(axis=0)
+    assert max_rel(res.parameters["centroids"][0], want) < 1e-6
+
+
+def test_kmeans_materialized_and_deterministic(fl):
+    g = load_golden("star3")
+    m = g.meta["trainers"]["kmeans"]
+    mh = fl.TargetHandle.materialized(fl.SparseMatrix.from_dense(g["materialized"]))
+    res = fl.train("kmeans", mh, _cfg(fl, m))
+    assert np.array_equal(res.parameters["assignments"], g["kmeans_assignments"])
+    assert max_rel(res.loss_history, g["kmeans_loss"]) < TOL
+    h = fl.TargetHandle.factorized(g.ft)
+    a = fl.train("kmeans", h, _cfg(fl, m))
+    b = fl.train("kmeans", h, _cfg(fl, m))
+    assert np.array_equal(a.parameters["centroids"], b.parameters["centroids"])
+    assert a.loss_history == b.loss_history
