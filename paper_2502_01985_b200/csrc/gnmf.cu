@@ -1,0 +1,981 @@
+// Gaussian NMF by multiplicative updates over a factorized table (reference
+// trainers.py:256-307, built on rmm / lmm of ops.py:219-253).
+//
+// The reference iteration is
+//     P = W^T T;  [loss of the previous iteration from P, W^T W, H]
+//     H <- H o P / (W^T W H + eps);  Q = T H^T;  W <- W o Q / (W H H^T + eps)
+// and a final rmm for the last loss.  Here every product with T is one fused
+// pass over the fact rows, and P / W^T W of the NEXT iteration are produced
+// by the same pass that writes the new W:
+//
+//  U  k_gnmf_h       (1 CTA) loss(it-1) from P, G = W^T W, H; H <- H o P /
+//                    (G H + eps); HH = H H^T; fp32 copies (fp64 math)
+//  D1 k_gnmf_dim_g   G_d = S_d H_d^T (r_d x R) for every dimension source;
+//                    zero Z_d
+//  F  k_gnmf_fact    per device row p (per-warp TMA pipelines, W tile in a
+//                    128B-swizzled layout, 3xTF32 mma.sync):
+//                      q    = F[p] H_F^T + sum_d G_d[fk_d[p]]
+//                      W[p] = W[p] o q / (W[p] HH + eps)       (TMA store)
+//                      P_F += W[p]^T F[p],  G += W[p]^T W[p]
+//                      Z_d[fk_d[p]] += W[p]   (I_d^T W: segment one-hot MMA,
+//                                             fp64 atomics of fp32 partials)
+//  D2 k_gnmf_dim_p   P_d = Z_d^T S_d (fp64 per-CTA partials)
+//  R  k_gnmf_reduce  fixed-order reduction of all partials into red = [P | G]
+//
+// A prologue (F without the update, D2, R) produces P_0, G_0 from W_0, and a
+// final U (loss only) records the last loss.  With fact rows sharded over
+// GPUs, `red` is all-reduced between R and the next U.
+#include <algorithm>
+#include <cstdlib>
+
+#include "internal.h"
+#include "mma_tf32.cuh"
+#include "reduce.cuh"
+
+namespace flb {
+
+constexpr int GN_WARPS = 8;
+constexpr int GN_FLUSH = 16;   // stages between fp32 -> fp64 flushes (512 rows)
+constexpr double GN_EPS = 1e-12;   // trainers.py:29
+
+struct GnState {
+  int it;           // iterations started (H updates applied)
+  int nloss;        // losses recorded (loss_hist[0 .. nloss))
+  int pad[2];
+};
+
+struct GnFactArgs {
+  int pf, c_T, R;
+  int64_t r_T, nunits;
+  int ng, sort_g;
+  const int32_t* fk[MAX_GATHER];
+  const float* Gd[MAX_GATHER];     // r_d x R
+  double* Z[MAX_GATHER];           // r_d x R
+  const float* H32;                // R x c_T
+  const float* HH32;               // R x R
+  const int32_t* f_tcol;
+  double* wpart;                   // per-warp fp64 partials [MR*16 x (SC + R)]
+  double* part;                    // per-CTA partials
+  uint32_t stage_bytes, off_f, off_fk;
+  int nst;
+};
+
+struct GnDimArgs {
+  int ng, R, c_T;
+  const float* S[MAX_GATHER];
+  int pitch[MAX_GATHER], cols[MAX_GATHER];
+  int64_t rows[MAX_GATHER];
+  int nblk[MAX_GATHER];
+  const int32_t* tcol[MAX_GATHER];
+  float* Gd[MAX_GATHER];
+  double* Z[MAX_GATHER];
+  double* part[MAX_GATHER];        // nblk x (R x cols)
+  const float* H32;
+};
+
+struct GnHArgs {
+  int c_T, R, rank;
+  double* H;                       // R x c_T fp64 master
+  float* H32;
+  float* HH32;
+  const double* red;
+  double t_sq;
+  double* loss_hist;
+  int loss_cap;
+  GnState* state;
+};
+
+// ---------------------------------------------------------------------------
+// U: loss of the previous iteration, H update, HH = H H^T (one CTA, fp64)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gnmf_h(GnHArgs a, int do_update, int do_loss) {
+  extern __shared__ double sh[];
+  const int R = a.R, c_T = a.c_T, tid = threadIdx.x;
+  double* GH = sh;                  // R x c_T
+  double* HH = GH + R * c_T;        // R x R
+  __shared__ double red_s[256];
+  const double* P = a.red;
+  const double* G = a.red + (size_t)R * c_T;
+  // HH of the current H (loss uses H of the iteration the products were made with)
+  for (int i = tid; i < R * R; i += blockDim.x) {
+    int r = i / R, q = i - r * R;
+    double s = 0.0;
+    for (int c = 0; c < c_T; c++) s += a.H[r * c_T + c] * a.H[q * c_T + c];
+    HH[i] = s;
+  }
+  __syncthreads();
+  if (do_loss) {
+    double part = 0.0;
+    for (int i = tid; i < R * c_T; i += blockDim.x) part -= 2.0 * P[i] * a.H[i];
+    for (int i = tid; i < R * R; i += blockDim.x) part += G[i] * HH[i];
+    red_s[tid] = part;
+    __syncthreads();
+    if (tid == 0) {
+      // the products in `red` were made with W of iteration it - 1's update
+      double s = a.t_sq;
+      for (int i = 0; i < (int)blockDim.x; i++) s += red_s[i];
+      const int n = a.state->it - 1;
+      if (n >= 0 && n < a.loss_cap) a.loss_hist[n] = s;
+      if (n + 1 > a.state->nloss) a.state->nloss = n + 1;
+    }
+    __syncthreads();
+  }
+  if (do_update) {
+    // GH = G H (R x c_T), then H <- H o P / (GH + eps)
+    for (int i = tid; i < R * c_T; i += blockDim.x) {
+      int r = i / c_T, c = i - r * c_T;
+      double s = 0.0;
+      for (int q = 0; q < R; q++) s += G[r * R + q] * a.H[q * c_T + c];
+      GH[i] = s;
+    }
+    __syncthreads();
+    for (int i = tid; i < R * c_T; i += blockDim.x) {
+      int r = i / c_T;
+      a.H[i] = r < a.rank ? a.H[i] * P[i] / (GH[i] + GN_EPS) : 0.0;
+    }
+    __syncthreads();
+    for (int i = tid; i < R * R; i += blockDim.x) {
+      int r = i / R, q = i - r * R;
+      double s = 0.0;
+      for (int c = 0; c < c_T; c++) s += a.H[r * c_T + c] * a.H[q * c_T + c];
+      a.HH32[i] = (float)s;
+    }
+    if (tid == 0) a.state->it += 1;
+  }
+  for (int i = tid; i < R * c_T; i += blockDim.x) a.H32[i] = (float)a.H[i];
+}
+
+// ---------------------------------------------------------------------------
+// D1: G_d = S_d H_d^T, zero Z_d
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gnmf_dim_g(GnDimArgs a) {
+  const int d = blockIdx.y;
+  if (d >= a.ng) return;
+  extern __shared__ float hs[];    // R x cols
+  const int R = a.R, cols = a.cols[d], pitch = a.pitch[d];
+  for (int i = threadIdx.x; i < R * cols; i += blockDim.x) {
+    int j = i / cols, c = i - j * cols;
+    hs[i] = a.H32[(size_t)j * a.c_T + a.tcol[d][c]];
+  }
+  __syncthreads();
+  const int64_t total = a.rows[d] * R;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / R;
+    const int j = (int)(idx - r * R);
+    const float* srow = a.S[d] + r * pitch;
+    const float* hrow = hs + j * cols;
+    float acc = 0.f;
+    for (int c = 0; c < cols; c++) acc = fmaf(srow[c], hrow[c], acc);
+    a.Gd[d][idx] = acc;
+    a.Z[d][idx] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// F: the fact-row pass
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ int widx(int row, int col) {
+  // element (row, col) of a 32 x R fp32 tile written by TMA with a (4R)-byte
+  // swizzle: 16-byte chunk index XOR-ed with the row's swizzle phase
+  constexpr int RB = R * 4;
+  constexpr int CH = RB / 16;
+  const int sw = ((row * RB) >> 7) & (CH - 1);
+  return row * R + ((((col >> 2) ^ sw)) << 2) + (col & 3);
+}
+
+__device__ __forceinline__ uint32_t hi_bits(float x) { return __float_as_uint(x) & 0xffffe000u; }
+__device__ __forceinline__ uint32_t lo_bits(float x) {
+  return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xffffe000u));
+}
+
+template <int NR, int KC, bool UPDATE>
+__global__ void __launch_bounds__(GN_WARPS * 32, 1)
+    k_gnmf_fact(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmF,
+                GnFactArgs a) {
+  constexpr int R = NR * 8;
+  constexpr int MR = (NR + 1) / 2;     // 16-rank tiles (W^T as the A operand)
+  constexpr int SC = KC * 8;
+  constexpr int FP = SC + 4;
+  constexpr int WP = MR * 16 * (SC + R);   // per-warp fp64 partial entries
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ uint64_t bar[GN_WARPS][4];
+
+  // the swizzle phase of a W tile is taken from smem address bits [7:9]:
+  // place everything relative to a 1024-byte aligned base
+  char* sm = smem + ((1024u - (smem_u32(smem) & 1023u)) & 1023u);
+  uint4* hf = reinterpret_cast<uint4*>(sm);            // KC*NR*32: B = H_F^T
+  uint4* hh = hf + KC * NR * 32;                       // NR*NR*32: B = HH
+  char* stages = sm + round_up((int64_t)((KC * NR + NR * NR) * 32 * 16), 1024);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int pf = a.pf;
+
+  if (UPDATE) {
+    for (int i = threadIdx.x; i < KC * NR * 32; i += blockDim.x) {
+      int l = i & 31, kn = i >> 5;
+      int kc = kn / NR, n = kn - kc * NR;
+      int gg = l >> 2, tt = l & 3;
+      float b[2];
+      for (int h = 0; h < 2; h++) {
+        int col = kc * 8 + tt + 4 * h;
+        int tc = col < pf ? a.f_tcol[col] : -1;
+        b[h] = tc >= 0 ? a.H32[(size_t)(n * 8 + gg) * a.c_T + tc] : 0.f;
+      }
+      Split s0 = split_tf32(b[0]), s1 = split_tf32(b[1]);
+      hf[i] = make_uint4(s0.hi, s1.hi, s0.lo, s1.lo);
+    }
+    for (int i = threadIdx.x; i < NR * NR * 32; i += blockDim.x) {
+      int l = i & 31, kn = i >> 5;
+      int kc = kn / NR, n = kn - kc * NR;
+      int gg = l >> 2, tt = l & 3;
+      Split s0 = split_tf32(a.HH32[(kc * 8 + tt) * R + n * 8 + gg]);
+      Split s1 = split_tf32(a.HH32[(kc * 8 + tt + 4) * R + n * 8 + gg]);
+      hh[i] = make_uint4(s0.hi, s1.hi, s0.lo, s1.lo);
+    }
+  }
+  if (lane == 0) {
+    for (int s = 0; s < a.nst; s++) mbar_init(&bar[warp][s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int64_t gw = (int64_t)blockIdx.x * GN_WARPS + warp;
+  const int64_t NW = (int64_t)gridDim.x * GN_WARPS;
+  const int64_t base = a.nunits / NW, rem = a.nunits % NW;
+  const int64_t u0 = gw * base + min64(gw, rem);
+  const int64_t cnt = base + (gw < rem ? 1 : 0);
+  const bool has_sort = a.sort_g >= 0;
+  const uint32_t tx = 32u * R * 4u + 32u * FP * 4u + (has_sort ? 128u : 0u);
+  char* wsm = stages + (size_t)warp * a.nst * a.stage_bytes;
+  uint64_t* wbar = bar[warp];
+  double* wp = a.wpart + gw * WP;
+  for (int i = lane; i < WP; i += 32) wp[i] = 0.0;
+  __syncwarp();
+  auto issue = [&](int s, int64_t unit) {
+    char* st = wsm + (size_t)s * a.stage_bytes;
+    mbar_arrive_expect_tx(&wbar[s], tx);
+    tma_load_2d(st, &tmW, 0, (int)(unit * 32), &wbar[s]);
+    tma_load_2d(st + a.off_f, &tmF, 0, (int)(unit * 32), &wbar[s]);
+    if (has_sort) bulk_g2s(st + a.off_fk, a.fk[a.sort_g] + unit * 32, 128, &wbar[s]);
+  };
+  if (lane == 0)
+    for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
+
+  float pacc[MR][KC][4], gacc[MR][NR][4];
+#pragma unroll
+  for (int m = 0; m < MR; m++) {
+#pragma unroll
+    for (int c = 0; c < KC; c++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) pacc[m][c][e] = 0.f;
+#pragma unroll
+    for (int c = 0; c < NR; c++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) gacc[m][c][e] = 0.f;
+  }
+  auto flush = [&]() {
+#pragma unroll
+    for (int m = 0; m < MR; m++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int row = m * 16 + g + (e >> 1) * 8;
+#pragma unroll
+        for (int c = 0; c < KC; c++) {
+          wp[row * (SC + R) + c * 8 + 2 * t + (e & 1)] += (double)pacc[m][c][e];
+          pacc[m][c][e] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < NR; c++) {
+          wp[row * (SC + R) + SC + c * 8 + 2 * t + (e & 1)] += (double)gacc[m][c][e];
+          gacc[m][c][e] = 0.f;
+        }
+      }
+  };
+
+  for (int64_t i = 0; i < cnt; i++) {
+    const int s = (int)(i % a.nst);
+    mbar_wait(&wbar[s], (uint32_t)((i / a.nst) & 1));
+    char* st = wsm + (size_t)s * a.stage_bytes;
+    float* Wt = reinterpret_cast<float*>(st);
+    const float* Fs = reinterpret_cast<const float*>(st + a.off_f);
+    const int32_t* fks_s = reinterpret_cast<const int32_t*>(st + a.off_fk);
+    const int64_t p0 = (u0 + i) * 32;
+    int fkl[MAX_GATHER];
+#pragma unroll
+    for (int d = 0; d < MAX_GATHER; d++) {
+      if (d >= a.ng) break;
+      fkl[d] = (d == a.sort_g) ? fks_s[lane] : a.fk[d][p0 + lane];
+    }
+
+    if (UPDATE) {
+      // ---- q = F H_F^T (3xTF32), v = W HH (3xTF32)
+      float q[2][NR][4], v[2][NR][4];
+#pragma unroll
+      for (int m = 0; m < 2; m++)
+#pragma unroll
+        for (int n = 0; n < NR; n++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) q[m][n][e] = v[m][n][e] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < KC; kc++) {
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+          uint32_t x[4];
+          ldsm_x4(x[0], x[1], x[2], x[3],
+                  Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
+          uint32_t xh[4], xl[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            xh[e] = x[e] & 0xffffe000u;
+            xl[e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(xh[e]));
+          }
+#pragma unroll
+          for (int n = 0; n < NR; n++) {
+            const uint4 b = hf[(kc * NR + n) * 32 + lane];
+            mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b.x, b.y);
+            mma_tf32(q[m][n], xl[0], xl[1], xl[2], xl[3], b.x, b.y);
+            mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b.z, b.w);
+          }
+        }
+      }
+#pragma unroll
+      for (int kc = 0; kc < NR; kc++) {
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+          const int row = m * 16 + (lane & 15);
+          const int col = kc * 8 + (lane >> 4) * 4;
+          uint32_t x[4];
+          ldsm_x4(x[0], x[1], x[2], x[3], Wt + widx<R>(row, col));
+          uint32_t xh[4], xl[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            xh[e] = x[e] & 0xffffe000u;
+            xl[e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(xh[e]));
+          }
+#pragma unroll
+          for (int n = 0; n < NR; n++) {
+            const uint4 b = hh[(kc * NR + n) * 32 + lane];
+            mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b.x, b.y);
+            mma_tf32(v[m][n], xl[0], xl[1], xl[2], xl[3], b.x, b.y);
+            mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b.z, b.w);
+          }
+        }
+      }
+      // ---- gathers of the dimension products G_d[fk]
+#pragma unroll
+      for (int d = 0; d < MAX_GATHER; d++) {
+        if (d >= a.ng) break;
+#pragma unroll
+        for (int m = 0; m < 2; m++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int f = __shfl_sync(0xffffffffu, fkl[d], m * 16 + h * 8 + g);
+            if (f >= 0) {
+              const float* gr = a.Gd[d] + (int64_t)f * R + 2 * t;
+#pragma unroll
+              for (int n = 0; n < NR; n++) {
+                const float2 gv = *reinterpret_cast<const float2*>(gr + n * 8);
+                q[m][n][h * 2] += gv.x;
+                q[m][n][h * 2 + 1] += gv.y;
+              }
+            }
+          }
+      }
+      __syncwarp();
+      // ---- W <- W o q / (W HH + eps), in place in the swizzled tile
+#pragma unroll
+      for (int m = 0; m < 2; m++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int row = m * 16 + h * 8 + g;
+#pragma unroll
+          for (int n = 0; n < NR; n++) {
+            float2* wptr = reinterpret_cast<float2*>(Wt + widx<R>(row, n * 8 + 2 * t));
+            float2 w = *wptr;
+            w.x = w.x * __fdividef(q[m][n][h * 2], v[m][n][h * 2] + 1e-12f);
+            w.y = w.y * __fdividef(q[m][n][h * 2 + 1], v[m][n][h * 2 + 1] + 1e-12f);
+            *wptr = w;
+          }
+        }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        tma_store_2d(&tmW, 0, (int)p0, Wt);
+        bulk_commit();
+      }
+    }
+    // ---- P_F += W^T F,  G += W^T W  (3xTF32; W^T fragments from the tile)
+#pragma unroll
+    for (int kb = 0; kb < 4; kb++) {
+      const int r0 = kb * 8 + t, r1 = r0 + 4;
+      uint32_t ah[MR][4], alo[MR][4];
+#pragma unroll
+      for (int m = 0; m < MR; m++) {
+        const float w0 = Wt[widx<R>(r0, (m * 16 + g) % R)];
+        const float w1 = (m * 16 + g + 8 < R) ? Wt[widx<R>(r0, m * 16 + g + 8)] : 0.f;
+        const float w2 = Wt[widx<R>(r1, (m * 16 + g) % R)];
+        const float w3 = (m * 16 + g + 8 < R) ? Wt[widx<R>(r1, m * 16 + g + 8)] : 0.f;
+        const float wa[4] = {m * 16 + g < R ? w0 : 0.f, w1, m * 16 + g < R ? w2 : 0.f, w3};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          ah[m][e] = hi_bits(wa[e]);
+          alo[m][e] = lo_bits(wa[e]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KC; c++) {
+        const float b0 = Fs[r0 * FP + c * 8 + g], b1 = Fs[r1 * FP + c * 8 + g];
+        const uint32_t bh0 = hi_bits(b0), bh1 = hi_bits(b1);
+        const uint32_t bl0 = lo_bits(b0), bl1 = lo_bits(b1);
+#pragma unroll
+        for (int m = 0; m < MR; m++) {
+          mma_tf32(pacc[m][c], ah[m][0], ah[m][1], ah[m][2], ah[m][3], bh0, bh1);
+          mma_tf32(pacc[m][c], alo[m][0], alo[m][1], alo[m][2], alo[m][3], bh0, bh1);
+          mma_tf32(pacc[m][c], ah[m][0], ah[m][1], ah[m][2], ah[m][3], bl0, bl1);
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < NR; n++) {
+        const float b0 = Wt[widx<R>(r0, n * 8 + g)], b1 = Wt[widx<R>(r1, n * 8 + g)];
+        const uint32_t bh0 = hi_bits(b0), bh1 = hi_bits(b1);
+        const uint32_t bl0 = lo_bits(b0), bl1 = lo_bits(b1);
+#pragma unroll
+        for (int m = 0; m < MR; m++) {
+          mma_tf32(gacc[m][n], ah[m][0], ah[m][1], ah[m][2], ah[m][3], bh0, bh1);
+          mma_tf32(gacc[m][n], alo[m][0], alo[m][1], alo[m][2], alo[m][3], bh0, bh1);
+          mma_tf32(gacc[m][n], ah[m][0], ah[m][1], ah[m][2], ah[m][3], bl0, bl1);
+        }
+      }
+    }
+    // ---- Z_d[fk] += W rows: segment one-hot (runs of equal FK) x W, fp64
+    // atomics of the per-segment fp32 partials (sums of fp32 values in fp64
+    // are exact here, so the result does not depend on their order)
+#pragma unroll
+    for (int d = 0; d < MAX_GATHER; d++) {
+      if (d >= a.ng) break;
+      const int key = fkl[d];
+      const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
+      const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || key != kprev);
+      const int slot = __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
+      const int nslots = __popc(starts);
+      const int MS = nslots > 16 ? 2 : 1;
+      float zc[2][NR][4];
+#pragma unroll
+      for (int m = 0; m < 2; m++)
+#pragma unroll
+        for (int n = 0; n < NR; n++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) zc[m][n][e] = 0.f;
+#pragma unroll
+      for (int kb = 0; kb < 4; kb++) {
+        const int r0 = kb * 8 + t, r1 = r0 + 4;
+        const int s0 = __shfl_sync(0xffffffffu, slot, r0);
+        const int s1 = __shfl_sync(0xffffffffu, slot, r1);
+        uint32_t bh[NR][2], bl[NR][2];
+#pragma unroll
+        for (int n = 0; n < NR; n++) {
+          const float b0 = Wt[widx<R>(r0, n * 8 + g)], b1 = Wt[widx<R>(r1, n * 8 + g)];
+          bh[n][0] = hi_bits(b0);
+          bh[n][1] = hi_bits(b1);
+          bl[n][0] = lo_bits(b0);
+          bl[n][1] = lo_bits(b1);
+        }
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+          if (m >= MS) break;
+          const int j0 = m * 16 + g, j1 = j0 + 8;
+          const uint32_t o0 = s0 == j0 ? kTf32One : 0u, o1 = s0 == j1 ? kTf32One : 0u;
+          const uint32_t o2 = s1 == j0 ? kTf32One : 0u, o3 = s1 == j1 ? kTf32One : 0u;
+#pragma unroll
+          for (int n = 0; n < NR; n++) {
+            mma_tf32(zc[m][n], o0, o1, o2, o3, bh[n][0], bh[n][1]);
+            mma_tf32(zc[m][n], o0, o1, o2, o3, bl[n][0], bl[n][1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 2; m++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int sl = m * 16 + h * 8 + g;
+          const int start = sl < nslots ? (int)__fns(starts, 0, sl + 1) : 0;
+          const int skey = __shfl_sync(0xffffffffu, key, start & 31);
+          if (sl < nslots && skey >= 0) {
+            double* zr = a.Z[d] + (int64_t)skey * R + 2 * t;
+#pragma unroll
+            for (int n = 0; n < NR; n++) {
+              atomicAdd(zr + n * 8, (double)zc[m][n][h * 2]);
+              atomicAdd(zr + n * 8 + 1, (double)zc[m][n][h * 2 + 1]);
+            }
+          }
+        }
+    }
+    __syncwarp();
+    if (lane == 0 && i + a.nst < cnt) {
+      if (UPDATE) bulk_wait_read<0>();   // the W store has left this stage
+      fence_proxy_async();
+      issue(s, u0 + i + a.nst);
+    }
+    if ((i % GN_FLUSH) == GN_FLUSH - 1) flush();
+  }
+  flush();
+  if (UPDATE && lane == 0) bulk_wait<0>();
+  __syncthreads();
+  // CTA partial (fixed warp order): [R x SC] P_F | [R x R] G
+  double* out = a.part + (int64_t)blockIdx.x * (R * SC + R * R);
+  const double* wbase = a.wpart + (int64_t)blockIdx.x * GN_WARPS * WP;
+  for (int i = threadIdx.x; i < R * (SC + R); i += blockDim.x) {
+    const int row = i / (SC + R), col = i - row * (SC + R);
+    double s = 0.0;
+    for (int w2 = 0; w2 < GN_WARPS; w2++) s += wbase[(int64_t)w2 * WP + row * (SC + R) + col];
+    if (col < SC) out[row * SC + col] = s;
+    else out[R * SC + row * R + (col - SC)] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// D2: P_d = Z_d^T S_d (fp64 per-CTA partials over row ranges)
+// ---------------------------------------------------------------------------
+constexpr int GND_ROWS = 32;
+
+__global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
+  const int d = blockIdx.y;
+  if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
+  extern __shared__ __align__(16) char smem_p[];
+  const int R = a.R, cols = a.cols[d], pitch = a.pitch[d];
+  const int64_t rows = a.rows[d];
+  const int nb = a.nblk[d];
+  const int64_t rpb = ceil_div(ceil_div(rows, nb), GND_ROWS) * GND_ROWS;
+  const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
+  double* zs = reinterpret_cast<double*>(smem_p);       // GND_ROWS x R
+  double* acc = zs + GND_ROWS * R;                      // R x cols
+  float* ss = reinterpret_cast<float*>(acc + R * cols); // GND_ROWS x cols
+  const int npair = R * cols;
+  for (int i = threadIdx.x; i < npair; i += blockDim.x) acc[i] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += GND_ROWS) {
+    const int nr = (int)min64(GND_ROWS, r1 - rb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * R; i += blockDim.x) zs[i] = a.Z[d][rb * R + i];
+    for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
+      int r = i / cols, c = i - r * cols;
+      ss[i] = a.S[d][(rb + r) * pitch + c];
+    }
+    __syncthreads();
+    for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+      const int j = pr / cols, c = pr - j * cols;
+      double s = 0.0;
+      for (int r = 0; r < nr; r++) s = fma(zs[r * R + j], (double)ss[r * cols + c], s);
+      acc[pr] += s;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npair; i += blockDim.x)
+    a.part[d][(int64_t)blockIdx.x * npair + i] = acc[i];
+}
+
+// ---------------------------------------------------------------------------
+// R: red = [P | G], each element reduced over the partials in a fixed order
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gnmf_reduce(const RedDesc* descs, int n, double* red) {
+  reduce_descs(descs, n, red);
+}
+
+__global__ void k_gnmf_w_in(const double* __restrict__ w0, const int32_t* __restrict__ perm,
+                            int64_t r_pad, int rank, int R, float* __restrict__ W) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= r_pad * R) return;
+  int64_t p = idx / R;
+  int j = (int)(idx - p * R);
+  int32_t tr = perm[p];
+  W[idx] = (tr >= 0 && j < rank) ? (float)w0[(int64_t)tr * rank + j] : 0.f;
+}
+
+__global__ void k_gnmf_w_out(const float* __restrict__ W, const int32_t* __restrict__ perm,
+                             int64_t r_T, int rank, int R, double* __restrict__ out) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= r_T * rank) return;
+  int64_t p = idx / rank;
+  int j = (int)(idx - p * rank);
+  out[(int64_t)perm[p] * rank + j] = (double)W[p * R + j];
+}
+
+#define GN_CASES(X, U) \
+  X(1, 1, U) X(1, 2, U) X(1, 3, U) X(1, 4, U) X(1, 6, U) X(1, 8, U) \
+  X(2, 1, U) X(2, 2, U) X(2, 3, U) X(2, 4, U) X(2, 6, U) X(2, 8, U) \
+  X(4, 1, U) X(4, 2, U) X(4, 3, U) X(4, 4, U) X(4, 6, U) X(4, 8, U)
+static int gn_kc_for(int pf) {
+  const int need = (pf + 7) / 8;
+  const int opts[] = {1, 2, 3, 4, 6, 8};
+  for (int v : opts)
+    if (v >= need) return v;
+  return -1;
+}
+static const void* gn_fact_ptr(int nr, int kc, bool upd) {
+#define GN_PTR(NR_, KC_, U_) \
+  if (nr == NR_ && kc == KC_ && upd == U_) return (const void*)k_gnmf_fact<NR_, KC_, U_>;
+  GN_CASES(GN_PTR, true) GN_CASES(GN_PTR, false)
+#undef GN_PTR
+  return nullptr;
+}
+static void gn_fact_launch(int nr, int kc, bool upd, const CUtensorMap& tw, const CUtensorMap& tf,
+                           const GnFactArgs& a, int grid, size_t smem, cudaStream_t st) {
+#define GN_LAUNCH(NR_, KC_, U_)                                                         \
+  if (nr == NR_ && kc == KC_ && upd == U_) {                                            \
+    k_gnmf_fact<NR_, KC_, U_><<<grid, GN_WARPS * 32, smem, st>>>(tw, tf, a);            \
+    return;                                                                             \
+  }
+  GN_CASES(GN_LAUNCH, true) GN_CASES(GN_LAUNCH, false)
+#undef GN_LAUNCH
+}
+
+}  // namespace flb
+
+using namespace flb;
+
+struct fl_gnmf {
+  CUtensorMap tmW, tmF;
+  fl_table* t = nullptr;
+  int rank = 0, R = 0, NR = 0, KC = 0, SC = 0;
+  GnFactArgs fa{};
+  GnDimArgs da{};
+  GnHArgs ha{};
+  int nblk_fact = 0, grid_g = 1, grid_p = 1, grid_red = 1;
+  size_t smem_fact = 0, smem_g = 0, smem_p = 0, smem_h = 0;
+  DevBuf descs;
+  int n_desc = 0;
+  DevBuf W, H, H32, HH32, Gd, Z, wpart, part_fact, part_dim, red, loss_hist, state;
+  int loss_cap = 1 << 16;
+  bool primed = false;
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+};
+
+namespace flb {
+
+static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
+  if (update && s->da.ng > 0) {
+    k_gnmf_dim_g<<<dim3(s->grid_g, s->da.ng), 256, s->smem_g, st>>>(s->da);
+    FL_CHECK_LAUNCH();
+  } else {
+    for (int d = 0; d < s->da.ng; d++)
+      FL_CUDA(cudaMemsetAsync(s->da.Z[d], 0, (size_t)s->da.rows[d] * s->R * 8, st));
+  }
+  gn_fact_launch(s->NR, s->KC, update, s->tmW, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
+  FL_CHECK_LAUNCH();
+  if (s->da.ng > 0) {
+    k_gnmf_dim_p<<<dim3(s->grid_p, s->da.ng), 256, s->smem_p, st>>>(s->da);
+    FL_CHECK_LAUNCH();
+  }
+  k_gnmf_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc,
+                                             s->red.as<double>());
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+static int gn_h(fl_gnmf* s, cudaStream_t st, bool update, bool loss) {
+  k_gnmf_h<<<1, 256, s->smem_h, st>>>(s->ha, update ? 1 : 0, loss ? 1 : 0);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+}  // namespace flb
+
+extern "C" {
+
+int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0, double t_sq,
+                   fl_gnmf** out, void* stream) {
+  if (!t || !t->finalized || !w0 || !h0 || !out) {
+    set_error("fl_gnmf_create: bad arguments");
+    return FL_ERR_ARG;
+  }
+  if (rank < 1 || rank > std::min<int64_t>(t->r_T, t->c_T)) {
+    set_error("rank = %d exceeds min(shape) = %lld", rank,
+              (long long)std::min<int64_t>(t->r_T, t->c_T));
+    return FL_ERR_CONFIG;
+  }
+  const int R = rank <= 8 ? 8 : rank <= 16 ? 16 : rank <= 32 ? 32 : -1;
+  const int KC = gn_kc_for(t->pf);
+  if (R < 0 || KC < 0 || (int)t->g.size() > MAX_GATHER) {
+    set_error("fused GNMF supports rank <= 32, <= 60 streamed columns and <= %d gathered "
+              "sources (rank=%d, streamed pitch=%d)", MAX_GATHER, rank, t->pf);
+    return FL_ERR_OP;
+  }
+  FL_CUDA(cudaSetDevice(t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* s = new fl_gnmf();
+  std::unique_ptr<fl_gnmf> guard(s);
+  s->t = t;
+  s->rank = rank;
+  s->R = R;
+  s->NR = R / 8;
+  s->KC = KC;
+  s->SC = KC * 8;
+  const int NR = s->NR, SC = s->SC, MR = (NR + 1) / 2, FP = SC + 4;
+  const int c_T = t->c_T, ng = (int)t->g.size();
+  int rc;
+  // W (device order, padded rank) and H
+  if ((rc = s->W.alloc((size_t)t->r_pad * R * 4))) return rc;
+  {
+    double* w0d = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&w0d, (size_t)t->r_T * rank * 8 + 16, st));
+    FL_CUDA(cudaMemcpyAsync(w0d, w0, (size_t)t->r_T * rank * 8, cudaMemcpyDefault, st));
+    k_gnmf_w_in<<<(unsigned)ceil_div(t->r_pad * R, 256), 256, 0, st>>>(
+        w0d, t->perm->as<int32_t>(), t->r_pad, rank, R, s->W.as<float>());
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaFreeAsync(w0d, st));
+  }
+  if ((rc = s->H.alloc((size_t)R * c_T * 8))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->H.p, 0, (size_t)R * c_T * 8, st));
+  FL_CUDA(cudaMemcpyAsync(s->H.p, h0, (size_t)rank * c_T * 8, cudaMemcpyDefault, st));
+  if ((rc = s->H32.alloc((size_t)R * c_T * 4))) return rc;
+  if ((rc = s->HH32.alloc((size_t)R * R * 4))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->HH32.p, 0, (size_t)R * R * 4, st));
+  size_t gd_total = 0;
+  for (auto& g : t->g) gd_total += (size_t)g.rows * R;
+  if ((rc = s->Gd.alloc(gd_total * 4 + 16))) return rc;
+  if ((rc = s->Z.alloc(gd_total * 8 + 16))) return rc;
+  if ((rc = s->red.alloc(((size_t)R * c_T + R * R) * 8))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->red.p, 0, ((size_t)R * c_T + R * R) * 8, st));
+  if ((rc = s->loss_hist.alloc((size_t)s->loss_cap * 8))) return rc;
+  if ((rc = s->state.alloc(sizeof(GnState)))) return rc;
+  FL_CUDA(cudaMemsetAsync(s->state.p, 0, sizeof(GnState), st));
+
+  // ---- fact pass
+  if ((rc = make_tmap_2d(&s->tmW, s->W.p, (uint64_t)t->r_pad, (uint64_t)R, (uint64_t)R * 4, 32,
+                         (uint32_t)R, R * 4)))
+    return rc;
+  if ((rc = make_tmap_2d(&s->tmF, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
+                         (uint64_t)t->pf * 4, 32, (uint32_t)FP, 0)))
+    return rc;
+  GnFactArgs& fa = s->fa;
+  fa.pf = t->pf;
+  fa.c_T = c_T;
+  fa.R = R;
+  fa.r_T = t->r_T;
+  fa.nunits = t->r_pad / 32;
+  fa.ng = ng;
+  fa.sort_g = t->sort_g;
+  {
+    size_t o = 0;
+    for (int d = 0; d < ng; d++) {
+      fa.fk[d] = t->g[d].fk->as<int32_t>();
+      fa.Gd[d] = s->Gd.as<float>() + o;
+      fa.Z[d] = s->Z.as<double>() + o;
+      o += (size_t)t->g[d].rows * R;
+    }
+  }
+  fa.H32 = s->H32.as<float>();
+  fa.HH32 = s->HH32.as<float>();
+  fa.f_tcol = t->d_f_tcol->as<int32_t>();
+  fa.off_f = (uint32_t)(32 * R * 4);
+  fa.off_fk = fa.off_f + (uint32_t)(32 * FP * 4);
+  fa.stage_bytes = (uint32_t)round_up(fa.off_fk + 128, 1024);
+  const size_t fixed = round_up((int64_t)((KC * NR + NR * NR) * 32 * 16), 1024);
+  int nst = (int)((200 * 1024 - fixed) / ((size_t)GN_WARPS * fa.stage_bytes));
+  if (const char* e = getenv("FL_GN_NST")) nst = atoi(e);
+  fa.nst = std::max(2, std::min(4, nst));
+  s->smem_fact = fixed + (size_t)GN_WARPS * fa.nst * fa.stage_bytes + 1024;  // + alignment slack
+  if (s->smem_fact > 227 * 1024) {
+    set_error("fused GNMF: shared memory budget exceeded (%zu bytes)", s->smem_fact);
+    return FL_ERR_OP;
+  }
+  int occ = 1;
+  for (int u = 0; u < 2; u++) {
+    const void* kf = gn_fact_ptr(NR, KC, u == 0);
+    FL_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)s->smem_fact));
+    if (u == 0)
+      FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, GN_WARPS * 32,
+                                                            s->smem_fact));
+  }
+  occ = std::max(1, occ);
+  s->nblk_fact = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(fa.nunits, GN_WARPS), (int64_t)t->sm_count * occ));
+  const size_t WP = (size_t)MR * 16 * (SC + R);
+  if ((rc = s->wpart.alloc((size_t)s->nblk_fact * GN_WARPS * WP * 8))) return rc;
+  if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (R * SC + R * R) * 8))) return rc;
+  fa.wpart = s->wpart.as<double>();
+  fa.part = s->part_fact.as<double>();
+
+  // ---- dimension kernels
+  GnDimArgs& da = s->da;
+  da.ng = ng;
+  da.R = R;
+  da.c_T = c_T;
+  da.H32 = s->H32.as<float>();
+  int max_cols = 1;
+  int64_t max_rows = 1;
+  size_t part_total = 0;
+  s->grid_p = 1;
+  for (int d = 0; d < ng; d++) {
+    const GatherSrc& g = t->g[d];
+    da.S[d] = g.S->as<float>();
+    da.pitch[d] = g.pitch;
+    da.cols[d] = g.cols;
+    da.rows[d] = g.rows;
+    da.tcol[d] = g.d_tcol->as<int32_t>();
+    da.Gd[d] = const_cast<float*>(fa.Gd[d]);
+    da.Z[d] = fa.Z[d];
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 512), 64));
+    da.nblk[d] = nb;
+    s->grid_p = std::max(s->grid_p, nb);
+    max_cols = std::max(max_cols, g.cols);
+    max_rows = std::max(max_rows, g.rows);
+    part_total += (size_t)nb * R * g.cols;
+  }
+  if ((rc = s->part_dim.alloc(part_total * 8 + 16))) return rc;
+  {
+    size_t po = 0;
+    for (int d = 0; d < ng; d++) {
+      da.part[d] = s->part_dim.as<double>() + po;
+      po += (size_t)da.nblk[d] * R * t->g[d].cols;
+    }
+  }
+  s->smem_g = (size_t)R * max_cols * 4;
+  s->grid_g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows * R, 256),
+                                                          (int64_t)t->sm_count * 8));
+  s->smem_p = (size_t)GND_ROWS * R * 8 + (size_t)R * max_cols * 8 + (size_t)GND_ROWS * max_cols * 4;
+  if (s->smem_p > 200 * 1024) {
+    set_error("fused GNMF: dimension source too wide");
+    return FL_ERR_OP;
+  }
+  FL_CUDA(cudaFuncSetAttribute(k_gnmf_dim_g, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(s->smem_g, 16)));
+  FL_CUDA(cudaFuncSetAttribute(k_gnmf_dim_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->smem_p));
+  {
+    std::vector<RedDesc> dv;
+    const int fst = R * SC + R * R;
+    const double* pfb = s->part_fact.as<double>();
+    for (int j = 0; j < R; j++) {
+      for (int c = 0; c < t->pf; c++)
+        if (t->f_tcol[c] >= 0) dv.push_back(RedDesc{pfb + j * SC + c, fst, s->nblk_fact, j * c_T + t->f_tcol[c], 0});
+      for (int q = 0; q < R; q++)
+        dv.push_back(RedDesc{pfb + R * SC + j * R + q, fst, s->nblk_fact, R * c_T + j * R + q, 0});
+    }
+    for (int d = 0; d < ng; d++) {
+      const int cols = t->g[d].cols;
+      for (int j = 0; j < R; j++)
+        for (int c = 0; c < cols; c++)
+          dv.push_back(RedDesc{da.part[d] + j * cols + c, R * cols, da.nblk[d], j * c_T + t->g[d].tcol[c], 0});
+    }
+    s->n_desc = (int)dv.size();
+    if ((rc = s->descs.alloc(dv.size() * sizeof(RedDesc)))) return rc;
+    FL_CUDA(cudaMemcpy(s->descs.p, dv.data(), dv.size() * sizeof(RedDesc), cudaMemcpyHostToDevice));
+    s->grid_red = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(s->n_desc, 8), 4 * t->sm_count));
+  }
+  GnHArgs& ha = s->ha;
+  ha.c_T = c_T;
+  ha.R = R;
+  ha.rank = rank;
+  ha.H = s->H.as<double>();
+  ha.H32 = s->H32.as<float>();
+  ha.HH32 = s->HH32.as<float>();
+  ha.red = s->red.as<double>();
+  ha.t_sq = t_sq;
+  ha.loss_hist = s->loss_hist.as<double>();
+  ha.loss_cap = s->loss_cap;
+  ha.state = s->state.as<GnState>();
+  s->smem_h = ((size_t)R * c_T + (size_t)R * R) * 8;
+  if (s->smem_h > 200 * 1024) {
+    set_error("fused GNMF: rank x columns too large for the H update");
+    return FL_ERR_OP;
+  }
+  FL_CUDA(cudaFuncSetAttribute(k_gnmf_h, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->smem_h));
+  FL_CUDA(cudaStreamSynchronize(st));
+  *out = guard.release();
+  return FL_OK;
+}
+
+int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
+  if (!s || iterations < 1) {
+    set_error("iterations must be >= 1");
+    return FL_ERR_CONFIG;
+  }
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (!s->primed) {   // P_0 = W_0^T T, G_0 = W_0^T W_0
+    if ((rc = gn_h(s, st, false, false))) return rc;   // fp32 copy of H_0
+    if ((rc = gn_products(s, st, false))) return rc;
+    s->primed = true;
+  }
+  if (!s->graph) {
+    if (!s->cap_stream) FL_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+    // loss of the previous iteration is recorded by U when it > 0
+    rc = gn_h(s, s->cap_stream, true, true);
+    if (!rc) rc = gn_products(s, s->cap_stream, true);
+    cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
+    if (rc) return rc;
+    FL_CUDA(e);
+    FL_CUDA(cudaGraphInstantiate(&s->graph, g, 0));
+    FL_CUDA(cudaGraphDestroy(g));
+  }
+  GnState h{};
+  FL_CUDA(cudaMemcpyAsync(&h, s->state.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < iterations; i++) {
+    if (h.it + i == 0) {
+      // first iteration: no previous loss
+      if ((rc = gn_h(s, st, true, false))) return rc;
+      if ((rc = gn_products(s, st, true))) return rc;
+    } else {
+      FL_CUDA(cudaGraphLaunch(s->graph, st));
+    }
+  }
+  return FL_OK;
+}
+
+int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n, int32_t* n_done,
+                   void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  GnState hs{};
+  FL_CUDA(cudaMemcpyAsync(&hs, s->state.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  // the last iteration's loss (from the products of the final W) is recorded
+  // on demand, once per iteration count
+  if (hs.it > 0 && hs.nloss < hs.it) {
+    int rc = gn_h(s, st, false, true);
+    if (rc) return rc;
+    FL_CUDA(cudaMemcpyAsync(&hs, s->state.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+  }
+  const fl_table* t = s->t;
+  if (w) {
+    double* tmp = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&tmp, (size_t)t->r_T * s->rank * 8 + 16, st));
+    k_gnmf_w_out<<<(unsigned)ceil_div(t->r_T * s->rank, 256), 256, 0, st>>>(
+        s->W.as<float>(), t->perm->as<int32_t>(), t->r_T, s->rank, s->R, tmp);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaMemcpyAsync(w, tmp, (size_t)t->r_T * s->rank * 8, cudaMemcpyDefault, st));
+    FL_CUDA(cudaFreeAsync(tmp, st));
+  }
+  if (h) FL_CUDA(cudaMemcpyAsync(h, s->H.p, (size_t)s->rank * t->c_T * 8, cudaMemcpyDefault, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  const int nd = std::min(hs.nloss, s->loss_cap);
+  if (n_done) *n_done = nd;
+  if (loss && n > 0) {
+    const int m = std::min(n, nd);
+    if (m > 0) FL_CUDA(cudaMemcpy(loss, s->loss_hist.p, (size_t)m * 8, cudaMemcpyDefault));
+  }
+  return FL_OK;
+}
+
+int fl_gnmf_destroy(fl_gnmf* s) {
+  if (!s) return FL_OK;
+  cudaSetDevice(s->t->device);
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  delete s;
+  return FL_OK;
+}
+
+}  // extern "C"

@@ -32,6 +32,7 @@
 
 #include "internal.h"
 #include "mma_tf32.cuh"
+#include "reduce.cuh"
 
 namespace flb {
 
@@ -332,12 +333,13 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         float4 x = fr[c4];
         xn = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, xn))));
       }
-      const float tol = 3.2e-3f * (xn + cn_max) + 2e-5f * (fabsf(v1) + fabsf(v2));
+      // v2 is +inf when k == 1: keep the bound finite
+      const float tol = 3.2e-3f * (xn + cn_max) + 2e-5f * (fabsf(v1) + fminf(fabsf(v2), 3e38f));
       if (!(v2 - v1 > tol)) {
         uint32_t cand = 0;   // clusters that can still win
 #pragma unroll
         for (int j = 0; j < KP; j++)
-          if (dv[j] - v1 <= tol) cand |= 1u << j;
+          if (j < k && dv[j] - v1 <= tol) cand |= 1u << j;
         float bd = kInf;
         int bj = 0;
         while (cand) {
@@ -458,49 +460,14 @@ __device__ void km_apply_update(const KmUpdateArgs& u) {
   if (tid == 0) u.state->it = it + 1;
 }
 
-__device__ void km_reduce_all(const KmUpdateArgs& u) {
-  const int tid = threadIdx.x;
-  const int n_red = u.k * u.c_T + u.k + 1;
-  for (int i = tid; i < n_red; i += blockDim.x) u.red[i] = 0.0;
-  __syncthreads();
-  const int stride = u.KP * u.SC + 1;
-  // fact sums (+ count column pf, + loss)
-  for (int i = tid; i < u.k * u.SC; i += blockDim.x) {
-    int j = i / u.SC, c = i - j * u.SC;
-    if (c > u.pf) continue;
-    int tc = c < u.pf ? u.f_tcol[c] : -2;
-    if (tc == -1) continue;
-    double s = 0.0;
-    for (int b = 0; b < u.nblk_fact; b++) s += u.part_fact[(int64_t)b * stride + j * u.SC + c];
-    if (c == u.pf) u.red[(int64_t)u.k * u.c_T + j] = s;
-    else u.red[(int64_t)j * u.c_T + tc] = s;
-  }
-  if (tid == 0) {
-    double s = 0.0;
-    for (int b = 0; b < u.nblk_fact; b++) s += u.part_fact[(int64_t)b * stride + u.KP * u.SC];
-    u.red[(int64_t)u.k * u.c_T + u.k] = s;
-  }
-  for (int d = 0; d < u.ng; d++) {
-    const int cols = u.d_cols[d];
-    const int st = u.KP * cols;
-    for (int i = tid; i < u.k * cols; i += blockDim.x) {
-      int j = i / cols, c = i - j * cols;
-      double s = 0.0;
-      for (int b = 0; b < u.nblk_dim[d]; b++) s += u.part_dim[d][(int64_t)b * st + i];
-      u.red[(int64_t)j * u.c_T + u.d_tcol[d][c]] = s;
-    }
-  }
-  __syncthreads();
-}
-
 constexpr int KMD_ROWS = 32;
 
-__global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a, KmUpdateArgs u,
-                                                     int fuse_update, int* done) {
+__global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
   extern __shared__ __align__(16) char smem_d[];
   const int d = blockIdx.y;
   const bool active = d < a.ng && (int)blockIdx.x < a.nblk[d];
-  if (active) {
+  if (!active) return;
+  {
     const int KP = a.KP, cols = a.cols[d], pitch = a.pitch[d];
     const int64_t rows = a.rows[d];
     const int nb = a.nblk[d];
@@ -532,16 +499,13 @@ __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a, KmUpdateArgs u
     for (int i = threadIdx.x; i < npair; i += blockDim.x)
       a.part[d][(int64_t)blockIdx.x * npair + i] = acc[i];
   }
-  __threadfence();
-  __syncthreads();
-  __shared__ int is_last;
-  if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == (int)(gridDim.x * gridDim.y) - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  km_reduce_all(u);
-  if (fuse_update) km_apply_update(u);
-  if (threadIdx.x == 0) *done = 0;
+}
+
+// R: fixed-order reduction of every partial into `red` (+ update)
+__global__ void __launch_bounds__(256) k_km_reduce(const RedDesc* descs, int n, KmUpdateArgs u,
+                                                   int fuse_update, int* done) {
+  reduce_descs(descs, n, u.red);
+  if (last_cta_done(done) && fuse_update) km_apply_update(u);
 }
 
 __global__ void k_km_update(KmUpdateArgs u) { km_apply_update(u); }
@@ -590,7 +554,8 @@ struct fl_kmeans {
   KmUpdateArgs ua{};
   int nblk_fact = 0;
   size_t smem_fact = 0, smem_e = 0, smem_sum = 0;
-  int grid_e = 1, grid_sum = 1;
+  int grid_e = 1, grid_sum = 1, grid_red = 1, n_desc = 0;
+  DevBuf descs;
   DevBuf C64, C32, E, cnt, part_fact, part_dim, red, loss_hist, state, assign, done;
   int loss_cap = 1 << 16;
   cudaGraphExec_t graph = nullptr, graph_assign = nullptr;
@@ -610,9 +575,12 @@ static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
   fa.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
   km_fact_launch(s->NT, s->KC, s->tmF, fa, s->nblk_fact, s->smem_fact, st);
   FL_CHECK_LAUNCH();
-  dim3 gs(std::max(1, s->grid_sum), std::max(1, s->da.ng));
-  k_km_dim_sums<<<gs, 256, s->smem_sum, st>>>(s->da, s->ua, fuse_update ? 1 : 0,
-                                              s->done.as<int>());
+  if (s->da.ng > 0) {
+    k_km_dim_sums<<<dim3(s->grid_sum, s->da.ng), 256, s->smem_sum, st>>>(s->da);
+    FL_CHECK_LAUNCH();
+  }
+  k_km_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc, s->ua,
+                                           fuse_update ? 1 : 0, s->done.as<int>());
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
@@ -827,6 +795,27 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   ua.loss_hist = s->loss_hist.as<double>();
   ua.loss_cap = s->loss_cap;
   ua.state = s->state.as<KmState>();
+  {
+    std::vector<RedDesc> dv;
+    const int fst = KP * SC + 1;
+    const double* pfb = s->part_fact.as<double>();
+    for (int j = 0; j < k; j++) {
+      for (int c = 0; c < t->pf; c++)
+        if (t->f_tcol[c] >= 0) dv.push_back(RedDesc{pfb + j * SC + c, fst, s->nblk_fact, j * c_T + t->f_tcol[c], 0});
+      dv.push_back(RedDesc{pfb + j * SC + t->pf, fst, s->nblk_fact, k * c_T + j, 0});
+    }
+    dv.push_back(RedDesc{pfb + KP * SC, fst, s->nblk_fact, k * c_T + k, 0});
+    for (int d = 0; d < ng; d++) {
+      const int cols = t->g[d].cols;
+      for (int j = 0; j < k; j++)
+        for (int c = 0; c < cols; c++)
+          dv.push_back(RedDesc{da.part[d] + j * cols + c, KP * cols, da.nblk[d], j * c_T + t->g[d].tcol[c], 0});
+    }
+    s->n_desc = (int)dv.size();
+    if ((rc = s->descs.alloc(dv.size() * sizeof(RedDesc)))) return rc;
+    FL_CUDA(cudaMemcpy(s->descs.p, dv.data(), dv.size() * sizeof(RedDesc), cudaMemcpyHostToDevice));
+    s->grid_red = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(s->n_desc, 8), 4 * t->sm_count));
+  }
   FL_CUDA(cudaStreamSynchronize(st));
   *out = guard.release();
   return FL_OK;

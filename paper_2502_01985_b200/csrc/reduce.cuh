@@ -1,0 +1,59 @@
+// Deterministic cross-CTA reduction of fp64 partials.
+//
+// Every output element red[dst] = sum_b base[b * stride] over nblk per-CTA
+// partials is owned by ONE warp: lane l sums b = l, l + 32, ... in order and
+// the warp combines the 32 lane sums with a fixed xor tree, so the result is
+// bit-identical run to run (no atomics) while the partial loads of all
+// elements proceed in parallel across the grid.
+#pragma once
+#include "internal.h"
+
+namespace flb {
+
+struct RedDesc {
+  const double* base;   // &part[0][offset]
+  int stride;           // doubles between consecutive CTA partials
+  int nblk;             // number of partials
+  int dst;              // index into the output
+  int pad;
+};
+
+__device__ __forceinline__ double warp_reduce_desc(const RedDesc& d, int lane) {
+  double s = 0.0;
+  for (int b = lane; b < d.nblk; b += 32) s += d.base[(int64_t)b * d.stride];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// all warps of the grid walk the descriptor list; returns after writing
+__device__ __forceinline__ void reduce_descs(const RedDesc* __restrict__ descs, int n,
+                                             double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e = w0; e < n; e += nw) {
+    const RedDesc d = descs[e];
+    const double s = warp_reduce_desc(d, lane);
+    if (lane == 0) out[d.dst] = s;
+  }
+}
+
+// last-CTA-done helper: true in exactly one CTA, after every CTA's writes
+__device__ __forceinline__ bool last_cta_done(int* counter) {
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int total = gridDim.x * gridDim.y * gridDim.z;
+    is_last = atomicAdd(counter, 1) == total - 1;
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+  return is_last;
+}
+
+}  // namespace flb

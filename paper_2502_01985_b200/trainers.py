@@ -430,10 +430,18 @@ class GnmfSession:
         self.rank = rank
         self.c_T = h.shape[1]
         ptr = C.c_void_p()
-        w0 = np.ascontiguousarray(w0, dtype=np.float64)
-        h0 = np.ascontiguousarray(h0, dtype=np.float64)
-        _lib.call("fl_gnmf_create", h._dev.ptr, int(rank), w0.ctypes.data_as(C.c_void_p),
-                  h0.ctypes.data_as(C.c_void_p), float(t_sq), C.byref(ptr), C.c_void_p(0))
+
+        def _ptr(a):   # host (numpy) or device (CUDA torch) fp64 operand
+            if _is_torch(a):
+                a = a.contiguous().double()
+                return a, C.c_void_p(a.data_ptr())
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            return a, a.ctypes.data_as(C.c_void_p)
+
+        w0, wp = _ptr(w0)
+        h0, hp = _ptr(h0)
+        _lib.call("fl_gnmf_create", h._dev.ptr, int(rank), wp, hp, float(t_sq), C.byref(ptr),
+                  C.c_void_p(0))
         self.ptr = ptr
 
     def run(self, iterations: int, stream=None):

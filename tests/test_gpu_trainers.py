@@ -217,3 +217,58 @@ def test_kmeans_materialized_and_deterministic(fl):
     b = fl.train("kmeans", h, _cfg(fl, m))
     assert np.array_equal(a.parameters["centroids"], b.parameters["centroids"])
     assert a.loss_history == b.loss_history
+
+
+# ---------------------------------------------------------------------------
+# Gaussian NMF (trainers.py:256-307)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,model", _cases(("gnmf",)))
+def test_gnmf_matches_reference(fl, name, model):
+    g = load_golden(name)
+    m = g.meta["trainers"]["gnmf"]
+    res = fl.train("gnmf", fl.TargetHandle.factorized(g.ft), _cfg(fl, m))
+    assert len(res.loss_history) == m["iterations"]
+    assert max_rel(res.loss_history, g["gnmf_loss"]) < TOL
+    assert max_rel(res.parameters["h"], g["gnmf_h"]) < TOL
+    assert max_rel(res.parameters["w"], g["gnmf_w"]) < TOL
+
+
+@pytest.mark.parametrize("rank,dims,c_fact", [(32, [(2000, 50)], 20),
+                                              (5, [(900, 11), (40, 3)], 12),
+                                              (12, [(30000, 6)], 7)])
+def test_gnmf_random_star_vs_oracle(fl, rank, dims, c_fact):
+    ft = star_table(31, 40_000, dims, c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    want = rt.gaussian_nmf(tab, 6, rank, 5)
+    res = fl.train("gnmf", fl.TargetHandle.factorized(ft),
+                   fl.TrainConfig(iterations=6, rank=rank, seed=5))
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+    assert max_rel(res.parameters["h"], want["parameters"]["h"]) < TOL
+    assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
+
+
+def test_gnmf_materialized_agrees(fl):
+    g = load_golden("star3")
+    m = g.meta["trainers"]["gnmf"]
+    mh = fl.TargetHandle.materialized(fl.SparseMatrix.from_dense(g["materialized"]))
+    res = fl.train("gnmf", mh, _cfg(fl, m))
+    assert max_rel(res.loss_history, g["gnmf_loss"]) < TOL
+    assert max_rel(res.parameters["w"], g["gnmf_w"]) < TOL
+
+
+def test_gnmf_config_errors(fl):
+    g = load_golden("two_source")
+    h = fl.TargetHandle.factorized(g.ft)
+    with pytest.raises(fl.ConfigError):
+        fl.train("gnmf", h, fl.TrainConfig(rank=5))
+    neg = fl.TargetHandle.factorized(star_table(3, 300, [(10, 3)], 4, nonneg=False))
+    with pytest.raises(fl.ConfigError, match="non-negative"):
+        fl.train("gnmf", neg, fl.TrainConfig(rank=2))
+
+
+def test_gnmf_monotone_loss(fl):
+    """Acceptance C5 (test_acceptance.py:229-250): MU-NMF loss is monotone."""
+    ft = star_table(8, 20_000, [(500, 9)], 10)
+    res = fl.train("gnmf", fl.TargetHandle.factorized(ft), fl.TrainConfig(iterations=15, rank=8))
+    lh = np.asarray(res.loss_history)
+    assert np.all(np.diff(lh) <= 1e-6 * np.abs(lh[:-1]))
