@@ -148,6 +148,9 @@ int fl_kmeans_partial(fl_kmeans* s, int32_t write_assign, void* stream);
 int fl_kmeans_reduce_buffer(fl_kmeans* s, double** buf, int32_t* len);
 int fl_kmeans_update(fl_kmeans* s, void* stream);
 int fl_kmeans_run(fl_kmeans* s, int32_t iterations, void* stream);
+/* measurement hook: `iters` iterations with CUDA events between the kernels;
+ * ms_out[4] = mean ms of [dim E, fact pass, dim sums, reduce + update] */
+int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* stream);
 /* centroids k x c_T fp64, assignments r_T int32 (target order), losses */
 int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* loss,
                      int32_t n, int32_t* n_done, void* stream);
@@ -158,6 +161,15 @@ int fl_kmeans_destroy(fl_kmeans* s);
 int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0,
                    double t_sq, fl_gnmf** out, void* stream);
 int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream);
+/* multi-GPU stepping: the first call computes the products of W_0, every
+ * later call applies one H update (recording the previous loss) and computes
+ * the products of the new W; all-reduce the buffer (R*c_T + R*R doubles,
+ * [W^T T | W^T W], R = rank padded to 8/16/32) after every call. */
+int fl_gnmf_partial(fl_gnmf* s, void* stream);
+/* measurement hook (after >= 1 iteration): ms_out[5] = mean ms of
+ * [H update, dim G, fact pass, dim P, reduce] per iteration */
+int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream);
+int fl_gnmf_reduce_buffer(fl_gnmf* s, double** buf, int32_t* len);
 int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n,
                    int32_t* n_done, void* stream);
 int fl_gnmf_destroy(fl_gnmf* s);

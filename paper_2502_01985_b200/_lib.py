@@ -78,10 +78,14 @@ SIGNATURES = {
     "fl_kmeans_reduce_buffer": [_P, C.POINTER(C.c_void_p), C.POINTER(_I32)],
     "fl_kmeans_update": [_P, _P],
     "fl_kmeans_run": [_P, _I32, _P],
+    "fl_kmeans_kernel_times": [_P, _I32, _P, _P],
     "fl_kmeans_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_kmeans_destroy": [_P],
     "fl_gnmf_create": [_P, _I32, _P, _P, _D, _PP, _P],
     "fl_gnmf_run": [_P, _I32, _P],
+    "fl_gnmf_partial": [_P, _P],
+    "fl_gnmf_kernel_times": [_P, _I32, _P, _P],
+    "fl_gnmf_reduce_buffer": [_P, C.POINTER(C.c_void_p), C.POINTER(_I32)],
     "fl_gnmf_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_gnmf_destroy": [_P],
 }

@@ -932,6 +932,74 @@ int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
   return FL_OK;
 }
 
+int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream) {
+  if (!s || iters < 1 || !ms_out || !s->primed) {
+    set_error("fl_gnmf_kernel_times: run at least one iteration first");
+    return FL_ERR_ARG;
+  }
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[6];
+  for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
+  float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < iters; i++) {
+    FL_CUDA(cudaEventRecord(ev[0], st));
+    int rc = gn_h(s, st, true, true);
+    if (rc) return rc;
+    FL_CUDA(cudaEventRecord(ev[1], st));
+    if (s->da.ng > 0) {
+      k_gnmf_dim_g<<<dim3(s->grid_g, s->da.ng), 256, s->smem_g, st>>>(s->da);
+      FL_CHECK_LAUNCH();
+    }
+    FL_CUDA(cudaEventRecord(ev[2], st));
+    gn_fact_launch(s->NR, s->KC, true, s->tmW, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord(ev[3], st));
+    if (s->da.ng > 0) {
+      k_gnmf_dim_p<<<dim3(s->grid_p, s->da.ng), 256, s->smem_p, st>>>(s->da);
+      FL_CHECK_LAUNCH();
+    }
+    FL_CUDA(cudaEventRecord(ev[4], st));
+    k_gnmf_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc,
+                                               s->red.as<double>());
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord(ev[5], st));
+    FL_CUDA(cudaEventSynchronize(ev[5]));
+    for (int j = 0; j < 5; j++) {
+      float ms = 0.f;
+      FL_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+      acc[j] += ms;
+    }
+  }
+  for (int j = 0; j < 5; j++) ms_out[j] = acc[j] / iters;
+  for (auto& e : ev) cudaEventDestroy(e);
+  return FL_OK;
+}
+
+int fl_gnmf_partial(fl_gnmf* s, void* stream) {
+  if (!s) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (!s->primed) {   // products of W_0 only
+    if ((rc = gn_h(s, st, false, false))) return rc;
+    s->primed = true;
+    return gn_products(s, st, false);
+  }
+  GnState h{};
+  FL_CUDA(cudaMemcpyAsync(&h, s->state.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  if ((rc = gn_h(s, st, true, h.it > 0))) return rc;
+  return gn_products(s, st, true);
+}
+
+int fl_gnmf_reduce_buffer(fl_gnmf* s, double** buf, int32_t* len) {
+  if (!s || !buf || !len) return FL_ERR_ARG;
+  *buf = s->red.as<double>();
+  *len = s->R * s->t->c_T + s->R * s->R;
+  return FL_OK;
+}
+
 int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n, int32_t* n_done,
                    void* stream) {
   if (!s) return FL_ERR_ARG;

@@ -858,6 +858,44 @@ int fl_kmeans_run(fl_kmeans* s, int32_t iterations, void* stream) {
   return FL_OK;
 }
 
+int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* stream) {
+  if (!s || iters < 1 || !ms_out) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[5];
+  for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < iters; i++) {
+    FL_CUDA(cudaEventRecord(ev[0], st));
+    if (s->da.ng > 0) {
+      k_km_dim_e<<<dim3(s->grid_e, s->da.ng), 256, s->smem_e, st>>>(s->da);
+      FL_CHECK_LAUNCH();
+    }
+    FL_CUDA(cudaEventRecord(ev[1], st));
+    km_fact_launch(s->NT, s->KC, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord(ev[2], st));
+    if (s->da.ng > 0) {
+      k_km_dim_sums<<<dim3(s->grid_sum, s->da.ng), 256, s->smem_sum, st>>>(s->da);
+      FL_CHECK_LAUNCH();
+    }
+    FL_CUDA(cudaEventRecord(ev[3], st));
+    k_km_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc, s->ua, 1,
+                                             s->done.as<int>());
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord(ev[4], st));
+    FL_CUDA(cudaEventSynchronize(ev[4]));
+    for (int j = 0; j < 4; j++) {
+      float ms = 0.f;
+      FL_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+      acc[j] += ms;
+    }
+  }
+  for (int j = 0; j < 4; j++) ms_out[j] = acc[j] / iters;
+  for (auto& e : ev) cudaEventDestroy(e);
+  return FL_OK;
+}
+
 int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* loss, int32_t n,
                      int32_t* n_done, void* stream) {
   if (!s) return FL_ERR_ARG;

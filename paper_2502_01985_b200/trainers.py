@@ -294,7 +294,7 @@ class KMeansSession:
         _lib.call("fl_kmeans_run", self.ptr, int(iterations),
                   stream if stream is not None else C.c_void_p(0))
 
-    def partial(self, write_assign: bool, stream=None):
+    def partial(self, write_assign: bool = False, stream=None):
         _lib.call("fl_kmeans_partial", self.ptr, int(write_assign),
                   stream if stream is not None else C.c_void_p(0))
 
@@ -306,6 +306,13 @@ class KMeansSession:
         n = C.c_int32()
         _lib.call("fl_kmeans_reduce_buffer", self.ptr, C.byref(buf), C.byref(n))
         return buf.value, n.value
+
+    def kernel_times(self, iters: int, stream=None) -> list[float]:
+        """Mean ms of [dim E, fact pass, dim sums, reduce + update]."""
+        out = (C.c_float * 4)()
+        _lib.call("fl_kmeans_kernel_times", self.ptr, int(iters), out,
+                  stream if stream is not None else C.c_void_p(0))
+        return [float(v) for v in out]
 
     def result(self, n: int):
         r_t, _ = self.h.shape
@@ -330,16 +337,23 @@ class KMeansSession:
         self.close()
 
 
+def target_rows(t: TargetHandle, rows) -> np.ndarray:
+    """Rows of T (target order) gathered on the device: exact fp32 copies."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty((rows.size, t.shape[1]), dtype=np.float32)
+    if rows.size:
+        _lib.call("fl_target_rows", t._dev.ptr, rows.ctypes.data_as(C.c_void_p), int(rows.size),
+                  out.ctypes.data_as(C.c_void_p), C.c_void_p(0))
+    return out
+
+
 def kmeans_init(t: TargetHandle, k: int, seed: int) -> np.ndarray:
     """Seed centroids = k distinct target rows (trainers.py:209-218); the
     rows are fetched on the device (exact copies)."""
-    r_t, c_t = t.shape
+    r_t, _ = t.shape
     rng = np.random.default_rng(seed)
     pick = np.sort(rng.choice(r_t, size=k, replace=False)).astype(np.int64)
-    out = np.empty((k, c_t), dtype=np.float32)
-    _lib.call("fl_target_rows", t._dev.ptr, pick.ctypes.data_as(C.c_void_p), int(k),
-              out.ctypes.data_as(C.c_void_p), C.c_void_p(0))
-    return out.astype(np.float64)
+    return target_rows(t, pick).astype(np.float64)
 
 
 def kmeans(t: TargetHandle, cfg: TrainConfig) -> TrainResult:
@@ -444,9 +458,33 @@ class GnmfSession:
                   C.c_void_p(0))
         self.ptr = ptr
 
+    # sharded stepping needs one extra partial up front: the products of W_0
+    needs_prime = True
+
     def run(self, iterations: int, stream=None):
         _lib.call("fl_gnmf_run", self.ptr, int(iterations),
                   stream if stream is not None else C.c_void_p(0))
+        self.needs_prime = False
+
+    def partial(self, stream=None):
+        _lib.call("fl_gnmf_partial", self.ptr, stream if stream is not None else C.c_void_p(0))
+        self.needs_prime = False
+
+    def update(self, stream=None):
+        """The H update runs at the start of the next partial()."""
+
+    def reduce_buffer(self) -> tuple[int, int]:
+        buf = C.c_void_p()
+        n = C.c_int32()
+        _lib.call("fl_gnmf_reduce_buffer", self.ptr, C.byref(buf), C.byref(n))
+        return buf.value, n.value
+
+    def kernel_times(self, iters: int, stream=None) -> list[float]:
+        """Mean ms of [H update, dim G, fact pass, dim P, reduce]."""
+        out = (C.c_float * 5)()
+        _lib.call("fl_gnmf_kernel_times", self.ptr, int(iters), out,
+                  stream if stream is not None else C.c_void_p(0))
+        return [float(v) for v in out]
 
     def result(self, n: int):
         r_t, c_t = self.h.shape
@@ -538,5 +576,5 @@ def train(model: str, t: TargetHandle, cfg: TrainConfig, y=None) -> TrainResult:
 
 
 __all__ = ["ConfigError", "DivergenceError", "EPS_NMF", "GlmSession", "GnmfSession",
-           "KMeansSession", "TRAINER_FUNCS", "TrainConfig", "TrainResult", "gaussian_nmf",
+           "KMeansSession", "TRAINER_FUNCS", "target_rows", "TrainConfig", "TrainResult", "gaussian_nmf",
            "kmeans", "kmeans_init", "linear_regression", "logistic_regression", "train"]
