@@ -174,6 +174,14 @@ int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n,
                    int32_t* n_done, void* stream);
 int fl_gnmf_destroy(fl_gnmf* s);
 
+/* ---- diagnostics ---------------------------------------------------------
+ * Known-answer test of the tcgen05 (5th-gen tensor core) operand layouts:
+ * D[128 x N] = A[128 x K] B[K x N] (row-major host or device buffers) through
+ * kind::tf32 MMAs from shared memory into TMEM.  mode 0: K-major interleave;
+ * 1: MN-major interleave; 2: K-major SWIZZLE_128B A (K = 32); 3: MN-major
+ * SWIZZLE_128B A and B with 32 valid A rows (N = 32). */
+int fl_tc_selftest(int32_t mode, const float* A, const float* B, float* D, int32_t K, int32_t N);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,9 +132,10 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
     lacc = 0.f;
   };
 
-  for (int64_t i = 0; i < cnt; i++) {
-    const int s = (int)(i % a.nst);
-    mbar_wait(&wbar[s], (uint32_t)((i / a.nst) & 1));
+  int s = 0;            // stage slot and its mbarrier phase
+  uint32_t ph = 0;
+  for (int64_t i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0)) {
+    mbar_wait(&wbar[s], ph);
     const char* st = wsm + (size_t)s * a.stage_bytes;
     const float4* Ft = reinterpret_cast<const float4*>(st);
     const int64_t unit_row0 = (u0 + i) * RW;

@@ -148,27 +148,49 @@ __global__ void __launch_bounds__(256) k_gnmf_h(GnHArgs a, int do_update, int do
 // ---------------------------------------------------------------------------
 // D1: G_d = S_d H_d^T, zero Z_d
 // ---------------------------------------------------------------------------
+// thread per dimension row, R accumulators; H_d sits transposed in smem
+template <int R>
 __global__ void __launch_bounds__(256) k_gnmf_dim_g(GnDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng) return;
-  extern __shared__ float hs[];    // R x cols
-  const int R = a.R, cols = a.cols[d], pitch = a.pitch[d];
-  for (int i = threadIdx.x; i < R * cols; i += blockDim.x) {
-    int j = i / cols, c = i - j * cols;
-    hs[i] = a.H32[(size_t)j * a.c_T + a.tcol[d][c]];
+  extern __shared__ __align__(16) float sm_g[];   // pitch x R
+  const int cols = a.cols[d], pitch = a.pitch[d];
+  const int64_t rows = a.rows[d];
+  for (int i = threadIdx.x; i < pitch * R; i += blockDim.x) {
+    const int c = i / R, j = i - c * R;
+    sm_g[i] = c < cols ? a.H32[(size_t)j * a.c_T + a.tcol[d][c]] : 0.f;
   }
   __syncthreads();
-  const int64_t total = a.rows[d] * R;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / R;
-    const int j = (int)(idx - r * R);
-    const float* srow = a.S[d] + r * pitch;
-    const float* hrow = hs + j * cols;
-    float acc = 0.f;
-    for (int c = 0; c < cols; c++) acc = fmaf(srow[c], hrow[c], acc);
-    a.Gd[d][idx] = acc;
-    a.Z[d][idx] = 0.0;
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    float acc[R];
+#pragma unroll
+    for (int j = 0; j < R; j++) acc[j] = 0.f;
+    const float4* sr = reinterpret_cast<const float4*>(a.S[d] + row * pitch);
+    for (int c4 = 0; c4 < pitch / 4; c4++) {
+      const float4 v = sr[c4];
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const float4* hr = reinterpret_cast<const float4*>(sm_g + (c4 * 4 + e) * R);
+#pragma unroll
+        for (int q = 0; q < R / 4; q++) {
+          const float4 h = hr[q];
+          acc[q * 4 + 0] = fmaf(vv[e], h.x, acc[q * 4 + 0]);
+          acc[q * 4 + 1] = fmaf(vv[e], h.y, acc[q * 4 + 1]);
+          acc[q * 4 + 2] = fmaf(vv[e], h.z, acc[q * 4 + 2]);
+          acc[q * 4 + 3] = fmaf(vv[e], h.w, acc[q * 4 + 3]);
+        }
+      }
+    }
+    float4* gr = reinterpret_cast<float4*>(a.Gd[d] + row * R);
+    double2* zr = reinterpret_cast<double2*>(a.Z[d] + row * R);
+#pragma unroll
+    for (int q = 0; q < R / 4; q++) {
+      gr[q] = make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
+      zr[2 * q] = make_double2(0.0, 0.0);
+      zr[2 * q + 1] = make_double2(0.0, 0.0);
+    }
   }
 }
 
@@ -295,9 +317,10 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
       }
   };
 
-  for (int64_t i = 0; i < cnt; i++) {
-    const int s = (int)(i % a.nst);
-    mbar_wait(&wbar[s], (uint32_t)((i / a.nst) & 1));
+  int s = 0;            // stage slot and its mbarrier phase
+  uint32_t ph = 0;
+  for (int64_t i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0)) {
+    mbar_wait(&wbar[s], ph);
     char* st = wsm + (size_t)s * a.stage_bytes;
     float* Wt = reinterpret_cast<float*>(st);
     const float* Fs = reinterpret_cast<const float*>(st + a.off_f);
@@ -539,41 +562,78 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
 // ---------------------------------------------------------------------------
 // D2: P_d = Z_d^T S_d (fp64 per-CTA partials over row ranges)
 // ---------------------------------------------------------------------------
-constexpr int GND_ROWS = 32;
-
+// P_d[j, c] = sum_r Z_d[r, j] S_d[r, c]: 32-row tiles of S and Z (Z converted
+// to fp32 once) in smem; thread = (column, 8 ranks); fp32 within a tile,
+// fp64 across tiles
+template <int R>
 __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
-  extern __shared__ __align__(16) char smem_p[];
-  const int R = a.R, cols = a.cols[d], pitch = a.pitch[d];
+  constexpr int JB = 8, NJB = R / JB;
+  __shared__ float ss[32 * 257];
+  __shared__ __align__(16) float zs[32 * R];
+  const int cols = a.cols[d], pitch = a.pitch[d];
   const int64_t rows = a.rows[d];
   const int nb = a.nblk[d];
-  const int64_t rpb = ceil_div(ceil_div(rows, nb), GND_ROWS) * GND_ROWS;
+  const int64_t rpb = ceil_div(ceil_div(rows, nb), 32) * 32;
   const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
-  double* zs = reinterpret_cast<double*>(smem_p);       // GND_ROWS x R
-  double* acc = zs + GND_ROWS * R;                      // R x cols
-  float* ss = reinterpret_cast<float*>(acc + R * cols); // GND_ROWS x cols
-  const int npair = R * cols;
-  for (int i = threadIdx.x; i < npair; i += blockDim.x) acc[i] = 0.0;
-  for (int64_t rb = r0; rb < r1; rb += GND_ROWS) {
-    const int nr = (int)min64(GND_ROWS, r1 - rb);
+  const int nwork = cols * NJB;
+  double acc64[2][JB];
+#pragma unroll
+  for (int u = 0; u < 2; u++)
+#pragma unroll
+    for (int j = 0; j < JB; j++) acc64[u][j] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    const int nr = (int)min64(32, r1 - rb);
     __syncthreads();
-    for (int i = threadIdx.x; i < nr * R; i += blockDim.x) zs[i] = a.Z[d][rb * R + i];
-    for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
-      int r = i / cols, c = i - r * cols;
-      ss[i] = a.S[d][(rb + r) * pitch + c];
+    for (int i = threadIdx.x; i < 32 * cols; i += blockDim.x) {
+      const int r = i / cols, c = i - r * cols;
+      ss[r * 257 + c] = r < nr ? a.S[d][(rb + r) * pitch + c] : 0.f;
     }
+    for (int i = threadIdx.x; i < 32 * R; i += blockDim.x)
+      zs[i] = i < nr * R ? (float)a.Z[d][rb * R + i] : 0.f;
     __syncthreads();
-    for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
-      const int j = pr / cols, c = pr - j * cols;
-      double s = 0.0;
-      for (int r = 0; r < nr; r++) s = fma(zs[r * R + j], (double)ss[r * cols + c], s);
-      acc[pr] += s;
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int w = threadIdx.x + u * 256;
+      if (w >= nwork) break;
+      const int c = w % cols, jb = w / cols;
+      float acc[JB];
+#pragma unroll
+      for (int j = 0; j < JB; j++) acc[j] = 0.f;
+      for (int r = 0; r < 32; r++) {
+        const float v = ss[r * 257 + c];
+        const float4 z0 = *reinterpret_cast<const float4*>(zs + r * R + jb * JB);
+        const float4 z1 = *reinterpret_cast<const float4*>(zs + r * R + jb * JB + 4);
+        acc[0] = fmaf(z0.x, v, acc[0]); acc[1] = fmaf(z0.y, v, acc[1]);
+        acc[2] = fmaf(z0.z, v, acc[2]); acc[3] = fmaf(z0.w, v, acc[3]);
+        acc[4] = fmaf(z1.x, v, acc[4]); acc[5] = fmaf(z1.y, v, acc[5]);
+        acc[6] = fmaf(z1.z, v, acc[6]); acc[7] = fmaf(z1.w, v, acc[7]);
+      }
+#pragma unroll
+      for (int j = 0; j < JB; j++) acc64[u][j] += (double)acc[j];
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < npair; i += blockDim.x)
-    a.part[d][(int64_t)blockIdx.x * npair + i] = acc[i];
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    const int w = threadIdx.x + u * 256;
+    if (w >= nwork) break;
+    const int c = w % cols, jb = w / cols;
+#pragma unroll
+    for (int j = 0; j < JB; j++)
+      a.part[d][(int64_t)blockIdx.x * R * cols + (jb * JB + j) * cols + c] = acc64[u][j];
+  }
+}
+
+static void gn_dim_g_launch(int R, dim3 g, size_t smem, cudaStream_t st, const GnDimArgs& a) {
+  if (R == 8) k_gnmf_dim_g<8><<<g, 256, smem, st>>>(a);
+  else if (R == 16) k_gnmf_dim_g<16><<<g, 256, smem, st>>>(a);
+  else k_gnmf_dim_g<32><<<g, 256, smem, st>>>(a);
+}
+static void gn_dim_p_launch(int R, dim3 g, size_t smem, cudaStream_t st, const GnDimArgs& a) {
+  if (R == 8) k_gnmf_dim_p<8><<<g, 256, smem, st>>>(a);
+  else if (R == 16) k_gnmf_dim_p<16><<<g, 256, smem, st>>>(a);
+  else k_gnmf_dim_p<32><<<g, 256, smem, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -657,7 +717,7 @@ namespace flb {
 
 static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
   if (update && s->da.ng > 0) {
-    k_gnmf_dim_g<<<dim3(s->grid_g, s->da.ng), 256, s->smem_g, st>>>(s->da);
+    gn_dim_g_launch(s->R, dim3(s->grid_g, s->da.ng), s->smem_g, st, s->da);
     FL_CHECK_LAUNCH();
   } else {
     for (int d = 0; d < s->da.ng; d++)
@@ -666,7 +726,7 @@ static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
   gn_fact_launch(s->NR, s->KC, update, s->tmW, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
   FL_CHECK_LAUNCH();
   if (s->da.ng > 0) {
-    k_gnmf_dim_p<<<dim3(s->grid_p, s->da.ng), 256, s->smem_p, st>>>(s->da);
+    gn_dim_p_launch(s->R, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da);
     FL_CHECK_LAUNCH();
   }
   k_gnmf_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc,
@@ -819,7 +879,8 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.Gd[d] = const_cast<float*>(fa.Gd[d]);
     da.Z[d] = fa.Z[d];
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 512), 64));
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 256),
+                                                               (int64_t)t->sm_count * 2));
     da.nblk[d] = nb;
     s->grid_p = std::max(s->grid_p, nb);
     max_cols = std::max(max_cols, g.cols);
@@ -834,18 +895,30 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
       po += (size_t)da.nblk[d] * R * t->g[d].cols;
     }
   }
-  s->smem_g = (size_t)R * max_cols * 4;
-  s->grid_g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows * R, 256),
-                                                          (int64_t)t->sm_count * 8));
-  s->smem_p = (size_t)GND_ROWS * R * 8 + (size_t)R * max_cols * 8 + (size_t)GND_ROWS * max_cols * 4;
+  int max_pitch = 4;
+  for (auto& g : t->g) max_pitch = std::max(max_pitch, g.pitch);
+  s->smem_g = (size_t)max_pitch * R * 4;
+  s->grid_g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows, 256),
+                                                          (int64_t)t->sm_count * 4));
+  s->smem_p = 0;   // static tiles
+  for (auto& g : t->g)
+    if (g.cols > 256 || g.cols * R / 8 > 512) {
+      set_error("fused GNMF: dimension source with %d columns is too wide", g.cols);
+      return FL_ERR_OP;
+    }
   if (s->smem_p > 200 * 1024) {
     set_error("fused GNMF: dimension source too wide");
     return FL_ERR_OP;
   }
-  FL_CUDA(cudaFuncSetAttribute(k_gnmf_dim_g, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)std::max<size_t>(s->smem_g, 16)));
-  FL_CUDA(cudaFuncSetAttribute(k_gnmf_dim_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->smem_p));
+  {
+    const void* fg = R == 8 ? (const void*)k_gnmf_dim_g<8> : R == 16 ? (const void*)k_gnmf_dim_g<16>
+                                                                    : (const void*)k_gnmf_dim_g<32>;
+    const void* fp = R == 8 ? (const void*)k_gnmf_dim_p<8> : R == 16 ? (const void*)k_gnmf_dim_p<16>
+                                                                    : (const void*)k_gnmf_dim_p<32>;
+    FL_CUDA(cudaFuncSetAttribute(fg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(s->smem_g, 16)));
+    (void)fp;
+  }
   {
     std::vector<RedDesc> dv;
     const int fst = R * SC + R * R;
@@ -948,7 +1021,7 @@ int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream)
     if (rc) return rc;
     FL_CUDA(cudaEventRecord(ev[1], st));
     if (s->da.ng > 0) {
-      k_gnmf_dim_g<<<dim3(s->grid_g, s->da.ng), 256, s->smem_g, st>>>(s->da);
+      gn_dim_g_launch(s->R, dim3(s->grid_g, s->da.ng), s->smem_g, st, s->da);
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[2], st));
@@ -956,7 +1029,7 @@ int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream)
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaEventRecord(ev[3], st));
     if (s->da.ng > 0) {
-      k_gnmf_dim_p<<<dim3(s->grid_p, s->da.ng), 256, s->smem_p, st>>>(s->da);
+      gn_dim_p_launch(s->R, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da);
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[4], st));

@@ -97,38 +97,58 @@ struct KmUpdateArgs {
 // ---------------------------------------------------------------------------
 // K1: E_d and counter reset
 // ---------------------------------------------------------------------------
+// thread per dimension row; the centroid slice sits transposed in smem
+// ([column][cluster]) so every row step is one broadcast LDS.128 per 4 clusters
+template <int KP>
 __global__ void __launch_bounds__(256) k_km_dim_e(KmDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng) return;
-  const int KP = a.KP;
+  const int k = a.k;
   const int64_t rows = a.rows[d];
   const int cols = a.cols[d], pitch = a.pitch[d];
-  extern __shared__ float cs[];  // KP x cols centroid slice
-  for (int i = threadIdx.x; i < KP * cols; i += blockDim.x) {
-    int j = i / cols, c = i - j * cols;
-    cs[i] = j < a.k ? a.C32[(int64_t)j * a.c_T + a.tcol[d][c]] : 0.f;
+  extern __shared__ __align__(16) float sm_e[];   // pitch x KP (transposed slice)
+  for (int i = threadIdx.x; i < pitch * KP; i += blockDim.x) {
+    const int c = i / KP, j = i - c * KP;
+    sm_e[i] = (j < k && c < cols) ? a.C32[(int64_t)j * a.c_T + a.tcol[d][c]] : 0.f;
   }
   __syncthreads();
-  const int64_t total = (rows + 1) * KP;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / KP;
-    const int j = (int)(idx - r * KP);
-    float e = 0.f;
-    if (j < a.k) {
-      const float* srow = a.S[d] + r * pitch;
-      const float* crow = cs + j * cols;
-      if (r < rows) {
-        for (int c = 0; c < cols; c++) {
-          float df = srow[c] - crow[c];
-          e = fmaf(df, df, e);
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row <= rows;
+       row += (int64_t)gridDim.x * blockDim.x) {   // row == rows: the "no match" row
+    float acc[KP];
+#pragma unroll
+    for (int j = 0; j < KP; j++) acc[j] = 0.f;
+    const float4* sr = reinterpret_cast<const float4*>(a.S[d] + row * pitch);
+    for (int c4 = 0; c4 < pitch / 4; c4++) {
+      const float4 v = row < rows ? sr[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const float4* cr = reinterpret_cast<const float4*>(sm_e + (c4 * 4 + e) * KP);
+#pragma unroll
+        for (int q = 0; q < KP / 4; q++) {
+          const float4 cc = cr[q];
+          const float d0 = vv[e] - cc.x, d1 = vv[e] - cc.y, d2 = vv[e] - cc.z, d3 = vv[e] - cc.w;
+          acc[q * 4 + 0] = fmaf(d0, d0, acc[q * 4 + 0]);
+          acc[q * 4 + 1] = fmaf(d1, d1, acc[q * 4 + 1]);
+          acc[q * 4 + 2] = fmaf(d2, d2, acc[q * 4 + 2]);
+          acc[q * 4 + 3] = fmaf(d3, d3, acc[q * 4 + 3]);
         }
-      } else {
-        for (int c = 0; c < cols; c++) e = fmaf(crow[c], crow[c], e);
       }
     }
-    a.E[d][idx] = e;
-    if (r < rows) a.cnt[d][idx] = 0;
+    // pitch padding columns hold S = 0 and C = 0: they add nothing; clusters
+    // past k are zeroed so the screen never sees garbage
+    float4* er = reinterpret_cast<float4*>(a.E[d] + row * KP);
+    int4* cr = reinterpret_cast<int4*>(a.cnt[d] + row * KP);
+#pragma unroll
+    for (int q = 0; q < KP / 4; q++) {
+      float4 o;
+      o.x = q * 4 + 0 < k ? acc[q * 4 + 0] : 0.f;
+      o.y = q * 4 + 1 < k ? acc[q * 4 + 1] : 0.f;
+      o.z = q * 4 + 2 < k ? acc[q * 4 + 2] : 0.f;
+      o.w = q * 4 + 3 < k ? acc[q * 4 + 3] : 0.f;
+      er[q] = o;
+      if (row < rows) cr[q] = make_int4(0, 0, 0, 0);
+    }
   }
 }
 
@@ -148,7 +168,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   __shared__ uint64_t bar[KM_WARPS][4];
   __shared__ double lsum[KM_WARPS];
 
-  uint2* bfrag = reinterpret_cast<uint2*>(smem);                       // KC*NT*32
+  uint4* bfrag = reinterpret_cast<uint4*>(smem);                       // KC*NT*32 (hi, lo)
   float* cf = reinterpret_cast<float*>(bfrag + KC * NT * 32);          // KP x CFP
   float* cn = cf + KP * CFP;                                           // KP (+4)
   double* acc64 = reinterpret_cast<double*>(cn + KP + 4);              // warps x MT*16*SC
@@ -158,7 +178,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int pf = a.pf, k = a.k;
+  const int pf = a.pf, k = a.k, pf4 = a.pf / 4;
 
   // centroid fact slice (zero past pf and past k), tf32 B fragments, norms
   for (int i = threadIdx.x; i < KP * CFP; i += blockDim.x) {
@@ -182,8 +202,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     int l = i & 31, kn = i >> 5;
     int kc = kn / NT, n = kn - kc * NT;
     int gg = l >> 2, tt = l & 3;
-    bfrag[i] = make_uint2(tf32_bits(cf[(n * 8 + gg) * CFP + kc * 8 + tt]),
-                          tf32_bits(cf[(n * 8 + gg) * CFP + kc * 8 + tt + 4]));
+    const Split b0 = split_tf32(cf[(n * 8 + gg) * CFP + kc * 8 + tt]);
+    const Split b1 = split_tf32(cf[(n * 8 + gg) * CFP + kc * 8 + tt + 4]);
+    bfrag[i] = make_uint4(b0.hi, b1.hi, b0.lo, b1.lo);
   }
   for (int j = threadIdx.x; j < KP; j += blockDim.x) {
     float s = 0.f;
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   const int64_t cnt = base + (gw < rem ? 1 : 0);
   const bool has_sort = a.sort_g >= 0;
   constexpr uint32_t F_BYTES = 32u * FP * 4u;
-  const uint32_t tx = F_BYTES + (has_sort ? 128u : 0u);
+  const uint32_t tx = F_BYTES + 128u * a.ng;   // F tile + every source's 32 FKs
   char* wsm = stages + (size_t)warp * a.nst * a.stage_bytes;
   float* zs = zs_all + warp * 32 * ZP;
   uint64_t* wbar = bar[warp];
@@ -210,7 +231,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
     tma_load_2d(st, &tmF, 0, (int)(unit * 32), &wbar[s]);
-    if (has_sort) bulk_g2s(st + F_BYTES, a.fk[a.sort_g] + unit * 32, 128, &wbar[s]);
+    for (int d = 0; d < a.ng; d++) bulk_g2s(st + F_BYTES + 128 * d, a.fk[d] + unit * 32, 128, &wbar[s]);
   };
   if (lane == 0)
     for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
@@ -242,16 +263,36 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     lacc = 0.f;
   };
 
-  for (int64_t i = 0; i < cnt; i++) {
-    const int s = (int)(i % a.nst);
-    mbar_wait(&wbar[s], (uint32_t)((i / a.nst) & 1));
+  int s = 0;            // stage slot and its mbarrier phase
+  uint32_t ph = 0;
+  for (int64_t i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0)) {
+    mbar_wait(&wbar[s], ph);
     float* Fs = reinterpret_cast<float*>(wsm + (size_t)s * a.stage_bytes);
     const int32_t* fks_s = reinterpret_cast<const int32_t*>(wsm + (size_t)s * a.stage_bytes + F_BYTES);
     const int64_t p0 = (u0 + i) * 32;
     const bool valid = p0 + lane < a.r_T;
+    // E terms of every cluster: sum_d E_d[fk_d, j] (kept apart for the loss);
+    // issued first so the L2 latency overlaps the tensor-core screen
+    float eacc[KP];
+#pragma unroll
+    for (int j = 0; j < KP; j++) eacc[j] = 0.f;
+#pragma unroll
+    for (int d = 0; d < MAX_GATHER; d++) {
+      if (d >= a.ng) break;
+      const int f = fks_s[d * 32 + lane];
+      const float4* er = reinterpret_cast<const float4*>(a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP);
+#pragma unroll
+      for (int q = 0; q < KP / 4; q++) {
+        const float4 ev = er[q];
+        eacc[q * 4 + 0] += ev.x;
+        eacc[q * 4 + 1] += ev.y;
+        eacc[q * 4 + 2] += ev.z;
+        eacc[q * 4 + 3] += ev.w;
+      }
+    }
 
-    // ---- screen: z = F C_F^T on the tensor cores (1xTF32, operands straight
-    // from the TMA tile via ldmatrix)
+    // ---- screen: z = F C_F^T on the tensor cores (3xTF32, A fragments
+    // straight from the TMA tile via ldmatrix)
     float z[2][NT][4];
 #pragma unroll
     for (int m = 0; m < 2; m++)
@@ -261,15 +302,24 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         for (int e = 0; e < 4; e++) z[m][n][e] = 0.f;
 #pragma unroll
     for (int kc = 0; kc < KC; kc++) {
-      uint2 bf[NT];
+      uint4 bf[NT];
 #pragma unroll
       for (int n = 0; n < NT; n++) bf[n] = bfrag[(kc * NT + n) * 32 + lane];
 #pragma unroll
       for (int m = 0; m < 2; m++) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(a0, a1, a2, a3, Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
+        uint32_t x[4], xh[4], xl[4];
+        ldsm_x4(x[0], x[1], x[2], x[3], Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
 #pragma unroll
-        for (int n = 0; n < NT; n++) mma_tf32(z[m][n], a0, a1, a2, a3, bf[n].x, bf[n].y);
+        for (int e = 0; e < 4; e++) {
+          xh[e] = x[e] & 0xffffe000u;
+          xl[e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(xh[e]));
+        }
+#pragma unroll
+        for (int n = 0; n < NT; n++) {
+          mma_tf32(z[m][n], xh[0], xh[1], xh[2], xh[3], bf[n].x, bf[n].y);
+          mma_tf32(z[m][n], xl[0], xl[1], xl[2], xl[3], bf[n].x, bf[n].y);
+          mma_tf32(z[m][n], xh[0], xh[1], xh[2], xh[3], bf[n].z, bf[n].w);
+        }
       }
     }
     // transpose to lane-per-row through the warp's smem scratch
@@ -288,53 +338,39 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     float dv[KP];
 #pragma unroll
     for (int q = 0; q < KP / 4; q++) {
-      float4 zz = *reinterpret_cast<const float4*>(zs + lane * ZP + q * 4);
-      dv[q * 4 + 0] = fmaf(-2.f, zz.x, cn[q * 4 + 0]);
-      dv[q * 4 + 1] = fmaf(-2.f, zz.y, cn[q * 4 + 1]);
-      dv[q * 4 + 2] = fmaf(-2.f, zz.z, cn[q * 4 + 2]);
-      dv[q * 4 + 3] = fmaf(-2.f, zz.w, cn[q * 4 + 3]);
-    }
-    int fkl[MAX_GATHER];
-#pragma unroll
-    for (int d = 0; d < MAX_GATHER; d++) {
-      if (d >= a.ng) break;
-      const int f = (d == a.sort_g) ? fks_s[lane] : a.fk[d][p0 + lane];
-      fkl[d] = f;
-      const float4* er = reinterpret_cast<const float4*>(a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP);
-#pragma unroll
-      for (int q = 0; q < KP / 4; q++) {
-        float4 ev = er[q];
-        dv[q * 4 + 0] += ev.x;
-        dv[q * 4 + 1] += ev.y;
-        dv[q * 4 + 2] += ev.z;
-        dv[q * 4 + 3] += ev.w;
-      }
+      const float4 zz = *reinterpret_cast<const float4*>(zs + lane * ZP + q * 4);
+      dv[q * 4 + 0] = fmaf(-2.f, zz.x, cn[q * 4 + 0]) + eacc[q * 4 + 0];
+      dv[q * 4 + 1] = fmaf(-2.f, zz.y, cn[q * 4 + 1]) + eacc[q * 4 + 1];
+      dv[q * 4 + 2] = fmaf(-2.f, zz.z, cn[q * 4 + 2]) + eacc[q * 4 + 2];
+      dv[q * 4 + 3] = fmaf(-2.f, zz.w, cn[q * 4 + 3]) + eacc[q * 4 + 3];
     }
     // best / runner-up (ties -> lowest index)
-    float v1 = dv[0];
+    float v1 = dv[0], v2 = kInf;
     int al = 0;
 #pragma unroll
-    for (int j = 1; j < KP; j++)
-      if (dv[j] < v1) {
-        v1 = dv[j];
-        al = j;
-      }
-    float v2 = kInf;
-#pragma unroll
-    for (int j = 0; j < KP; j++)
-      if (j != al) v2 = fminf(v2, dv[j]);
+    for (int j = 1; j < KP; j++) {
+      const bool lt = dv[j] < v1;
+      v2 = lt ? v1 : fminf(v2, dv[j]);
+      al = lt ? j : al;
+      v1 = lt ? dv[j] : v1;
+    }
+    // F row in registers
     const float4* fr = reinterpret_cast<const float4*>(Fs + lane * FP);
+    float4 xr[2 * KC];
+#pragma unroll
+    for (int c4 = 0; c4 < 2 * KC; c4++) xr[c4] = c4 < pf4 ? fr[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
     // ---- certify: keep the screened winner unless the runner-up lies within
-    // the screen's error bound; near-ties are re-decided from direct fp32
-    // differences (the reference orders them in fp64)
+    // the 3xTF32 screen's error bound; near-ties are re-decided from direct
+    // fp32 differences (the reference orders them in fp64)
+    float el = 0.f;
     if (valid) {
       float xn = 0.f;
-      for (int c4 = 0; c4 < pf / 4; c4++) {
-        float4 x = fr[c4];
-        xn = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, xn))));
-      }
+#pragma unroll
+      for (int c4 = 0; c4 < 2 * KC; c4++)
+        xn = fmaf(xr[c4].x, xr[c4].x, fmaf(xr[c4].y, xr[c4].y,
+             fmaf(xr[c4].z, xr[c4].z, fmaf(xr[c4].w, xr[c4].w, xn))));
       // v2 is +inf when k == 1: keep the bound finite
-      const float tol = 3.2e-3f * (xn + cn_max) + 2e-5f * (fabsf(v1) + fminf(fabsf(v2), 3e38f));
+      const float tol = 1e-5f * (xn + cn_max) + 1e-5f * (fabsf(v1) + fminf(fabsf(v2), 3e38f));
       if (!(v2 - v1 > tol)) {
         uint32_t cand = 0;   // clusters that can still win
 #pragma unroll
@@ -347,16 +383,17 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
           cand &= cand - 1;
           const float4* cr = reinterpret_cast<const float4*>(cf + j * CFP);
           float dj = 0.f;
-          for (int c4 = 0; c4 < pf / 4; c4++) {
-            float4 x = fr[c4], c = cr[c4];
-            float d0 = x.x - c.x, d1 = x.y - c.y, d2 = x.z - c.z, d3 = x.w - c.w;
+#pragma unroll
+          for (int c4 = 0; c4 < 2 * KC; c4++) {
+            const float4 c = cr[c4];
+            const float d0 = xr[c4].x - c.x, d1 = xr[c4].y - c.y;
+            const float d2 = xr[c4].z - c.z, d3 = xr[c4].w - c.w;
             dj = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, dj))));
           }
+          float ej = 0.f;
 #pragma unroll
-          for (int d = 0; d < MAX_GATHER; d++) {
-            if (d >= a.ng) break;
-            dj += a.E[d][(fkl[d] >= 0 ? (int64_t)fkl[d] : a.rows[d]) * KP + j];
-          }
+          for (int jj = 0; jj < KP; jj++) ej = jj == j ? eacc[jj] : ej;
+          dj += ej;
           if (dj < bd) {
             bd = dj;
             bj = j;
@@ -364,16 +401,20 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         }
         al = bj;
       }
+#pragma unroll
+      for (int jj = 0; jj < KP; jj++) el = jj == al ? eacc[jj] : el;
     } else {
       al = -1;
     }
     // ---- loss (direct differences), I_d^T A counters, assignments
     if (valid) {
       const float4* cr = reinterpret_cast<const float4*>(cf + al * CFP);
-      float l = 0.f;
-      for (int c4 = 0; c4 < pf / 4; c4++) {
-        float4 x = fr[c4], c = cr[c4];
-        float d0 = x.x - c.x, d1 = x.y - c.y, d2 = x.z - c.z, d3 = x.w - c.w;
+      float l = el;
+#pragma unroll
+      for (int c4 = 0; c4 < 2 * KC; c4++) {
+        const float4 c = cr[c4];
+        const float d0 = xr[c4].x - c.x, d1 = xr[c4].y - c.y;
+        const float d2 = xr[c4].z - c.z, d3 = xr[c4].w - c.w;
         l = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, l))));
       }
       lacc += l;
@@ -381,11 +422,14 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
 #pragma unroll
     for (int d = 0; d < MAX_GATHER; d++) {
       if (d >= a.ng) break;
-      const int f = fkl[d];
-      if (valid) lacc += a.E[d][(f >= 0 ? (int64_t)f : a.rows[d]) * KP + al];
+      const int f = fks_s[d * 32 + lane];
       const int key = (valid && f >= 0) ? f * KP + al : -1 - lane;
-      const unsigned mask = __match_any_sync(0xffffffffu, key);
-      if (key >= 0 && (__ffs(mask) - 1) == lane) atomicAdd(&a.cnt[d][key], __popc(mask));
+      if (d == a.sort_g) {   // sorted FKs: runs of equal keys, one atomic per run
+        const unsigned mask = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && (__ffs(mask) - 1) == lane) atomicAdd(&a.cnt[d][key], __popc(mask));
+      } else if (key >= 0) {
+        atomicAdd(&a.cnt[d][key], 1);
+      }
     }
     if (a.assign && valid) a.assign[p0 + lane] = al;
     // ---- sums_F | counts = one-hot^T [F | 1]: 2-term tf32 split of F (hi =
@@ -460,44 +504,66 @@ __device__ void km_apply_update(const KmUpdateArgs& u) {
   if (tid == 0) u.state->it = it + 1;
 }
 
-constexpr int KMD_ROWS = 32;
-
+// sums_d[j, c] = sum_r cnt_d[r, j] S_d[r, c]: 32-row tiles of S and of the
+// counters (converted to fp32 once) in smem; thread = (column, 8 clusters);
+// fp32 within a tile, fp64 across tiles
+template <int KP>
 __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
-  extern __shared__ __align__(16) char smem_d[];
   const int d = blockIdx.y;
-  const bool active = d < a.ng && (int)blockIdx.x < a.nblk[d];
-  if (!active) return;
-  {
-    const int KP = a.KP, cols = a.cols[d], pitch = a.pitch[d];
-    const int64_t rows = a.rows[d];
-    const int nb = a.nblk[d];
-    const int64_t rpb = ceil_div(ceil_div(rows, nb), KMD_ROWS) * KMD_ROWS;
-    const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
-    float* ss = reinterpret_cast<float*>(smem_d);            // KMD_ROWS x cols
-    float* cs = ss + KMD_ROWS * cols;                          // KMD_ROWS x KP
-    double* acc = reinterpret_cast<double*>(cs + KMD_ROWS * KP + 2);  // KP x cols
-    const int npair = KP * cols;
-    for (int i = threadIdx.x; i < npair; i += blockDim.x) acc[i] = 0.0;
-    for (int64_t rb = r0; rb < r1; rb += KMD_ROWS) {
-      const int nr = (int)min64(KMD_ROWS, r1 - rb);
-      __syncthreads();
-      for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
-        int r = i / cols, c = i - r * cols;
-        ss[i] = a.S[d][(rb + r) * pitch + c];
-      }
-      for (int i = threadIdx.x; i < nr * KP; i += blockDim.x)
-        cs[i] = (float)a.cnt[d][rb * KP + i];
-      __syncthreads();
-      for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
-        int j = pr / cols, c = pr - j * cols;
-        double sd = 0.0;
-        for (int r = 0; r < nr; r++) sd = fma((double)cs[r * KP + j], (double)ss[r * cols + c], sd);
-        acc[pr] += sd;
-      }
-    }
+  if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
+  constexpr int JB = 8, NJB = KP / JB;
+  __shared__ float ss[32 * 257];
+  __shared__ __align__(16) float cs[32 * KP];
+  const int cols = a.cols[d], pitch = a.pitch[d];
+  const int64_t rows = a.rows[d];
+  const int nb = a.nblk[d];
+  const int64_t rpb = ceil_div(ceil_div(rows, nb), 32) * 32;
+  const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
+  const int nwork = cols * NJB;
+  double acc64[2][JB];
+#pragma unroll
+  for (int u = 0; u < 2; u++)
+#pragma unroll
+    for (int j = 0; j < JB; j++) acc64[u][j] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    const int nr = (int)min64(32, r1 - rb);
     __syncthreads();
-    for (int i = threadIdx.x; i < npair; i += blockDim.x)
-      a.part[d][(int64_t)blockIdx.x * npair + i] = acc[i];
+    for (int i = threadIdx.x; i < 32 * cols; i += blockDim.x) {
+      const int r = i / cols, c = i - r * cols;
+      ss[r * 257 + c] = r < nr ? a.S[d][(rb + r) * pitch + c] : 0.f;
+    }
+    for (int i = threadIdx.x; i < 32 * KP; i += blockDim.x)
+      cs[i] = i < nr * KP ? (float)a.cnt[d][rb * KP + i] : 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int w = threadIdx.x + u * 256;
+      if (w >= nwork) break;
+      const int c = w % cols, jb = w / cols;
+      float acc[JB];
+#pragma unroll
+      for (int j = 0; j < JB; j++) acc[j] = 0.f;
+      for (int r = 0; r < 32; r++) {
+        const float v = ss[r * 257 + c];
+        const float4 c0 = *reinterpret_cast<const float4*>(cs + r * KP + jb * JB);
+        const float4 c1 = *reinterpret_cast<const float4*>(cs + r * KP + jb * JB + 4);
+        acc[0] = fmaf(c0.x, v, acc[0]); acc[1] = fmaf(c0.y, v, acc[1]);
+        acc[2] = fmaf(c0.z, v, acc[2]); acc[3] = fmaf(c0.w, v, acc[3]);
+        acc[4] = fmaf(c1.x, v, acc[4]); acc[5] = fmaf(c1.y, v, acc[5]);
+        acc[6] = fmaf(c1.z, v, acc[6]); acc[7] = fmaf(c1.w, v, acc[7]);
+      }
+#pragma unroll
+      for (int j = 0; j < JB; j++) acc64[u][j] += (double)acc[j];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    const int w = threadIdx.x + u * 256;
+    if (w >= nwork) break;
+    const int c = w % cols, jb = w / cols;
+#pragma unroll
+    for (int j = 0; j < JB; j++)
+      a.part[d][(int64_t)blockIdx.x * KP * cols + (jb * JB + j) * cols + c] = acc64[u][j];
   }
 }
 
@@ -515,6 +581,17 @@ __global__ void k_km_assign_to_target(const int32_t* __restrict__ a_dev,
                                       int32_t* __restrict__ out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < r_T) out[perm[p]] = a_dev[p];
+}
+
+static void km_dim_e_launch(int KP, dim3 g, size_t smem, cudaStream_t st, const KmDimArgs& a) {
+  if (KP == 8) k_km_dim_e<8><<<g, 256, smem, st>>>(a);
+  else if (KP == 16) k_km_dim_e<16><<<g, 256, smem, st>>>(a);
+  else k_km_dim_e<32><<<g, 256, smem, st>>>(a);
+}
+static void km_dim_sums_launch(int KP, dim3 g, size_t smem, cudaStream_t st, const KmDimArgs& a) {
+  if (KP == 8) k_km_dim_sums<8><<<g, 256, smem, st>>>(a);
+  else if (KP == 16) k_km_dim_sums<16><<<g, 256, smem, st>>>(a);
+  else k_km_dim_sums<32><<<g, 256, smem, st>>>(a);
 }
 
 // instantiation table: NT in {1,2,4} (k <= 8/16/32), KC in {1,2,3,4,6,8,12,16}
@@ -568,7 +645,7 @@ static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
                                bool write_assign) {
   if (s->da.ng > 0) {
     dim3 ge(s->grid_e, s->da.ng);
-    k_km_dim_e<<<ge, 256, s->smem_e, st>>>(s->da);
+    km_dim_e_launch(s->KP, ge, s->smem_e, st, s->da);
     FL_CHECK_LAUNCH();
   }
   KmFactArgs fa = s->fa;
@@ -576,7 +653,7 @@ static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
   km_fact_launch(s->NT, s->KC, s->tmF, fa, s->nblk_fact, s->smem_fact, st);
   FL_CHECK_LAUNCH();
   if (s->da.ng > 0) {
-    k_km_dim_sums<<<dim3(s->grid_sum, s->da.ng), 256, s->smem_sum, st>>>(s->da);
+    km_dim_sums_launch(s->KP, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da);
     FL_CHECK_LAUNCH();
   }
   k_km_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc, s->ua,
@@ -691,11 +768,11 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   fa.f_tcol = t->d_f_tcol->as<int32_t>();
   fa.assign = nullptr;
   const int FP = SC + 4, ZP = KP + 4;
-  fa.stage_bytes = (uint32_t)round_up(32 * FP * 4 + 128, 128);
+  fa.stage_bytes = (uint32_t)round_up(32 * FP * 4 + 128 * ng, 128);
   if ((rc = make_tmap_2d(&s->tmF, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
                          (uint64_t)t->pf * 4, 32, (uint32_t)FP, 0)))
     return rc;
-  const size_t fixed = (size_t)KC * NT * 32 * 8 + (size_t)KP * (SC + 4) * 4 + (KP + 4) * 4 +
+  const size_t fixed = (size_t)KC * NT * 32 * 16 + (size_t)KP * (SC + 4) * 4 + (KP + 4) * 4 +
                        (size_t)KM_WARPS * MT * 16 * SC * 8 + (size_t)KM_WARPS * 32 * ZP * 4;
   const size_t fixed_al = round_up((int64_t)fixed, 128);
   // two CTAs (16 warps) per SM when the tile fits in half the shared memory
@@ -759,19 +836,31 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
       po += (size_t)da.nblk[d] * KP * t->g[d].cols;
     }
   }
-  s->smem_e = (size_t)KP * max_cols * 4;
-  s->grid_e = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows * KP, 256),
-                                                          (int64_t)t->sm_count * 8));
-  s->smem_sum = (size_t)KMD_ROWS * max_cols * 4 + (size_t)KMD_ROWS * KP * 4 + 16 +
-                (size_t)KP * max_cols * 8;
+  int max_pitch = 4;
+  for (auto& g : t->g) max_pitch = std::max(max_pitch, g.pitch);
+  s->smem_e = (size_t)max_pitch * KP * 4;
+  s->grid_e = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows + 1, 256),
+                                                          (int64_t)t->sm_count * 4));
+  s->smem_sum = 0;   // static tiles
+  for (auto& g : t->g)
+    if (g.cols > 256 || g.cols * KP / 8 > 512) {
+      set_error("fused K-means: dimension source with %d columns is too wide", g.cols);
+      return FL_ERR_OP;
+    }
   if (s->smem_e > 200 * 1024 || s->smem_sum > 200 * 1024) {
     set_error("fused K-means: dimension source too wide");
     return FL_ERR_OP;
   }
-  FL_CUDA(cudaFuncSetAttribute(k_km_dim_e, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)std::max<size_t>(s->smem_e, 16)));
-  FL_CUDA(cudaFuncSetAttribute(k_km_dim_sums, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->smem_sum));
+  {
+    const void* fe = KP == 8 ? (const void*)k_km_dim_e<8> : KP == 16 ? (const void*)k_km_dim_e<16>
+                                                                     : (const void*)k_km_dim_e<32>;
+    const void* fs = KP == 8 ? (const void*)k_km_dim_sums<8>
+                             : KP == 16 ? (const void*)k_km_dim_sums<16> : (const void*)k_km_dim_sums<32>;
+    FL_CUDA(cudaFuncSetAttribute(fe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(s->smem_e, 16)));
+    FL_CUDA(cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)s->smem_sum));
+  }
 
   KmUpdateArgs& ua = s->ua;
   ua.c_T = c_T;
@@ -868,7 +957,7 @@ int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* str
   for (int i = 0; i < iters; i++) {
     FL_CUDA(cudaEventRecord(ev[0], st));
     if (s->da.ng > 0) {
-      k_km_dim_e<<<dim3(s->grid_e, s->da.ng), 256, s->smem_e, st>>>(s->da);
+      km_dim_e_launch(s->KP, dim3(s->grid_e, s->da.ng), s->smem_e, st, s->da);
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[1], st));
@@ -876,7 +965,7 @@ int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* str
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaEventRecord(ev[2], st));
     if (s->da.ng > 0) {
-      k_km_dim_sums<<<dim3(s->grid_sum, s->da.ng), 256, s->smem_sum, st>>>(s->da);
+      km_dim_sums_launch(s->KP, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da);
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[3], st));
