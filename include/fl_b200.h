@@ -178,9 +178,11 @@ int fl_gnmf_destroy(fl_gnmf* s);
  * Known-answer test of the tcgen05 (5th-gen tensor core) operand layouts:
  * D[128 x N] = A[128 x K] B[K x N] (row-major host or device buffers) through
  * kind::tf32 MMAs from shared memory into TMEM.  mode 0: K-major interleave;
- * 1: MN-major interleave; 2: K-major SWIZZLE_128B A (K = 32); 3: MN-major
- * SWIZZLE_128B A and B with 32 valid A rows (N = 32). */
-int fl_tc_selftest(int32_t mode, const float* A, const float* B, float* D, int32_t K, int32_t N);
+ * 1: K-major interleave with padded K-chunk strides and 32 stored A rows;
+ * 2: K-major SWIZZLE_128B A (K = 32).  lbo_sbo: NULL, or 4 byte offsets
+ * {A LBO, A SBO, B LBO, B SBO} overriding mode 1 (-1 keeps the default). */
+int fl_tc_selftest(int32_t mode, const float* A, const float* B, float* D, int32_t K, int32_t N,
+                   const int32_t* lbo_sbo);
 
 #ifdef __cplusplus
 }

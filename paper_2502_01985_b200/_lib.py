@@ -88,7 +88,7 @@ SIGNATURES = {
     "fl_gnmf_reduce_buffer": [_P, C.POINTER(C.c_void_p), C.POINTER(_I32)],
     "fl_gnmf_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_gnmf_destroy": [_P],
-    "fl_tc_selftest": [_I32, _P, _P, _P, _I32, _I32],
+    "fl_tc_selftest": [_I32, _P, _P, _P, _I32, _I32, _P],
 }
 
 _lib = None

@@ -33,6 +33,7 @@
 #include "internal.h"
 #include "mma_tf32.cuh"
 #include "reduce.cuh"
+#include "tc05.cuh"
 
 namespace flb {
 
@@ -486,6 +487,22 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   }
 }
 
+#include "kmeans_tc.cuh"
+
+__global__ void k_km_block(const float* __restrict__ F, int pf, int64_t r_pad, int C4P,
+                           float* __restrict__ Fb) {
+  // stream block -> 128-row tiles of [chunk][row][4]
+  const int64_t n = r_pad * C4P * 4;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx / (C4P * 4);
+    const int c = (int)(idx - p * C4P * 4);
+    const int64_t t = p / KT_TILE;
+    const int r = (int)(p - t * KT_TILE);
+    Fb[((t * C4P + (c >> 2)) * KT_TILE + r) * 4 + (c & 3)] = F[p * pf + c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3: sums_d = cnt_d^T S_d, then fixed-order reduction (+ update)
 // ---------------------------------------------------------------------------
@@ -625,6 +642,13 @@ using namespace flb;
 struct fl_kmeans {
   CUtensorMap tmF;               // F as [r_pad x pf] fp32, box 32 x (8 KC + 4)
   fl_table* t = nullptr;
+  // tcgen05 path (default): blocked copy of F and kernel geometry
+  bool tc = false;
+  DevBuf Fblk;
+  KmTcArgs ta{};
+  int C4P = 0;
+  KtGeom gm{};
+  size_t smem_tc = 0;
   int k = 0, KP = 0, NT = 0, KC = 0, SC = 0;
   KmFactArgs fa{};
   KmDimArgs da{};
@@ -641,6 +665,23 @@ struct fl_kmeans {
 
 namespace flb {
 
+static int km_fact_run(fl_kmeans* s, cudaStream_t st, bool write_assign) {
+  if (s->tc) {
+    KmTcArgs ta = s->ta;
+    ta.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
+    if (s->KP == 16)
+      k_km_tc<16><<<s->nblk_fact, KT_THREADS, s->smem_tc, st>>>(ta, s->C4P, s->gm);
+    else
+      k_km_tc<32><<<s->nblk_fact, KT_THREADS, s->smem_tc, st>>>(ta, s->C4P, s->gm);
+  } else {
+    KmFactArgs fa = s->fa;
+    fa.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
+    km_fact_launch(s->NT, s->KC, s->tmF, fa, s->nblk_fact, s->smem_fact, st);
+  }
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
 static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
                                bool write_assign) {
   if (s->da.ng > 0) {
@@ -648,10 +689,8 @@ static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
     km_dim_e_launch(s->KP, ge, s->smem_e, st, s->da);
     FL_CHECK_LAUNCH();
   }
-  KmFactArgs fa = s->fa;
-  fa.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
-  km_fact_launch(s->NT, s->KC, s->tmF, fa, s->nblk_fact, s->smem_fact, st);
-  FL_CHECK_LAUNCH();
+  int rc = km_fact_run(s, st, write_assign);
+  if (rc) return rc;
   if (s->da.ng > 0) {
     km_dim_sums_launch(s->KP, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da);
     FL_CHECK_LAUNCH();
@@ -711,6 +750,17 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   s->KP = NT * 8;
   s->KC = KC;
   s->SC = KC * 8;
+  // tcgen05 variant (opt-in, FL_KM_TC=1; narrow stream blocks only): parity-
+  // green but 2.9x slower than the per-warp mma.sync pass at C3 (1.57 vs
+  // 0.54 ms, profiles/r01_kmeans_tc_vs_mma.txt): the row-contracting sums
+  // need M >= 64 tcgen05 tiles over a 24-column / 16-cluster problem and
+  // transposed operand copies, so operand fetch, not math, dominates.
+  s->C4P = t->pf / 4;
+  s->tc = (s->C4P + 1) * 4 <= 32 && getenv("FL_KM_TC") && atoi(getenv("FL_KM_TC")) != 0;
+  if (s->tc) {
+    s->KP = std::max(16, NT * 8);
+    s->SC = (s->C4P + 1) * 4;
+  }
   const int KP = s->KP, SC = s->SC, MT = (NT + 1) / 2;
   const int ng = (int)t->g.size();
   const int c_T = t->c_T;
@@ -797,8 +847,59 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   occ = std::max(1, occ);
   s->nblk_fact = (int)std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(fa.nunits, KM_WARPS), (int64_t)t->sm_count * occ));
+  if (s->tc) {
+    // blocked copy of F, smem layout, one persistent CTA per SM
+    const int C4P = s->C4P;
+    const int64_t ntiles = t->r_pad / KT_TILE;
+    if ((rc = s->Fblk.alloc((size_t)t->r_pad * C4P * 16))) return rc;
+    k_km_block<<<(unsigned)std::min<int64_t>(ceil_div(t->r_pad * C4P * 4, 256), 65535 * 8), 256,
+                 0, st>>>(t->F->as<float>(), t->pf, t->r_pad, C4P, s->Fblk.as<float>());
+    FL_CHECK_LAUNCH();
+    KtGeom& gm = s->gm;
+    gm.lbo_ft = (uint32_t)(ceil_div(SC, 8) * 128 + 16);
+    gm.lbo_oh = (uint32_t)((KP / 8) * 128 + 16);
+    gm.o_flo = (uint32_t)(C4P + 1) * 2048u;
+    gm.o_fth = gm.o_flo + (uint32_t)(C4P + 1) * 2048u;
+    const uint32_t ft_bytes = (uint32_t)round_up(32 * gm.lbo_ft + 2048, 128);
+    gm.o_ftl = gm.o_fth + ft_bytes;
+    gm.o_oht = gm.o_ftl + ft_bytes;
+    gm.o_fk = gm.o_oht + (uint32_t)round_up(32 * gm.lbo_oh, 128);
+    gm.stage = (uint32_t)round_up(gm.o_fk + 512 * std::max(ng, 1), 1024);
+    gm.off_cf = KT_NS * gm.stage;
+    const int CFP = (C4P + 1) * 4 + 4;
+    const size_t cf_bytes = (size_t)2 * (C4P + 1) * KP * 16 + (size_t)KP * CFP * 4 +
+                            (size_t)(KP + 4) * 4 + (size_t)32 * KP * 8 + 64;
+    s->smem_tc = gm.off_cf + cf_bytes + 1024;
+    if (s->smem_tc > 227 * 1024) {
+      set_error("fused K-means (tcgen05): shared memory budget exceeded (%zu bytes)", s->smem_tc);
+      return FL_ERR_OP;
+    }
+    const void* kt = KP == 16 ? (const void*)k_km_tc<16> : (const void*)k_km_tc<32>;
+    FL_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tc));
+    s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+    KmTcArgs& ta = s->ta;
+    ta.Fblk = s->Fblk.as<float>();
+    ta.pf = t->pf;
+    ta.c_T = c_T;
+    ta.k = k;
+    ta.r_T = t->r_T;
+    ta.ntiles = ntiles;
+    ta.ng = ng;
+    ta.sort_g = t->sort_g;
+    for (int d = 0; d < ng; d++) {
+      ta.fk[d] = fa.fk[d];
+      ta.E[d] = fa.E[d];
+      ta.cnt[d] = fa.cnt[d];
+      ta.rows[d] = fa.rows[d];
+    }
+    ta.C32 = s->C32.as<float>();
+    ta.f_tcol = t->d_f_tcol->as<int32_t>();
+    ta.assign = nullptr;
+    ta.SC = SC;
+  }
   if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (KP * SC + 1) * 8))) return rc;
   fa.part = s->part_fact.as<double>();
+  s->ta.part = fa.part;
 
   // ---- dimension kernels
   KmDimArgs& da = s->da;
@@ -961,8 +1062,8 @@ int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* str
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[1], st));
-    km_fact_launch(s->NT, s->KC, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
-    FL_CHECK_LAUNCH();
+    int rc = km_fact_run(s, st, false);
+    if (rc) return rc;
     FL_CUDA(cudaEventRecord(ev[2], st));
     if (s->da.ng > 0) {
       km_dim_sums_launch(s->KP, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da);

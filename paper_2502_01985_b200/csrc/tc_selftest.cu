@@ -4,10 +4,13 @@
 // tcgen05.ld.  Inputs that are exact in tf32 make the answer exact.
 //
 //   mode 0: A K-major interleave,      B K-major interleave
-//   mode 1: A MN-major interleave,     B MN-major interleave
+//   mode 1: A K-major interleave with a padded K-chunk stride and only 32
+//           stored rows (D rows >= 32 read neighbouring data and are not
+//           checked), B K-major interleave with a padded K-chunk stride --
+//           the transposed tiles of the K-means / GNMF row contractions
 //   mode 2: A K-major SWIZZLE_128B (K = 32), B K-major interleave
-//   mode 3: A MN-major SWIZZLE_128B (32 valid rows, aliased groups),
-//           B MN-major SWIZZLE_128B (N = 32)          -- the GNMF W^T W shape
+// (kind::tf32 accepts MN-major operands only in the 128B_BASE32B swizzle;
+// the kernels use K-major operands throughout.)
 #include "internal.h"
 #include "tc05.cuh"
 
@@ -15,7 +18,8 @@ namespace flb {
 
 __global__ void __launch_bounds__(128) k_tc_selftest(int mode, const float* __restrict__ A,
                                                      const float* __restrict__ B,
-                                                     float* __restrict__ D, int K, int N) {
+                                                     float* __restrict__ D, int K, int N,
+                                                     int lbo_a, int sbo_a, int lbo_b, int sbo_b) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
@@ -27,16 +31,15 @@ __global__ void __launch_bounds__(128) k_tc_selftest(int mode, const float* __re
     const int m = i / K, k = i - m * K;
     const float v = A[i];
     if (mode == 0) As[(k / 4) * 512 + m * 4 + (k & 3)] = v;
-    else if (mode == 1) As[(m / 4) * K * 4 + k * 4 + (m & 3)] = v;
-    else if (mode == 2) As[m * 32 + (((k >> 2) ^ (m & 7)) << 2) + (k & 3)] = v;
-    else if (m < 32) As[k * 32 + (((m >> 2) ^ (k & 7)) << 2) + (m & 3)] = v;   // W[k][m]
+    else if (mode == 1) {
+      if (m < 32) As[(k / 4) * 132 + (m / 8) * 32 + (m & 7) * 4 + (k & 3)] = v;   // LBO 528 B
+    } else As[m * 32 + (((k >> 2) ^ (m & 7)) << 2) + (k & 3)] = v;
   }
   for (int i = tid; i < K * N; i += blockDim.x) {
     const int k = i / N, n = i - k * N;
     const float v = B[i];
     if (mode == 0 || mode == 2) Bs[(k / 4) * N * 4 + n * 4 + (k & 3)] = v;
-    else if (mode == 1) Bs[(n / 4) * K * 4 + k * 4 + (n & 3)] = v;
-    else Bs[k * 32 + (((n >> 2) ^ (k & 7)) << 2) + (n & 3)] = v;
+    else Bs[(k / 4) * (N * 4 + 4) + (n / 8) * 32 + (n & 7) * 4 + (k & 3)] = v;   // LBO N*16+16
   }
   tc::fence_smem_to_async();
   if (tid == 0) {
@@ -51,22 +54,19 @@ __global__ void __launch_bounds__(128) k_tc_selftest(int mode, const float* __re
   const uint32_t tmem = tbase;
   if (tid == 0) {
     const uint32_t a0 = smem_u32(As), b0 = smem_u32(Bs);
-    const bool a_mn = mode == 1 || mode == 3, b_mn = mode == 1 || mode == 3;
-    const uint32_t idesc = tc::idesc_tf32(128, N, a_mn, b_mn);
+    const uint32_t idesc = tc::idesc_tf32(128, N, false, false);
     for (int kk = 0; kk < K / 8; kk++) {
       uint64_t ad, bd;
       if (mode == 0) {
         ad = tc::smem_desc(a0 + kk * 2 * 2048, 2048, 128, tc::kInterleave);
         bd = tc::smem_desc(b0 + kk * 2 * N * 16, N * 16, 128, tc::kInterleave);
       } else if (mode == 1) {
-        ad = tc::smem_desc(a0 + kk * 128, 128, K * 16, tc::kInterleave);
-        bd = tc::smem_desc(b0 + kk * 128, 128, K * 16, tc::kInterleave);
-      } else if (mode == 2) {
+        const int la = lbo_a >= 0 ? lbo_a : 528, lb = lbo_b >= 0 ? lbo_b : N * 16 + 16;
+        ad = tc::smem_desc(a0 + kk * 2 * la, la, sbo_a >= 0 ? sbo_a : 128, tc::kInterleave);
+        bd = tc::smem_desc(b0 + kk * 2 * lb, lb, sbo_b >= 0 ? sbo_b : 128, tc::kInterleave);
+      } else {
         ad = tc::smem_desc(a0 + kk * 32, 16, 1024, tc::kSw128);
         bd = tc::smem_desc(b0 + kk * 2 * N * 16, N * 16, 128, tc::kInterleave);
-      } else {
-        ad = tc::smem_desc(a0 + kk * 1024, 0, 1024, tc::kSw128);
-        bd = tc::smem_desc(b0 + kk * 1024, 0, 1024, tc::kSw128);
       }
       tc::mma_tf32(tmem, ad, bd, idesc, kk > 0);
     }
@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(128) k_tc_selftest(int mode, const float* __re
 using namespace flb;
 
 extern "C" int fl_tc_selftest(int32_t mode, const float* A, const float* B, float* D, int32_t K,
-                              int32_t N) {
-  if (mode < 0 || mode > 3 || K < 8 || K > 128 || (K & 7) || N < 16 || N > 256 || (N & 15) ||
-      (mode == 2 && K != 32) || (mode == 3 && N != 32)) {
+                              int32_t N, const int32_t* lbo_sbo) {
+  if (mode < 0 || mode > 2 || K < 8 || K > 128 || (K & 7) || N < 16 || N > 256 || (N & 15) ||
+      (mode == 2 && K != 32)) {
     set_error("fl_tc_selftest: unsupported shape (mode %d, K %d, N %d)", mode, K, N);
     return FL_ERR_ARG;
   }
@@ -104,7 +104,10 @@ extern "C" int fl_tc_selftest(int32_t mode, const float* A, const float* B, floa
   FL_CUDA(cudaMemcpy(dB, B, (size_t)K * N * 4, cudaMemcpyDefault));
   const size_t smem = 1024 + 128 * 128 * 4 + 128 * 256 * 4;
   FL_CUDA(cudaFuncSetAttribute(k_tc_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_tc_selftest<<<1, 128, smem>>>(mode, dA, dB, dD, K, N);
+  int ov[4] = {-1, -1, -1, -1};
+  if (lbo_sbo)
+    for (int i = 0; i < 4; i++) ov[i] = lbo_sbo[i];
+  k_tc_selftest<<<1, 128, smem>>>(mode, dA, dB, dD, K, N, ov[0], ov[1], ov[2], ov[3]);
   FL_CHECK_LAUNCH();
   FL_CUDA(cudaDeviceSynchronize());
   FL_CUDA(cudaMemcpy(D, dD, (size_t)128 * N * 4, cudaMemcpyDefault));

@@ -272,3 +272,16 @@ def test_gnmf_monotone_loss(fl):
     res = fl.train("gnmf", fl.TargetHandle.factorized(ft), fl.TrainConfig(iterations=15, rank=8))
     lh = np.asarray(res.loss_history)
     assert np.all(np.diff(lh) <= 1e-6 * np.abs(lh[:-1]))
+
+
+@pytest.mark.parametrize("name", ["clusters", "star", "star3"])
+def test_kmeans_tcgen05_variant_matches_reference(fl, name, monkeypatch):
+    """The opt-in tcgen05 fact pass (FL_KM_TC=1, csrc/kmeans_tc.cuh) against
+    the reference goldens."""
+    monkeypatch.setenv("FL_KM_TC", "1")
+    g = load_golden(name)
+    m = g.meta["trainers"]["kmeans"]
+    res = fl.train("kmeans", fl.TargetHandle.factorized(g.ft), _cfg(fl, m))
+    assert np.array_equal(res.parameters["assignments"], g["kmeans_assignments"])
+    assert max_rel(res.loss_history, g["kmeans_loss"]) < TOL
+    assert max_rel(res.parameters["centroids"], g["kmeans_centroids"]) < TOL
