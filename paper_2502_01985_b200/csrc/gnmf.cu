@@ -355,13 +355,16 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
             xh[e] = x[e] & 0xffffe000u;
             xl[e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(xh[e]));
           }
+          uint4 b[NR];
 #pragma unroll
-          for (int n = 0; n < NR; n++) {
-            const uint4 b = hf[(kc * NR + n) * 32 + lane];
-            mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b.x, b.y);
-            mma_tf32(q[m][n], xl[0], xl[1], xl[2], xl[3], b.x, b.y);
-            mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b.z, b.w);
-          }
+          for (int n = 0; n < NR; n++) b[n] = hf[(kc * NR + n) * 32 + lane];
+          // the three split terms as three sweeps over independent accumulators
+#pragma unroll
+          for (int n = 0; n < NR; n++) mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b[n].x, b[n].y);
+#pragma unroll
+          for (int n = 0; n < NR; n++) mma_tf32(q[m][n], xl[0], xl[1], xl[2], xl[3], b[n].x, b[n].y);
+#pragma unroll
+          for (int n = 0; n < NR; n++) mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b[n].z, b[n].w);
         }
       }
 #pragma unroll
@@ -378,13 +381,15 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
             xh[e] = x[e] & 0xffffe000u;
             xl[e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(xh[e]));
           }
+          uint4 b[NR];
 #pragma unroll
-          for (int n = 0; n < NR; n++) {
-            const uint4 b = hh[(kc * NR + n) * 32 + lane];
-            mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b.x, b.y);
-            mma_tf32(v[m][n], xl[0], xl[1], xl[2], xl[3], b.x, b.y);
-            mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b.z, b.w);
-          }
+          for (int n = 0; n < NR; n++) b[n] = hh[(kc * NR + n) * 32 + lane];
+#pragma unroll
+          for (int n = 0; n < NR; n++) mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b[n].x, b[n].y);
+#pragma unroll
+          for (int n = 0; n < NR; n++) mma_tf32(v[m][n], xl[0], xl[1], xl[2], xl[3], b[n].x, b[n].y);
+#pragma unroll
+          for (int n = 0; n < NR; n++) mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b[n].z, b[n].w);
         }
       }
       // ---- gathers of the dimension products G_d[fk]

@@ -81,46 +81,64 @@ struct YView {
 
 // Per-block partial of A^T Y over a contiguous row range, A = row-major
 // (pitch) fp32 rows; Y rows either from a device-ordered fp64 buffer (bins)
-// or from the strided target-order view through perm.  Partials are fp64:
-// part[block][j * cy + col].
+// or from the strided target-order view through perm.  Rows are staged in
+// 128-row chunks; each (a, y-column) pair is split over up to 8 row groups
+// (fp32 within a chunk, fp64 across chunks, groups combined in a fixed
+// order), so narrow outputs still use the whole CTA.  part[block][a*cy + c].
+constexpr int TM_RC = 128;
+constexpr int TM_AC = 40;    // A columns per pass
+constexpr int TM_YC = 16;    // y columns per pass
 template <bool BINS>
-__global__ void k_tmm_partial(const float* __restrict__ A, int pitch, int acols, int64_t rows,
-                              YView yv, const int32_t* __restrict__ perm,
-                              const double* __restrict__ bins, int cy, int64_t rows_per_block,
-                              double* __restrict__ part) {
+__global__ void __launch_bounds__(256) k_tmm_partial(const float* __restrict__ A, int pitch,
+                                                     int acols, int64_t rows, YView yv,
+                                                     const int32_t* __restrict__ perm,
+                                                     const double* __restrict__ bins, int cy,
+                                                     int64_t rows_per_block,
+                                                     double* __restrict__ part) {
   extern __shared__ double acc[];  // acols * cy
-  constexpr int RC = 32;
-  __shared__ float as_[RC * 80];
-  __shared__ double ys[RC * 32];
+  __shared__ float as_[TM_RC * (TM_AC + 1)];
+  __shared__ float ys[TM_RC * (TM_YC + 1)];
+  __shared__ float gsum[256];
   const int npair = acols * cy;
   for (int i = threadIdx.x; i < npair; i += blockDim.x) acc[i] = 0.0;
-  int64_t r0 = blockIdx.x * rows_per_block;
-  int64_t r1 = min(rows, r0 + rows_per_block);
-  // process in chunks of RC rows; columns of A in chunks of 80, y cols in chunks of 32
-  for (int64_t rb = r0; rb < r1; rb += RC) {
-    int nr = (int)min64(RC, r1 - rb);
-    for (int a0 = 0; a0 < acols; a0 += 80) {
-      int na = min(80, acols - a0);
-      for (int y0 = 0; y0 < cy; y0 += 32) {
-        int ny = min(32, cy - y0);
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  for (int64_t rb = r0; rb < r1; rb += TM_RC) {
+    const int nr = (int)min64(TM_RC, r1 - rb);
+    for (int a0 = 0; a0 < acols; a0 += TM_AC) {
+      const int na = min(TM_AC, acols - a0);
+      for (int y0 = 0; y0 < cy; y0 += TM_YC) {
+        const int ny = min(TM_YC, cy - y0);
         __syncthreads();
         for (int i = threadIdx.x; i < nr * na; i += blockDim.x) {
-          int r = i / na, c = i - r * na;
-          as_[r * 80 + c] = A[(rb + r) * pitch + a0 + c];
+          const int r = i / na, c = i - r * na;
+          as_[r * (TM_AC + 1) + c] = A[(rb + r) * pitch + a0 + c];
         }
         for (int i = threadIdx.x; i < nr * ny; i += blockDim.x) {
-          int r = i / ny, c = i - r * ny;
-          double v;
-          if (BINS) v = bins[(rb + r) * cy + y0 + c];
-          else v = (double)yv.at(perm[rb + r], y0 + c);
-          ys[r * 32 + c] = v;
+          const int r = i / ny, c = i - r * ny;
+          float v;
+          if (BINS) v = (float)bins[(rb + r) * cy + y0 + c];
+          else v = yv.at(perm[rb + r], y0 + c);
+          ys[r * (TM_YC + 1) + c] = v;
         }
         __syncthreads();
-        for (int pr = threadIdx.x; pr < na * ny; pr += blockDim.x) {
-          int a = pr / ny, c = pr - a * ny;
-          double s = 0.0;
-          for (int r = 0; r < nr; r++) s = fma((double)as_[r * 80 + a], ys[r * 32 + c], s);
-          acc[(a0 + a) * cy + y0 + c] += s;
+        const int np = na * ny;
+        const int G = max(1, min(8, (int)blockDim.x / np));
+        const int pr = threadIdx.x % np, grp = threadIdx.x / np;
+        float sf = 0.f;
+        if (grp < G) {
+          const int a = pr / ny, c = pr - a * ny;
+          for (int r = grp; r < nr; r += G)
+            sf = fmaf(as_[r * (TM_AC + 1) + a], ys[r * (TM_YC + 1) + c], sf);
+        }
+        __syncthreads();
+        if (grp < G && threadIdx.x < np * G) gsum[threadIdx.x] = sf;
+        __syncthreads();
+        for (int q = threadIdx.x; q < np; q += blockDim.x) {
+          double t = 0.0;
+          for (int g2 = 0; g2 < G; g2++) t += (double)gsum[g2 * np + q];
+          const int a = q / ny, c = q - a * ny;
+          acc[(a0 + a) * cy + y0 + c] += t;
         }
       }
     }
@@ -231,7 +249,7 @@ static int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int
     double* part = nullptr;
     FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
     size_t sm = (size_t)npair * 8;
-    if (sm > 200 * 1024) {
+    if (sm > 190 * 1024) {
       set_error("tlmm: %d x %d output too wide for one pass", acols, cy);
       return FL_ERR_OP;
     }
