@@ -623,6 +623,69 @@ static void fw_launch(int model, int c4, const GlmFactWArgs& a, int grid, size_t
 }
 }  // namespace flb
 
+namespace flb {
+// ---- width-general GLM iteration (generic operators around two small kernels)
+template <int MODEL>
+__global__ void __launch_bounds__(256) k_glm_u_resid(const float* __restrict__ z,
+                                                     const float* __restrict__ y, int64_t r_T,
+                                                     float* __restrict__ r,
+                                                     double* __restrict__ lpart) {
+  __shared__ double red_s[256];
+  double l64 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r_T;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float zz = z[i], yv = y[i];
+    float rv, l;
+    if (MODEL == 0) {
+      rv = zz - yv;
+      l = 0.5f * rv * rv;
+    } else {
+      const float e = __expf(-fabsf(zz));
+      const float sp = log1pf(e);
+      const float inv = __frcp_rn(1.f + e);
+      rv = (zz >= 0.f ? inv : e * inv) - yv;
+      const float lp = zz >= 0.f ? sp : sp - zz, lq = zz >= 0.f ? sp + zz : sp;
+      l = yv != 0.f ? fminf(lp, kLogClip) : fminf(lq, kLogClip);
+    }
+    r[i] = rv;
+    l64 += (double)l;
+  }
+  red_s[threadIdx.x] = l64;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red_s[threadIdx.x] += red_s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lpart[blockIdx.x] = red_s[0];
+}
+
+__global__ void k_glm_u_loss(const double* __restrict__ lpart, int n, double* red, int c_T) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < n; b++) s += lpart[b];
+    red[c_T] = s;
+  }
+}
+
+__global__ void k_glm_u_update(double* w64, float* w32, const double* red, int c_T, double lr,
+                               double* loss_hist, int loss_cap, GlmState* state) {
+  const int it = state->it;
+  if (threadIdx.x == 0 && it < loss_cap) loss_hist[it] = red[c_T];
+  for (int c = threadIdx.x; c < c_T; c += blockDim.x) {
+    w64[c] -= lr * red[c];
+    w32[c] = (float)w64[c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) state->it = it + 1;
+}
+
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ a, int64_t n, float* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+}  // namespace flb
+
 using namespace flb;
 
 struct fl_glm {
@@ -650,11 +713,48 @@ struct fl_glm {
   GlmFactWArgs fw{};
   int nblk_fw = 0;
   size_t smem_fw = 0;
+  // width-general path (stream blocks / dimensions too wide for the fused
+  // passes): z = T w, residual, T^T r through the generic operators
+  bool unfused = false;
+  DevBuf y_t, z, r, w32, lpart;
+  int u_blocks = 0;
 };
 
 namespace flb {
 
+static int glm_u_partial(fl_glm* s, cudaStream_t st) {
+  fl_table* t = s->t;
+  int rc = do_lmm(t, s->w32.as<float>(), 1, s->z.as<float>(), st);
+  if (rc) return rc;
+  if (s->model == FL_MODEL_LINREG)
+    k_glm_u_resid<0><<<s->u_blocks, 256, 0, st>>>(s->z.as<float>(), s->y_t.as<float>(), t->r_T,
+                                                  s->r.as<float>(), s->lpart.as<double>());
+  else
+    k_glm_u_resid<1><<<s->u_blocks, 256, 0, st>>>(s->z.as<float>(), s->y_t.as<float>(), t->r_T,
+                                                  s->r.as<float>(), s->lpart.as<double>());
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaMemsetAsync(s->red.p, 0, (size_t)(t->c_T + 1) * 8, st));
+  rc = do_tlmm(t, YView{s->r.as<float>(), 1, 0}, 1, s->red.as<double>(), 1, 0, st);
+  if (rc) return rc;
+  k_glm_u_loss<<<1, 32, 0, st>>>(s->lpart.as<double>(), s->u_blocks, s->red.as<double>(), t->c_T);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+static int glm_u_update(fl_glm* s, cudaStream_t st) {
+  k_glm_u_update<<<1, 256, 0, st>>>(s->w64.as<double>(), s->w32.as<float>(), s->red.as<double>(),
+                                    s->t->c_T, s->lr, s->loss_hist.as<double>(), s->loss_cap,
+                                    s->state.as<GlmState>());
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
 static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
+  if (s->unfused) {
+    int rc = glm_u_partial(s, st);
+    if (rc) return rc;
+    return fuse_update ? glm_u_update(s, st) : FL_OK;
+  }
   fl_table* t = s->t;
   if (s->bins_rows > 0) FL_CUDA(cudaMemsetAsync(s->bins.p, 0, (size_t)s->bins_rows * 4, st));
   if (s->da.ng > 0) {
@@ -694,9 +794,59 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     set_error("learning_rate must be > 0");
     return FL_ERR_CONFIG;
   }
-  if ((int)t->g.size() > MAX_GATHER || t->pf > 252) {
-    set_error("fused GLM supports <= %d gathered sources and <= 252 streamed columns", MAX_GATHER);
+  if ((int)t->g.size() > MAX_GATHER) {
+    set_error("GLM supports <= %d gathered sources", MAX_GATHER);
     return FL_ERR_OP;
+  }
+  bool wide = t->pf > 252;
+  for (auto& g : t->g) wide |= (size_t)TILE * g.pitch * 4 * 2 > 200 * 1024;
+  {
+    const int yb0 = model == FL_MODEL_LOGREG ? 1 : 4;
+    const uint32_t off_y0 = (uint32_t)(TILE * t->pf * 4);
+    const uint32_t stage0 = (uint32_t)round_up(off_y0 + round_up(TILE * yb0, 128) +
+                                               (t->sort_g >= 0 ? TILE * 4 : 0), 128);
+    wide |= (size_t)2 * stage0 > 200 * 1024;
+  }
+  if (wide || getenv("FL_GLM_UNFUSED")) {
+    // width-general path: generic operators (any width), same ABI and results
+    FL_CUDA(cudaSetDevice(t->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    auto* s = new fl_glm();
+    std::unique_ptr<fl_glm> guard(s);
+    s->t = t;
+    s->model = model;
+    s->lr = learning_rate;
+    s->unfused = true;
+    int rc;
+    const int64_t r_T = t->r_T;
+    if ((rc = s->y_t.alloc((size_t)r_T * 4 + 16))) return rc;
+    if (model == FL_MODEL_LOGREG) {
+      uint8_t* yd = nullptr;
+      FL_CUDA(cudaMallocAsync((void**)&yd, (size_t)r_T + 16, st));
+      FL_CUDA(cudaMemcpyAsync(yd, y, (size_t)r_T, cudaMemcpyDefault, st));
+      k_u8_to_f32<<<(unsigned)std::min<int64_t>(ceil_div(r_T, 256), 4096), 256, 0, st>>>(
+          yd, r_T, s->y_t.as<float>());
+      FL_CHECK_LAUNCH();
+      FL_CUDA(cudaFreeAsync(yd, st));
+    } else {
+      FL_CUDA(cudaMemcpyAsync(s->y_t.p, y, (size_t)r_T * 4, cudaMemcpyDefault, st));
+    }
+    if ((rc = s->z.alloc((size_t)r_T * 4 + 16))) return rc;
+    if ((rc = s->r.alloc((size_t)r_T * 4 + 16))) return rc;
+    if ((rc = s->w32.alloc((size_t)t->c_T * 4 + 16))) return rc;
+    FL_CUDA(cudaMemsetAsync(s->w32.p, 0, (size_t)t->c_T * 4, st));
+    if ((rc = s->w64.alloc((size_t)t->c_T * 8))) return rc;
+    FL_CUDA(cudaMemsetAsync(s->w64.p, 0, (size_t)t->c_T * 8, st));
+    s->u_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(r_T, 256), 4 * t->sm_count));
+    if ((rc = s->lpart.alloc((size_t)s->u_blocks * 8))) return rc;
+    if ((rc = s->red.alloc((size_t)(t->c_T + 1) * 8))) return rc;
+    FL_CUDA(cudaMemsetAsync(s->red.p, 0, (size_t)(t->c_T + 1) * 8, st));
+    if ((rc = s->loss_hist.alloc((size_t)s->loss_cap * 8))) return rc;
+    if ((rc = s->state.alloc(sizeof(GlmState)))) return rc;
+    FL_CUDA(cudaMemsetAsync(s->state.p, 0, sizeof(GlmState), st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    *out = guard.release();
+    return FL_OK;
   }
   FL_CUDA(cudaSetDevice(t->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -934,6 +1084,7 @@ int fl_glm_reduce_buffer(fl_glm* s, double** buf, int32_t* len) {
 int fl_glm_update(fl_glm* s, void* stream) {
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
+  if (s->unfused) return glm_u_update(s, (cudaStream_t)stream);
   k_glm_update<<<1, NTHREADS, 0, (cudaStream_t)stream>>>(s->ua);
   FL_CHECK_LAUNCH();
   return FL_OK;
@@ -946,6 +1097,13 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
   }
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->unfused) {
+    for (int i = 0; i < iterations; i++) {
+      int rc = glm_launch_iteration(s, st, true);
+      if (rc) return rc;
+    }
+    return FL_OK;
+  }
   if (!s->graph) {
     if (!s->cap_stream) FL_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t g;
@@ -965,6 +1123,26 @@ int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
   if (!s || iters < 1 || !ms_out) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->unfused) {   // [0, whole iteration, 0]
+    cudaEvent_t e0, e1;
+    FL_CUDA(cudaEventCreate(&e0));
+    FL_CUDA(cudaEventCreate(&e1));
+    FL_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; i++) {
+      int rc = glm_launch_iteration(s, st, true);
+      if (rc) return rc;
+    }
+    FL_CUDA(cudaEventRecord(e1, st));
+    FL_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FL_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    ms_out[0] = 0.f;
+    ms_out[1] = ms / iters;
+    ms_out[2] = 0.f;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return FL_OK;
+  }
   cudaEvent_t ev[4];
   for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
   float acc[3] = {0.f, 0.f, 0.f};

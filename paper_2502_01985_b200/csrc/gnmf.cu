@@ -34,7 +34,7 @@
 
 namespace flb {
 
-constexpr int GN_WARPS = 8;
+constexpr int GN_WARPS = 12;
 constexpr int GN_FLUSH = 16;   // stages between fp32 -> fp64 flushes (512 rows)
 constexpr double GN_EPS = 1e-12;   // trainers.py:29
 
@@ -334,18 +334,18 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
     }
 
     if (UPDATE) {
-      // ---- q = F H_F^T (3xTF32), v = W HH (3xTF32)
-      float q[2][NR][4], v[2][NR][4];
-#pragma unroll
-      for (int m = 0; m < 2; m++)
+      // one 16-row half at a time (halves the live accumulators: 8 warps of
+      // 255 registers is this kernel's occupancy limit)
+#pragma unroll 1
+      for (int m = 0; m < 2; m++) {
+        // ---- q = F H_F^T (3xTF32), v = W HH (3xTF32)
+        float q[NR][4], v[NR][4];
 #pragma unroll
         for (int n = 0; n < NR; n++)
 #pragma unroll
-          for (int e = 0; e < 4; e++) q[m][n][e] = v[m][n][e] = 0.f;
+          for (int e = 0; e < 4; e++) q[n][e] = v[n][e] = 0.f;
 #pragma unroll
-      for (int kc = 0; kc < KC; kc++) {
-#pragma unroll
-        for (int m = 0; m < 2; m++) {
+        for (int kc = 0; kc < KC; kc++) {
           uint32_t x[4];
           ldsm_x4(x[0], x[1], x[2], x[3],
                   Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
@@ -360,17 +360,14 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
           for (int n = 0; n < NR; n++) b[n] = hf[(kc * NR + n) * 32 + lane];
           // the three split terms as three sweeps over independent accumulators
 #pragma unroll
-          for (int n = 0; n < NR; n++) mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b[n].x, b[n].y);
+          for (int n = 0; n < NR; n++) mma_tf32(q[n], xh[0], xh[1], xh[2], xh[3], b[n].x, b[n].y);
 #pragma unroll
-          for (int n = 0; n < NR; n++) mma_tf32(q[m][n], xl[0], xl[1], xl[2], xl[3], b[n].x, b[n].y);
+          for (int n = 0; n < NR; n++) mma_tf32(q[n], xl[0], xl[1], xl[2], xl[3], b[n].x, b[n].y);
 #pragma unroll
-          for (int n = 0; n < NR; n++) mma_tf32(q[m][n], xh[0], xh[1], xh[2], xh[3], b[n].z, b[n].w);
+          for (int n = 0; n < NR; n++) mma_tf32(q[n], xh[0], xh[1], xh[2], xh[3], b[n].z, b[n].w);
         }
-      }
 #pragma unroll
-      for (int kc = 0; kc < NR; kc++) {
-#pragma unroll
-        for (int m = 0; m < 2; m++) {
+        for (int kc = 0; kc < NR; kc++) {
           const int row = m * 16 + (lane & 15);
           const int col = kc * 8 + (lane >> 4) * 4;
           uint32_t x[4];
@@ -385,19 +382,16 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
 #pragma unroll
           for (int n = 0; n < NR; n++) b[n] = hh[(kc * NR + n) * 32 + lane];
 #pragma unroll
-          for (int n = 0; n < NR; n++) mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b[n].x, b[n].y);
+          for (int n = 0; n < NR; n++) mma_tf32(v[n], xh[0], xh[1], xh[2], xh[3], b[n].x, b[n].y);
 #pragma unroll
-          for (int n = 0; n < NR; n++) mma_tf32(v[m][n], xl[0], xl[1], xl[2], xl[3], b[n].x, b[n].y);
+          for (int n = 0; n < NR; n++) mma_tf32(v[n], xl[0], xl[1], xl[2], xl[3], b[n].x, b[n].y);
 #pragma unroll
-          for (int n = 0; n < NR; n++) mma_tf32(v[m][n], xh[0], xh[1], xh[2], xh[3], b[n].z, b[n].w);
+          for (int n = 0; n < NR; n++) mma_tf32(v[n], xh[0], xh[1], xh[2], xh[3], b[n].z, b[n].w);
         }
-      }
-      // ---- gathers of the dimension products G_d[fk]
+        // ---- gathers of the dimension products G_d[fk]
 #pragma unroll
-      for (int d = 0; d < MAX_GATHER; d++) {
-        if (d >= a.ng) break;
-#pragma unroll
-        for (int m = 0; m < 2; m++)
+        for (int d = 0; d < MAX_GATHER; d++) {
+          if (d >= a.ng) break;
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int f = __shfl_sync(0xffffffffu, fkl[d], m * 16 + h * 8 + g);
@@ -406,16 +400,14 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
 #pragma unroll
               for (int n = 0; n < NR; n++) {
                 const float2 gv = *reinterpret_cast<const float2*>(gr + n * 8);
-                q[m][n][h * 2] += gv.x;
-                q[m][n][h * 2 + 1] += gv.y;
+                q[n][h * 2] += gv.x;
+                q[n][h * 2 + 1] += gv.y;
               }
             }
           }
-      }
-      __syncwarp();
-      // ---- W <- W o q / (W HH + eps), in place in the swizzled tile
-#pragma unroll
-      for (int m = 0; m < 2; m++)
+        }
+        __syncwarp();
+        // ---- W <- W o q / (W HH + eps), in place in the swizzled tile
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int row = m * 16 + h * 8 + g;
@@ -423,11 +415,13 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
           for (int n = 0; n < NR; n++) {
             float2* wptr = reinterpret_cast<float2*>(Wt + widx<R>(row, n * 8 + 2 * t));
             float2 w = *wptr;
-            w.x = w.x * __fdividef(q[m][n][h * 2], v[m][n][h * 2] + 1e-12f);
-            w.y = w.y * __fdividef(q[m][n][h * 2 + 1], v[m][n][h * 2 + 1] + 1e-12f);
+            w.x = w.x * __fdividef(q[n][h * 2], v[n][h * 2] + 1e-12f);
+            w.y = w.y * __fdividef(q[n][h * 2 + 1], v[n][h * 2 + 1] + 1e-12f);
             *wptr = w;
           }
         }
+        __syncwarp();
+      }
       __syncwarp();
       if (lane == 0) {
         fence_proxy_async();

@@ -141,6 +141,19 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t col
 // table.cu
 int table_upload_tcols(fl_table* t);
 // ops.cu helpers used by trainers
+// Strided fp32 operand view: element (target row t, col) at base[t*sr + col*sc]
+struct YView {
+  const float* base;
+  int64_t sr, sc;
+#ifdef __CUDACC__
+  __device__ float at(int64_t t, int col) const { return base[t * sr + (int64_t)col * sc]; }
+#endif
+};
+// generic operators (ops.cu), device operands, stream-ordered:
+//   out (r_T x c_x, target order) = T x;   out[tcol*os_t + col*os_c] += (T^T y)
+int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s);
+int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
+            cudaStream_t s);
 int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target,
                                        void* dst_dev, int elem_bytes, cudaStream_t s);
 int device_sm_count(int device);

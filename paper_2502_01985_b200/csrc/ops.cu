@@ -72,12 +72,6 @@ __global__ void k_lmm_main(const float* __restrict__ F, int pf, const int32_t* _
   out[(int64_t)perm[p] * c_x + col0 + col] = acc;
 }
 
-// Strided fp32 operand view: element (target row t, col) at base[t*sr + col*sc]
-struct YView {
-  const float* base;
-  int64_t sr, sc;
-  __device__ float at(int64_t t, int col) const { return base[t * sr + (int64_t)col * sc]; }
-};
 
 // Per-block partial of A^T Y over a contiguous row range, A = row-major
 // (pitch) fp32 rows; Y rows either from a device-ordered fp64 buffer (bins)
@@ -202,7 +196,7 @@ int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target
 }
 
 // ---------------------------------------------------------------------------
-static int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s) {
+int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s) {
   if ((int)t->g.size() > MAX_GATHER) {
     set_error("lmm: at most %d gathered sources supported", MAX_GATHER);
     return FL_ERR_OP;
@@ -236,7 +230,7 @@ static int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cuda
 }
 
 // generic T^T y with strided y view and strided fp64 output
-static int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
+int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
                    cudaStream_t s) {
   const int sms = t->sm_count;
   auto launch_tmm = [&](const float* A, int pitch, int acols, int64_t rows, const double* bins,

@@ -285,3 +285,34 @@ def test_kmeans_tcgen05_variant_matches_reference(fl, name, monkeypatch):
     assert np.array_equal(res.parameters["assignments"], g["kmeans_assignments"])
     assert max_rel(res.loss_history, g["kmeans_loss"]) < TOL
     assert max_rel(res.parameters["centroids"], g["kmeans_centroids"]) < TOL
+
+
+@pytest.mark.parametrize("name,model", [("star", "linreg"), ("star3", "logreg"),
+                                        ("gen_outer_3_0", "linreg"), ("gen_left_2_1", "logreg")])
+def test_glm_width_general_path_matches_reference(fl, name, model, monkeypatch):
+    """The generic-operator GLM iteration (used for tables too wide for the
+    fused passes), forced on the golden tables."""
+    monkeypatch.setenv("FL_GLM_UNFUSED", "1")
+    g = load_golden(name)
+    m = g.meta["trainers"][model]
+    y = g["y_lin"] if model == "linreg" else g["y_log"]
+    res = fl.train(model, fl.TargetHandle.factorized(g.ft), _cfg(fl, m), fl.SparseMatrix.from_dense(y))
+    assert max_rel(res.loss_history, g[f"{model}_loss"]) < TOL
+    assert max_rel(res.parameters["w"], g[f"{model}_w"]) < TOL
+
+
+@pytest.mark.parametrize("model", ["linreg", "logreg"])
+def test_glm_wide_tables_vs_oracle(fl, model):
+    """Widths past the fused passes: a 300-column fact table with a 260-column
+    dimension, factorized and materialized."""
+    ft = star_table(17, 6_000, [(60, 260)], 300)
+    tab = oracle.OracleTable.from_ft(ft)
+    rng = np.random.default_rng(8)
+    y = (rng.random(ft.r_T) if model == "linreg" else rng.integers(0, 2, ft.r_T)).astype(np.float64)
+    lr = rt.safe_learning_rate(tab)
+    want = rt.train(model, tab, iterations=5, learning_rate=lr, y=y)
+    for h in (fl.TargetHandle.factorized(ft),
+              fl.TargetHandle.materialized(fl.SparseMatrix.from_dense(oracle.materialize(tab)))):
+        res = fl.train(model, h, fl.TrainConfig(iterations=5, learning_rate=lr), y.reshape(-1, 1))
+        assert max_rel(res.loss_history, want["loss_history"]) < TOL
+        assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
