@@ -296,6 +296,31 @@ __device__ __forceinline__ void bulk_wait() {
 // 4 fp32 8x4 matrices -> the m16n8k8 tf32 A fragment (rows 0-7 / 8-15,
 // cols 0-3 / 4-7); lane l supplies the address of row (l & 15) at column
 // offset (l >> 4) * 4.  Rows must be 16-byte aligned.
+// Ampere-style async copies (LDGSTS): 4 / 16 bytes per thread, grouped.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Pinned read-only loads: volatile so the compiler cannot sink a prefetch
+// down to its first use (it otherwise does, which defeats the prefetch).
+__device__ __forceinline__ float4 ld_nc_pinned_f4(const void* p) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_nc_pinned_s32(const void* p) {
+  int v;
+  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
                                         const void* row_ptr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"

@@ -39,6 +39,11 @@ namespace flb {
 
 constexpr int KM_WARPS = 8;
 constexpr int KM_FLUSH = 16;   // stages between fp32 -> fp64 flushes (<= 512 rows)
+constexpr int KM_PF_MAX = 2;   // gathered sources whose E rows are prefetched by async copies
+// per-warp scratch: the prefetched E rows, also the z transpose (32 x (KP+4))
+__host__ __device__ constexpr int km_scratch_floats(int KP) {
+  return KM_PF_MAX * 32 * KP > 32 * (KP + 4) ? KM_PF_MAX * 32 * KP : 32 * (KP + 4);
+}
 #define kInf __int_as_float(0x7f800000)
 
 struct KmState {
@@ -60,6 +65,7 @@ struct KmFactArgs {
   const int32_t* f_tcol;         // pf
   int32_t* assign;               // r_pad device order, or null
   double* part;                  // gridDim.x x (KP * SC + 1)
+  double* part_w;                // gridDim.x x KM_WARPS x (MT * 16 * SC): per-warp sums
   uint32_t stage_bytes;          // 32 x FP fp32 TMA tile | 32 int32 sort-source FK
   int nst;
 };
@@ -165,16 +171,27 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   constexpr int FP = SC + 4;          // smem F row pitch (TMA box width, zero-filled)
   constexpr int CFP = SC + 4;         // fp32 centroid row pitch in smem
   constexpr int ZP = KP + 4;          // per-warp distance transpose pitch
+  // E rows of the first KM_PF gathered sources are prefetched one unit ahead
+  // by async copies (LDGSTS) straight into the warp's scratch; their FKs two
+  // units ahead into a 2-slot ring.  Rows are copied ROW-SPLIT: QR = KP/4
+  // consecutive lanes fetch the QR float4 quads of one row (one L1 tag per
+  // row, not per lane); quad q of row r lands at physical quad q ^ sw(r), so
+  // the lane-per-row read-back is bank-conflict free.
+  constexpr int KM_PF = KM_PF_MAX;
+  constexpr int QR = KP / 4, RPI = 32 / QR;
+  constexpr int EW = km_scratch_floats(KP);
+  // fp64 sums accumulators in registers when they fit, else per-warp global
+  constexpr bool ACC_REG = MT * KC <= 4;
   extern __shared__ __align__(128) char smem[];
   __shared__ uint64_t bar[KM_WARPS][4];
   __shared__ double lsum[KM_WARPS];
 
-  uint4* bfrag = reinterpret_cast<uint4*>(smem);                       // KC*NT*32 (hi, lo)
+  uint4* bfrag = reinterpret_cast<uint4*>(smem);                       // KC*NT*32
   float* cf = reinterpret_cast<float*>(bfrag + KC * NT * 32);          // KP x CFP
   float* cn = cf + KP * CFP;                                           // KP (+4)
-  double* acc64 = reinterpret_cast<double*>(cn + KP + 4);              // warps x MT*16*SC
-  float* zs_all = reinterpret_cast<float*>(acc64 + KM_WARPS * MT * 16 * SC);  // warps x 32*ZP
-  char* stages = smem + round_up((int64_t)(reinterpret_cast<char*>(zs_all + KM_WARPS * 32 * ZP) -
+  float* ebuf_all = cn + KP + 4;                                       // warps x EW
+  int32_t* fkr_all = reinterpret_cast<int32_t*>(ebuf_all + KM_WARPS * EW);  // warps x 3 x KM_PF x 32
+  char* stages = smem + round_up((int64_t)(reinterpret_cast<char*>(fkr_all + KM_WARPS * 3 * KM_PF * 32) -
                                            smem), 128);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -191,8 +208,10 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     }
     cf[i] = v;
   }
-  double* wacc = acc64 + warp * (MT * 16 * SC);
-  for (int i = lane; i < MT * 16 * SC; i += 32) wacc[i] = 0.0;
+  // this warp's fp64 sums region (global, L2-resident)
+  double* wacc = a.part_w + ((int64_t)blockIdx.x * KM_WARPS + warp) * (MT * 16 * SC);
+  if (!ACC_REG)
+    for (int i = lane; i < MT * 16 * SC; i += 32) wacc[i] = 0.0;
   if (lane == 0) {
     lsum[warp] = 0.0;
     for (int s = 0; s < a.nst; s++) mbar_init(&bar[warp][s], 1);
@@ -203,9 +222,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     int l = i & 31, kn = i >> 5;
     int kc = kn / NT, n = kn - kc * NT;
     int gg = l >> 2, tt = l & 3;
-    const Split b0 = split_tf32(cf[(n * 8 + gg) * CFP + kc * 8 + tt]);
-    const Split b1 = split_tf32(cf[(n * 8 + gg) * CFP + kc * 8 + tt + 4]);
-    bfrag[i] = make_uint4(b0.hi, b1.hi, b0.lo, b1.lo);
+    // screen B fragments: one rounded tf32 term, packed (conflict-free LDS.64)
+    reinterpret_cast<uint2*>(bfrag)[i] = make_uint2(tf32_bits(cf[(n * 8 + gg) * CFP + kc * 8 + tt]),
+                                                    tf32_bits(cf[(n * 8 + gg) * CFP + kc * 8 + tt + 4]));
   }
   for (int j = threadIdx.x; j < KP; j += blockDim.x) {
     float s = 0.f;
@@ -222,28 +241,61 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   const int64_t base = a.nunits / NW, rem = a.nunits % NW;
   const int64_t u0 = gw * base + min64(gw, rem);
   const int64_t cnt = base + (gw < rem ? 1 : 0);
-  const bool has_sort = a.sort_g >= 0;
   constexpr uint32_t F_BYTES = 32u * FP * 4u;
-  const uint32_t tx = F_BYTES + 128u * a.ng;   // F tile + every source's 32 FKs
+  // F tile + the 32 FKs of every source not in the async-copied FK ring
+  const int npf = min(a.ng, KM_PF);
+  const uint32_t tx = F_BYTES + 128u * (a.ng - npf);
   char* wsm = stages + (size_t)warp * a.nst * a.stage_bytes;
-  float* zs = zs_all + warp * 32 * ZP;
+  float* ebuf = ebuf_all + warp * EW;   // [KM_PF][32][KP] E rows; also the z transpose scratch
+  float* zs = ebuf;
+  int32_t* fkr = fkr_all + warp * 3 * KM_PF * 32;
   uint64_t* wbar = bar[warp];
   auto issue = [&](int s, int64_t unit) {
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
     tma_load_2d(st, &tmF, 0, (int)(unit * 32), &wbar[s]);
-    for (int d = 0; d < a.ng; d++) bulk_g2s(st + F_BYTES + 128 * d, a.fk[d] + unit * 32, 128, &wbar[s]);
+    for (int d = npf; d < a.ng; d++) bulk_g2s(st + F_BYTES + 128 * d, a.fk[d] + unit * 32, 128, &wbar[s]);
   };
   if (lane == 0)
     for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
 
+  auto issue_fk = [&](int64_t unit, int slot) {
+    for (int d = 0; d < npf; d++) cp_async4(fkr + (slot * KM_PF + d) * 32 + lane, a.fk[d] + unit * 32 + lane);
+  };
+  auto issue_e = [&](int slot) {
+    for (int d = 0; d < npf; d++) {
+      const int32_t* fr = fkr + (slot * KM_PF + d) * 32;
+#pragma unroll
+      for (int jj = 0; jj < QR; jj++) {
+        const int r = jj * RPI + lane / QR, q = lane % QR;
+        // FK -1 (no match) -> the all-zero row r_d: one unsigned min
+        const unsigned f = min((unsigned)fr[r], (unsigned)a.rows[d]);
+        cp_async16(ebuf + d * 32 * KP + r * KP + 4 * (q ^ ((r / (8 / QR)) & (QR - 1))),
+                   a.E[d] + (f * KP + q * 4));
+      }
+    }
+  };
+  if (cnt > 0 && npf > 0) {
+    issue_fk(u0, 0);
+    if (cnt > 1) issue_fk(u0 + 1, 1);   // FK ring: unit u0 + j in slot j % 3
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    issue_e(0);
+    cp_async_commit();
+  }
+
   float sacc[MT][KC][4];
+  double sacc64[ACC_REG ? MT : 1][ACC_REG ? KC : 1][4];
 #pragma unroll
   for (int m = 0; m < MT; m++)
 #pragma unroll
     for (int c = 0; c < KC; c++)
 #pragma unroll
-      for (int e = 0; e < 4; e++) sacc[m][c][e] = 0.f;
+      for (int e = 0; e < 4; e++) {
+        sacc[m][c][e] = 0.f;
+        if (ACC_REG) sacc64[ACC_REG ? m : 0][ACC_REG ? c : 0][e] = 0.0;
+      }
   float lacc = 0.f;
 
   auto flush = [&]() {
@@ -253,8 +305,12 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       for (int c = 0; c < KC; c++)
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-          int row = m * 16 + g + (e >> 1) * 8, col = c * 8 + 2 * t + (e & 1);
-          wacc[row * SC + col] += (double)sacc[m][c][e];
+          if (ACC_REG) {
+            sacc64[ACC_REG ? m : 0][ACC_REG ? c : 0][e] += (double)sacc[m][c][e];
+          } else {
+            const int row = m * 16 + g + (e >> 1) * 8, col = c * 8 + 2 * t + (e & 1);
+            wacc[row * SC + col] += (double)sacc[m][c][e];
+          }
           sacc[m][c][e] = 0.f;
         }
     float v = lacc;
@@ -266,19 +322,38 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
 
   int s = 0;            // stage slot and its mbarrier phase
   uint32_t ph = 0;
-  for (int64_t i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0)) {
+  int fslot = 0;        // FK ring slot of this unit
+  for (int64_t i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0),
+               fslot = fslot == 2 ? 0 : fslot + 1) {
     mbar_wait(&wbar[s], ph);
     float* Fs = reinterpret_cast<float*>(wsm + (size_t)s * a.stage_bytes);
     const int32_t* fks_s = reinterpret_cast<const int32_t*>(wsm + (size_t)s * a.stage_bytes + F_BYTES);
     const int64_t p0 = (u0 + i) * 32;
     const bool valid = p0 + lane < a.r_T;
-    // E terms of every cluster: sum_d E_d[fk_d, j] (kept apart for the loss);
-    // issued first so the L2 latency overlaps the tensor-core screen
+    // E terms of every cluster: sum_d E_d[fk_d, j] (kept apart for the loss).
+    // The first KM_PF sources were gathered into registers during the
+    // previous unit; any further source is gathered here, before the screen
     float eacc[KP];
 #pragma unroll
     for (int j = 0; j < KP; j++) eacc[j] = 0.f;
+    if (npf > 0) {
+      cp_async_wait_all();   // this unit's E rows (and the next unit's FKs)
+      __syncwarp();
+      for (int d = 0; d < npf; d++) {
 #pragma unroll
-    for (int d = 0; d < MAX_GATHER; d++) {
+        for (int q = 0; q < QR; q++) {
+          const float4 v = *reinterpret_cast<const float4*>(
+              ebuf + d * 32 * KP + lane * KP + 4 * (q ^ ((lane / (8 / QR)) & (QR - 1))));
+          eacc[q * 4 + 0] += v.x;
+          eacc[q * 4 + 1] += v.y;
+          eacc[q * 4 + 2] += v.z;
+          eacc[q * 4 + 3] += v.w;
+        }
+      }
+      __syncwarp();   // the scratch is reused for the distance transpose
+    }
+#pragma unroll
+    for (int d = KM_PF; d < MAX_GATHER; d++) {
       if (d >= a.ng) break;
       const int f = fks_s[d * 32 + lane];
       const float4* er = reinterpret_cast<const float4*>(a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP);
@@ -292,8 +367,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       }
     }
 
-    // ---- screen: z = F C_F^T on the tensor cores (3xTF32, A fragments
-    // straight from the TMA tile via ldmatrix)
+    // ---- screen: z = F C_F^T on the tensor cores, ONE tf32 term (A
+    // truncated, B rounded): the screen only proposes the winner, every row
+    // whose runner-up lies inside the tf32 error bound is certified below
     float z[2][NT][4];
 #pragma unroll
     for (int m = 0; m < 2; m++)
@@ -303,24 +379,17 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         for (int e = 0; e < 4; e++) z[m][n][e] = 0.f;
 #pragma unroll
     for (int kc = 0; kc < KC; kc++) {
-      uint4 bf[NT];
+      uint2 bf[NT];
 #pragma unroll
-      for (int n = 0; n < NT; n++) bf[n] = bfrag[(kc * NT + n) * 32 + lane];
+      for (int n = 0; n < NT; n++) bf[n] = reinterpret_cast<const uint2*>(bfrag)[(kc * NT + n) * 32 + lane];
 #pragma unroll
       for (int m = 0; m < 2; m++) {
-        uint32_t x[4], xh[4], xl[4];
+        uint32_t x[4];
         ldsm_x4(x[0], x[1], x[2], x[3], Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          xh[e] = x[e] & 0xffffe000u;
-          xl[e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(xh[e]));
-        }
+        for (int e = 0; e < 4; e++) x[e] &= 0xffffe000u;
 #pragma unroll
-        for (int n = 0; n < NT; n++) {
-          mma_tf32(z[m][n], xh[0], xh[1], xh[2], xh[3], bf[n].x, bf[n].y);
-          mma_tf32(z[m][n], xl[0], xl[1], xl[2], xl[3], bf[n].x, bf[n].y);
-          mma_tf32(z[m][n], xh[0], xh[1], xh[2], xh[3], bf[n].z, bf[n].w);
-        }
+        for (int n = 0; n < NT; n++) mma_tf32(z[m][n], x[0], x[1], x[2], x[3], bf[n].x, bf[n].y);
       }
     }
     // transpose to lane-per-row through the warp's smem scratch
@@ -333,8 +402,6 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         *reinterpret_cast<float2*>(zs + (m * 16 + g + 8) * ZP + n * 8 + 2 * t) =
             make_float2(z[m][n][2], z[m][n][3]);
       }
-    // count column of [F | 1] (read by the sums MMA below)
-    Fs[lane * FP + pf] = 1.f;
     __syncwarp();
     float dv[KP];
 #pragma unroll
@@ -361,7 +428,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
 #pragma unroll
     for (int c4 = 0; c4 < 2 * KC; c4++) xr[c4] = c4 < pf4 ? fr[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
     // ---- certify: keep the screened winner unless the runner-up lies within
-    // the 3xTF32 screen's error bound; near-ties are re-decided from direct
+    // the tf32 screen's error bound; near-ties are re-decided from direct
     // fp32 differences (the reference orders them in fp64)
     float el = 0.f;
     if (valid) {
@@ -371,7 +438,10 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         xn = fmaf(xr[c4].x, xr[c4].x, fmaf(xr[c4].y, xr[c4].y,
              fmaf(xr[c4].z, xr[c4].z, fmaf(xr[c4].w, xr[c4].w, xn))));
       // v2 is +inf when k == 1: keep the bound finite
-      const float tol = 1e-5f * (xn + cn_max) + 1e-5f * (fabsf(v1) + fminf(fabsf(v2), 3e38f));
+      // |screen error| per distance <= 2 sum_c |x_c (c_c - c~_c) + (x_c - x~_c) c~_c|
+      // <= 1.6e-3 (xn + cn_j) for a truncated A (2^-10) and a rounded B
+      // (2^-11); two distances differ by at most twice that
+      const float tol = 4e-3f * (xn + cn_max) + 1e-5f * (fabsf(v1) + fminf(fabsf(v2), 3e38f));
       if (!(v2 - v1 > tol)) {
         uint32_t cand = 0;   // clusters that can still win
 #pragma unroll
@@ -407,6 +477,15 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     } else {
       al = -1;
     }
+    // ---- prefetch the next unit's E rows (its FKs arrived a unit ago) and
+    // the FKs of the unit after it: their L2 latency overlaps the rest of
+    // this unit (loss, counters, sums)
+    if (npf > 0 && i + 1 < cnt) {
+      __syncwarp();   // every lane is done with the z scratch
+      issue_e(fslot == 2 ? 0 : fslot + 1);
+      if (i + 2 < cnt) issue_fk(u0 + i + 2, fslot == 0 ? 2 : fslot - 1);
+      cp_async_commit();
+    }
     // ---- loss (direct differences), I_d^T A counters, assignments
     if (valid) {
       const float4* cr = reinterpret_cast<const float4*>(cf + al * CFP);
@@ -423,7 +502,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
 #pragma unroll
     for (int d = 0; d < MAX_GATHER; d++) {
       if (d >= a.ng) break;
-      const int f = fks_s[d * 32 + lane];
+      const int f = d < npf ? fkr[(fslot * KM_PF + d) * 32 + lane] : fks_s[d * 32 + lane];
       const int key = (valid && f >= 0) ? f * KP + al : -1 - lane;
       if (d == a.sort_g) {   // sorted FKs: runs of equal keys, one atomic per run
         const unsigned mask = __match_any_sync(0xffffffffu, key);
@@ -437,7 +516,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     // truncated mantissa, lo = exact remainder), one-hot exact
 #pragma unroll
     for (int kb = 0; kb < 4; kb++) {
-      const int rr0 = kb * 8 + t, rr1 = rr0 + 4;
+      // k index t <-> row kb*8 + 2t, t + 4 <-> row kb*8 + 2t + 1: with the
+      // F pitch of 4 * odd words these rows hit distinct bank octets
+      const int rr0 = kb * 8 + 2 * t, rr1 = rr0 + 1;
       const int ar0 = __shfl_sync(0xffffffffu, al, rr0);
       const int ar1 = __shfl_sync(0xffffffffu, al, rr1);
       uint32_t oh[MT][4];
@@ -451,8 +532,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       }
 #pragma unroll
       for (int c = 0; c < KC; c++) {
-        const float b0 = Fs[rr0 * FP + c * 8 + g];
-        const float b1 = Fs[rr1 * FP + c * 8 + g];
+        // column pf of [F | 1] is the count column (TMA zero-fills it)
+        const float b0 = c * 8 + g == pf ? 1.f : Fs[rr0 * FP + c * 8 + g];
+        const float b1 = c * 8 + g == pf ? 1.f : Fs[rr1 * FP + c * 8 + g];
         const uint32_t h0 = __float_as_uint(b0) & 0xffffe000u;
         const uint32_t h1 = __float_as_uint(b1) & 0xffffe000u;
         const uint32_t l0 = __float_as_uint(b0 - __uint_as_float(h0));
@@ -472,12 +554,24 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     if ((i % KM_FLUSH) == KM_FLUSH - 1) flush();
   }
   flush();
+  if (ACC_REG) {
+#pragma unroll
+    for (int m = 0; m < MT; m++)
+#pragma unroll
+      for (int c = 0; c < KC; c++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int row = m * 16 + g + (e >> 1) * 8, col = c * 8 + 2 * t + (e & 1);
+          wacc[row * SC + col] = sacc64[ACC_REG ? m : 0][ACC_REG ? c : 0][e];
+        }
+  }
   __syncthreads();
   // CTA partial in fixed warp order: [KP x SC] sums (count at column pf) | loss
   double* out = a.part + (int64_t)blockIdx.x * (KP * SC + 1);
+  const double* wall = a.part_w + (int64_t)blockIdx.x * KM_WARPS * (MT * 16 * SC);
   for (int i = threadIdx.x; i < KP * SC; i += blockDim.x) {
     double s = 0.0;
-    for (int w2 = 0; w2 < KM_WARPS; w2++) s += acc64[w2 * (MT * 16 * SC) + i];
+    for (int w2 = 0; w2 < KM_WARPS; w2++) s += wall[w2 * (MT * 16 * SC) + i];
     out[i] = s;
   }
   if (threadIdx.x == 0) {
@@ -657,7 +751,7 @@ struct fl_kmeans {
   size_t smem_fact = 0, smem_e = 0, smem_sum = 0;
   int grid_e = 1, grid_sum = 1, grid_red = 1, n_desc = 0;
   DevBuf descs;
-  DevBuf C64, C32, E, cnt, part_fact, part_dim, red, loss_hist, state, assign, done;
+  DevBuf C64, C32, E, cnt, part_fact, part_w, part_dim, red, loss_hist, state, assign, done;
   int loss_cap = 1 << 16;
   cudaGraphExec_t graph = nullptr, graph_assign = nullptr;
   cudaStream_t cap_stream = nullptr;
@@ -822,8 +916,10 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   if ((rc = make_tmap_2d(&s->tmF, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
                          (uint64_t)t->pf * 4, 32, (uint32_t)FP, 0)))
     return rc;
+  (void)ZP;
   const size_t fixed = (size_t)KC * NT * 32 * 16 + (size_t)KP * (SC + 4) * 4 + (KP + 4) * 4 +
-                       (size_t)KM_WARPS * MT * 16 * SC * 8 + (size_t)KM_WARPS * 32 * ZP * 4;
+                       (size_t)KM_WARPS * km_scratch_floats(KP) * 4 +
+                       (size_t)KM_WARPS * 3 * KM_PF_MAX * 32 * 4;
   const size_t fixed_al = round_up((int64_t)fixed, 128);
   // two CTAs (16 warps) per SM when the tile fits in half the shared memory
   const bool two = NT <= 2 && KC <= 4 && fixed_al + (size_t)KM_WARPS * 2 * fa.stage_bytes <= 110 * 1024;
@@ -898,6 +994,8 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
     ta.SC = SC;
   }
   if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (KP * SC + 1) * 8))) return rc;
+  if ((rc = s->part_w.alloc((size_t)s->nblk_fact * KM_WARPS * MT * 16 * SC * 8))) return rc;
+  fa.part_w = s->part_w.as<double>();
   fa.part = s->part_fact.as<double>();
   s->ta.part = fa.part;
 

@@ -182,6 +182,22 @@ def test_kmeans_planted_star_vs_oracle(fl, k, dims, c_fact):
     assert max_rel(res.parameters["centroids"], want["parameters"]["centroids"]) < TOL
 
 
+@pytest.mark.parametrize("k,noise", [(16, 0.35), (8, 1.0)])
+def test_kmeans_overlapping_clusters_certified(fl, k, noise):
+    """Heavily overlapping clusters: many rows have a runner-up inside the
+    tf32 screen's error bound, so the exact certification path decides them.
+    One iteration (identical initial centroids): assignments may differ from
+    the fp64 oracle only on true fp32-level ties."""
+    ft = planted_star(5, 40_000, [(2000, 24), (300, 6)], 20, k, noise=noise)
+    tab = oracle.OracleTable.from_ft(ft)
+    want = rt.kmeans(tab, 1, k, 7)
+    res = fl.train("kmeans", fl.TargetHandle.factorized(ft),
+                   fl.TrainConfig(iterations=1, k_clusters=k, seed=7))
+    diff = np.count_nonzero(res.parameters["assignments"] != want["parameters"]["assignments"])
+    assert diff <= 2
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+
+
 def test_kmeans_tie_and_empty_cluster(fl):
     """test_trainers.py:261-270: [[0],[0],[10]], k=3 -> [0, 0, 2], loss 0 and
     the empty cluster keeps its centroid."""
