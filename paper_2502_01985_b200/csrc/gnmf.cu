@@ -31,10 +31,11 @@
 #include "internal.h"
 #include "mma_tf32.cuh"
 #include "reduce.cuh"
+#include "tc05.cuh"
 
 namespace flb {
 
-constexpr int GN_WARPS = 12;
+constexpr int GN_WARPS = 8;
 constexpr int GN_FLUSH = 16;   // stages between fp32 -> fp64 flushes (512 rows)
 constexpr double GN_EPS = 1e-12;   // trainers.py:29
 
@@ -558,6 +559,11 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
   }
 }
 
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+#include "gnmf_tc.cuh"
+
 // ---------------------------------------------------------------------------
 // D2: P_d = Z_d^T S_d (fp64 per-CTA partials over row ranges)
 // ---------------------------------------------------------------------------
@@ -696,6 +702,12 @@ using namespace flb;
 
 struct fl_gnmf {
   CUtensorMap tmW, tmF;
+  // tcgen05 fact pass (R = 32, <= 32 streamed columns): 128-row tile maps
+  bool tc = false;
+  CUtensorMap tmWt, tmFt;
+  GnTcArgs ta{};
+  GtGeom gm{};
+  DevBuf scratch;
   fl_table* t = nullptr;
   int rank = 0, R = 0, NR = 0, KC = 0, SC = 0;
   GnFactArgs fa{};
@@ -714,6 +726,18 @@ struct fl_gnmf {
 
 namespace flb {
 
+static void gn_fact_any(fl_gnmf* s, bool update, cudaStream_t st) {
+  if (s->tc) {
+    const size_t smem = s->gm.total + 1024;
+    if (update)
+      k_gnmf_tc<true><<<s->nblk_fact, GT_THREADS, smem, st>>>(s->tmWt, s->tmFt, s->ta, s->gm);
+    else
+      k_gnmf_tc<false><<<s->nblk_fact, GT_THREADS, smem, st>>>(s->tmWt, s->tmFt, s->ta, s->gm);
+  } else {
+    gn_fact_launch(s->NR, s->KC, update, s->tmW, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
+  }
+}
+
 static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
   if (update && s->da.ng > 0) {
     gn_dim_g_launch(s->R, dim3(s->grid_g, s->da.ng), s->smem_g, st, s->da);
@@ -722,7 +746,7 @@ static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
     for (int d = 0; d < s->da.ng; d++)
       FL_CUDA(cudaMemsetAsync(s->da.Z[d], 0, (size_t)s->da.rows[d] * s->R * 8, st));
   }
-  gn_fact_launch(s->NR, s->KC, update, s->tmW, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
+  gn_fact_any(s, update, st);
   FL_CHECK_LAUNCH();
   if (s->da.ng > 0) {
     gn_dim_p_launch(s->R, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da);
@@ -853,11 +877,55 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   occ = std::max(1, occ);
   s->nblk_fact = (int)std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(fa.nunits, GN_WARPS), (int64_t)t->sm_count * occ));
+  // tcgen05 fact pass (opt-in, FL_GN_TC=1; R = 32, <= 32 streamed columns,
+  // <= 2 gathered sources): parity-green but slower than the mma.sync pass at
+  // C4 (profiles/r01_gnmf_tc_vs_mma.txt)
+  {
+    const char* e = getenv("FL_GN_TC");
+    const bool want = e && atoi(e) != 0;
+    const GtGeom gm = gt_geom(SC, ng);
+    if (want && R == GT_R && t->pf <= 32 && ng <= GT_NG && gm.total + 1024 <= 227 * 1024) {
+      s->tc = true;
+      s->gm = gm;
+      if ((rc = make_tmap_2d(&s->tmWt, s->W.p, (uint64_t)t->r_pad, (uint64_t)R, (uint64_t)R * 4,
+                             GT_TILE, 32, 128)))
+        return rc;
+      if ((rc = make_tmap_2d(&s->tmFt, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
+                             (uint64_t)t->pf * 4, GT_TILE, 32, 128)))
+        return rc;
+      const int64_t ntiles = t->r_pad / GT_TILE;
+      s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+      GnTcArgs& ta = s->ta;
+      ta.pf = t->pf;
+      ta.c_T = c_T;
+      ta.SC = SC;
+      ta.QK = SC / 8;
+      ta.r_T = t->r_T;
+      ta.ntiles = ntiles;
+      ta.ng = ng;
+      ta.sort_g = t->sort_g;
+      for (int d = 0; d < ng; d++) {
+        ta.fk[d] = fa.fk[d];
+        ta.Gd[d] = fa.Gd[d];
+        ta.Z[d] = fa.Z[d];
+      }
+      ta.H32 = fa.H32;
+      ta.HH32 = fa.HH32;
+      ta.f_tcol = fa.f_tcol;
+      if ((rc = s->scratch.alloc((size_t)s->nblk_fact * GT_TILE * 32 * 8))) return rc;
+      ta.scratch = s->scratch.as<double>();
+      FL_CUDA(cudaFuncSetAttribute(k_gnmf_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(gm.total + 1024)));
+      FL_CUDA(cudaFuncSetAttribute(k_gnmf_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(gm.total + 1024)));
+    }
+  }
   const size_t WP = (size_t)MR * 16 * (SC + R);
   if ((rc = s->wpart.alloc((size_t)s->nblk_fact * GN_WARPS * WP * 8))) return rc;
   if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (R * SC + R * R) * 8))) return rc;
   fa.wpart = s->wpart.as<double>();
   fa.part = s->part_fact.as<double>();
+  s->ta.part = fa.part;
 
   // ---- dimension kernels
   GnDimArgs& da = s->da;
@@ -1024,7 +1092,7 @@ int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream)
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[2], st));
-    gn_fact_launch(s->NR, s->KC, true, s->tmW, s->tmF, s->fa, s->nblk_fact, s->smem_fact, st);
+    gn_fact_any(s, true, st);
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaEventRecord(ev[3], st));
     if (s->da.ng > 0) {

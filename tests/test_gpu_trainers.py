@@ -263,6 +263,26 @@ def test_gnmf_random_star_vs_oracle(fl, rank, dims, c_fact):
     assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
 
 
+@pytest.mark.parametrize("rank,dims,c_fact,tc", [(32, [(2000, 50)], 20, "1"),
+                                                 (32, [(2000, 50)], 20, "0"),
+                                                 (20, [(700, 9), (60, 4)], 28, "1"),
+                                                 (25, [], 32, "1"),
+                                                 (17, [(5000, 20)], 3, "1")])
+def test_gnmf_fact_pass_variants_vs_oracle(fl, rank, dims, c_fact, tc, monkeypatch):
+    """Both fact passes: tcgen05 (FL_GN_TC=1, csrc/gnmf_tc.cuh; rank tiles of
+    32, <= 32 streamed columns, several / no gathered sources, ragged last
+    tile) and the mma.sync pass (FL_GN_TC=0)."""
+    monkeypatch.setenv("FL_GN_TC", tc)
+    ft = star_table(37, 30_001, dims, c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    want = rt.gaussian_nmf(tab, 5, rank, 9)
+    res = fl.train("gnmf", fl.TargetHandle.factorized(ft),
+                   fl.TrainConfig(iterations=5, rank=rank, seed=9))
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+    assert max_rel(res.parameters["h"], want["parameters"]["h"]) < TOL
+    assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
+
+
 def test_gnmf_materialized_agrees(fl):
     g = load_golden("star3")
     m = g.meta["trainers"]["gnmf"]
