@@ -14,8 +14,14 @@ with CUDA events over `--iters` iterations after a warm-up.  Models whose
 fused kernels do not cover a width (K-means / GNMF on very wide materialized
 T) are recorded as unsupported.
 
-Output: a CSV corpus (one row per cell x model: shape, TR, FR, model,
-t_fact, t_mat per iteration, label = factorized faster) and a JSON summary.
+Output: a CSV table (one row per cell x model: shape, TR, FR, model,
+t_fact, t_mat per iteration, label = factorized faster), a JSON summary, and
+`<out>_corpus.csv`: the same runs as the reference estimator's training
+corpus (33-entry feature vectors of `paper_2502_01985_b200.costmodel`, which
+reproduces the reference's `extract_features` bit for bit, label, t_fact /
+t_mat of the whole `--iters`-iteration run, TR&FR decision; the reference's
+`estimator.read_corpus` format).  Hardware group: parallelism = SMs,
+memory bandwidth = MEASURED_PEAKS.json's HBM copy bandwidth.
 
     python bench_sweep.py [--rows 10000000] [--iters 10] [--out profiles/r01_c5_sweep]
 """
@@ -148,6 +154,25 @@ def main():
                      for m in models},
         "seconds": time.time() - t_start,
     }
+    # the estimator corpus (reference estimator.py:54-61 format)
+    from paper_2502_01985_b200 import costmodel as cm
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    bw = 6650e9
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        with open(pk) as fh:
+            bw = float(json.load(fh).get("hbm_gbs", 6650.0)) * 1e9
+    corpus = []
+    for r in sup:
+        prof = cm.Profile.star(R, C_FACT, [(r["r_dim"], r["c_dim"])])
+        f = cm.extract_features(prof, r["model"], args.iters, 8, 8, sms, bw)
+        if r["t_fact"] * args.iters == r["t_mat"] * args.iters:
+            continue   # exact tie: no label
+        corpus.append((f, r["t_fact"] * args.iters, r["t_mat"] * args.iters,
+                       cm.tr_fr_decision(prof)))
+    cm.write_corpus(args.out + "_corpus.csv", corpus)
+    summary["corpus"] = {"runs": len(corpus), "parallelism": sms, "memory_bandwidth": bw,
+                         "path": os.path.basename(args.out) + "_corpus.csv"}
     with open(args.out + ".json", "w") as fh:
         json.dump(summary, fh, indent=1)
     print(json.dumps(summary))

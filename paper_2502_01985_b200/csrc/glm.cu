@@ -525,9 +525,10 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u,
     const bool pb = tid < Gr * c4;
     const int pj = tid % c4, pg = tid / c4;
     double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-    for (int64_t i = 0; i < cnt; i++) {
-      const int s = (int)(i % a.nst);
-      int64_t row = (t0 + i) * TILE + tid;
+    // bins value of this thread's row of tile i (loaded one tile ahead, so
+    // the L2 latency overlaps the previous tile instead of stalling the CTA)
+    auto load_b = [&](int64_t i) -> float {
+      const int64_t row = (t0 + i) * TILE + tid;
       float b = 0.f;
       if (row < rows) {
         if (a.bins[d]) {
@@ -537,6 +538,13 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u,
           for (int64_t m = m0; m < m1; m++) b += a.resid[a.grp_rows[d][m]];
         }
       }
+      return b;
+    };
+    float b_next = cnt > 0 ? load_b(0) : 0.f;
+    for (int64_t i = 0; i < cnt; i++) {
+      const int s = (int)(i % a.nst);
+      const float b = b_next;
+      if (i + 1 < cnt) b_next = load_b(i + 1);
       b_s[tid] = b;
       mbar_wait(&bar[s], (uint32_t)((i / a.nst) & 1));
       __syncthreads();

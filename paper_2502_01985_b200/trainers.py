@@ -197,7 +197,7 @@ class GlmSession:
         return w, loss[:min(done.value, n)]
 
     def close(self):
-        if self.ptr:
+        if getattr(self, "ptr", None):
             try:
                 _lib.load().fl_glm_destroy(self.ptr)
             except Exception:
@@ -326,7 +326,7 @@ class KMeansSession:
         return cents, assign.astype(np.int64), loss[:min(done.value, n)]
 
     def close(self):
-        if self.ptr:
+        if getattr(self, "ptr", None):
             try:
                 _lib.load().fl_kmeans_destroy(self.ptr)
             except Exception:
@@ -498,7 +498,7 @@ class GnmfSession:
         return w, hh, loss[:min(done.value, n)]
 
     def close(self):
-        if self.ptr:
+        if getattr(self, "ptr", None):
             try:
                 _lib.load().fl_gnmf_destroy(self.ptr)
             except Exception:

@@ -29,7 +29,8 @@ def pytest_configure(config):
 
 def golden_names():
     return sorted(os.path.basename(p)[:-4]
-                  for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+                  for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                  if os.path.basename(p) != "features.npz")
 
 
 class Golden(dict):
