@@ -1,3 +1,12 @@
+#!/usr/bin/env python
+"""Per-CUDA-line work of an ncu --set full capture, normalised per work unit:
+instructions, L1 shared-memory wavefronts (and the ideal count), global L1
+tag requests and the share of warp-stall samples.
+
+    python tools/ncu_lines.py <rep> <units> [top] [sort-column 0..4]
+
+units = work units in the captured launch (e.g. 32-row units of a fact pass).
+"""
 import csv,io,sys,subprocess
 rep=sys.argv[1]; units=float(sys.argv[2])
 out=subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","cuda,sass"],capture_output=True,text=True).stdout
