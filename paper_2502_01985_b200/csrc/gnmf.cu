@@ -467,74 +467,36 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
         const uint32_t bl0 = lo_bits(b0), bl1 = lo_bits(b1);
 #pragma unroll
         for (int m = 0; m < MR; m++) {
+          // G = W^T W is symmetric: tiles strictly below the diagonal are
+          // skipped (the reduction reads their transposes)
+          if (n < 2 * m) continue;
           mma_tf32(gacc[m][n], ah[m][0], ah[m][1], ah[m][2], ah[m][3], bh0, bh1);
           mma_tf32(gacc[m][n], alo[m][0], alo[m][1], alo[m][2], alo[m][3], bh0, bh1);
           mma_tf32(gacc[m][n], ah[m][0], ah[m][1], ah[m][2], ah[m][3], bl0, bl1);
         }
       }
     }
-    // ---- Z_d[fk] += W rows: segment one-hot (runs of equal FK) x W, fp64
-    // atomics of the per-segment fp32 partials (sums of fp32 values in fp64
-    // are exact here, so the result does not depend on their order)
+    // ---- Z_d[fk] += W rows: lane = rank column, the unit's 32 rows in order,
+    // one fp64 atomic per run of equal FK (run ends from one ballot).  Sums
+    // of the fp32 run partials are exact in fp64 here, so the result does
+    // not depend on the order the atomics land in.
 #pragma unroll
     for (int d = 0; d < MAX_GATHER; d++) {
       if (d >= a.ng) break;
       const int key = fkl[d];
-      const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
-      const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || key != kprev);
-      const int slot = __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
-      const int nslots = __popc(starts);
-      const int MS = nslots > 16 ? 2 : 1;
-      float zc[2][NR][4];
-#pragma unroll
-      for (int m = 0; m < 2; m++)
-#pragma unroll
-        for (int n = 0; n < NR; n++)
-#pragma unroll
-          for (int e = 0; e < 4; e++) zc[m][n][e] = 0.f;
-#pragma unroll
-      for (int kb = 0; kb < 4; kb++) {
-        const int r0 = kb * 8 + t, r1 = r0 + 4;
-        const int s0 = __shfl_sync(0xffffffffu, slot, r0);
-        const int s1 = __shfl_sync(0xffffffffu, slot, r1);
-        uint32_t bh[NR][2], bl[NR][2];
-#pragma unroll
-        for (int n = 0; n < NR; n++) {
-          const float b0 = Wt[widx<R>(r0, n * 8 + g)], b1 = Wt[widx<R>(r1, n * 8 + g)];
-          bh[n][0] = hi_bits(b0);
-          bh[n][1] = hi_bits(b1);
-          bl[n][0] = lo_bits(b0);
-          bl[n][1] = lo_bits(b1);
-        }
-#pragma unroll
-        for (int m = 0; m < 2; m++) {
-          if (m >= MS) break;
-          const int j0 = m * 16 + g, j1 = j0 + 8;
-          const uint32_t o0 = s0 == j0 ? kTf32One : 0u, o1 = s0 == j1 ? kTf32One : 0u;
-          const uint32_t o2 = s1 == j0 ? kTf32One : 0u, o3 = s1 == j1 ? kTf32One : 0u;
-#pragma unroll
-          for (int n = 0; n < NR; n++) {
-            mma_tf32(zc[m][n], o0, o1, o2, o3, bh[n][0], bh[n][1]);
-            mma_tf32(zc[m][n], o0, o1, o2, o3, bl[n][0], bl[n][1]);
-          }
+      const int knext = __shfl_down_sync(0xffffffffu, key, 1);
+      const unsigned ends = __ballot_sync(0xffffffffu, lane == 31 || knext != key);
+      const int col = lane < R ? lane : 0;
+      float run = 0.f;
+#pragma unroll 8
+      for (int p = 0; p < 32; p++) {
+        run += Wt[widx<R>(p, col)];
+        if ((ends >> p) & 1u) {
+          const int k = __shfl_sync(0xffffffffu, key, p);
+          if (k >= 0 && lane < R) atomicAdd(a.Z[d] + (int64_t)k * R + lane, (double)run);
+          run = 0.f;
         }
       }
-#pragma unroll
-      for (int m = 0; m < 2; m++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int sl = m * 16 + h * 8 + g;
-          const int start = sl < nslots ? (int)__fns(starts, 0, sl + 1) : 0;
-          const int skey = __shfl_sync(0xffffffffu, key, start & 31);
-          if (sl < nslots && skey >= 0) {
-            double* zr = a.Z[d] + (int64_t)skey * R + 2 * t;
-#pragma unroll
-            for (int n = 0; n < NR; n++) {
-              atomicAdd(zr + n * 8, (double)zc[m][n][h * 2]);
-              atomicAdd(zr + n * 8 + 1, (double)zc[m][n][h * 2 + 1]);
-            }
-          }
-        }
     }
     __syncwarp();
     if (lane == 0 && i + a.nst < cnt) {
@@ -993,8 +955,13 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
     for (int j = 0; j < R; j++) {
       for (int c = 0; c < t->pf; c++)
         if (t->f_tcol[c] >= 0) dv.push_back(RedDesc{pfb + j * SC + c, fst, s->nblk_fact, j * c_T + t->f_tcol[c], 0});
-      for (int q = 0; q < R; q++)
-        dv.push_back(RedDesc{pfb + R * SC + j * R + q, fst, s->nblk_fact, R * c_T + j * R + q, 0});
+      for (int q = 0; q < R; q++) {
+        // the fact pass skips G tiles strictly below the diagonal (rank rows
+        // 16..31 x columns 0..15 when R = 32): read the transposed entry
+        const bool lower = R == 32 && j >= 16 && q < 16;
+        const int src = lower ? q * R + j : j * R + q;
+        dv.push_back(RedDesc{pfb + R * SC + src, fst, s->nblk_fact, R * c_T + j * R + q, 0});
+      }
     }
     for (int d = 0; d < ng; d++) {
       const int cols = t->g[d].cols;
