@@ -908,8 +908,10 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.Gd[d] = const_cast<float*>(fa.Gd[d]);
     da.Z[d] = fa.Z[d];
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 256),
-                                                               (int64_t)t->sm_count * 2));
+    // many short row ranges: each CTA walks its 32-row tiles with plain
+    // loads, so latency hiding comes from CTAs in flight (6 per SM)
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 64),
+                                                               (int64_t)t->sm_count * 6));
     da.nblk[d] = nb;
     s->grid_p = std::max(s->grid_p, nb);
     max_cols = std::max(max_cols, g.cols);

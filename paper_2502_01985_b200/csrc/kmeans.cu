@@ -1019,8 +1019,10 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.E[d] = const_cast<float*>(fa.E[d]);
     da.cnt[d] = fa.cnt[d];
-    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 256),
-                                                         (int64_t)t->sm_count * 2));
+    // many short row ranges: each CTA walks its 32-row tiles with plain
+    // loads, so latency hiding comes from CTAs in flight (6 per SM)
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 64),
+                                                         (int64_t)t->sm_count * 6));
     da.nblk[d] = nb;
     s->grid_sum = std::max(s->grid_sum, nb);
     max_cols = std::max(max_cols, g.cols);
