@@ -470,24 +470,37 @@ __device__ void glm_apply_update(const UpdateArgs& u) {
 }
 
 __device__ void glm_reduce_all(const UpdateArgs& u) {
-  const int tid = threadIdx.x;
+  // one warp per output element (fixed-order lane sums + a fixed xor tree:
+  // deterministic), so the ~300 partial loads of every element are in flight
+  // together instead of walking one chain per thread
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int c = tid; c <= u.c_T; c += blockDim.x) u.red[c] = 0.0;
   __syncthreads();
   const int pf1 = u.pf + 1;
-  for (int j = tid; j < pf1; j += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < u.nblk_fact; b++) s += u.part_fact[(int64_t)b * pf1 + j];
-    if (j == u.pf) u.red[u.c_T] = s;
-    else if (u.f_tcol[j] >= 0) u.red[u.f_tcol[j]] = s;
-  }
-  for (int d = 0; d < u.ng; d++) {
-    for (int c = tid; c < u.pitch[d]; c += blockDim.x) {
-      int tc = u.d_tcol[d][c];
-      if (tc < 0) continue;
-      double s = 0.0;
-      for (int b = 0; b < u.nblk_dim[d]; b++) s += u.part_dim[d][(int64_t)b * u.pitch[d] + c];
-      u.red[tc] = s;
+  int total = pf1;
+  for (int d = 0; d < u.ng; d++) total += u.pitch[d];
+  for (int e = warp; e < total; e += nw) {
+    const double* base;
+    int stride, nblk, dst;
+    if (e < pf1) {
+      base = u.part_fact + e;
+      stride = pf1;
+      nblk = u.nblk_fact;
+      dst = e == u.pf ? u.c_T : u.f_tcol[e];
+    } else {
+      int c = e - pf1, d = 0;
+      while (c >= u.pitch[d]) c -= u.pitch[d++];
+      base = u.part_dim[d] + c;
+      stride = u.pitch[d];
+      nblk = u.nblk_dim[d];
+      dst = u.d_tcol[d][c];
     }
+    if (dst < 0) continue;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += base[(int64_t)b * stride];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) u.red[dst] = s;
   }
   __syncthreads();
 }
