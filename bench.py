@@ -633,6 +633,9 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
     torch.cuda.synchronize()
 
     def job(J):
+        import gc
+        gc.collect()              # the previous job's device buffers are freed outside the timing
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         h2 = fl.TargetHandle.from_arrays([t.numpy() for t in host],
                                          [None] + [f.numpy() for f in fks], maps, sh["rows"], c_t)
@@ -640,31 +643,41 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
         t_up = time.perf_counter()
         if wl["model"] in ("linreg", "logreg"):
             s2 = GlmSession(h2, wl["model"], y_h.numpy(), hyper["learning_rate"])
+            torch.cuda.synchronize()
+            t_s = time.perf_counter()
             s2.run(J)
+            torch.cuda.synchronize()
+            t_r = time.perf_counter()
             w, losses = s2.result(J)
             d2h = 8 * (c_t + J)
         else:
             from paper_2502_01985_b200.trainers import kmeans_init
             s2 = KMeansSession(h2, wl["k"], kmeans_init(h2, wl["k"], 0))
+            torch.cuda.synchronize()
+            t_s = time.perf_counter()
             s2.run(J)
+            torch.cuda.synchronize()
+            t_r = time.perf_counter()
             cents, assign, losses = s2.result(J)
             d2h = 8 * (wl["k"] * c_t + J) + 4 * sh["rows"]
         t1 = time.perf_counter()
         s2.close()
         del h2
         torch.cuda.empty_cache()
-        return t1 - t0, t_up - t0, d2h
+        return t1 - t0, t_up - t0, d2h, (t_up - t0, t_s - t_up, t_r - t_s, t1 - t_r)
 
     J = args.e2e_iters
     job(3)                                     # warm-up job (allocator, module load)
     runs = sorted(job(J) for _ in range(3))    # median of three timed jobs
-    t_job, t_up, d2h = runs[1]
+    t_job, t_up, d2h, phases = runs[1]
     h2d = sum(t.numel() * t.element_size() for t in host + fks) + (
         y_h.numel() * y_h.element_size() if y_h is not None else 0)
     return {"value": J / t_job, "unit": UNIT, "h2d_bytes_per_step": h2d / J,
             "d2h_bytes_per_step": d2h / J, "iterations_per_job": J,
             "job_seconds": t_job, "upload_layout_seconds": t_up,
             "h2d_gbs": h2d / t_up / 1e9, "jobs_seconds": [r[0] for r in runs],
+            "phases_seconds": dict(zip(("upload_layout", "session", "iterations", "readback"),
+                                       phases)),
             "note": ("one job through the public API from pinned host buffers: H2D of all "
                      "inputs + device layout (FK sort) + J iterations + D2H of the model and "
                      "losses, amortised per iteration; median of 3 jobs after a warm-up job")}
