@@ -486,6 +486,45 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
       const int key = fkl[d];
       const int knext = __shfl_down_sync(0xffffffffu, key, 1);
       const unsigned ends = __ballot_sync(0xffffffffu, lane == 31 || knext != key);
+      if (__popc(ends) <= 2) {
+        // one or two runs cover the unit (the common case for the sorted
+        // source): lane = (4-column group, row group), float4 row reads into
+        // one accumulator per run, then a fixed xor tree over the row groups
+        constexpr int CG = R / 4, RG = 32 / CG;
+        const int cg = lane % CG, rg = lane / CG;
+        const int last0 = __ffs(ends) - 1;           // last row of the first run
+        float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+#pragma unroll
+        for (int k = 0; k < CG; k++) {
+          const int p = rg * CG + k;
+          const float4 v = *reinterpret_cast<const float4*>(Wt + widx<R>(p, cg * 4));
+          const float m0 = p <= last0 ? 1.f : 0.f, m1 = 1.f - m0;   // exact 0 / 1 weights
+          acc[0].x = fmaf(m0, v.x, acc[0].x); acc[0].y = fmaf(m0, v.y, acc[0].y);
+          acc[0].z = fmaf(m0, v.z, acc[0].z); acc[0].w = fmaf(m0, v.w, acc[0].w);
+          acc[1].x = fmaf(m1, v.x, acc[1].x); acc[1].y = fmaf(m1, v.y, acc[1].y);
+          acc[1].z = fmaf(m1, v.z, acc[1].z); acc[1].w = fmaf(m1, v.w, acc[1].w);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          const int k2 = __shfl_sync(0xffffffffu, key, u == 0 ? last0 : 31);
+          if (u == 1 && last0 == 31) break;
+#pragma unroll
+          for (int o = CG; o < 32; o <<= 1) {
+            acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, o);
+            acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, o);
+            acc[u].z += __shfl_xor_sync(0xffffffffu, acc[u].z, o);
+            acc[u].w += __shfl_xor_sync(0xffffffffu, acc[u].w, o);
+          }
+          if (k2 >= 0 && rg == 0) {
+            double* zr = a.Z[d] + (int64_t)k2 * R + cg * 4;
+            atomicAdd(zr + 0, (double)acc[u].x);
+            atomicAdd(zr + 1, (double)acc[u].y);
+            atomicAdd(zr + 2, (double)acc[u].z);
+            atomicAdd(zr + 3, (double)acc[u].w);
+          }
+        }
+        continue;
+      }
       const int col = lane < R ? lane : 0;
       float run = 0.f;
 #pragma unroll 8
