@@ -100,6 +100,8 @@ struct Staged {            // source data between add_source and finalize
   std::shared_ptr<DevBuf> vals;     // rows x cols fp32 (compact)
   std::shared_ptr<DevBuf> ind_sel;  // r_T int32 (target order)
   std::vector<int32_t> col_map;     // cols target columns
+  // the uploads run on the table's copy streams; finalize waits on these
+  std::shared_ptr<void> ev_vals, ev_idx;   // cudaEvent_t (owned)
 };
 
 struct Workspace {
@@ -118,6 +120,9 @@ struct fl_table {
   int64_t r_pad = 0;
   bool finalized = false;
   std::vector<flb::Staged> staged;
+  // copy streams of the staged uploads (values / FKs): the FK-only part of
+  // finalize (sorts, fanout, device order) overlaps the value copies
+  std::shared_ptr<void> cp_vals, cp_idx;   // cudaStream_t (owned)
   std::vector<flb::SrcInfo> src;
   // stream block
   int pf = 0;                        // pitch of F in floats (0 = no stream source)

@@ -334,14 +334,54 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
   if (rc) return rc;
   st.ind_sel = make_buf((size_t)t->r_T * 4, &rc);
   if (rc) return rc;
-  FL_CUDA(cudaMemcpy(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault));
-  if (ind_sel) {
-    FL_CUDA(cudaMemcpy(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault));
-  } else {  // identity indicator (the fact table of a star schema)
-    k_iota_perm<<<grid_for(t->r_T), 256>>>(st.ind_sel->as<int32_t>(), t->r_T, t->r_T);
-    FL_CHECK_LAUNCH();
-    FL_CUDA(cudaDeviceSynchronize());
+  // asynchronous uploads on the table's copy streams (values and FKs on
+  // separate streams, so the FKs land early and finalize's index work
+  // overlaps the large value copies); the caller keeps `values` / `ind_sel`
+  // valid until fl_table_finalize returns
+  auto mk_stream = []() -> std::shared_ptr<void> {
+    cudaStream_t cs = nullptr;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    return std::shared_ptr<void>(cs, [](void* p) { cudaStreamDestroy((cudaStream_t)p); });
+  };
+  auto mk_event = []() -> std::shared_ptr<void> {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    return std::shared_ptr<void>(e, [](void* p) { cudaEventDestroy((cudaEvent_t)p); });
+  };
+  if (!t->cp_vals) t->cp_vals = mk_stream();
+  if (!t->cp_idx) t->cp_idx = mk_stream();
+  st.ev_vals = mk_event();
+  st.ev_idx = mk_event();
+  if (!t->cp_vals || !t->cp_idx || !st.ev_vals || !st.ev_idx) {
+    set_error("fl_table_add_source: stream / event creation failed");
+    return FL_ERR_CUDA;
   }
+  cudaStream_t cv = (cudaStream_t)t->cp_vals.get(), ci = (cudaStream_t)t->cp_idx.get();
+  // device operands may still be in flight on the caller's streams: copy
+  // them synchronously (as cudaMemcpy orders them); host buffers go async
+  auto on_device = [](const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  };
+  if (ind_sel) {
+    if (on_device(ind_sel))
+      FL_CUDA(cudaMemcpy(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault));
+    else
+      FL_CUDA(cudaMemcpyAsync(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault, ci));
+  } else {  // identity indicator (the fact table of a star schema)
+    k_iota_perm<<<grid_for(t->r_T), 256, 0, ci>>>(st.ind_sel->as<int32_t>(), t->r_T, t->r_T);
+    FL_CHECK_LAUNCH();
+  }
+  FL_CUDA(cudaEventRecord((cudaEvent_t)st.ev_idx.get(), ci));
+  if (on_device(values))
+    FL_CUDA(cudaMemcpy(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault));
+  else
+    FL_CUDA(cudaMemcpyAsync(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault, cv));
+  FL_CUDA(cudaEventRecord((cudaEvent_t)st.ev_vals.get(), cv));
   t->staged.push_back(std::move(st));
   return FL_OK;
 }
@@ -356,6 +396,9 @@ int fl_table_finalize(fl_table* t, void* stream) {
   const int64_t r_T = t->r_T, r_pad = t->r_pad;
   int rc;
   const int n = (int)t->staged.size();
+  // the index work below needs every FK array; the values are waited for
+  // just before their first use (stream block / gathered copies)
+  for (auto& st : t->staged) FL_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)st.ev_idx.get(), 0));
   // column disjointness (metadata.py:196-206)
   std::vector<int> owner(t->c_T, -1);
   for (int k = 0; k < n; k++)
@@ -439,7 +482,8 @@ int fl_table_finalize(fl_table* t, void* stream) {
   k_inverse_perm<<<grid_for(r_T), 256, 0, s>>>(t->perm->as<int32_t>(), r_T,
                                                t->iperm->as<int32_t>());
   FL_CHECK_LAUNCH();
-  // 3. stream block F
+  // 3. stream block F (from here on the values are read)
+  for (auto& st : t->staged) FL_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)st.ev_vals.get(), 0));
   // every table gets a stream block; a table with no injective source keeps
   // a 4-column all-zero block so the fused passes have one code path
   t->nf = stream_cols;

@@ -87,6 +87,7 @@ def upload_arrays(sources, ind_sels, col_maps, r_T: int, c_T: int, *,
     ptr = C.c_void_p()
     _lib.check(lib.fl_table_create(device, int(r_T), int(c_T), C.byref(ptr)), "fl_table_create")
     tab = DeviceTable(ptr, int(r_T), int(c_T), len(sources), device)
+    alive = []   # host buffers must outlive the asynchronous uploads (until finalize)
     for vals, sel, cmap in zip(sources, ind_sels, col_maps):
         if _is_torch(vals):
             v_ptr, r_k, c_k = vals.data_ptr(), vals.shape[0], vals.shape[1]
@@ -105,9 +106,10 @@ def upload_arrays(sources, ind_sels, col_maps, r_T: int, c_T: int, *,
         _lib.check(lib.fl_table_add_source(ptr, int(r_k), int(c_k), C.c_void_p(v_ptr),
                                            C.c_void_p(s_ptr), m_keep.ctypes.data_as(C.c_void_p)),
                    "fl_table_add_source")
-        del keep, s_keep
+        alive.append((keep, s_keep, m_keep))
     _lib.check(lib.fl_table_finalize(ptr, stream if stream is not None else C.c_void_p(0)),
                "fl_table_finalize")
+    del alive
     return tab
 
 
