@@ -11,7 +11,8 @@ from .metadata import (JOIN_TYPES, FactorizedTable, IndicatorMatrix,
                        MappingMatrix, MetadataError, ValidationReport,
                        block_mapping, fk_indicator, redundancy_stats)
 from .ops import OpError, TargetHandle, export_trace_csv
-from .sparse import OpTrace, ShapeError, SparseMatrix, SparseStructureError
+from .sparse import OpTrace, ShapeError, SparseMatrix, SparseStructureError, as_dense
+from . import costmodel, formats
 from .trainers import (ConfigError, DivergenceError, TrainConfig, TrainResult,
                        gaussian_nmf, kmeans, linear_regression,
                        logistic_regression, train)
@@ -25,7 +26,7 @@ def materialize(ft, *, device: int = 0, check: bool = True) -> SparseMatrix:
     return TargetHandle.factorized(ft, check=check, device=device).materialize_target()
 
 
-__all__ = ["ConfigError", "DivergenceError", "FactorizedTable", "IndicatorMatrix",
+__all__ = ["as_dense", "costmodel", "formats", "ConfigError", "DivergenceError", "FactorizedTable", "IndicatorMatrix",
            "JOIN_TYPES", "MappingMatrix", "MetadataError", "OpError", "OpTrace",
            "ShapeError", "SparseMatrix", "SparseStructureError", "TargetHandle",
            "TrainConfig", "TrainResult", "ValidationReport", "block_mapping",
