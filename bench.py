@@ -56,6 +56,10 @@ WORKLOADS = {
     "c2": dict(model="logreg", rows=100_000_000, c_fact=20, dims=[(1_000_000, 50)],
                desc="C2: 2-source star, fact 100M x 20 + dim 1M x 50 (TR 100), "
                     "factorized logistic regression GD"),
+    "c2s": dict(model="logreg", rows=100_000_000, c_fact=20, dims=[(1_000_000, 50)],
+                density=0.1,
+                desc="C2-sparse (SURVEY.md §8 row f3): C2 with 90% of the fact values zero, "
+                     "factorized logistic regression GD on the CSR stream block"),
     "c3": dict(model="kmeans", rows=10_000_000, c_fact=20, dims=[(100_000, 60), (10_000, 5)],
                k=16, desc="C3: 3-source star, fact 10M x 20 + dims 100K x 60 (TR 100) and "
                           "10K x 5 (TR 1000), K-means k=16, planted clusters"),
@@ -186,6 +190,8 @@ def make_shard(torch, wl, rank, world, device, seed=1234):
                        .to(torch.int32))
     else:
         fact = torch.rand((rows, c_f), generator=g, device=device, dtype=torch.float32)
+        if wl.get("density"):    # sparse fact table (c2s): zero 1 - density of the values
+            fact *= (torch.rand((rows, c_f), generator=g, device=device) < wl["density"])
         dims.append(torch.rand((d1 - d0, c_d0), generator=g, device=device))
         fks.append(fk0.to(torch.int32))
         grep = torch.Generator(device=device)
@@ -437,7 +443,7 @@ def main():
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.steps is None:
-        args.steps = {"c1": 100, "c2": 200, "c3": 100, "c4": 20}[args.workload]
+        args.steps = {"c1": 100, "c2": 200, "c2s": 200, "c3": 100, "c4": 20}[args.workload]
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
@@ -517,6 +523,15 @@ def main():
     d0, d1 = sh["dim0"]
     dims_local = [(d1 - d0, wl["dims"][0][1])] + list(wl["dims"][1:])
     fact_bytes, iter_bytes = algorithmic_bytes(wl, sh["rows"], dims_local, lay)
+    if wl["model"] in ("linreg", "logreg") and sess.path[0] == "csr":
+        # CSR stream block: row extents (8 B/row) + 6 B per nonzero replace 4 pf B/row
+        dens = sess.path[1]
+        csr_bytes = sh["rows"] * (8 + 6 * dens * lay["stream_cols"]) - \
+            sh["rows"] * 4 * lay["stream_pitch"]
+        fact_bytes += csr_bytes
+        iter_bytes += csr_bytes
+        kernel = "k_glm_fact_csr"
+        hyper["stream_density"] = dens
     peak, peak_src = measured_peaks()
     achieved = fact_bytes / (kt[fact_idx] * 1e-3) / 1e9
     traffic = None

@@ -137,6 +137,11 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream);
 /* measurement hook: run `iters` iterations launching K1 / K2 / K3 separately
  * with CUDA events between them on `stream`; ms_out[3] = mean ms per kernel
  * (K1 includes the bins memset).  Advances the model like fl_glm_run. */
+/* Which fact pass the session runs: 0 CTA tiles, 1 per-warp TMA pipelines
+ * (dense stream block), 2 CSR stream block (sparse F),
+ * 3 generic operators.  stream_density: measured nonzero density of the
+ * real stream columns (1.0 when not measured). */
+int fl_glm_path(fl_glm* s, int32_t* path, double* stream_density);
 int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream);
 /* copy out w (c_T fp64) and the first n losses (fp64); host or device */
 int fl_glm_result(fl_glm* s, double* w, double* loss, int32_t n, int32_t* n_done, void* stream);

@@ -18,6 +18,8 @@
 //
 // Algorithmic HBM bytes per iteration:
 //   4 r_T pf + 4 r_T n_gather + b_y r_T + sum_d 2 * 4 r_d pitch_d (+ 4 r_T if resid)
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -447,6 +449,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_glm_fact(GlmFactArgs a) {
 }
 
 #include "glm_fact_warp.cuh"
+#include "glm_fact_csr.cuh"
+// auto-selection threshold of the CSR pass: it must beat the dense pass,
+// which streams F at the HBM roofline (profiles/r01_glm_csr.txt)
+constexpr double kCsrAutoDensity = 0.0;
 
 // ---------------------------------------------------------------------------
 // update: w <- w - lr * red; loss_hist[it] = red[c_T]; refresh fp32 copies
@@ -723,6 +729,12 @@ struct fl_glm {
   int dim_grid_x = 0;
   DevBuf y, wF, wd, w64, q, bins, resid, part_fact, part_dim, carry, red, loss_hist, state;
   DevBuf fw_carry, fw_part;
+  // sparse stream block (CSR copy of F, f3)
+  bool use_csr = false;
+  GlmCsrArgs csr{};
+  DevBuf csr_rp, csr_col, csr_val;
+  size_t smem_csr = 0;
+  double csr_density = 1.0;
   GlmFactArgs fa{};
   DimArgs da{};
   UpdateArgs ua{};
@@ -783,7 +795,12 @@ static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
     k_glm_dim_q<<<grid, NTHREADS, s->smem_dim, st>>>(s->da);
     FL_CHECK_LAUNCH();
   }
-  if (s->use_fw)
+  if (s->use_csr) {
+    if (s->model == FL_MODEL_LINREG)
+      k_glm_fact_csr<0><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
+    else
+      k_glm_fact_csr<1><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
+  } else if (s->use_fw)
     fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st);
   else if (s->model == FL_MODEL_LINREG)
     k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
@@ -1012,6 +1029,84 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     }
   }
 
+  // sparse stream block: when F is sparse, a CSR copy
+  // (device order) feeds k_glm_fact_csr, which reads 6 bytes per nonzero
+  // instead of 4 bytes per entry.  FL_GLM_SPARSE: unset = auto (density of
+  // the real stream columns < kCsrAutoDensity), 1 = force, 0 = never.
+  {
+    const char* e = getenv("FL_GLM_SPARSE");
+    const int mode = e ? atoi(e) : -1;
+    if (mode != 0 && s->use_fw && t->pf <= CSR_MAXP && t->nf > 0) {
+      DevBuf cnt;
+      if ((rc = cnt.alloc((size_t)(r_pad + 1) * 8))) return rc;
+      FL_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)(r_pad + 1) * 8, st));
+      const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(r_pad, 256), 65535);
+      k_csr_count<<<gb, 256, 0, st>>>(t->F->as<float>(), r_pad, t->pf, cnt.as<int64_t>());
+      FL_CHECK_LAUNCH();
+      if ((rc = s->csr_rp.alloc((size_t)(r_pad + 1) * 8))) return rc;
+      size_t tb = 0;
+      FL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int64_t>(), s->csr_rp.as<int64_t>(),
+                                            r_pad + 1, st));
+      DevBuf tmp;
+      if ((rc = tmp.alloc(tb + 16))) return rc;
+      FL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int64_t>(), s->csr_rp.as<int64_t>(),
+                                            r_pad + 1, st));
+      int64_t nnz = 0;
+      FL_CUDA(cudaMemcpyAsync(&nnz, s->csr_rp.as<int64_t>() + r_pad, 8, cudaMemcpyDeviceToHost, st));
+      FL_CUDA(cudaStreamSynchronize(st));
+      s->csr_density = (double)nnz / ((double)std::max<int64_t>(1, t->r_T) * t->nf);
+      if (mode == 1 || s->csr_density < kCsrAutoDensity) {
+        if ((rc = s->csr_col.alloc((size_t)nnz * 2 + 16))) return rc;
+        if ((rc = s->csr_val.alloc((size_t)nnz * 4 + 16))) return rc;
+        k_csr_fill<<<gb, 256, 0, st>>>(t->F->as<float>(), r_pad, t->pf, s->csr_rp.as<int64_t>(),
+                                       s->csr_col.as<uint16_t>(), s->csr_val.as<float>());
+        FL_CHECK_LAUNCH();
+        GlmCsrArgs& ca = s->csr;
+        ca.rp = s->csr_rp.as<int64_t>();
+        ca.col = s->csr_col.as<uint16_t>();
+        ca.val = s->csr_val.as<float>();
+        ca.pf = t->pf;
+        ca.y = s->fw.y;
+        ca.r_T = t->r_T;
+        ca.nunits = r_pad / 32;
+        ca.ng = s->fw.ng;
+        ca.sort_g = s->fw.sort_g;
+        for (int d = 0; d < ng; d++) {
+          ca.fk[d] = s->fw.fk[d];
+          ca.q[d] = s->fw.q[d];
+        }
+        ca.bins = s->fw.bins;
+        ca.resid = s->fw.resid;
+        ca.wF = s->fw.wF;
+        ca.state = s->fw.state;
+        s->smem_csr = ((size_t)round_up(t->pf, 4) + (size_t)FW_WARPS * 32 * (t->pf | 1) + 1) * 4 +
+                      (size_t)FW_WARPS * 32 * CSR_K * 8;
+        for (int m = 0; m < 2; m++) {
+          const void* kc = m == 0 ? (const void*)k_glm_fact_csr<0> : (const void*)k_glm_fact_csr<1>;
+          FL_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)s->smem_csr));
+        }
+        int occc = 1;
+        FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occc, model == 0 ? (const void*)k_glm_fact_csr<0> : (const void*)k_glm_fact_csr<1>,
+            FW_WARPS * 32, s->smem_csr));
+        occc = std::max(1, occc);
+        const int64_t want = ceil_div(ca.nunits, FW_WARPS);
+        s->nblk_fw = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)t->sm_count * occc));
+        if ((rc = s->fw_carry.alloc((size_t)s->nblk_fw * FW_WARPS * sizeof(WarpCarry)))) return rc;
+        if ((rc = s->fw_part.alloc((size_t)s->nblk_fw * (t->pf + 1) * 8))) return rc;
+        ca.carry = s->fw_carry.as<WarpCarry>();
+        ca.part = s->fw_part.as<double>();
+        s->fw.carry = ca.carry;
+        s->fw.part = ca.part;
+        s->use_csr = true;
+      } else {
+        s->csr_rp.alloc(16);   // dense pass: release the extents
+      }
+      FL_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+
   // dim geometry
   DimArgs& da = s->da;
   da.ng = ng;
@@ -1140,6 +1235,16 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
   return FL_OK;
 }
 
+int fl_glm_path(fl_glm* s, int32_t* path, double* stream_density) {
+  if (!s) {
+    set_error("fl_glm_path: null session");
+    return FL_ERR_ARG;
+  }
+  if (path) *path = s->unfused ? 3 : s->use_csr ? 2 : s->use_fw ? 1 : 0;
+  if (stream_density) *stream_density = s->csr_density;
+  return FL_OK;
+}
+
 int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
   if (!s || iters < 1 || !ms_out) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
@@ -1176,7 +1281,12 @@ int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[1], st));
-    if (s->use_fw)
+    if (s->use_csr) {
+      if (s->model == FL_MODEL_LINREG)
+        k_glm_fact_csr<0><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
+      else
+        k_glm_fact_csr<1><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
+    } else if (s->use_fw)
       fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st);
     else if (s->model == FL_MODEL_LINREG)
       k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);

@@ -1,0 +1,317 @@
+// K2 for SPARSE stream blocks: the GLM fact-row pass
+// over a CSR copy of the stream block F (device row order).  Per nonzero
+// only its value (fp32) and column (uint16) are read, so at density rho the
+// pass moves ~6 rho pf + 8 bytes per row of F instead of 4 pf.
+//
+// One warp owns a contiguous range of 32-row units (lane = row).  Per row:
+//   z = sum_nz v w_F[col] + sum_d q_d[fk_d]        (w_F in smem)
+//   r = z - y | sigmoid(z) - y, loss
+//   grad_F[col] += r v  into a LANE-PRIVATE smem row (deterministic: the
+//                       32 lane rows are folded in a fixed order every
+//                       FW_FLUSH units, fp32 -> fp64)
+//   bins_sort[fk] += r  (the dense pass's warp segmented scan + carries)
+// (included inside namespace flb by glm.cu)
+#pragma once
+
+struct GlmCsrArgs {
+  const int64_t* rp;         // r_pad + 1 row extents (device order)
+  const uint16_t* col;       // nnz stream-block columns
+  const float* val;          // nnz values
+  int pf;                    // gradient width (stream pitch)
+  const void* y;
+  int64_t r_T, nunits;       // units of 32 device rows
+  int ng, sort_g;
+  const int32_t* fk[MAX_GATHER];
+  const float* q[MAX_GATHER];
+  float* bins;
+  float* resid;
+  const float* wF;
+  double* part;              // gridDim.x x (pf + 1)
+  WarpCarry* carry;          // gridDim.x * FW_WARPS
+  GlmState* state;
+};
+
+constexpr int CSR_MAXP = 128;   // stream pitch handled by the sparse pass
+
+constexpr int CSR_K = 4;        // nonzeros per lane staged per unit (128 per 32 rows)
+
+template <int MODEL>
+__global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
+  // smem: w_F | per-warp lane-private gradient rows (32 x GP) | per-warp
+  // staged nonzeros of the current unit (32 CSR_K x {col, val})
+  extern __shared__ __align__(16) float csr_sm[];
+  __shared__ double gsum[FW_WARPS][CSR_MAXP];
+  __shared__ double lsum[FW_WARPS];
+  __shared__ int is_last;
+  const int pf = a.pf, GP = pf | 1;                          // odd pitch: conflict-free
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* w_s = csr_sm;
+  float* g_s = csr_sm + round_up(pf, 4) + warp * 32 * GP;
+  float2* nz_s = reinterpret_cast<float2*>(csr_sm + round_up(pf, 4) + FW_WARPS * 32 * GP +
+                                           (FW_WARPS * 32 * GP & 1)) + warp * 32 * CSR_K;
+  const int64_t gw = (int64_t)blockIdx.x * FW_WARPS + warp;
+  const int64_t NW = (int64_t)gridDim.x * FW_WARPS;
+  const int64_t base = a.nunits / NW, rem = a.nunits % NW;
+  const int64_t u0 = gw * base + min64(gw, rem);
+  const int64_t cnt = base + (gw < rem ? 1 : 0);
+  const int64_t W0 = u0 * 32;
+  const int64_t W1 = min64((u0 + cnt) * 32, a.r_T);
+  const bool has_sort = a.sort_g >= 0;
+  const int32_t* fks = has_sort ? a.fk[a.sort_g] : nullptr;
+
+  for (int j = threadIdx.x; j < pf; j += blockDim.x) w_s[j] = a.wF[j];
+  for (int j = lane; j < CSR_MAXP; j += 32) gsum[warp][j] = 0.0;
+  for (int j = lane; j < 32 * GP; j += 32) g_s[j] = 0.f;
+  if (lane == 0) lsum[warp] = 0.0;
+  __syncthreads();
+
+  int head_key = -1;
+  if (has_sort && cnt > 0 && W0 > 0 && W0 < a.r_T) {
+    int k0 = fks[W0];
+    if (k0 >= 0 && fks[W0 - 1] == k0) head_key = k0;
+  }
+  bool head_open = head_key >= 0;
+  float head_val = 0.f;
+  int ck = -1;
+  float cv = 0.f;
+  float lacc = 0.f;
+  float* grow = g_s + lane * GP;
+
+  // per-unit row metadata, prefetched two units ahead: extents of the lane's
+  // row, sort FK, label, and the gathered terms sum_d q_d[fk_d]
+  struct Meta {
+    int64_t e0, e1;
+    int key;
+    float y, gq;
+  };
+  auto load_meta = [&](int64_t i) {
+    Meta m;
+    const int64_t p = (u0 + i) * 32 + lane;
+    m.e0 = a.rp[p];
+    m.e1 = a.rp[p + 1];
+    m.key = has_sort ? fks[p] : -1;
+    m.y = MODEL == 0 ? reinterpret_cast<const float*>(a.y)[p]
+                     : (float)reinterpret_cast<const uint8_t*>(a.y)[p];
+    float gq = 0.f;
+    for (int d = 0; d < a.ng; d++) {
+      const int32_t fk = (d == a.sort_g) ? m.key : a.fk[d][p];
+      if (fk >= 0) gq += __ldg(a.q[d] + fk);
+    }
+    m.gq = gq;
+    return m;
+  };
+  // the unit's nonzero block [E0, E1) is contiguous: lanes fetch it
+  // coalesced (CSR_K per lane) into registers one unit ahead
+  float2 nzr[CSR_K];
+  auto load_nz = [&](const Meta& m) {
+    const int64_t E0 = __shfl_sync(0xffffffffu, m.e0, 0);
+    const int64_t E1 = __shfl_sync(0xffffffffu, m.e1, 31);
+#pragma unroll
+    for (int k = 0; k < CSR_K; k++) {
+      const int64_t e = E0 + k * 32 + lane;
+      nzr[k] = e < E1 ? make_float2(__int_as_float((int)__ldg(a.col + e)), __ldg(a.val + e))
+                      : make_float2(0.f, 0.f);
+    }
+  };
+
+  auto flush = [&]() {
+    __syncwarp();
+    for (int c = lane; c < pf; c += 32) {       // fixed lane order per column
+      float s = 0.f;
+      for (int l = 0; l < 32; l++) {
+        s += g_s[l * GP + c];
+        g_s[l * GP + c] = 0.f;
+      }
+      gsum[warp][c] += (double)s;
+    }
+    __syncwarp();
+    float v = lacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) lsum[warp] += (double)v;
+    lacc = 0.f;
+  };
+
+  Meta mc{}, mn{};
+  if (cnt > 0) {
+    mc = load_meta(0);
+    load_nz(mc);
+  }
+  if (cnt > 1) mn = load_meta(1);
+  for (int64_t i = 0; i < cnt; i++) {
+    const int64_t p = (u0 + i) * 32 + lane;
+    const bool valid = p < a.r_T;
+    // stage this unit's prefetched nonzeros, then prefetch the next unit's
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < CSR_K; k++) nz_s[k * 32 + lane] = nzr[k];
+    __syncwarp();
+    const int64_t E0 = __shfl_sync(0xffffffffu, mc.e0, 0);
+    if (i + 1 < cnt) load_nz(mn);
+    Meta m2{};
+    if (i + 2 < cnt) m2 = load_meta(i + 2);
+    // the row: staged entries (slot < 32 CSR_K) or, past that, global memory
+    const int s0 = (int)(mc.e0 - E0), s1 = (int)(mc.e1 - E0);
+    float z = 0.f;
+    for (int sl = s0; sl < s1; sl++) {
+      float2 nv;
+      if (sl < 32 * CSR_K) nv = nz_s[sl];
+      else nv = make_float2(__int_as_float((int)__ldg(a.col + E0 + sl)), __ldg(a.val + E0 + sl));
+      z = fmaf(nv.y, w_s[__float_as_int(nv.x)], z);
+    }
+    z += mc.gq;
+    int key = mc.key;
+    const float yv = mc.y;
+    float r, l;
+    if (MODEL == 0) {
+      r = z - yv;
+      l = 0.5f * r * r;
+    } else {
+      float ex = __expf(-fabsf(z));
+      float sp = log1pf(ex);
+      const float inv = __frcp_rn(1.f + ex);
+      float pr = z >= 0.f ? inv : ex * inv;
+      r = pr - yv;
+      float lp = z >= 0.f ? sp : sp - z;
+      float lq = z >= 0.f ? sp + z : sp;
+      l = yv != 0.f ? fminf(lp, kLogClip) : fminf(lq, kLogClip);
+    }
+    if (!valid) {
+      r = 0.f;
+      l = 0.f;
+      key = -1;
+    }
+    lacc += l;
+    for (int sl = s0; sl < s1; sl++) {
+      float2 nv;
+      if (sl < 32 * CSR_K) nv = nz_s[sl];
+      else nv = make_float2(__int_as_float((int)__ldg(a.col + E0 + sl)), __ldg(a.val + E0 + sl));
+      const int c = __float_as_int(nv.x);
+      grow[c] = fmaf(r, nv.y, grow[c]);
+    }
+    if (a.resid && valid) a.resid[p] = r;
+    if (has_sort) {   // segmented sum of r by FK (as k_glm_fact_w)
+      float v = r;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        float vu = __shfl_up_sync(0xffffffffu, v, off);
+        int ku = __shfl_up_sync(0xffffffffu, key, off);
+        if (lane >= off && ku == key) v += vu;
+      }
+      if (key >= 0 && key == ck) v += cv;
+      const int k0 = __shfl_sync(0xffffffffu, key, 0);
+      if (ck >= 0 && k0 != ck) {
+        if (head_open && ck == head_key) {
+          head_val = cv;
+          head_open = false;
+        } else if (lane == 0) {
+          a.bins[ck] = cv;
+        }
+      }
+      const int kn = __shfl_down_sync(0xffffffffu, key, 1);
+      const bool end = lane < 31 && key >= 0 && kn != key;
+      const bool eh = end && head_open && key == head_key;
+      const unsigned bm = __ballot_sync(0xffffffffu, eh);
+      if (bm) {
+        head_val = __shfl_sync(0xffffffffu, v, __ffs(bm) - 1);
+        head_open = false;
+      }
+      if (end && !eh) a.bins[key] = v;
+      ck = __shfl_sync(0xffffffffu, key, 31);
+      cv = __shfl_sync(0xffffffffu, v, 31);
+    }
+    if ((i % FW_FLUSH) == FW_FLUSH - 1) flush();
+    mc = mn;
+    mn = m2;
+  }
+  flush();
+
+  if (has_sort) {
+    WarpCarry c;
+    c.head_key = -1;
+    c.tail_key = -1;
+    c.through = 0;
+    c.pad = 0;
+    c.head_val = 0.0;
+    c.tail_val = 0.0;
+    if (cnt > 0) {
+      if (ck >= 0) {
+        const bool cont = W1 < a.r_T && fks[W1] == ck;
+        if (head_open && ck == head_key) {
+          head_val = cv;
+          head_open = false;
+          c.head_key = ck;
+          c.through = cont ? 1 : 0;
+        } else if (cont) {
+          c.tail_key = ck;
+          c.tail_val = (double)cv;
+        } else if (lane == 0) {
+          a.bins[ck] = cv;
+        }
+      }
+      if (!head_open && head_key >= 0) {
+        c.head_key = head_key;
+        c.head_val = (double)head_val;
+      }
+    }
+    if (lane == 0) a.carry[gw] = c;
+  }
+  __syncthreads();
+  double* out = a.part + (int64_t)blockIdx.x * (pf + 1);
+  for (int t = threadIdx.x; t <= pf; t += blockDim.x) {
+    double sum = 0.0;
+    if (t < pf)
+      for (int w2 = 0; w2 < FW_WARPS; w2++) sum += gsum[w2][t];
+    else
+      for (int w2 = 0; w2 < FW_WARPS; w2++) sum += lsum[w2];
+    out[t] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(&a.state->done_fact, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (has_sort) {
+    volatile WarpCarry* cr = a.carry;
+    for (int64_t c = threadIdx.x; c < NW; c += blockDim.x) {
+      int K = cr[c].tail_key;
+      if (K < 0) continue;
+      double total = cr[c].tail_val;
+      for (int64_t c2 = c + 1; c2 < NW; c2++) {
+        if (cr[c2].head_key != K) break;
+        total += cr[c2].head_val;
+        if (!cr[c2].through) break;
+      }
+      a.bins[K] = (float)total;
+    }
+  }
+  if (threadIdx.x == 0) a.state->done_fact = 0;
+}
+
+// CSR copy of the stream block: per-row nonzero counts, scan, compaction
+__global__ void k_csr_count(const float* __restrict__ F, int64_t r_pad, int pf,
+                            int64_t* __restrict__ cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r_pad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int n = 0;
+    for (int c = 0; c < pf; c++) n += F[r * pf + c] != 0.f;
+    cnt[r] = n;
+  }
+}
+__global__ void k_csr_fill(const float* __restrict__ F, int64_t r_pad, int pf,
+                           const int64_t* __restrict__ rp, uint16_t* __restrict__ col,
+                           float* __restrict__ val) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r_pad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = rp[r];
+    for (int c = 0; c < pf; c++) {
+      const float v = F[r * pf + c];
+      if (v != 0.f) {
+        col[e] = (uint16_t)c;
+        val[e] = v;
+        e++;
+      }
+    }
+  }
+}

@@ -180,6 +180,16 @@ class GlmSession:
         _lib.call("fl_glm_reduce_buffer", self.ptr, C.byref(buf), C.byref(n))
         return buf.value, n.value
 
+    @property
+    def path(self) -> tuple[str, float]:
+        """(fact-pass variant, measured stream-block density): "cta_tiles",
+        "warp_tma" (dense F), "csr" (sparse F) or
+        "generic"."""
+        p = C.c_int32()
+        dens = C.c_double()
+        _lib.call("fl_glm_path", self.ptr, C.byref(p), C.byref(dens))
+        return ("cta_tiles", "warp_tma", "csr", "generic")[p.value], dens.value
+
     def kernel_times(self, iters: int, stream=None) -> list[float]:
         """Mean ms of [dim q, fact pass, dim t + update] over `iters` iterations
         (CUDA events between the kernels, recorded by the library)."""

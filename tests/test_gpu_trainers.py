@@ -69,6 +69,67 @@ def test_glm_random_star_vs_oracle(fl, model, dims):
     assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
 
 
+@pytest.mark.parametrize("name,model", _cases(("linreg", "logreg")))
+def test_glm_csr_pass_matches_reference(fl, name, model, monkeypatch):
+    """The sparse fact pass (CSR copy of the stream block, FL_GLM_SPARSE=1
+    forces it) against the reference goldens."""
+    monkeypatch.setenv("FL_GLM_SPARSE", "1")
+    g = load_golden(name)
+    m = g.meta["trainers"][model]
+    h = fl.TargetHandle.factorized(g.ft)
+    y = g["y_lin"] if model == "linreg" else g["y_log"]
+    cfg = fl.TrainConfig(iterations=m["iterations"], learning_rate=m["learning_rate"],
+                         k_clusters=m["k_clusters"], rank=m["rank"], seed=m["seed"])
+    res = fl.train(model, h, cfg, fl.SparseMatrix.from_dense(y))
+    assert max_rel(res.loss_history, g[f"{model}_loss"]) < TOL
+    assert max_rel(res.parameters["w"], g[f"{model}_w"]) < TOL
+
+
+def sparse_star(seed, r_fact, dims, c_fact, density):
+    """star_table with the fact values zeroed at random (kept fp32-exact)."""
+    from paper_2502_01985_b200.metadata import FactorizedTable
+    ft = star_table(seed, r_fact, dims, c_fact)
+    rng = np.random.default_rng(seed + 100)
+    f = ft.sources[0].to_dense()
+    f[rng.random(f.shape) >= density] = 0.0
+    return FactorizedTable([fl_sparse(f)] + list(ft.sources[1:]), ft.mappings, ft.indicators,
+                           ft.join_type, ft.r_T, ft.c_T)
+
+
+def fl_sparse(a):
+    from paper_2502_01985_b200.sparse import SparseMatrix
+    return SparseMatrix.from_dense(a)
+
+
+@pytest.mark.parametrize("model", ["linreg", "logreg"])
+@pytest.mark.parametrize("dims,density", [([(2000, 17)], 0.1), ([(900, 11), (40, 3)], 0.05),
+                                          ([(30000, 6)], 0.2)])
+def test_glm_sparse_star_auto_csr_vs_oracle(fl, model, dims, density, monkeypatch):
+    """Sparse fact tables on the CSR pass match the oracle; the session is
+    deterministic run to run."""
+    from paper_2502_01985_b200.trainers import GlmSession
+    monkeypatch.setenv("FL_GLM_SPARSE", "1")
+    ft = sparse_star(13, 100_003, dims, 20, density)
+    tab = oracle.OracleTable.from_ft(ft)
+    rng = np.random.default_rng(3)
+    y = (rng.random(ft.r_T).astype(np.float32).astype(np.float64) if model == "linreg"
+         else rng.integers(0, 2, ft.r_T).astype(np.float64))
+    lr = rt.safe_learning_rate(tab)
+    want = rt.train(model, tab, iterations=8, learning_rate=lr, y=y)
+    h = fl.TargetHandle.factorized(ft)
+    s = GlmSession(h, model, y, lr)
+    try:
+        path, dens = s.path
+    finally:
+        s.close()
+    assert path == "csr" and dens < 0.25
+    res = fl.train(model, h, fl.TrainConfig(iterations=8, learning_rate=lr), y.reshape(-1, 1))
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+    assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
+    again = fl.train(model, h, fl.TrainConfig(iterations=8, learning_rate=lr), y.reshape(-1, 1))
+    assert np.array_equal(res.parameters["w"], again.parameters["w"])
+
+
 def test_glm_deterministic(fl):
     ft = star_table(12, 90_000, [(500, 9)], 12)
     y = np.random.default_rng(1).random((ft.r_T, 1))
