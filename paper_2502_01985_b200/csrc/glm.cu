@@ -1079,8 +1079,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         ca.resid = s->fw.resid;
         ca.wF = s->fw.wF;
         ca.state = s->fw.state;
-        s->smem_csr = ((size_t)round_up(t->pf, 4) + (size_t)FW_WARPS * 32 * (t->pf | 1) + 1) * 4 +
-                      (size_t)FW_WARPS * 32 * CSR_K * 8;
+        s->smem_csr = ((size_t)round_up(t->pf, 4) + (size_t)FW_WARPS * 32 * (t->pf | 1)) * 4;
         for (int m = 0; m < 2; m++) {
           const void* kc = m == 0 ? (const void*)k_glm_fact_csr<0> : (const void*)k_glm_fact_csr<1>;
           FL_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize,

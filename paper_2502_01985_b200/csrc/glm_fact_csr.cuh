@@ -33,22 +33,19 @@ struct GlmCsrArgs {
 
 constexpr int CSR_MAXP = 128;   // stream pitch handled by the sparse pass
 
-constexpr int CSR_K = 4;        // nonzeros per lane staged per unit (128 per 32 rows)
-
 template <int MODEL>
 __global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
-  // smem: w_F | per-warp lane-private gradient rows (32 x GP) | per-warp
-  // staged nonzeros of the current unit (32 CSR_K x {col, val})
+  // smem: w_F | per-warp lane-private gradient rows (32 x GP).  Measured
+  // variants (profiles/r01_glm_csr.txt): this direct-load version beat a
+  // register-prefetch pipeline and a per-warp TMA ring of small bulk copies.
   extern __shared__ __align__(16) float csr_sm[];
   __shared__ double gsum[FW_WARPS][CSR_MAXP];
   __shared__ double lsum[FW_WARPS];
   __shared__ int is_last;
   const int pf = a.pf, GP = pf | 1;                          // odd pitch: conflict-free
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* w_s = csr_sm;
-  float* g_s = csr_sm + round_up(pf, 4) + warp * 32 * GP;
-  float2* nz_s = reinterpret_cast<float2*>(csr_sm + round_up(pf, 4) + FW_WARPS * 32 * GP +
-                                           (FW_WARPS * 32 * GP & 1)) + warp * 32 * CSR_K;
+  float* g_s = csr_sm + round_up(pf, 4) + (threadIdx.x >> 5) * 32 * GP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * FW_WARPS + warp;
   const int64_t NW = (int64_t)gridDim.x * FW_WARPS;
   const int64_t base = a.nunits / NW, rem = a.nunits % NW;
@@ -77,43 +74,6 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
   float lacc = 0.f;
   float* grow = g_s + lane * GP;
 
-  // per-unit row metadata, prefetched two units ahead: extents of the lane's
-  // row, sort FK, label, and the gathered terms sum_d q_d[fk_d]
-  struct Meta {
-    int64_t e0, e1;
-    int key;
-    float y, gq;
-  };
-  auto load_meta = [&](int64_t i) {
-    Meta m;
-    const int64_t p = (u0 + i) * 32 + lane;
-    m.e0 = a.rp[p];
-    m.e1 = a.rp[p + 1];
-    m.key = has_sort ? fks[p] : -1;
-    m.y = MODEL == 0 ? reinterpret_cast<const float*>(a.y)[p]
-                     : (float)reinterpret_cast<const uint8_t*>(a.y)[p];
-    float gq = 0.f;
-    for (int d = 0; d < a.ng; d++) {
-      const int32_t fk = (d == a.sort_g) ? m.key : a.fk[d][p];
-      if (fk >= 0) gq += __ldg(a.q[d] + fk);
-    }
-    m.gq = gq;
-    return m;
-  };
-  // the unit's nonzero block [E0, E1) is contiguous: lanes fetch it
-  // coalesced (CSR_K per lane) into registers one unit ahead
-  float2 nzr[CSR_K];
-  auto load_nz = [&](const Meta& m) {
-    const int64_t E0 = __shfl_sync(0xffffffffu, m.e0, 0);
-    const int64_t E1 = __shfl_sync(0xffffffffu, m.e1, 31);
-#pragma unroll
-    for (int k = 0; k < CSR_K; k++) {
-      const int64_t e = E0 + k * 32 + lane;
-      nzr[k] = e < E1 ? make_float2(__int_as_float((int)__ldg(a.col + e)), __ldg(a.val + e))
-                      : make_float2(0.f, 0.f);
-    }
-  };
-
   auto flush = [&]() {
     __syncwarp();
     for (int c = lane; c < pf; c += 32) {       // fixed lane order per column
@@ -132,36 +92,22 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
     lacc = 0.f;
   };
 
-  Meta mc{}, mn{};
-  if (cnt > 0) {
-    mc = load_meta(0);
-    load_nz(mc);
-  }
-  if (cnt > 1) mn = load_meta(1);
   for (int64_t i = 0; i < cnt; i++) {
     const int64_t p = (u0 + i) * 32 + lane;
     const bool valid = p < a.r_T;
-    // stage this unit's prefetched nonzeros, then prefetch the next unit's
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < CSR_K; k++) nz_s[k * 32 + lane] = nzr[k];
-    __syncwarp();
-    const int64_t E0 = __shfl_sync(0xffffffffu, mc.e0, 0);
-    if (i + 1 < cnt) load_nz(mn);
-    Meta m2{};
-    if (i + 2 < cnt) m2 = load_meta(i + 2);
-    // the row: staged entries (slot < 32 CSR_K) or, past that, global memory
-    const int s0 = (int)(mc.e0 - E0), s1 = (int)(mc.e1 - E0);
-    float z = 0.f;
-    for (int sl = s0; sl < s1; sl++) {
-      float2 nv;
-      if (sl < 32 * CSR_K) nv = nz_s[sl];
-      else nv = make_float2(__int_as_float((int)__ldg(a.col + E0 + sl)), __ldg(a.val + E0 + sl));
-      z = fmaf(nv.y, w_s[__float_as_int(nv.x)], z);
+    const int64_t e0 = a.rp[p], e1 = a.rp[p + 1];
+    int key = has_sort ? fks[p] : -1;
+    float gq = 0.f;
+    for (int d = 0; d < a.ng; d++) {
+      const int32_t fk = (d == a.sort_g) ? key : a.fk[d][p];
+      if (fk >= 0) gq += __ldg(a.q[d] + fk);
     }
-    z += mc.gq;
-    int key = mc.key;
-    const float yv = mc.y;
+    float yv;
+    if (MODEL == 0) yv = reinterpret_cast<const float*>(a.y)[p];
+    else yv = (float)reinterpret_cast<const uint8_t*>(a.y)[p];
+    float z = 0.f;
+    for (int64_t e = e0; e < e1; e++) z = fmaf(__ldg(a.val + e), w_s[__ldg(a.col + e)], z);
+    z += gq;
     float r, l;
     if (MODEL == 0) {
       r = z - yv;
@@ -182,12 +128,9 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
       key = -1;
     }
     lacc += l;
-    for (int sl = s0; sl < s1; sl++) {
-      float2 nv;
-      if (sl < 32 * CSR_K) nv = nz_s[sl];
-      else nv = make_float2(__int_as_float((int)__ldg(a.col + E0 + sl)), __ldg(a.val + E0 + sl));
-      const int c = __float_as_int(nv.x);
-      grow[c] = fmaf(r, nv.y, grow[c]);
+    for (int64_t e = e0; e < e1; e++) {
+      const int c = __ldg(a.col + e);
+      grow[c] = fmaf(r, __ldg(a.val + e), grow[c]);
     }
     if (a.resid && valid) a.resid[p] = r;
     if (has_sort) {   // segmented sum of r by FK (as k_glm_fact_w)
@@ -221,8 +164,6 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
       cv = __shfl_sync(0xffffffffu, v, 31);
     }
     if ((i % FW_FLUSH) == FW_FLUSH - 1) flush();
-    mc = mn;
-    mn = m2;
   }
   flush();
 
