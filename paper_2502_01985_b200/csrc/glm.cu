@@ -886,6 +886,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     *out = guard.release();
     return FL_OK;
   }
+  const PhaseTrace trace("fl_glm_create");
   FL_CUDA(cudaSetDevice(t->device));
   cudaStream_t st = (cudaStream_t)stream;
   auto* s = new fl_glm();
@@ -907,6 +908,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     if (rc) return rc;
     FL_CUDA(cudaFreeAsync(ydev, st));
   }
+  trace.mark("labels issued");
   // parameters
   if ((rc = s->w64.alloc((size_t)t->c_T * 8))) return rc;
   FL_CUDA(cudaMemsetAsync(s->w64.p, 0, (size_t)t->c_T * 8, st));
@@ -1029,6 +1031,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     }
   }
 
+  trace.mark("fact-pass geometry");
   // sparse stream block: when F is sparse, a CSR copy
   // (device order) feeds k_glm_fact_csr, which reads 6 bytes per nonzero
   // instead of 4 bytes per entry.  FL_GLM_SPARSE: unset = auto (density of
@@ -1036,7 +1039,22 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
   {
     const char* e = getenv("FL_GLM_SPARSE");
     const int mode = e ? atoi(e) : -1;
+    bool want_csr = false;
     if (mode != 0 && s->use_fw && t->pf <= CSR_MAXP && t->nf > 0) {
+      DevBuf tot;
+      if ((rc = tot.alloc(16))) return rc;
+      FL_CUDA(cudaMemsetAsync(tot.p, 0, 8, st));
+      k_nnz_total<<<(unsigned)(t->sm_count * 16), 256, 0, st>>>(
+          reinterpret_cast<const float4*>(t->F->p), r_pad * t->pf / 4,
+          reinterpret_cast<unsigned long long*>(tot.p));
+      FL_CHECK_LAUNCH();
+      unsigned long long nnz_all = 0;
+      FL_CUDA(cudaMemcpyAsync(&nnz_all, tot.p, 8, cudaMemcpyDeviceToHost, st));
+      FL_CUDA(cudaStreamSynchronize(st));
+      s->csr_density = (double)nnz_all / ((double)std::max<int64_t>(1, t->r_T) * t->nf);
+      want_csr = mode == 1 || s->csr_density < kCsrAutoDensity;
+    }
+    if (want_csr) {
       DevBuf cnt;
       if ((rc = cnt.alloc((size_t)(r_pad + 1) * 8))) return rc;
       FL_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)(r_pad + 1) * 8, st));
@@ -1054,8 +1072,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
       int64_t nnz = 0;
       FL_CUDA(cudaMemcpyAsync(&nnz, s->csr_rp.as<int64_t>() + r_pad, 8, cudaMemcpyDeviceToHost, st));
       FL_CUDA(cudaStreamSynchronize(st));
-      s->csr_density = (double)nnz / ((double)std::max<int64_t>(1, t->r_T) * t->nf);
-      if (mode == 1 || s->csr_density < kCsrAutoDensity) {
+      {
         if ((rc = s->csr_col.alloc((size_t)nnz * 2 + 16))) return rc;
         if ((rc = s->csr_val.alloc((size_t)nnz * 4 + 16))) return rc;
         k_csr_fill<<<gb, 256, 0, st>>>(t->F->as<float>(), r_pad, t->pf, s->csr_rp.as<int64_t>(),
@@ -1099,13 +1116,12 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         s->fw.carry = ca.carry;
         s->fw.part = ca.part;
         s->use_csr = true;
-      } else {
-        s->csr_rp.alloc(16);   // dense pass: release the extents
       }
       FL_CUDA(cudaStreamSynchronize(st));
     }
   }
 
+  trace.mark("density probe");
   // dim geometry
   DimArgs& da = s->da;
   da.ng = ng;
@@ -1178,7 +1194,9 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     ua.part_dim[d] = da.part[d];
     ua.nblk_dim[d] = da.nblk[d];
   }
+  trace.mark("dim geometry");
   FL_CUDA(cudaStreamSynchronize(st));
+  trace.mark("done");
   *out = guard.release();
   return FL_OK;
 }

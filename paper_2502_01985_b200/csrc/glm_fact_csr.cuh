@@ -230,6 +230,30 @@ __global__ void __launch_bounds__(FW_WARPS * 32) k_glm_fact_csr(GlmCsrArgs a) {
   if (threadIdx.x == 0) a.state->done_fact = 0;
 }
 
+// density probe: nonzeros of the whole stream block (coalesced float4 reads,
+// one atomic per warp) -- decides whether the CSR copy below is built at all
+__global__ void k_nnz_total(const float4* __restrict__ F4, int64_t n4,
+                            unsigned long long* __restrict__ total) {
+  unsigned n = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {   // 4 independent loads in flight
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = __ldcs(F4 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      n += (v[u].x != 0.f) + (v[u].y != 0.f) + (v[u].z != 0.f) + (v[u].w != 0.f);
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = F4[i];
+    n += (v.x != 0.f) + (v.y != 0.f) + (v.z != 0.f) + (v.w != 0.f);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(total, (unsigned long long)n);
+}
+
 // CSR copy of the stream block: per-row nonzero counts, scan, compaction
 __global__ void k_csr_count(const float* __restrict__ F, int64_t r_pad, int pf,
                             int64_t* __restrict__ cnt) {

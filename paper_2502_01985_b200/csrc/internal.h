@@ -22,6 +22,9 @@
 //    copy moves whole, 16-byte aligned tiles.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -97,11 +100,30 @@ struct SrcInfo {
 struct Staged {            // source data between add_source and finalize
   int64_t rows = 0;
   int cols = 0;
-  std::shared_ptr<DevBuf> vals;     // rows x cols fp32 (compact)
+  std::shared_ptr<DevBuf> vals;     // rows x cols fp32 (compact); null for host values
+  const float* h_vals = nullptr;    // host values: copied by finalize straight to their
+                                    // final place (chunked ring -> stream block, or S_d)
   std::shared_ptr<DevBuf> ind_sel;  // r_T int32 (target order)
+  bool sel_given = false;           // false: identity indicator (built on the device)
   std::vector<int32_t> col_map;     // cols target columns
   // the uploads run on the table's copy streams; finalize waits on these
   std::shared_ptr<void> ev_vals, ev_idx;   // cudaEvent_t (owned)
+};
+
+// FL_TRACE_UPLOAD=1: host-side phase timestamps of table / session setup
+struct PhaseTrace {
+  const char* scope;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseTrace(const char* sc)
+      : scope(sc), on(std::getenv("FL_TRACE_UPLOAD") != nullptr),
+        t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) const {
+    if (on)
+      std::fprintf(stderr, "[%s] %-28s %8.3f ms\n", scope, what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
+  }
 };
 
 struct Workspace {

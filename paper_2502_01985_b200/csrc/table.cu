@@ -3,8 +3,10 @@
 // ops.py:55-74 (_build_selectors), ops.py:273-295 (elementwise).
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -123,6 +125,31 @@ __global__ void k_build_stream(const float* __restrict__ vals, int cols,
   F[p * pf + off + c] = v;
 }
 
+// host-value upload, one ring chunk: source rows [r0, r0 + nrows) of an
+// injective source land at their device rows.  inv (source row -> target row,
+// -1 = unreferenced) is null for the identity indicator.
+__global__ void k_scatter_rows(const float* __restrict__ chunk, int cols, int64_t r0,
+                               int64_t nrows, const int32_t* __restrict__ inv,
+                               const int32_t* __restrict__ iperm, float* __restrict__ F, int pf,
+                               int off) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= nrows * cols) return;
+  int64_t row = idx / cols;
+  int c = (int)(idx - row * cols);
+  int64_t src = r0 + row;
+  int64_t tr = inv ? (int64_t)inv[src] : src;
+  if (tr < 0) return;
+  F[(int64_t)iperm[tr] * pf + off + c] = chunk[idx];
+}
+
+// inv[ind_sel[t]] = t for an injective indicator (inv preset to -1)
+__global__ void k_invert_sel(const int32_t* __restrict__ ind_sel, int64_t r_T, int32_t* inv) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= r_T) return;
+  int32_t s = ind_sel[t];
+  if (s >= 0) inv[s] = (int32_t)t;
+}
+
 __global__ void k_fk_device_order(const int32_t* __restrict__ ind_sel,
                                   const int32_t* __restrict__ perm, int64_t r_pad, int32_t* fk) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -220,8 +247,11 @@ static inline unsigned grid_for(int64_t n, int block = 256) {
 }
 
 // stable (key = ind_sel + 1, value = target row) sort over target rows
+// `keep` (optional) receives the temporaries instead of freeing them here:
+// cudaFree waits for the whole device, which would stall behind the upload's
+// in-flight copies
 static int stable_order(const int32_t* ind_sel, int64_t r_T, int64_t r_k, int32_t* order_out,
-                        cudaStream_t s) {
+                        cudaStream_t s, std::vector<std::shared_ptr<DevBuf>>* keep = nullptr) {
   int rc;
   auto keys = make_buf(r_T * 4, &rc);
   if (rc) return rc;
@@ -244,6 +274,7 @@ static int stable_order(const int32_t* ind_sel, int64_t r_T, int64_t r_k, int32_
                                           keys2->as<uint32_t>(), vals->as<int32_t>(), order_out,
                                           (int)r_T, 0, end_bit, s));
   FL_CUDA(cudaStreamSynchronize(s));
+  if (keep) keep->insert(keep->end(), {keys, keys2, vals, tmp});
   return FL_OK;
 }
 
@@ -330,8 +361,6 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     }
   }
   int rc;
-  st.vals = make_buf((size_t)r_k * c_k * 4, &rc);
-  if (rc) return rc;
   st.ind_sel = make_buf((size_t)t->r_T * 4, &rc);
   if (rc) return rc;
   // asynchronous uploads on the table's copy streams (values and FKs on
@@ -367,6 +396,7 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
   };
+  st.sel_given = ind_sel != nullptr;
   if (ind_sel) {
     if (on_device(ind_sel))
       FL_CUDA(cudaMemcpy(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault));
@@ -377,11 +407,19 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     FL_CHECK_LAUNCH();
   }
   FL_CUDA(cudaEventRecord((cudaEvent_t)st.ev_idx.get(), ci));
-  if (on_device(values))
+  if (on_device(values)) {
+    st.vals = make_buf((size_t)r_k * c_k * 4, &rc);
+    if (rc) return rc;
     FL_CUDA(cudaMemcpy(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault));
-  else
-    FL_CUDA(cudaMemcpyAsync(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault, cv));
+  } else {
+    // host values are not staged: finalize copies them once it knows where
+    // they go (chunks through a small ring into the stream block, or straight
+    // into the pitched S_d), so PCIe carries every byte exactly once and the
+    // device-order scatter overlaps the copy
+    st.h_vals = values;
+  }
   FL_CUDA(cudaEventRecord((cudaEvent_t)st.ev_vals.get(), cv));
+  (void)cv;
   t->staged.push_back(std::move(st));
   return FL_OK;
 }
@@ -391,11 +429,16 @@ int fl_table_finalize(fl_table* t, void* stream) {
     set_error("fl_table_finalize: nothing to finalize");
     return FL_ERR_ARG;
   }
+  const PhaseTrace tr("fl_table_finalize");
+  auto mark = [&](const char* what) { tr.mark(what); };
   FL_CUDA(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t r_T = t->r_T, r_pad = t->r_pad;
   int rc;
   const int n = (int)t->staged.size();
+  // temporaries live until the end: no cudaFree (a device-wide wait) while
+  // the value copies are in flight
+  std::vector<std::shared_ptr<DevBuf>> keep;
   // the index work below needs every FK array; the values are waited for
   // just before their first use (stream block / gathered copies)
   for (auto& st : t->staged) FL_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)st.ev_idx.get(), 0));
@@ -440,12 +483,14 @@ int fl_table_finalize(fl_table* t, void* stream) {
     int h_max = 0;
     FL_CUDA(cudaMemcpyAsync(&h_max, dmax->p, 4, cudaMemcpyDeviceToHost, s));
     FL_CUDA(cudaStreamSynchronize(s));
+    keep.insert(keep.end(), {dmax, tmp});
     if (h_bad) {
       set_error("[source %d] indicator shape: row index outside [0,%lld)", k, (long long)st.rows);
       return FL_ERR_METADATA;
     }
     maxfan[k] = h_max;
   }
+  mark("fanout (FKs landed)");
   t->src.assign(n, SrcInfo());
   int stream_cols = 0;
   int sort_k = -1;
@@ -461,6 +506,87 @@ int fl_table_finalize(fl_table* t, void* stream) {
       sort_k = k;
     }
   }
+  // 1b. host values go out now, on the value copy stream, while the row
+  // order below is derived: stream-source chunks fill a small device ring
+  // (scattered to their device rows once the order exists), gathered
+  // sources land directly in their pitched S_d.  Every host byte crosses
+  // PCIe once, in one stream, back to back.
+  cudaStream_t cv = (cudaStream_t)t->cp_vals.get();
+  t->nf = stream_cols;
+  t->pf = pitch_for(std::max(stream_cols, 1));
+  t->f_tcol.assign(t->pf, -1);
+  t->F = make_buf((size_t)r_pad * t->pf * 4 + 64, &rc);
+  if (rc) return rc;
+  FL_CUDA(cudaMemsetAsync(t->F->p, 0, (size_t)r_pad * t->pf * 4, s));
+  struct Chunk {
+    int k;
+    int64_t r0, nrows;
+  };
+  std::vector<Chunk> chunks;
+  constexpr size_t kChunkBytes = (size_t)64 << 20;
+  size_t slot_bytes = kChunkBytes;
+  for (int k = 0; k < n; k++) {
+    const Staged& st = t->staged[k];
+    if (!t->src[k].stream || !st.h_vals) continue;
+    const size_t row_bytes = (size_t)st.cols * 4;
+    const int64_t per = std::max<int64_t>(1, (int64_t)(kChunkBytes / row_bytes));
+    slot_bytes = std::max(slot_bytes, row_bytes);
+    for (int64_t r0 = 0; r0 < st.rows; r0 += per)
+      chunks.push_back({k, r0, std::min(per, st.rows - r0)});
+  }
+  const int nch = (int)chunks.size();
+  const int ring_n = std::min(nch, 16);   // 1 GB: covers the row-order sort
+  std::shared_ptr<DevBuf> ring;
+  std::vector<std::shared_ptr<void>> ev_ready(nch), ev_free(nch);
+  auto mk_ev = []() -> std::shared_ptr<void> {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    return std::shared_ptr<void>(e, [](void* p) { cudaEventDestroy((cudaEvent_t)p); });
+  };
+  auto issue_chunk = [&](int c) -> int {
+    const Chunk& ch = chunks[c];
+    const Staged& st = t->staged[ch.k];
+    char* slot = ring->as<char>() + (size_t)(c % ring_n) * slot_bytes;
+    if (c >= ring_n) FL_CUDA(cudaStreamWaitEvent(cv, (cudaEvent_t)ev_free[c - ring_n].get(), 0));
+    FL_CUDA(cudaMemcpyAsync(slot, st.h_vals + ch.r0 * st.cols, (size_t)ch.nrows * st.cols * 4,
+                            cudaMemcpyHostToDevice, cv));
+    FL_CUDA(cudaEventRecord((cudaEvent_t)ev_ready[c].get(), cv));
+    return FL_OK;
+  };
+  if (nch > 0) {
+    ring = make_buf(slot_bytes * ring_n, &rc);
+    if (rc) return rc;
+    for (int c = 0; c < nch; c++) {
+      ev_ready[c] = mk_ev();
+      ev_free[c] = mk_ev();
+      if (!ev_ready[c] || !ev_free[c]) {
+        set_error("fl_table_finalize: event creation failed");
+        return FL_ERR_CUDA;
+      }
+    }
+    for (int c = 0; c < ring_n; c++)
+      if ((rc = issue_chunk(c))) return rc;
+  }
+  // (a pitched H2D copy of short rows runs far below PCIe speed: the compact
+  // rows cross as one contiguous copy and are re-pitched on the device)
+  std::vector<std::shared_ptr<DevBuf>> host_S(n), host_tmp(n);
+  for (int k = 0; k < n; k++) {
+    const Staged& st = t->staged[k];
+    if (t->src[k].stream || !st.h_vals) continue;
+    const int pitch = pitch_for(st.cols);
+    const int64_t rows_pad = round_up(st.rows, TILE);
+    host_S[k] = make_buf((size_t)rows_pad * pitch * 4 + 64, &rc);
+    if (rc) return rc;
+    host_tmp[k] = make_buf((size_t)st.rows * st.cols * 4, &rc);
+    if (rc) return rc;
+    FL_CUDA(cudaMemcpyAsync(host_tmp[k]->p, st.h_vals, (size_t)st.rows * st.cols * 4,
+                            cudaMemcpyHostToDevice, cv));
+    FL_CUDA(cudaMemsetAsync(host_S[k]->p, 0, (size_t)rows_pad * pitch * 4, cv));
+    FL_CUDA(cudaMemcpy2DAsync(host_S[k]->p, pitch * 4, host_tmp[k]->p, st.cols * 4, st.cols * 4,
+                              st.rows, cudaMemcpyDeviceToDevice, cv));
+  }
+
+  mark("value copies issued");
   // 2. device row order
   t->perm = make_buf(r_pad * 4, &rc);
   if (rc) return rc;
@@ -471,7 +597,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
     orders[sort_k] = make_buf(r_T * 4, &rc);
     if (rc) return rc;
     rc = stable_order(t->staged[sort_k].ind_sel->as<int32_t>(), r_T, t->staged[sort_k].rows,
-                      orders[sort_k]->as<int32_t>(), s);
+                      orders[sort_k]->as<int32_t>(), s, &keep);
     if (rc) return rc;
     FL_CUDA(cudaMemcpyAsync(t->perm->p, orders[sort_k]->p, r_T * 4, cudaMemcpyDeviceToDevice, s));
     if (r_pad > r_T) k_pad_perm<<<grid_for(r_pad - r_T), 256, 0, s>>>(t->perm->as<int32_t>(), r_T, r_pad);
@@ -482,29 +608,48 @@ int fl_table_finalize(fl_table* t, void* stream) {
   k_inverse_perm<<<grid_for(r_T), 256, 0, s>>>(t->perm->as<int32_t>(), r_T,
                                                t->iperm->as<int32_t>());
   FL_CHECK_LAUNCH();
-  // 3. stream block F (from here on the values are read)
+  mark("row order (sorted)");
+  // 3. stream block F.  Every table gets one; a table with no injective
+  // source keeps a 4-column all-zero block so the fused passes have one
+  // code path.  Device values: gathered into device order; host values:
+  // each ring chunk scattered to its device rows as it lands.
   for (auto& st : t->staged) FL_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)st.ev_vals.get(), 0));
-  // every table gets a stream block; a table with no injective source keeps
-  // a 4-column all-zero block so the fused passes have one code path
-  t->nf = stream_cols;
-  t->pf = pitch_for(std::max(stream_cols, 1));
-  t->f_tcol.assign(t->pf, -1);
-  if (t->pf > 0) {
-    t->F = make_buf((size_t)r_pad * t->pf * 4 + 64, &rc);
-    if (rc) return rc;
-    FL_CUDA(cudaMemsetAsync(t->F->p, 0, (size_t)r_pad * t->pf * 4, s));
-    for (int k = 0; k < n; k++) {
-      if (!t->src[k].stream) continue;
-      Staged& st = t->staged[k];
-      for (int c = 0; c < st.cols; c++) t->f_tcol[t->src[k].f_off + c] = st.col_map[c];
-      int64_t total = r_pad * st.cols;
-      k_build_stream<<<grid_for(total), 256, 0, s>>>(st.vals->as<float>(), st.cols,
-                                                     st.ind_sel->as<int32_t>(),
-                                                     t->perm->as<int32_t>(), r_pad,
-                                                     t->F->as<float>(), t->pf, t->src[k].f_off);
+  std::vector<std::shared_ptr<DevBuf>> invs(n);
+  for (int k = 0; k < n; k++) {
+    if (!t->src[k].stream) continue;
+    Staged& st = t->staged[k];
+    for (int c = 0; c < st.cols; c++) t->f_tcol[t->src[k].f_off + c] = st.col_map[c];
+    if (st.h_vals) {
+      if (st.rows == r_T && !st.sel_given) continue;   // identity indicator
+      invs[k] = make_buf((size_t)st.rows * 4, &rc);
+      if (rc) return rc;
+      FL_CUDA(cudaMemsetAsync(invs[k]->p, 0xff, (size_t)st.rows * 4, s));
+      k_invert_sel<<<grid_for(r_T), 256, 0, s>>>(st.ind_sel->as<int32_t>(), r_T,
+                                                 invs[k]->as<int32_t>());
       FL_CHECK_LAUNCH();
+      continue;
     }
+    int64_t total = r_pad * st.cols;
+    k_build_stream<<<grid_for(total), 256, 0, s>>>(st.vals->as<float>(), st.cols,
+                                                   st.ind_sel->as<int32_t>(),
+                                                   t->perm->as<int32_t>(), r_pad,
+                                                   t->F->as<float>(), t->pf, t->src[k].f_off);
+    FL_CHECK_LAUNCH();
   }
+  for (int c = 0; c < nch; c++) {
+    const Chunk& ch = chunks[c];
+    const Staged& st = t->staged[ch.k];
+    FL_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)ev_ready[c].get(), 0));
+    const float* slot = reinterpret_cast<const float*>(ring->as<char>() +
+                                                       (size_t)(c % ring_n) * slot_bytes);
+    k_scatter_rows<<<grid_for(ch.nrows * st.cols), 256, 0, s>>>(
+        slot, st.cols, ch.r0, ch.nrows, invs[ch.k] ? invs[ch.k]->as<int32_t>() : nullptr,
+        t->iperm->as<int32_t>(), t->F->as<float>(), t->pf, t->src[ch.k].f_off);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaEventRecord((cudaEvent_t)ev_free[c].get(), s));
+    if (c + ring_n < nch && (rc = issue_chunk(c + ring_n))) return rc;
+  }
+  mark("scatter chunks issued");
   // 4. gathered sources
   for (int k = 0; k < n; k++) {
     if (t->src[k].stream) continue;
@@ -517,11 +662,15 @@ int fl_table_finalize(fl_table* t, void* stream) {
     g.tcol.assign(g.pitch, -1);
     for (int c = 0; c < st.cols; c++) g.tcol[c] = st.col_map[c];
     int64_t rows_pad = round_up(st.rows, TILE);
-    g.S = make_buf((size_t)rows_pad * g.pitch * 4 + 64, &rc);
-    if (rc) return rc;
-    FL_CUDA(cudaMemsetAsync(g.S->p, 0, (size_t)rows_pad * g.pitch * 4, s));
-    FL_CUDA(cudaMemcpy2DAsync(g.S->p, g.pitch * 4, st.vals->p, st.cols * 4, st.cols * 4, st.rows,
-                              cudaMemcpyDeviceToDevice, s));
+    if (host_S[k]) {   // already in flight on the value copy stream (1b)
+      g.S = host_S[k];
+    } else {
+      g.S = make_buf((size_t)rows_pad * g.pitch * 4 + 64, &rc);
+      if (rc) return rc;
+      FL_CUDA(cudaMemsetAsync(g.S->p, 0, (size_t)rows_pad * g.pitch * 4, s));
+      FL_CUDA(cudaMemcpy2DAsync(g.S->p, g.pitch * 4, st.vals->p, st.cols * 4, st.cols * 4,
+                                st.rows, cudaMemcpyDeviceToDevice, s));
+    }
     g.fk = make_buf(r_pad * 4, &rc);
     if (rc) return rc;
     k_fk_device_order<<<grid_for(r_pad), 256, 0, s>>>(st.ind_sel->as<int32_t>(),
@@ -547,14 +696,16 @@ int fl_table_finalize(fl_table* t, void* stream) {
     FL_CUDA(cudaMemcpyAsync(&h_matched, g.grp_ptr->as<int64_t>() + st.rows, 8,
                             cudaMemcpyDeviceToHost, s));
     FL_CUDA(cudaStreamSynchronize(s));
+    keep.insert(keep.end(), {c64, tmp});
     g.matched = h_matched;
     g.n_neg = r_T - h_matched;
     g.sorted = (k == sort_k);
     if (!g.sorted) {
       auto order = make_buf(r_T * 4, &rc);
       if (rc) return rc;
-      rc = stable_order(st.ind_sel->as<int32_t>(), r_T, st.rows, order->as<int32_t>(), s);
+      rc = stable_order(st.ind_sel->as<int32_t>(), r_T, st.rows, order->as<int32_t>(), s, &keep);
       if (rc) return rc;
+      keep.push_back(order);
       g.grp_rows = make_buf(std::max<int64_t>(g.matched, 1) * 4, &rc);
       if (rc) return rc;
       if (g.matched > 0) {
@@ -570,7 +721,11 @@ int fl_table_finalize(fl_table* t, void* stream) {
   t->sort_g = sort_k >= 0 ? t->src[sort_k].gidx : -1;
   rc = table_upload_tcols(t);
   if (rc) return rc;
+  mark("gathered sources issued");
+  FL_CUDA(cudaStreamSynchronize(cv));
+  mark("value copies done");
   FL_CUDA(cudaStreamSynchronize(s));
+  mark("layout done");
   t->staged.clear();
   t->finalized = true;
   return FL_OK;
