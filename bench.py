@@ -440,8 +440,12 @@ def main():
     ap.add_argument("--no-materialized", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--density", type=float, default=None,
+                    help="c2s: fraction of non-zero fact values (default 0.1)")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.density is not None:
+        wl["density"] = args.density
     if args.steps is None:
         args.steps = {"c1": 100, "c2": 200, "c2s": 200, "c3": 100, "c4": 20}[args.workload]
     if args.warmup < 3:

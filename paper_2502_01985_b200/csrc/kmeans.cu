@@ -125,20 +125,30 @@ __global__ void __launch_bounds__(256) k_km_dim_e(KmDimArgs a) {
 #pragma unroll
     for (int j = 0; j < KP; j++) acc[j] = 0.f;
     const float4* sr = reinterpret_cast<const float4*>(a.S[d] + row * pitch);
-    for (int c4 = 0; c4 < pitch / 4; c4++) {
-      const float4 v = row < rows ? sr[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+    const int n4 = pitch / 4;
+    // the row is read in batches of 8 independent float4 loads (one latency
+    // per batch instead of one per float4: the kernel was latency-bound)
+    for (int c0 = 0; c0 < n4; c0 += 8) {
+      float4 vb[8];
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const float4* cr = reinterpret_cast<const float4*>(sm_e + (c4 * 4 + e) * KP);
+      for (int u = 0; u < 8; u++)
+        vb[u] = (row < rows && c0 + u < n4) ? sr[c0 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < KP / 4; q++) {
-          const float4 cc = cr[q];
-          const float d0 = vv[e] - cc.x, d1 = vv[e] - cc.y, d2 = vv[e] - cc.z, d3 = vv[e] - cc.w;
-          acc[q * 4 + 0] = fmaf(d0, d0, acc[q * 4 + 0]);
-          acc[q * 4 + 1] = fmaf(d1, d1, acc[q * 4 + 1]);
-          acc[q * 4 + 2] = fmaf(d2, d2, acc[q * 4 + 2]);
-          acc[q * 4 + 3] = fmaf(d3, d3, acc[q * 4 + 3]);
+      for (int u = 0; u < 8; u++) {
+        if (c0 + u >= n4) break;
+        const float vv[4] = {vb[u].x, vb[u].y, vb[u].z, vb[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float4* cr = reinterpret_cast<const float4*>(sm_e + ((c0 + u) * 4 + e) * KP);
+#pragma unroll
+          for (int q = 0; q < KP / 4; q++) {
+            const float4 cc = cr[q];
+            const float d0 = vv[e] - cc.x, d1 = vv[e] - cc.y, d2 = vv[e] - cc.z, d3 = vv[e] - cc.w;
+            acc[q * 4 + 0] = fmaf(d0, d0, acc[q * 4 + 0]);
+            acc[q * 4 + 1] = fmaf(d1, d1, acc[q * 4 + 1]);
+            acc[q * 4 + 2] = fmaf(d2, d2, acc[q * 4 + 2]);
+            acc[q * 4 + 3] = fmaf(d3, d3, acc[q * 4 + 3]);
+          }
         }
       }
     }
@@ -617,43 +627,77 @@ __device__ void km_apply_update(const KmUpdateArgs& u) {
 
 // sums_d[j, c] = sum_r cnt_d[r, j] S_d[r, c]: 32-row tiles of S and of the
 // counters (converted to fp32 once) in smem; thread = (column, 8 clusters);
-// fp32 within a tile, fp64 across tiles
+// fp32 within a tile, fp64 across tiles.  Each thread holds its share of the
+// NEXT tile in registers (float4 / int4 loads issued before the current
+// tile's math), so a CTA pays one load latency per kernel, not per tile.
+// Pitches up to 288 floats (KM_SUM_SL float4 slots per thread; cols <= 256
+// have pitch <= 260).
+constexpr int KM_SUM_SL = 9;
 template <int KP>
 __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
-  constexpr int JB = 8, NJB = KP / JB;
+  constexpr int JB = 8, NJB = KP / JB, Q4 = KP / 4;
   __shared__ float ss[32 * 257];
   __shared__ __align__(16) float cs[32 * KP];
-  const int cols = a.cols[d], pitch = a.pitch[d];
+  const int cols = a.cols[d], pitch = a.pitch[d], pitch4 = pitch / 4;
   const int64_t rows = a.rows[d];
   const int nb = a.nblk[d];
   const int64_t rpb = ceil_div(ceil_div(rows, nb), 32) * 32;
   const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
   const int nwork = cols * NJB;
+  const int nS4 = 32 * pitch4;
+  const int tid = threadIdx.x;
+  const float4* S4 = reinterpret_cast<const float4*>(a.S[d]);
+  const int4* C4 = reinterpret_cast<const int4*>(a.cnt[d]);
+  float4 pv[KM_SUM_SL];
+  int4 pc = make_int4(0, 0, 0, 0);
+  auto load = [&](int64_t rb) {
+#pragma unroll
+    for (int sl = 0; sl < KM_SUM_SL; sl++) {
+      const int i = tid + sl * 256;
+      const int r = i / pitch4, c4 = i - r * pitch4;
+      pv[sl] = (i < nS4 && rb + r < r1) ? S4[(rb + r) * pitch4 + c4]
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid < 32 * Q4) {
+      const int r = tid / Q4;
+      pc = rb + r < r1 ? C4[rb * Q4 + tid] : make_int4(0, 0, 0, 0);
+    }
+  };
   double acc64[2][JB];
 #pragma unroll
   for (int u = 0; u < 2; u++)
 #pragma unroll
     for (int j = 0; j < JB; j++) acc64[u][j] = 0.0;
+  if (r0 < r1) load(r0);
   for (int64_t rb = r0; rb < r1; rb += 32) {
-    const int nr = (int)min64(32, r1 - rb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < 32 * cols; i += blockDim.x) {
-      const int r = i / cols, c = i - r * cols;
-      ss[r * 257 + c] = r < nr ? a.S[d][(rb + r) * pitch + c] : 0.f;
+    __syncthreads();   // the previous tile's math is done with ss / cs
+#pragma unroll
+    for (int sl = 0; sl < KM_SUM_SL; sl++) {
+      const int i = tid + sl * 256;
+      if (i < nS4) {   // padding columns (c >= cols) are not stored
+        const int r = i / pitch4, c = 4 * (i - r * pitch4);
+        if (c + 0 < cols) ss[r * 257 + c + 0] = pv[sl].x;
+        if (c + 1 < cols) ss[r * 257 + c + 1] = pv[sl].y;
+        if (c + 2 < cols) ss[r * 257 + c + 2] = pv[sl].z;
+        if (c + 3 < cols) ss[r * 257 + c + 3] = pv[sl].w;
+      }
     }
-    for (int i = threadIdx.x; i < 32 * KP; i += blockDim.x)
-      cs[i] = i < nr * KP ? (float)a.cnt[d][rb * KP + i] : 0.f;
+    if (tid < 32 * Q4)
+      *reinterpret_cast<float4*>(cs + 4 * tid) =
+          make_float4((float)pc.x, (float)pc.y, (float)pc.z, (float)pc.w);
     __syncthreads();
+    if (rb + 32 < r1) load(rb + 32);   // in flight during this tile's math
 #pragma unroll
     for (int u = 0; u < 2; u++) {
-      const int w = threadIdx.x + u * 256;
+      const int w = tid + u * 256;
       if (w >= nwork) break;
       const int c = w % cols, jb = w / cols;
       float acc[JB];
 #pragma unroll
       for (int j = 0; j < JB; j++) acc[j] = 0.f;
+#pragma unroll 8
       for (int r = 0; r < 32; r++) {
         const float v = ss[r * 257 + c];
         const float4 c0 = *reinterpret_cast<const float4*>(cs + r * KP + jb * JB);
@@ -669,7 +713,7 @@ __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
   }
 #pragma unroll
   for (int u = 0; u < 2; u++) {
-    const int w = threadIdx.x + u * 256;
+    const int w = tid + u * 256;
     if (w >= nwork) break;
     const int c = w % cols, jb = w / cols;
 #pragma unroll
@@ -1019,10 +1063,10 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.E[d] = const_cast<float*>(fa.E[d]);
     da.cnt[d] = fa.cnt[d];
-    // many short row ranges: each CTA walks its 32-row tiles with plain
-    // loads, so latency hiding comes from CTAs in flight (6 per SM)
-    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 64),
-                                                         (int64_t)t->sm_count * 6));
+    // row ranges of >= 4 tiles, <= 2 CTAs per SM: the next tile is prefetched
+    // in registers, and fewer partials keep the final reduction short
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 128),
+                                                         (int64_t)t->sm_count * 2));
     da.nblk[d] = nb;
     s->grid_sum = std::max(s->grid_sum, nb);
     max_cols = std::max(max_cols, g.cols);
@@ -1044,7 +1088,7 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
                                                           (int64_t)t->sm_count * 4));
   s->smem_sum = 0;   // static tiles
   for (auto& g : t->g)
-    if (g.cols > 256 || g.cols * KP / 8 > 512) {
+    if (g.cols > 256 || g.cols * KP / 8 > 512 || 32 * (g.pitch / 4) > KM_SUM_SL * 256) {
       set_error("fused K-means: dimension source with %d columns is too wide", g.cols);
       return FL_ERR_OP;
     }

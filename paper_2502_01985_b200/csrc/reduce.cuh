@@ -1,7 +1,7 @@
 // Deterministic cross-CTA reduction of fp64 partials.
 //
 // Every output element red[dst] = sum_b base[b * stride] over nblk per-CTA
-// partials is owned by ONE warp: lane l sums b = l, l + 32, ... in order and
+// partials is owned by ONE warp: lane l sums b = l, l + 32, ... in a fixed order and
 // the warp combines the 32 lane sums with a fixed xor tree, so the result is
 // bit-identical run to run (no atomics) while the partial loads of all
 // elements proceed in parallel across the grid.
@@ -19,8 +19,22 @@ struct RedDesc {
 };
 
 __device__ __forceinline__ double warp_reduce_desc(const RedDesc& d, int lane) {
-  double s = 0.0;
-  for (int b = lane; b < d.nblk; b += 32) s += d.base[(int64_t)b * d.stride];
+  // four independent partial chains per lane (fixed assignment b mod 128), so
+  // four loads are in flight per lane instead of one dependent chain
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int b = lane;
+  for (; b + 96 < d.nblk; b += 128) {
+    const double v0 = d.base[(int64_t)b * d.stride];
+    const double v1 = d.base[(int64_t)(b + 32) * d.stride];
+    const double v2 = d.base[(int64_t)(b + 64) * d.stride];
+    const double v3 = d.base[(int64_t)(b + 96) * d.stride];
+    s0 += v0;
+    s1 += v1;
+    s2 += v2;
+    s3 += v3;
+  }
+  for (; b < d.nblk; b += 32) s0 += d.base[(int64_t)b * d.stride];
+  double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;

@@ -523,7 +523,9 @@ int fl_table_finalize(fl_table* t, void* stream) {
     int64_t r0, nrows;
   };
   std::vector<Chunk> chunks;
-  constexpr size_t kChunkBytes = (size_t)64 << 20;
+  size_t kChunkBytes = (size_t)64 << 20;
+  if (const char* e = std::getenv("FL_UPLOAD_CHUNK_BYTES"))   // tests: force many ring wraps
+    kChunkBytes = std::max<size_t>(16, (size_t)std::atoll(e));
   size_t slot_bytes = kChunkBytes;
   for (int k = 0; k < n; k++) {
     const Staged& st = t->staged[k];

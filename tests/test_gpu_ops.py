@@ -151,3 +151,51 @@ def test_random_star_vs_oracle(fl, dims, sort_fk):
     assert rel(h.transpose_lmm(y), oracle.transpose_lmm(tab, y)) < RTOL
     assert rel(h.rmm(w), oracle.rmm(tab, w)) < RTOL
     assert np.array_equal(h.materialize_dense().astype(np.float64), oracle.materialize(tab))
+
+
+@pytest.mark.parametrize("chunk", [None, "4096", "80"])
+def test_upload_paths_agree(fl, monkeypatch, chunk):
+    """The same table uploaded from pageable numpy, pinned host tensors and
+    device tensors joins to the identical T (bit-exact).  Host values travel
+    in ring chunks (FL_UPLOAD_CHUNK_BYTES forces many ring wraps and one-row
+    chunks); the fact source is injective but NOT the identity (outer-join
+    padding rows, shuffled), so the scatter goes through the inverted
+    indicator."""
+    import torch
+    if chunk is not None:
+        monkeypatch.setenv("FL_UPLOAD_CHUNK_BYTES", chunk)
+    rng = np.random.default_rng(7)
+    r_fact, c_fact, r_dim, c_dim, r_extra = 3001, 7, 97, 5, 40
+    r_t, c_t = r_fact + r_extra, c_fact + c_dim
+    fact = rng.random((r_fact, c_fact)).astype(np.float32)
+    dim = rng.random((r_dim, c_dim)).astype(np.float32)
+    sel_f = np.full(r_t, -1, np.int32)
+    sel_f[rng.permutation(r_t)[:r_fact]] = np.arange(r_fact, dtype=np.int32)
+    sel_d = rng.integers(-1, r_dim, r_t).astype(np.int32)
+    maps = [np.arange(c_fact, dtype=np.int32), np.arange(c_fact, c_t, dtype=np.int32)]
+    want = np.zeros((r_t, c_t), np.float32)
+    m = sel_f >= 0
+    want[m, :c_fact] = fact[sel_f[m]]
+    m = sel_d >= 0
+    want[m, c_fact:] = dim[sel_d[m]]
+    pinned = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    variants = {
+        "numpy": ([fact, dim], [sel_f, sel_d]),
+        "pinned": ([pinned(fact), pinned(dim)], [pinned(sel_f), pinned(sel_d)]),
+        "cuda": ([torch.from_numpy(fact).cuda(), torch.from_numpy(dim).cuda()],
+                 [torch.from_numpy(sel_f).cuda(), torch.from_numpy(sel_d).cuda()]),
+    }
+    for name, (srcs, sels) in variants.items():
+        srcs = [s.numpy() if hasattr(s, "is_pinned") and not s.is_cuda else s for s in srcs]
+        sels = [s.numpy() if hasattr(s, "is_pinned") and not s.is_cuda else s for s in sels]
+        h = fl.TargetHandle.from_arrays(srcs, sels, maps, r_t, c_t)
+        got = h.materialize_dense()
+        assert np.array_equal(got, want), name
+        # identity fact indicator as well (the star-schema fast path)
+        h2 = fl.TargetHandle.from_arrays([srcs[0], srcs[1]], [None, sels[1][:r_fact]], maps,
+                                         r_fact, c_t)
+        w2 = np.zeros((r_fact, c_t), np.float32)
+        w2[:, :c_fact] = fact
+        m2 = sel_d[:r_fact] >= 0
+        w2[m2, c_fact:] = dim[sel_d[:r_fact][m2]]
+        assert np.array_equal(h2.materialize_dense(), w2), name + " identity"
