@@ -77,7 +77,11 @@ struct DimArgs {
   double* part[MAX_GATHER];      // nblk x pitch
   uint32_t stage_bytes;
   int nst;
+  float* bins_zero;              // K1 zeroes the sort source's bins for this iteration
+  int64_t bins_n;
 };
+
+constexpr int kGlmGraphIters = 8;
 
 struct UpdateArgs {
   int c_T, pf, ng;
@@ -115,29 +119,37 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_q(DimArgs a) {
   __shared__ uint64_t bar[4];
   __shared__ float4 w4[64];
   const int d = blockIdx.y;
-  if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
+  const bool active = d < a.ng && (int)blockIdx.x < a.nblk[d];
   const int tid = threadIdx.x;
-  const int pitch = a.pitch[d], c4 = pitch / 4;
-  const int64_t rows = a.rows[d];
+  const int pitch = active ? a.pitch[d] : 4, c4 = pitch / 4;
+  const int64_t rows = active ? a.rows[d] : 0;
   const int64_t ntiles = ceil_div(rows, TILE);
-  const int nb = a.nblk[d];
+  const int nb = active ? a.nblk[d] : 1;
   const int64_t base = ntiles / nb, rem = ntiles % nb;
   const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
-  const int64_t cnt = base + (blockIdx.x < rem ? 1 : 0);
+  const int64_t cnt = active ? base + (blockIdx.x < rem ? 1 : 0) : 0;
   const uint32_t tile_bytes = TILE * pitch * 4;
-  for (int j = tid; j < c4; j += NTHREADS) w4[j] = reinterpret_cast<const float4*>(a.w[d])[j];
-  if (tid == 0) {
+  // S_d is immutable: its first tiles stream in before the dependency wait
+  if (tid == 0 && active) {
     for (int s = 0; s < a.nst; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
     for (int s = 0; s < a.nst && s < cnt; s++) {
       mbar_arrive_expect_tx(&bar[s], tile_bytes);
       bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + s) * TILE * (int64_t)pitch, tile_bytes,
                &bar[s]);
     }
   }
+  pdl_wait();      // w_d (previous update) final; previous dim_t done with bins
+  pdl_trigger();
+  if (a.bins_zero) {
+    const int64_t nt = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+    for (int64_t i = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + tid;
+         i < a.bins_n; i += nt)
+      a.bins_zero[i] = 0.f;
+  }
+  if (!active) return;
+  for (int j = tid; j < c4; j += NTHREADS) w4[j] = reinterpret_cast<const float4*>(a.w[d])[j];
+  __syncthreads();
   for (int64_t i = 0; i < cnt; i++) {
     const int s = (int)(i % a.nst);
     mbar_wait(&bar[s], (uint32_t)((i / a.nst) & 1));
@@ -529,17 +541,19 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u,
     const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
     const int64_t cnt = base + (blockIdx.x < rem ? 1 : 0);
     const uint32_t tile_bytes = TILE * pitch * 4;
+    // S_d is immutable: its first tiles stream in before the dependency wait
     if (tid == 0) {
       for (int s = 0; s < a.nst; s++) mbar_init(&bar[s], 1);
       fence_mbar_init();
-    }
-    __syncthreads();
-    if (tid == 0)
       for (int s = 0; s < a.nst && s < cnt; s++) {
         mbar_arrive_expect_tx(&bar[s], tile_bytes);
         bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + s) * TILE * (int64_t)pitch, tile_bytes,
                  &bar[s]);
       }
+    }
+    pdl_wait();      // bins / residuals of this iteration's fact pass are final
+    pdl_trigger();
+    __syncthreads();
     const int Gr = NTHREADS / c4;
     const bool pb = tid < Gr * c4;
     const int pj = tid % c4, pg = tid / c4;
@@ -604,6 +618,7 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u,
       }
     }
   }
+  if (!active) pdl_wait();   // the last-CTA election below reads / writes shared state
   // last-block-done over the whole grid
   __threadfence();
   __syncthreads();
@@ -624,9 +639,19 @@ __global__ void k_glm_update(UpdateArgs u) { glm_apply_update(u); }
 
 namespace flb {
 template <int MODEL, int C4>
-static void launch_fw(const GlmFactWArgs& a, int grid, size_t smem, cudaStream_t st) {
+static void launch_fw(const GlmFactWArgs& a, int grid, size_t smem, cudaStream_t st, bool pdl) {
   constexpr int RPL = C4 <= 7 ? 2 : 1;
-  k_glm_fact_w<MODEL, C4, RPL><<<grid, FW_WARPS * 32, smem, st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(FW_WARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && std::getenv("FL_NO_PDL") == nullptr) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_glm_fact_w<MODEL, C4, RPL>, a);
 }
 template <int MODEL, int C4>
 static const void* fw_ptr() {
@@ -643,8 +668,8 @@ static const void* fw_kernel(int model, int c4) {
   return nullptr;
 }
 static void fw_launch(int model, int c4, const GlmFactWArgs& a, int grid, size_t smem,
-                      cudaStream_t st) {
-#define FW_LAUNCH(M, C) if (c4 == C) { launch_fw<M, C>(a, grid, smem, st); return; }
+                      cudaStream_t st, bool pdl = false) {
+#define FW_LAUNCH(M, C) if (c4 == C) { launch_fw<M, C>(a, grid, smem, st, pdl); return; }
   if (model == 0) { FW_CASES(0, FW_LAUNCH) } else { FW_CASES(1, FW_LAUNCH) }
 #undef FW_LAUNCH
 }
@@ -740,6 +765,7 @@ struct fl_glm {
   UpdateArgs ua{};
   int loss_cap = 1 << 16;
   cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph_n = nullptr;   // kGlmGraphIters iterations
   cudaStream_t cap_stream = nullptr;
   int bins_rows = 0;
   bool use_fw = false;
@@ -782,6 +808,29 @@ static int glm_u_update(fl_glm* s, cudaStream_t st) {
   return FL_OK;
 }
 
+// PDL launch (FL_NO_PDL=1 turns the attribute off for A/B timing).  Only
+// kernels that call pdl_wait() before touching their predecessor's outputs
+// may be launched with pdl = true.
+static bool pdl_enabled() {
+  static const bool on = std::getenv("FL_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, size_t smem,
+                            cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
   if (s->unfused) {
     int rc = glm_u_partial(s, st);
@@ -789,11 +838,10 @@ static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
     return fuse_update ? glm_u_update(s, st) : FL_OK;
   }
   fl_table* t = s->t;
-  if (s->bins_rows > 0) FL_CUDA(cudaMemsetAsync(s->bins.p, 0, (size_t)s->bins_rows * 4, st));
+  // the sort source's bins are zeroed by k_glm_dim_q (after its PDL wait)
   if (s->da.ng > 0) {
     dim3 grid(s->dim_grid_x, s->da.ng);
-    k_glm_dim_q<<<grid, NTHREADS, s->smem_dim, st>>>(s->da);
-    FL_CHECK_LAUNCH();
+    FL_CUDA(launch_k(true, k_glm_dim_q, grid, dim3(NTHREADS), s->smem_dim, st, s->da));
   }
   if (s->use_csr) {
     if (s->model == FL_MODEL_LINREG)
@@ -801,15 +849,15 @@ static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
     else
       k_glm_fact_csr<1><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
   } else if (s->use_fw)
-    fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st);
+    fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st, true);
   else if (s->model == FL_MODEL_LINREG)
     k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
   else
     k_glm_fact<1><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
   FL_CHECK_LAUNCH();
   dim3 grid3(std::max(1, s->dim_grid_x), std::max(1, s->da.ng));
-  k_glm_dim_t<<<grid3, NTHREADS, s->smem_dim, st>>>(s->da, s->ua, fuse_update ? 1 : 0);
-  FL_CHECK_LAUNCH();
+  FL_CUDA(launch_k(true, k_glm_dim_t, grid3, dim3(NTHREADS), s->smem_dim, st, s->da, s->ua,
+                   fuse_update ? 1 : 0));
   (void)t;
   return FL_OK;
 }
@@ -1172,6 +1220,8 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
       po += (size_t)da.nblk[d] * g.pitch;
     }
     da.resid = fa.resid;
+    da.bins_zero = s->bins_rows > 0 ? s->bins.as<float>() : nullptr;
+    da.bins_n = s->bins_rows;
   }
   UpdateArgs& ua = s->ua;
   ua.c_T = t->c_T;
@@ -1237,18 +1287,29 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
     }
     return FL_OK;
   }
-  if (!s->graph) {
+  // two graphs: one iteration, and kGlmGraphIters iterations back to back
+  // (inside a graph the PDL edges let each kernel's prologue -- barrier
+  // setup, the first TMA tiles of its immutable operands -- overlap the
+  // previous kernel's tail, also across iteration boundaries)
+  auto capture = [&](int n, cudaGraphExec_t* out) -> int {
     if (!s->cap_stream) FL_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t g;
     FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
-    int rc = glm_launch_iteration(s, s->cap_stream, true);
+    int rc = FL_OK;
+    for (int i = 0; i < n && rc == FL_OK; i++) rc = glm_launch_iteration(s, s->cap_stream, true);
     cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
     if (rc) return rc;
     FL_CUDA(e);
-    FL_CUDA(cudaGraphInstantiate(&s->graph, g, 0));
+    FL_CUDA(cudaGraphInstantiate(out, g, 0));
     FL_CUDA(cudaGraphDestroy(g));
-  }
-  for (int i = 0; i < iterations; i++) FL_CUDA(cudaGraphLaunch(s->graph, st));
+    return FL_OK;
+  };
+  int rc;
+  if (!s->graph && (rc = capture(1, &s->graph))) return rc;
+  const int nbig = iterations / kGlmGraphIters;
+  if (nbig > 0 && !s->graph_n && (rc = capture(kGlmGraphIters, &s->graph_n))) return rc;
+  for (int i = 0; i < nbig; i++) FL_CUDA(cudaGraphLaunch(s->graph_n, st));
+  for (int i = nbig * kGlmGraphIters; i < iterations; i++) FL_CUDA(cudaGraphLaunch(s->graph, st));
   return FL_OK;
 }
 
@@ -1291,8 +1352,7 @@ int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
   float acc[3] = {0.f, 0.f, 0.f};
   for (int i = 0; i < iters; i++) {
     FL_CUDA(cudaEventRecord(ev[0], st));
-    if (s->bins_rows > 0) FL_CUDA(cudaMemsetAsync(s->bins.p, 0, (size_t)s->bins_rows * 4, st));
-    if (s->da.ng > 0) {
+    if (s->da.ng > 0) {   // (zeroes the bins too)
       dim3 grid(s->dim_grid_x, s->da.ng);
       k_glm_dim_q<<<grid, NTHREADS, s->smem_dim, st>>>(s->da);
       FL_CHECK_LAUNCH();
@@ -1349,6 +1409,7 @@ int fl_glm_destroy(fl_glm* s) {
   if (!s) return FL_OK;
   cudaSetDevice(s->t->device);
   if (s->graph) cudaGraphExecDestroy(s->graph);
+  if (s->graph_n) cudaGraphExecDestroy(s->graph_n);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   delete s;
   return FL_OK;

@@ -70,21 +70,6 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
   char* wsm = smem + (size_t)warp * a.nst * a.stage_bytes;
   uint64_t* wbar = bar[warp];
 
-  for (int j = threadIdx.x; j < C4; j += blockDim.x)
-    w_s[j] = reinterpret_cast<const float4*>(a.wF)[j];
-  for (int j = lane; j < C4 * 4; j += 32) gsum[warp][j] = 0.0;
-  if (lane == 0) {
-    lsum[warp] = 0.0;
-    for (int s = 0; s < a.nst; s++) mbar_init(&wbar[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  float4 w[W_REG ? C4 : 1];
-  if (W_REG) {
-#pragma unroll
-    for (int j = 0; j < C4; j++) w[j] = w_s[j];
-  }
-
   auto issue = [&](int s, int64_t unit) {
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
@@ -93,8 +78,25 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
              &wbar[s]);
     if (has_sort) bulk_g2s(st + a.off_fk, fks + unit * RW, RW * 4, &wbar[s]);
   };
-  if (lane == 0)
+  // F, labels and FKs are immutable: the warp's first stages stream in before
+  // the dependency wait (PDL), overlapping the previous kernel's tail
+  if (lane == 0) {
+    lsum[warp] = 0.0;
+    for (int s = 0; s < a.nst; s++) mbar_init(&wbar[s], 1);
+    fence_mbar_init();
     for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
+  }
+  for (int j = lane; j < C4 * 4; j += 32) gsum[warp][j] = 0.0;
+  pdl_wait();      // w (previous update) and q (this iteration's dim_q) are final
+  pdl_trigger();
+  for (int j = threadIdx.x; j < C4; j += blockDim.x)
+    w_s[j] = reinterpret_cast<const float4*>(a.wF)[j];
+  __syncthreads();
+  float4 w[W_REG ? C4 : 1];
+  if (W_REG) {
+#pragma unroll
+    for (int j = 0; j < C4; j++) w[j] = w_s[j];
+  }
 
   // the warp's first segment may have begun before W0
   int head_key = -1;

@@ -241,6 +241,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor
+// drains; everything before pdl_wait() must touch only data the predecessor
+// does not write (immutable inputs, own shared memory).  pdl_wait() returns
+// once the predecessor grid has completed and its writes are visible (a
+// no-op for a normal launch); pdl_trigger() lets the successor be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
