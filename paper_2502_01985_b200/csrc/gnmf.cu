@@ -89,7 +89,8 @@ struct GnHArgs {
 // ---------------------------------------------------------------------------
 // U: loss of the previous iteration, H update, HH = H H^T (one CTA, fp64)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_gnmf_h(GnHArgs a, int do_update, int do_loss) {
+__global__ void __launch_bounds__(256) k_gnmf_h(GnHArgs a, int do_update, int do_loss,
+                                                int stage) {
   extern __shared__ double sh[];
   const int R = a.R, c_T = a.c_T, tid = threadIdx.x;
   double* GH = sh;                  // R x c_T
@@ -97,18 +98,32 @@ __global__ void __launch_bounds__(256) k_gnmf_h(GnHArgs a, int do_update, int do
   __shared__ double red_s[256];
   const double* P = a.red;
   const double* G = a.red + (size_t)R * c_T;
+  // H and G staged in shared memory when they fit (every product reads them
+  // R times); otherwise the products read the global copies
+  double* Hs = stage ? HH + R * R : a.H;            // R x c_T
+  double* Gs = stage ? Hs + R * c_T : const_cast<double*>(G);   // R x R
+  if (stage) {
+    for (int i = tid; i < R * c_T; i += blockDim.x) Hs[i] = a.H[i];
+    for (int i = tid; i < R * R; i += blockDim.x) Gs[i] = G[i];
+  }
+  __syncthreads();
   // HH of the current H (loss uses H of the iteration the products were made with)
   for (int i = tid; i < R * R; i += blockDim.x) {
     int r = i / R, q = i - r * R;
-    double s = 0.0;
-    for (int c = 0; c < c_T; c++) s += a.H[r * c_T + c] * a.H[q * c_T + c];
-    HH[i] = s;
+    double s0 = 0.0, s1 = 0.0;
+    int c = 0;
+    for (; c + 1 < c_T; c += 2) {
+      s0 += Hs[r * c_T + c] * Hs[q * c_T + c];
+      s1 += Hs[r * c_T + c + 1] * Hs[q * c_T + c + 1];
+    }
+    if (c < c_T) s0 += Hs[r * c_T + c] * Hs[q * c_T + c];
+    HH[i] = s0 + s1;
   }
   __syncthreads();
   if (do_loss) {
     double part = 0.0;
-    for (int i = tid; i < R * c_T; i += blockDim.x) part -= 2.0 * P[i] * a.H[i];
-    for (int i = tid; i < R * R; i += blockDim.x) part += G[i] * HH[i];
+    for (int i = tid; i < R * c_T; i += blockDim.x) part -= 2.0 * P[i] * Hs[i];
+    for (int i = tid; i < R * R; i += blockDim.x) part += Gs[i] * HH[i];
     red_s[tid] = part;
     __syncthreads();
     if (tid == 0) {
@@ -126,24 +141,26 @@ __global__ void __launch_bounds__(256) k_gnmf_h(GnHArgs a, int do_update, int do
     for (int i = tid; i < R * c_T; i += blockDim.x) {
       int r = i / c_T, c = i - r * c_T;
       double s = 0.0;
-      for (int q = 0; q < R; q++) s += G[r * R + q] * a.H[q * c_T + c];
+      for (int q = 0; q < R; q++) s += Gs[r * R + q] * Hs[q * c_T + c];
       GH[i] = s;
     }
     __syncthreads();
     for (int i = tid; i < R * c_T; i += blockDim.x) {
       int r = i / c_T;
-      a.H[i] = r < a.rank ? a.H[i] * P[i] / (GH[i] + GN_EPS) : 0.0;
+      const double h = r < a.rank ? Hs[i] * P[i] / (GH[i] + GN_EPS) : 0.0;
+      a.H[i] = h;
+      Hs[i] = h;
     }
     __syncthreads();
     for (int i = tid; i < R * R; i += blockDim.x) {
       int r = i / R, q = i - r * R;
       double s = 0.0;
-      for (int c = 0; c < c_T; c++) s += a.H[r * c_T + c] * a.H[q * c_T + c];
+      for (int c = 0; c < c_T; c++) s += Hs[r * c_T + c] * Hs[q * c_T + c];
       a.HH32[i] = (float)s;
     }
     if (tid == 0) a.state->it += 1;
   }
-  for (int i = tid; i < R * c_T; i += blockDim.x) a.H32[i] = (float)a.H[i];
+  for (int i = tid; i < R * c_T; i += blockDim.x) a.H32[i] = (float)Hs[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -168,19 +185,27 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_g(GnDimArgs a) {
 #pragma unroll
     for (int j = 0; j < R; j++) acc[j] = 0.f;
     const float4* sr = reinterpret_cast<const float4*>(a.S[d] + row * pitch);
-    for (int c4 = 0; c4 < pitch / 4; c4++) {
-      const float4 v = sr[c4];
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+    const int n4 = pitch / 4;
+    // batches of 8 independent float4 loads: one latency per batch
+    for (int c0 = 0; c0 < n4; c0 += 8) {
+      float4 vb[8];
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const float4* hr = reinterpret_cast<const float4*>(sm_g + (c4 * 4 + e) * R);
+      for (int u = 0; u < 8; u++) vb[u] = c0 + u < n4 ? sr[c0 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < R / 4; q++) {
-          const float4 h = hr[q];
-          acc[q * 4 + 0] = fmaf(vv[e], h.x, acc[q * 4 + 0]);
-          acc[q * 4 + 1] = fmaf(vv[e], h.y, acc[q * 4 + 1]);
-          acc[q * 4 + 2] = fmaf(vv[e], h.z, acc[q * 4 + 2]);
-          acc[q * 4 + 3] = fmaf(vv[e], h.w, acc[q * 4 + 3]);
+      for (int u = 0; u < 8; u++) {
+        if (c0 + u >= n4) break;
+        const float vv[4] = {vb[u].x, vb[u].y, vb[u].z, vb[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float4* hr = reinterpret_cast<const float4*>(sm_g + ((c0 + u) * 4 + e) * R);
+#pragma unroll
+          for (int q = 0; q < R / 4; q++) {
+            const float4 h = hr[q];
+            acc[q * 4 + 0] = fmaf(vv[e], h.x, acc[q * 4 + 0]);
+            acc[q * 4 + 1] = fmaf(vv[e], h.y, acc[q * 4 + 1]);
+            acc[q * 4 + 2] = fmaf(vv[e], h.z, acc[q * 4 + 2]);
+            acc[q * 4 + 3] = fmaf(vv[e], h.w, acc[q * 4 + 3]);
+          }
         }
       }
     }
@@ -570,43 +595,81 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 // ---------------------------------------------------------------------------
 // P_d[j, c] = sum_r Z_d[r, j] S_d[r, c]: 32-row tiles of S and Z (Z converted
 // to fp32 once) in smem; thread = (column, 8 ranks); fp32 within a tile,
-// fp64 across tiles
+// fp64 across tiles.  Each thread holds its share of the NEXT tile in
+// registers (loads issued before the current tile's math): one load latency
+// per CTA instead of one per tile.  Pitches up to 288 floats.
+constexpr int GN_P_SL = 9;
 template <int R>
 __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
   constexpr int JB = 8, NJB = R / JB;
+  constexpr int ZL = (32 * R / 2 + 255) / 256;   // double2 slots per thread
   __shared__ float ss[32 * 257];
   __shared__ __align__(16) float zs[32 * R];
-  const int cols = a.cols[d], pitch = a.pitch[d];
+  const int cols = a.cols[d], pitch = a.pitch[d], pitch4 = pitch / 4;
   const int64_t rows = a.rows[d];
   const int nb = a.nblk[d];
   const int64_t rpb = ceil_div(ceil_div(rows, nb), 32) * 32;
   const int64_t r0 = blockIdx.x * rpb, r1 = min64(rows, r0 + rpb);
   const int nwork = cols * NJB;
+  const int nS4 = 32 * pitch4;
+  const int tid = threadIdx.x;
+  const float4* S4 = reinterpret_cast<const float4*>(a.S[d]);
+  const double2* Z2 = reinterpret_cast<const double2*>(a.Z[d]);
+  float4 pv[GN_P_SL];
+  double2 pz[ZL];
+  auto load = [&](int64_t rb) {
+#pragma unroll
+    for (int sl = 0; sl < GN_P_SL; sl++) {
+      const int i = tid + sl * 256;
+      const int r = i / pitch4, c4 = i - r * pitch4;
+      pv[sl] = (i < nS4 && rb + r < r1) ? S4[(rb + r) * pitch4 + c4]
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int zl = 0; zl < ZL; zl++) {
+      const int i = tid + zl * 256;   // double2 index inside the tile
+      const int r = (2 * i) / R;
+      pz[zl] = (i < 16 * R && rb + r < r1) ? Z2[rb * (R / 2) + i] : make_double2(0.0, 0.0);
+    }
+  };
   double acc64[2][JB];
 #pragma unroll
   for (int u = 0; u < 2; u++)
 #pragma unroll
     for (int j = 0; j < JB; j++) acc64[u][j] = 0.0;
+  if (r0 < r1) load(r0);
   for (int64_t rb = r0; rb < r1; rb += 32) {
-    const int nr = (int)min64(32, r1 - rb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < 32 * cols; i += blockDim.x) {
-      const int r = i / cols, c = i - r * cols;
-      ss[r * 257 + c] = r < nr ? a.S[d][(rb + r) * pitch + c] : 0.f;
+    __syncthreads();   // the previous tile's math is done with ss / zs
+#pragma unroll
+    for (int sl = 0; sl < GN_P_SL; sl++) {
+      const int i = tid + sl * 256;
+      if (i < nS4) {   // padding columns (c >= cols) are not stored
+        const int r = i / pitch4, c = 4 * (i - r * pitch4);
+        if (c + 0 < cols) ss[r * 257 + c + 0] = pv[sl].x;
+        if (c + 1 < cols) ss[r * 257 + c + 1] = pv[sl].y;
+        if (c + 2 < cols) ss[r * 257 + c + 2] = pv[sl].z;
+        if (c + 3 < cols) ss[r * 257 + c + 3] = pv[sl].w;
+      }
     }
-    for (int i = threadIdx.x; i < 32 * R; i += blockDim.x)
-      zs[i] = i < nr * R ? (float)a.Z[d][rb * R + i] : 0.f;
+#pragma unroll
+    for (int zl = 0; zl < ZL; zl++) {
+      const int i = tid + zl * 256;
+      if (i < 16 * R)
+        *reinterpret_cast<float2*>(zs + 2 * i) = make_float2((float)pz[zl].x, (float)pz[zl].y);
+    }
     __syncthreads();
+    if (rb + 32 < r1) load(rb + 32);   // in flight during this tile's math
 #pragma unroll
     for (int u = 0; u < 2; u++) {
-      const int w = threadIdx.x + u * 256;
+      const int w = tid + u * 256;
       if (w >= nwork) break;
       const int c = w % cols, jb = w / cols;
       float acc[JB];
 #pragma unroll
       for (int j = 0; j < JB; j++) acc[j] = 0.f;
+#pragma unroll 8
       for (int r = 0; r < 32; r++) {
         const float v = ss[r * 257 + c];
         const float4 z0 = *reinterpret_cast<const float4*>(zs + r * R + jb * JB);
@@ -622,7 +685,7 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
   }
 #pragma unroll
   for (int u = 0; u < 2; u++) {
-    const int w = threadIdx.x + u * 256;
+    const int w = tid + u * 256;
     if (w >= nwork) break;
     const int c = w % cols, jb = w / cols;
 #pragma unroll
@@ -716,6 +779,7 @@ struct fl_gnmf {
   GnHArgs ha{};
   int nblk_fact = 0, grid_g = 1, grid_p = 1, grid_red = 1;
   size_t smem_fact = 0, smem_g = 0, smem_p = 0, smem_h = 0;
+  int stage_h = 0;   // k_gnmf_h stages H and G in shared memory
   DevBuf descs;
   int n_desc = 0;
   DevBuf W, H, H32, HH32, Gd, Z, wpart, part_fact, part_dim, red, loss_hist, state;
@@ -760,7 +824,7 @@ static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
 }
 
 static int gn_h(fl_gnmf* s, cudaStream_t st, bool update, bool loss) {
-  k_gnmf_h<<<1, 256, s->smem_h, st>>>(s->ha, update ? 1 : 0, loss ? 1 : 0);
+  k_gnmf_h<<<1, 256, s->smem_h, st>>>(s->ha, update ? 1 : 0, loss ? 1 : 0, s->stage_h);
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
@@ -947,10 +1011,10 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.Gd[d] = const_cast<float*>(fa.Gd[d]);
     da.Z[d] = fa.Z[d];
-    // many short row ranges: each CTA walks its 32-row tiles with plain
-    // loads, so latency hiding comes from CTAs in flight (6 per SM)
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 64),
-                                                               (int64_t)t->sm_count * 6));
+    // row ranges of >= 4 tiles, <= 2 CTAs per SM: the next tile is prefetched
+    // in registers, and fewer partials keep the final reduction short
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 128),
+                                                               (int64_t)t->sm_count * 2));
     da.nblk[d] = nb;
     s->grid_p = std::max(s->grid_p, nb);
     max_cols = std::max(max_cols, g.cols);
@@ -972,7 +1036,7 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
                                                           (int64_t)t->sm_count * 4));
   s->smem_p = 0;   // static tiles
   for (auto& g : t->g)
-    if (g.cols > 256 || g.cols * R / 8 > 512) {
+    if (g.cols > 256 || g.cols * R / 8 > 512 || 32 * (g.pitch / 4) > GN_P_SL * 256) {
       set_error("fused GNMF: dimension source with %d columns is too wide", g.cols);
       return FL_ERR_OP;
     }
@@ -1028,6 +1092,8 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   ha.loss_cap = s->loss_cap;
   ha.state = s->state.as<GnState>();
   s->smem_h = ((size_t)R * c_T + (size_t)R * R) * 8;
+  s->stage_h = 2 * s->smem_h <= 200 * 1024;
+  if (s->stage_h) s->smem_h *= 2;
   if (s->smem_h > 200 * 1024) {
     set_error("fused GNMF: rank x columns too large for the H update");
     return FL_ERR_OP;
