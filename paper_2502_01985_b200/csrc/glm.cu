@@ -759,7 +759,7 @@ struct fl_glm {
   GlmCsrArgs csr{};
   DevBuf csr_rp, csr_col, csr_val;
   size_t smem_csr = 0;
-  double csr_density = 1.0;
+  double csr_density = -1.0;   // < 0: not measured yet
   GlmFactArgs fa{};
   DimArgs da{};
   UpdateArgs ua{};
@@ -829,6 +829,24 @@ static cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, size_
   cfg.attrs = at;
   cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+// nonzero fraction of the real stream-block columns (one coalesced pass)
+static int glm_stream_density(fl_glm* s, cudaStream_t st) {
+  const fl_table* t = s->t;
+  DevBuf tot;
+  int rc;
+  if ((rc = tot.alloc(16))) return rc;
+  FL_CUDA(cudaMemsetAsync(tot.p, 0, 8, st));
+  k_nnz_total<<<(unsigned)(t->sm_count * 16), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(t->F->p), t->r_pad * t->pf / 4,
+      reinterpret_cast<unsigned long long*>(tot.p));
+  FL_CHECK_LAUNCH();
+  unsigned long long nnz_all = 0;
+  FL_CUDA(cudaMemcpyAsync(&nnz_all, tot.p, 8, cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  s->csr_density = (double)nnz_all / ((double)std::max<int64_t>(1, t->r_T) * std::max(1, t->nf));
+  return FL_OK;
 }
 
 static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
@@ -1087,19 +1105,12 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
   {
     const char* e = getenv("FL_GLM_SPARSE");
     const int mode = e ? atoi(e) : -1;
+    // the density probe runs only when it can change the decision (forced
+    // CSR, or an auto threshold above 0); fl_glm_path measures it on demand
     bool want_csr = false;
-    if (mode != 0 && s->use_fw && t->pf <= CSR_MAXP && t->nf > 0) {
-      DevBuf tot;
-      if ((rc = tot.alloc(16))) return rc;
-      FL_CUDA(cudaMemsetAsync(tot.p, 0, 8, st));
-      k_nnz_total<<<(unsigned)(t->sm_count * 16), 256, 0, st>>>(
-          reinterpret_cast<const float4*>(t->F->p), r_pad * t->pf / 4,
-          reinterpret_cast<unsigned long long*>(tot.p));
-      FL_CHECK_LAUNCH();
-      unsigned long long nnz_all = 0;
-      FL_CUDA(cudaMemcpyAsync(&nnz_all, tot.p, 8, cudaMemcpyDeviceToHost, st));
-      FL_CUDA(cudaStreamSynchronize(st));
-      s->csr_density = (double)nnz_all / ((double)std::max<int64_t>(1, t->r_T) * t->nf);
+    if (mode != 0 && s->use_fw && t->pf <= CSR_MAXP && t->nf > 0 &&
+        (mode == 1 || kCsrAutoDensity > 0.0)) {
+      if ((rc = glm_stream_density(s, st))) return rc;
       want_csr = mode == 1 || s->csr_density < kCsrAutoDensity;
     }
     if (want_csr) {
@@ -1319,7 +1330,18 @@ int fl_glm_path(fl_glm* s, int32_t* path, double* stream_density) {
     return FL_ERR_ARG;
   }
   if (path) *path = s->unfused ? 3 : s->use_csr ? 2 : s->use_fw ? 1 : 0;
-  if (stream_density) *stream_density = s->csr_density;
+  if (stream_density) {
+    if (s->csr_density < 0.0) {
+      if (s->unfused || s->t->nf == 0) {
+        s->csr_density = 1.0;
+      } else {
+        FL_CUDA(cudaSetDevice(s->t->device));
+        int rc = glm_stream_density(s, nullptr);
+        if (rc) return rc;
+      }
+    }
+    *stream_density = s->csr_density;
+  }
   return FL_OK;
 }
 

@@ -348,6 +348,7 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     set_error("fl_table_add_source: invalid source %lld x %d", (long long)r_k, c_k);
     return FL_ERR_ARG;
   }
+  const PhaseTrace tr("fl_table_add_source");
   FL_CUDA(cudaSetDevice(t->device));
   Staged st;
   st.rows = r_k;
@@ -419,8 +420,8 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     st.h_vals = values;
   }
   FL_CUDA(cudaEventRecord((cudaEvent_t)st.ev_vals.get(), cv));
-  (void)cv;
   t->staged.push_back(std::move(st));
+  tr.mark("issued");
   return FL_OK;
 }
 
@@ -453,6 +454,71 @@ int fl_table_finalize(fl_table* t, void* stream) {
       }
       owner[c] = k;
     }
+  // 0. host values of stream sources travel in chunks through a small device
+  // ring and are scattered to their device rows once the row order exists.
+  // Identity-indicator sources are streamed for certain, so their chunks
+  // start right away, overlapping the fanout analysis and the sort below.
+  cudaStream_t cv = (cudaStream_t)t->cp_vals.get();
+  struct Chunk {
+    int k;
+    int64_t r0, nrows;
+  };
+  std::vector<Chunk> chunks;
+  size_t kChunkBytes = (size_t)64 << 20;
+  if (const char* e = std::getenv("FL_UPLOAD_CHUNK_BYTES"))   // tests: force many ring wraps
+    kChunkBytes = std::max<size_t>(16, (size_t)std::atoll(e));
+  size_t slot_bytes = kChunkBytes;
+  int64_t chunks_upper = 0;   // chunks if every host source turned out injective
+  for (int k = 0; k < n; k++) {
+    const Staged& st = t->staged[k];
+    if (!st.h_vals) continue;
+    const size_t row_bytes = (size_t)st.cols * 4;
+    slot_bytes = std::max(slot_bytes, row_bytes);
+    chunks_upper += ceil_div(st.rows, std::max<int64_t>(1, (int64_t)(kChunkBytes / row_bytes)));
+  }
+  const int ring_n = (int)std::min<int64_t>(chunks_upper, 16);   // <= 1 GB: covers the sort
+  std::shared_ptr<DevBuf> ring;
+  if (ring_n > 0) {
+    ring = make_buf(slot_bytes * ring_n, &rc);
+    if (rc) return rc;
+  }
+  std::vector<std::shared_ptr<void>> ev_ready, ev_free;
+  auto mk_ev = []() -> std::shared_ptr<void> {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    return std::shared_ptr<void>(e, [](void* p) { cudaEventDestroy((cudaEvent_t)p); });
+  };
+  auto add_chunks = [&](int k) {
+    const Staged& st = t->staged[k];
+    const int64_t per = std::max<int64_t>(1, (int64_t)(kChunkBytes / ((size_t)st.cols * 4)));
+    for (int64_t r0 = 0; r0 < st.rows; r0 += per) {
+      chunks.push_back({k, r0, std::min(per, st.rows - r0)});
+      ev_ready.push_back(mk_ev());
+      ev_free.push_back(mk_ev());
+    }
+  };
+  int nissued = 0;
+  auto issue_chunk = [&](int c) -> int {
+    const Chunk& ch = chunks[c];
+    const Staged& st = t->staged[ch.k];
+    if (!ev_ready[c] || !ev_free[c]) {
+      set_error("fl_table_finalize: event creation failed");
+      return FL_ERR_CUDA;
+    }
+    char* slot = ring->as<char>() + (size_t)(c % ring_n) * slot_bytes;
+    if (c >= ring_n) FL_CUDA(cudaStreamWaitEvent(cv, (cudaEvent_t)ev_free[c - ring_n].get(), 0));
+    FL_CUDA(cudaMemcpyAsync(slot, st.h_vals + ch.r0 * st.cols, (size_t)ch.nrows * st.cols * 4,
+                            cudaMemcpyHostToDevice, cv));
+    FL_CUDA(cudaEventRecord((cudaEvent_t)ev_ready[c].get(), cv));
+    nissued = c + 1;
+    return FL_OK;
+  };
+  for (int k = 0; k < n; k++)
+    if (t->staged[k].h_vals && !t->staged[k].sel_given) add_chunks(k);
+  for (int c = 0; c < std::min((int)chunks.size(), ring_n); c++)
+    if ((rc = issue_chunk(c))) return rc;
+  mark("first chunks issued");
+
   // 1. fanout histograms -> classification
   std::vector<std::shared_ptr<DevBuf>> cnts(n);
   std::vector<int> maxfan(n);
@@ -506,69 +572,20 @@ int fl_table_finalize(fl_table* t, void* stream) {
       sort_k = k;
     }
   }
-  // 1b. host values go out now, on the value copy stream, while the row
-  // order below is derived: stream-source chunks fill a small device ring
-  // (scattered to their device rows once the order exists), gathered
-  // sources land directly in their pitched S_d.  Every host byte crosses
-  // PCIe once, in one stream, back to back.
-  cudaStream_t cv = (cudaStream_t)t->cp_vals.get();
+  // 1b. stream block and the rest of the host values: remaining stream-source
+  // chunks join the ring queue, gathered sources land directly in their
+  // pitched S_d.  Every host byte crosses PCIe once, in one stream.
   t->nf = stream_cols;
   t->pf = pitch_for(std::max(stream_cols, 1));
   t->f_tcol.assign(t->pf, -1);
   t->F = make_buf((size_t)r_pad * t->pf * 4 + 64, &rc);
   if (rc) return rc;
   FL_CUDA(cudaMemsetAsync(t->F->p, 0, (size_t)r_pad * t->pf * 4, s));
-  struct Chunk {
-    int k;
-    int64_t r0, nrows;
-  };
-  std::vector<Chunk> chunks;
-  size_t kChunkBytes = (size_t)64 << 20;
-  if (const char* e = std::getenv("FL_UPLOAD_CHUNK_BYTES"))   // tests: force many ring wraps
-    kChunkBytes = std::max<size_t>(16, (size_t)std::atoll(e));
-  size_t slot_bytes = kChunkBytes;
-  for (int k = 0; k < n; k++) {
-    const Staged& st = t->staged[k];
-    if (!t->src[k].stream || !st.h_vals) continue;
-    const size_t row_bytes = (size_t)st.cols * 4;
-    const int64_t per = std::max<int64_t>(1, (int64_t)(kChunkBytes / row_bytes));
-    slot_bytes = std::max(slot_bytes, row_bytes);
-    for (int64_t r0 = 0; r0 < st.rows; r0 += per)
-      chunks.push_back({k, r0, std::min(per, st.rows - r0)});
-  }
+  for (int k = 0; k < n; k++)
+    if (t->src[k].stream && t->staged[k].h_vals && t->staged[k].sel_given) add_chunks(k);
+  for (int c = nissued; c < std::min((int)chunks.size(), ring_n); c++)
+    if ((rc = issue_chunk(c))) return rc;
   const int nch = (int)chunks.size();
-  const int ring_n = std::min(nch, 16);   // 1 GB: covers the row-order sort
-  std::shared_ptr<DevBuf> ring;
-  std::vector<std::shared_ptr<void>> ev_ready(nch), ev_free(nch);
-  auto mk_ev = []() -> std::shared_ptr<void> {
-    cudaEvent_t e = nullptr;
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    return std::shared_ptr<void>(e, [](void* p) { cudaEventDestroy((cudaEvent_t)p); });
-  };
-  auto issue_chunk = [&](int c) -> int {
-    const Chunk& ch = chunks[c];
-    const Staged& st = t->staged[ch.k];
-    char* slot = ring->as<char>() + (size_t)(c % ring_n) * slot_bytes;
-    if (c >= ring_n) FL_CUDA(cudaStreamWaitEvent(cv, (cudaEvent_t)ev_free[c - ring_n].get(), 0));
-    FL_CUDA(cudaMemcpyAsync(slot, st.h_vals + ch.r0 * st.cols, (size_t)ch.nrows * st.cols * 4,
-                            cudaMemcpyHostToDevice, cv));
-    FL_CUDA(cudaEventRecord((cudaEvent_t)ev_ready[c].get(), cv));
-    return FL_OK;
-  };
-  if (nch > 0) {
-    ring = make_buf(slot_bytes * ring_n, &rc);
-    if (rc) return rc;
-    for (int c = 0; c < nch; c++) {
-      ev_ready[c] = mk_ev();
-      ev_free[c] = mk_ev();
-      if (!ev_ready[c] || !ev_free[c]) {
-        set_error("fl_table_finalize: event creation failed");
-        return FL_ERR_CUDA;
-      }
-    }
-    for (int c = 0; c < ring_n; c++)
-      if ((rc = issue_chunk(c))) return rc;
-  }
   // (a pitched H2D copy of short rows runs far below PCIe speed: the compact
   // rows cross as one contiguous copy and are re-pitched on the device)
   std::vector<std::shared_ptr<DevBuf>> host_S(n), host_tmp(n);
