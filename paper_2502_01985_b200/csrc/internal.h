@@ -68,8 +68,14 @@ inline int pitch_for(int c) {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t astream = nullptr;   // pooled buffers: freed stream-ordered on this stream
+  bool pooled = false;
   ~DevBuf();
   int alloc(size_t n);
+  // stream-ordered allocation from the library's temporary pool (released
+  // memory stays cached in the pool, so repeated uploads neither cudaMalloc
+  // nor pay cudaFree's device-wide wait)
+  int alloc_tmp(size_t n, cudaStream_t st);
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 

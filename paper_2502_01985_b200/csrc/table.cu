@@ -32,14 +32,66 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 }
 
 DevBuf::~DevBuf() {
-  if (p) cudaFree(p);
+  if (p) {
+    if (pooled)
+      cudaFreeAsync(p, astream);
+    else
+      cudaFree(p);
+  }
+}
+
+// per-device pool for upload temporaries; up to 8 GB stays cached between
+// tables (the C2 upload needs ~3 GB of them)
+static cudaMemPool_t tmp_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return nullptr;
+  if (!pools[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&pools[device], &props) != cudaSuccess) {
+      cudaGetLastError();
+      pools[device] = nullptr;
+      return nullptr;
+    }
+    uint64_t thr = (uint64_t)8 << 30;
+    cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[device];
+}
+
+int DevBuf::alloc_tmp(size_t n, cudaStream_t st) {
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool = tmp_pool(dev);
+  if (!pool) return alloc(n);
+  if (p) {
+    if (pooled)
+      cudaFreeAsync(p, astream);
+    else
+      cudaFree(p);
+    p = nullptr;
+  }
+  if (n == 0) n = 16;
+  FL_CUDA(cudaMallocFromPoolAsync(&p, n, pool, st));
+  bytes = n;
+  astream = st;
+  pooled = true;
+  return FL_OK;
 }
 
 int DevBuf::alloc(size_t n) {
   if (p) {
-    cudaFree(p);
+    if (pooled)
+      cudaFreeAsync(p, astream);
+    else
+      cudaFree(p);
     p = nullptr;
     bytes = 0;
+    pooled = false;
   }
   if (n == 0) n = 16;
   FL_CUDA(cudaMalloc(&p, n));
@@ -58,9 +110,27 @@ int device_sm_count(int device) {
   return n > 0 ? n : 148;
 }
 
+// device operands may still be in flight on the caller's streams: they are
+// copied synchronously (as cudaMemcpy orders them); host buffers go async
+static bool on_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
 static std::shared_ptr<DevBuf> make_buf(size_t bytes, int* rc) {
   auto b = std::make_shared<DevBuf>();
   *rc = b->alloc(bytes);
+  return b;
+}
+
+// temporary of the upload path (stream-ordered pool allocation on `st`)
+static std::shared_ptr<DevBuf> make_tmp(size_t bytes, cudaStream_t st, int* rc) {
+  auto b = std::make_shared<DevBuf>();
+  *rc = b->alloc_tmp(bytes, st);
   return b;
 }
 
@@ -253,11 +323,11 @@ static inline unsigned grid_for(int64_t n, int block = 256) {
 static int stable_order(const int32_t* ind_sel, int64_t r_T, int64_t r_k, int32_t* order_out,
                         cudaStream_t s, std::vector<std::shared_ptr<DevBuf>>* keep = nullptr) {
   int rc;
-  auto keys = make_buf(r_T * 4, &rc);
+  auto keys = make_tmp(r_T * 4, s, &rc);
   if (rc) return rc;
-  auto keys2 = make_buf(r_T * 4, &rc);
+  auto keys2 = make_tmp(r_T * 4, s, &rc);
   if (rc) return rc;
-  auto vals = make_buf(r_T * 4, &rc);
+  auto vals = make_tmp(r_T * 4, s, &rc);
   if (rc) return rc;
   k_sort_keys<<<grid_for(r_T), 256, 0, s>>>(ind_sel, r_T, keys->as<uint32_t>(),
                                             vals->as<int32_t>());
@@ -268,7 +338,7 @@ static int stable_order(const int32_t* ind_sel, int64_t r_T, int64_t r_k, int32_
   FL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys->as<uint32_t>(),
                                           keys2->as<uint32_t>(), vals->as<int32_t>(), order_out,
                                           (int)r_T, 0, end_bit, s));
-  auto tmp = make_buf(tmp_bytes, &rc);
+  auto tmp = make_tmp(tmp_bytes, s, &rc);
   if (rc) return rc;
   FL_CUDA(cub::DeviceRadixSort::SortPairs(tmp->p, tmp_bytes, keys->as<uint32_t>(),
                                           keys2->as<uint32_t>(), vals->as<int32_t>(), order_out,
@@ -362,8 +432,6 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     }
   }
   int rc;
-  st.ind_sel = make_buf((size_t)t->r_T * 4, &rc);
-  if (rc) return rc;
   // asynchronous uploads on the table's copy streams (values and FKs on
   // separate streams, so the FKs land early and finalize's index work
   // overlaps the large value copies); the caller keeps `values` / `ind_sel`
@@ -387,19 +455,19 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     return FL_ERR_CUDA;
   }
   cudaStream_t cv = (cudaStream_t)t->cp_vals.get(), ci = (cudaStream_t)t->cp_idx.get();
+  // the target-order indicator is an upload temporary (finalize derives the
+  // device-order FKs from it); a device operand is copied synchronously, so
+  // its buffer comes from the plain allocator
+  st.sel_given = ind_sel != nullptr;
+  if (ind_sel && on_device_ptr(ind_sel))
+    st.ind_sel = make_buf((size_t)t->r_T * 4, &rc);
+  else
+    st.ind_sel = make_tmp((size_t)t->r_T * 4, ci, &rc);
+  if (rc) return rc;
   // device operands may still be in flight on the caller's streams: copy
   // them synchronously (as cudaMemcpy orders them); host buffers go async
-  auto on_device = [](const void* p) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
-  };
-  st.sel_given = ind_sel != nullptr;
   if (ind_sel) {
-    if (on_device(ind_sel))
+    if (on_device_ptr(ind_sel))
       FL_CUDA(cudaMemcpy(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault));
     else
       FL_CUDA(cudaMemcpyAsync(st.ind_sel->p, ind_sel, (size_t)t->r_T * 4, cudaMemcpyDefault, ci));
@@ -408,7 +476,7 @@ int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* valu
     FL_CHECK_LAUNCH();
   }
   FL_CUDA(cudaEventRecord((cudaEvent_t)st.ev_idx.get(), ci));
-  if (on_device(values)) {
+  if (on_device_ptr(values)) {
     st.vals = make_buf((size_t)r_k * c_k * 4, &rc);
     if (rc) return rc;
     FL_CUDA(cudaMemcpy(st.vals->p, values, (size_t)r_k * c_k * 4, cudaMemcpyDefault));
@@ -479,7 +547,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
   const int ring_n = (int)std::min<int64_t>(chunks_upper, 16);   // <= 1 GB: covers the sort
   std::shared_ptr<DevBuf> ring;
   if (ring_n > 0) {
-    ring = make_buf(slot_bytes * ring_n, &rc);
+    ring = make_tmp(slot_bytes * ring_n, cv, &rc);
     if (rc) return rc;
   }
   std::vector<std::shared_ptr<void>> ev_ready, ev_free;
@@ -527,7 +595,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
   if (rc) return rc;
   for (int k = 0; k < n; k++) {
     Staged& st = t->staged[k];
-    cnts[k] = make_buf((st.rows + 1) * 4, &rc);
+    cnts[k] = make_tmp((st.rows + 1) * 4, s, &rc);
     if (rc) return rc;
     FL_CUDA(cudaMemsetAsync(cnts[k]->p, 0, (st.rows + 1) * 4, s));
     FL_CUDA(cudaMemsetAsync(bad->p, 0, 4, s));
@@ -538,11 +606,11 @@ int fl_table_finalize(fl_table* t, void* stream) {
     FL_CUDA(cudaMemcpyAsync(&h_bad, bad->p, 4, cudaMemcpyDeviceToHost, s));
     // max + sum of fanout
     size_t tb = 0;
-    auto dmax = make_buf(16, &rc);
+    auto dmax = make_tmp(16, s, &rc);
     if (rc) return rc;
     FL_CUDA(cub::DeviceReduce::Max(nullptr, tb, cnts[k]->as<int32_t>(), dmax->as<int32_t>(),
                                    (int)st.rows, s));
-    auto tmp = make_buf(tb, &rc);
+    auto tmp = make_tmp(tb, s, &rc);
     if (rc) return rc;
     FL_CUDA(cub::DeviceReduce::Max(tmp->p, tb, cnts[k]->as<int32_t>(), dmax->as<int32_t>(),
                                    (int)st.rows, s));
@@ -596,7 +664,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
     const int64_t rows_pad = round_up(st.rows, TILE);
     host_S[k] = make_buf((size_t)rows_pad * pitch * 4 + 64, &rc);
     if (rc) return rc;
-    host_tmp[k] = make_buf((size_t)st.rows * st.cols * 4, &rc);
+    host_tmp[k] = make_tmp((size_t)st.rows * st.cols * 4, cv, &rc);
     if (rc) return rc;
     FL_CUDA(cudaMemcpyAsync(host_tmp[k]->p, st.h_vals, (size_t)st.rows * st.cols * 4,
                             cudaMemcpyHostToDevice, cv));
@@ -613,7 +681,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
   if (rc) return rc;
   std::vector<std::shared_ptr<DevBuf>> orders(n);
   if (sort_k >= 0) {
-    orders[sort_k] = make_buf(r_T * 4, &rc);
+    orders[sort_k] = make_tmp(r_T * 4, s, &rc);
     if (rc) return rc;
     rc = stable_order(t->staged[sort_k].ind_sel->as<int32_t>(), r_T, t->staged[sort_k].rows,
                       orders[sort_k]->as<int32_t>(), s, &keep);
@@ -640,7 +708,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
     for (int c = 0; c < st.cols; c++) t->f_tcol[t->src[k].f_off + c] = st.col_map[c];
     if (st.h_vals) {
       if (st.rows == r_T && !st.sel_given) continue;   // identity indicator
-      invs[k] = make_buf((size_t)st.rows * 4, &rc);
+      invs[k] = make_tmp((size_t)st.rows * 4, s, &rc);
       if (rc) return rc;
       FL_CUDA(cudaMemsetAsync(invs[k]->p, 0xff, (size_t)st.rows * 4, s));
       k_invert_sel<<<grid_for(r_T), 256, 0, s>>>(st.ind_sel->as<int32_t>(), r_T,
@@ -699,7 +767,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
     // group_indptr = exclusive scan of fanout (ops.py:63-65)
     g.grp_ptr = make_buf((st.rows + 1) * 8, &rc);
     if (rc) return rc;
-    auto c64 = make_buf((st.rows + 1) * 8, &rc);
+    auto c64 = make_tmp((st.rows + 1) * 8, s, &rc);
     if (rc) return rc;
     k_cnt_to_i64<<<grid_for(st.rows + 1), 256, 0, s>>>(cnts[k]->as<int32_t>(), st.rows,
                                                        c64->as<int64_t>());
@@ -707,7 +775,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
     size_t tb = 0;
     FL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c64->as<int64_t>(), g.grp_ptr->as<int64_t>(),
                                           (int)(st.rows + 1), s));
-    auto tmp = make_buf(tb, &rc);
+    auto tmp = make_tmp(tb, s, &rc);
     if (rc) return rc;
     FL_CUDA(cub::DeviceScan::ExclusiveSum(tmp->p, tb, c64->as<int64_t>(), g.grp_ptr->as<int64_t>(),
                                           (int)(st.rows + 1), s));
@@ -720,7 +788,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
     g.n_neg = r_T - h_matched;
     g.sorted = (k == sort_k);
     if (!g.sorted) {
-      auto order = make_buf(r_T * 4, &rc);
+      auto order = make_tmp(r_T * 4, s, &rc);
       if (rc) return rc;
       rc = stable_order(st.ind_sel->as<int32_t>(), r_T, st.rows, order->as<int32_t>(), s, &keep);
       if (rc) return rc;

@@ -16,6 +16,8 @@ result is returned as a CUDA tensor and nothing crosses PCIe).
 from __future__ import annotations
 
 import ctypes as C
+import os
+import sys
 import time
 
 import numpy as np
@@ -83,9 +85,18 @@ def upload_arrays(sources, ind_sels, col_maps, r_T: int, c_T: int, *,
                   device: int = 0, stream=None) -> DeviceTable:
     """Upload plain arrays: sources[k] (r_k x c_k, cast to fp32), ind_sels[k]
     (r_T int32, -1 = no match), col_maps[k] (c_k int32 target columns)."""
+    trace = os.environ.get("FL_TRACE_UPLOAD") is not None
+    t_0 = time.perf_counter()
+
+    def mark(what):
+        if trace:
+            print(f"[upload_arrays] {what:<28s} {1e3 * (time.perf_counter() - t_0):8.3f} ms",
+                  file=sys.stderr, flush=True)
+
     lib = _lib.load()
     ptr = C.c_void_p()
     _lib.check(lib.fl_table_create(device, int(r_T), int(c_T), C.byref(ptr)), "fl_table_create")
+    mark("created")
     tab = DeviceTable(ptr, int(r_T), int(c_T), len(sources), device)
     alive = []   # host buffers must outlive the asynchronous uploads (until finalize)
     for vals, sel, cmap in zip(sources, ind_sels, col_maps):
@@ -107,8 +118,10 @@ def upload_arrays(sources, ind_sels, col_maps, r_T: int, c_T: int, *,
                                            C.c_void_p(s_ptr), m_keep.ctypes.data_as(C.c_void_p)),
                    "fl_table_add_source")
         alive.append((keep, s_keep, m_keep))
+        mark("source added")
     _lib.check(lib.fl_table_finalize(ptr, stream if stream is not None else C.c_void_p(0)),
                "fl_table_finalize")
+    mark("finalized")
     del alive
     return tab
 

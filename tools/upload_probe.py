@@ -32,11 +32,15 @@ def main():
     for j in range(4):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        c0 = time.process_time()
         h = fl.TargetHandle.from_arrays([t.numpy() for t in host],
                                         [None] + [f.numpy() for f in fks], maps,
                                         host[0].shape[0], c_t)
+        ta = time.perf_counter()
         torch.cuda.synchronize()
         t1 = time.perf_counter()
+        print(f"  from_arrays returned {1e3 * (ta - t0):.1f} ms, sync {1e3 * (t1 - ta):.1f} ms, "
+              f"process cpu {1e3 * (time.process_time() - c0):.1f} ms", flush=True)
         s = GlmSession(h, wl["model"], y_h.numpy(), 1e-9)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
