@@ -269,11 +269,18 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   if (lane == 0)
     for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
 
+  // the prefetched sources' loops are unrolled: compile-time source indices
+  // turn a.fk[d] / a.E[d] / a.rows[d] into constant-bank operands instead
+  // of indexed parameter loads per unit
   auto issue_fk = [&](int64_t unit, int slot) {
-    for (int d = 0; d < npf; d++) cp_async4(fkr + (slot * KM_PF + d) * 32 + lane, a.fk[d] + unit * 32 + lane);
+#pragma unroll
+    for (int d = 0; d < KM_PF; d++)
+      if (d < npf) cp_async4(fkr + (slot * KM_PF + d) * 32 + lane, a.fk[d] + unit * 32 + lane);
   };
   auto issue_e = [&](int slot) {
-    for (int d = 0; d < npf; d++) {
+#pragma unroll
+    for (int d = 0; d < KM_PF; d++) {
+      if (d >= npf) break;
       const int32_t* fr = fkr + (slot * KM_PF + d) * 32;
 #pragma unroll
       for (int jj = 0; jj < QR; jj++) {
@@ -349,7 +356,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     if (npf > 0) {
       cp_async_wait_all();   // this unit's E rows (and the next unit's FKs)
       __syncwarp();
-      for (int d = 0; d < npf; d++) {
+#pragma unroll
+      for (int d = 0; d < KM_PF; d++) {
+        if (d >= npf) break;
 #pragma unroll
         for (int q = 0; q < QR; q++) {
           const float4 v = *reinterpret_cast<const float4*>(
