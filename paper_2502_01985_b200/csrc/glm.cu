@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "reduce.cuh"
 
 namespace flb {
 
@@ -514,10 +515,7 @@ __device__ void glm_reduce_all(const UpdateArgs& u) {
       dst = u.d_tcol[d][c];
     }
     if (dst < 0) continue;
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += base[(int64_t)b * stride];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double s = warp_sum_strided(base, stride, nblk, lane);
     if (lane == 0) u.red[dst] = s;
   }
   __syncthreads();

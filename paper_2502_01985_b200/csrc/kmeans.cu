@@ -264,7 +264,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
     tma_load_2d(st, &tmF, 0, (int)(unit * 32), &wbar[s]);
-    for (int d = npf; d < a.ng; d++) bulk_g2s(st + F_BYTES + 128 * d, a.fk[d] + unit * 32, 128, &wbar[s]);
+#pragma unroll
+    for (int d = 0; d < MAX_GATHER; d++)   // FKs of the sources without an FK ring
+      if (d >= npf && d < a.ng) bulk_g2s(st + F_BYTES + 128 * d, a.fk[d] + unit * 32, 128, &wbar[s]);
   };
   if (lane == 0)
     for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);

@@ -18,26 +18,35 @@ struct RedDesc {
   int pad;
 };
 
-__device__ __forceinline__ double warp_reduce_desc(const RedDesc& d, int lane) {
-  // four independent partial chains per lane (fixed assignment b mod 128), so
-  // four loads are in flight per lane instead of one dependent chain
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+// sum of base[b * stride] over b < nblk by one warp, in a fixed order: lane
+// l owns b = l (mod 32) and keeps eight independent chains (b mod 256), so
+// eight loads per lane are in flight instead of one dependent chain; the 32
+// lane sums meet in a fixed xor tree
+__device__ __forceinline__ double warp_sum_strided(const double* __restrict__ base, int stride,
+                                                   int nblk, int lane) {
+  constexpr int CH = 8;
+  double acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; c++) acc[c] = 0.0;
   int b = lane;
-  for (; b + 96 < d.nblk; b += 128) {
-    const double v0 = d.base[(int64_t)b * d.stride];
-    const double v1 = d.base[(int64_t)(b + 32) * d.stride];
-    const double v2 = d.base[(int64_t)(b + 64) * d.stride];
-    const double v3 = d.base[(int64_t)(b + 96) * d.stride];
-    s0 += v0;
-    s1 += v1;
-    s2 += v2;
-    s3 += v3;
+  for (; b + 32 * (CH - 1) < nblk; b += 32 * CH) {
+    double v[CH];
+#pragma unroll
+    for (int c = 0; c < CH; c++) v[c] = base[(int64_t)(b + 32 * c) * stride];
+#pragma unroll
+    for (int c = 0; c < CH; c++) acc[c] += v[c];
   }
-  for (; b < d.nblk; b += 32) s0 += d.base[(int64_t)b * d.stride];
-  double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int c = 0; c < CH - 1; c++)
+    if (b + 32 * c < nblk) acc[c] += base[(int64_t)(b + 32 * c) * stride];
+  double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
+}
+
+__device__ __forceinline__ double warp_reduce_desc(const RedDesc& d, int lane) {
+  return warp_sum_strided(d.base, d.stride, d.nblk, lane);
 }
 
 // all warps of the grid walk the descriptor list; returns after writing
