@@ -195,6 +195,26 @@ __global__ void k_build_stream(const float* __restrict__ vals, int cols,
   F[p * pf + off + c] = v;
 }
 
+// float4 form of k_build_stream (cols % 4 == 0, off % 4 == 0): thread per
+// (device row, quad) -- coalesced stores, each source row read as whole
+// 16-byte quads by consecutive threads
+__global__ void k_build_stream4(const float4* __restrict__ vals, int c4,
+                                const int32_t* __restrict__ ind_sel,
+                                const int32_t* __restrict__ perm, int64_t r_pad,
+                                float4* __restrict__ F, int pf4, int off4) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= r_pad * c4) return;
+  const int64_t p = idx / c4;
+  const int q = (int)(idx - p * c4);
+  const int32_t t = perm[p];
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t >= 0) {
+    const int32_t s = ind_sel[t];
+    if (s >= 0) v = vals[(int64_t)s * c4 + q];
+  }
+  F[p * pf4 + off4 + q] = v;
+}
+
 // host-value upload, one ring chunk: source rows [r0, r0 + nrows) of an
 // injective source land at their device rows.  inv (source row -> target row,
 // -1 = unreferenced) is null for the identity indicator.
@@ -716,11 +736,19 @@ int fl_table_finalize(fl_table* t, void* stream) {
       FL_CHECK_LAUNCH();
       continue;
     }
-    int64_t total = r_pad * st.cols;
-    k_build_stream<<<grid_for(total), 256, 0, s>>>(st.vals->as<float>(), st.cols,
-                                                   st.ind_sel->as<int32_t>(),
-                                                   t->perm->as<int32_t>(), r_pad,
-                                                   t->F->as<float>(), t->pf, t->src[k].f_off);
+    if (st.cols % 4 == 0 && t->src[k].f_off % 4 == 0) {
+      const int c4 = st.cols / 4;
+      k_build_stream4<<<grid_for(r_pad * c4), 256, 0, s>>>(
+          reinterpret_cast<const float4*>(st.vals->p), c4, st.ind_sel->as<int32_t>(),
+          t->perm->as<int32_t>(), r_pad, reinterpret_cast<float4*>(t->F->p), t->pf / 4,
+          t->src[k].f_off / 4);
+    } else {
+      int64_t total = r_pad * st.cols;
+      k_build_stream<<<grid_for(total), 256, 0, s>>>(st.vals->as<float>(), st.cols,
+                                                     st.ind_sel->as<int32_t>(),
+                                                     t->perm->as<int32_t>(), r_pad,
+                                                     t->F->as<float>(), t->pf, t->src[k].f_off);
+    }
     FL_CHECK_LAUNCH();
   }
   for (int c = 0; c < nch; c++) {
