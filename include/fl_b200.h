@@ -69,13 +69,18 @@ int fl_table_create(int device, int64_t r_T, int32_t c_T, fl_table** out);
  * ind_sel: r_T int32 source row per target row, -1 = no match (ops.py:58-61);
  * NULL = identity indicator (requires r_k == r_T: the fact table of a star).
  * col_map: c_k int32 target column of each source column (map_sel_t,
- * ops.py:67-72), host memory.  The value and FK uploads are asynchronous
- * (pinned host memory overlaps them with finalize's index work): `values`
- * and `ind_sel` must stay valid until fl_table_finalize returns. */
+ * ops.py:67-72), host memory.  Host FKs are uploaded asynchronously here;
+ * host VALUES are read by fl_table_finalize (64 MB chunks through a device
+ * ring, scattered to device order as they land, so every byte crosses PCIe
+ * once; pinned memory runs at the link rate): `values` and `ind_sel` must
+ * stay valid until fl_table_finalize returns.  Device operands are copied
+ * synchronously (ordered after the caller's work, as cudaMemcpy is). */
 int fl_table_add_source(fl_table* t, int64_t r_k, int32_t c_k, const float* values,
                         const int32_t* ind_sel, const int32_t* col_map);
 /* Build the device layout: classify sources, derive the device row order
- * (stable sort by the largest gathered source's FK) and inverse CSRs. */
+ * (stable sort by the largest gathered source's FK) and inverse CSRs, and
+ * move the host values into place (identity-indicator sources start moving
+ * before the classification).  FL_TRACE_UPLOAD=1 prints the phases. */
 int fl_table_finalize(fl_table* t, void* stream);
 int fl_table_destroy(fl_table* t);
 int fl_table_shape(const fl_table* t, int64_t* r_T, int32_t* c_T, int32_t* n_sources);
