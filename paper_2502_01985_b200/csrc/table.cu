@@ -564,12 +564,17 @@ int fl_table_finalize(fl_table* t, void* stream) {
     slot_bytes = std::max(slot_bytes, row_bytes);
     chunks_upper += ceil_div(st.rows, std::max<int64_t>(1, (int64_t)(kChunkBytes / row_bytes)));
   }
-  const int ring_n = (int)std::min<int64_t>(chunks_upper, 16);   // <= 1 GB: covers the sort
+  // <= 16 slots (1 GB): covers the FK sort.  Sized for the worst case when
+  // identity sources start early, else once the classification is known.
+  int ring_n = 0;
   std::shared_ptr<DevBuf> ring;
-  if (ring_n > 0) {
-    ring = make_tmp(slot_bytes * ring_n, cv, &rc);
-    if (rc) return rc;
-  }
+  auto make_ring = [&](int64_t nchunks) -> int {
+    ring_n = (int)std::min<int64_t>(nchunks, 16);
+    if (ring_n <= 0) return FL_OK;
+    int rc2;
+    ring = make_tmp(slot_bytes * ring_n, cv, &rc2);
+    return rc2;
+  };
   std::vector<std::shared_ptr<void>> ev_ready, ev_free;
   auto mk_ev = []() -> std::shared_ptr<void> {
     cudaEvent_t e = nullptr;
@@ -603,6 +608,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
   };
   for (int k = 0; k < n; k++)
     if (t->staged[k].h_vals && !t->staged[k].sel_given) add_chunks(k);
+  if (!chunks.empty() && (rc = make_ring(chunks_upper))) return rc;
   for (int c = 0; c < std::min((int)chunks.size(), ring_n); c++)
     if ((rc = issue_chunk(c))) return rc;
   mark("first chunks issued");
@@ -671,6 +677,7 @@ int fl_table_finalize(fl_table* t, void* stream) {
   FL_CUDA(cudaMemsetAsync(t->F->p, 0, (size_t)r_pad * t->pf * 4, s));
   for (int k = 0; k < n; k++)
     if (t->src[k].stream && t->staged[k].h_vals && t->staged[k].sel_given) add_chunks(k);
+  if (!ring && !chunks.empty() && (rc = make_ring((int64_t)chunks.size()))) return rc;
   for (int c = nissued; c < std::min((int)chunks.size(), ring_n); c++)
     if ((rc = issue_chunk(c))) return rc;
   const int nch = (int)chunks.size();
