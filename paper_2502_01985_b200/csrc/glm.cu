@@ -130,13 +130,17 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_q(DimArgs a) {
   const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
   const int64_t cnt = active ? base + (blockIdx.x < rem ? 1 : 0) : 0;
   const uint32_t tile_bytes = TILE * pitch * 4;
+  // the CTA walks its tile range BACKWARDS: k_glm_dim_t (the previous
+  // kernel) walked the same ranges forwards, so the most recently read S_d
+  // tiles -- still in L2 -- come first
+  auto tile_of = [&](int64_t i) { return t0 + (cnt - 1 - i); };
   // S_d is immutable: its first tiles stream in before the dependency wait
   if (tid == 0 && active) {
     for (int s = 0; s < a.nst; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
     for (int s = 0; s < a.nst && s < cnt; s++) {
       mbar_arrive_expect_tx(&bar[s], tile_bytes);
-      bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + s) * TILE * (int64_t)pitch, tile_bytes,
+      bulk_g2s(smem + s * a.stage_bytes, a.S[d] + tile_of(s) * TILE * (int64_t)pitch, tile_bytes,
                &bar[s]);
     }
   }
@@ -164,13 +168,13 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_q(DimArgs a) {
       z = fmaf(v.z, w.z, z);
       z = fmaf(v.w, w.w, z);
     }
-    int64_t row = (t0 + i) * TILE + tid;
+    int64_t row = tile_of(i) * TILE + tid;
     if (row < rows) a.q[d][row] = z;
     __syncthreads();
     if (tid == 0 && i + a.nst < cnt) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bar[s], tile_bytes);
-      bulk_g2s(smem + s * a.stage_bytes, a.S[d] + (t0 + i + a.nst) * TILE * (int64_t)pitch,
+      bulk_g2s(smem + s * a.stage_bytes, a.S[d] + tile_of(i + a.nst) * TILE * (int64_t)pitch,
                tile_bytes, &bar[s]);
     }
   }
