@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libfl_b200.so")
+LIB_PATH = os.environ.get("FL_LIB_PATH") or os.path.join(HERE, "_lib", "libfl_b200.so")
 
 FL_OK = 0
 FL_ERR_SHAPE = 1

@@ -29,7 +29,7 @@ def main():
     del sh
     torch.cuda.empty_cache()
     nbytes = sum(t.numel() * t.element_size() for t in host + fks)
-    for j in range(4):
+    for j in range(int(os.environ.get('PROBE_JOBS', '4'))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         c0 = time.process_time()
