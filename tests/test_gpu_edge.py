@@ -2,8 +2,8 @@
 not multiples of the 256-row tile or the 32/64-row warp units, a dimension
 no fact row matches (left join), a one-row dimension (fanout = r_T), and an
 injective "dimension" larger than the fact table (it joins the stream block
-through the inverted indicator).  Join and selectors bit-exact; operators,
-GLM weights / losses and K-means results against the oracle (1e-4 relative,
+through the inverted indicator).  Join bit-exact; operators, GLM weights /
+losses, K-means and GNMF results against the oracle (1e-4 relative, K-means
 assignments identical)."""
 
 import numpy as np
@@ -110,3 +110,17 @@ def test_edge_tables_kmeans(fl, name):
     res = fl.train("kmeans", h, fl.TrainConfig(iterations=4, k_clusters=k, seed=5))
     assert np.array_equal(res.parameters["assignments"], ref["parameters"]["assignments"])
     assert _rel(res.loss_history, ref["loss_history"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["ragged_257_unmatched_dim", "one_row_dim", "injective_dim",
+                                  "ragged_4097"])
+def test_edge_tables_gnmf(fl, name):
+    r, c_f, dims = CASES[name]
+    srcs, sels, maps, r_t, c_t = _table(14, r, c_f, dims)
+    tab = _oracle(srcs, sels, maps, r_t, c_t)
+    h = fl.TargetHandle.from_arrays(srcs, sels, maps, r_t, c_t)
+    ref = rt.gaussian_nmf(tab, 4, 3, 2)
+    res = fl.train("gnmf", h, fl.TrainConfig(iterations=4, rank=3, seed=2))
+    assert _rel(res.loss_history, ref["loss_history"]) < TOL
+    assert _rel(res.parameters["h"], ref["parameters"]["h"]) < TOL
+    assert _rel(res.parameters["w"], ref["parameters"]["w"]) < TOL
