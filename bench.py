@@ -678,7 +678,7 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
             torch.cuda.synchronize()
             t_r = time.perf_counter()
             cents, assign, losses = s2.result(J)
-            d2h = 8 * (wl["k"] * c_t + J) + 4 * sh["rows"]
+            d2h = 8 * (wl["k"] * c_t + J) + 8 * sh["rows"]   # int64 assignments
         t1 = time.perf_counter()
         s2.close()
         del h2

@@ -166,6 +166,10 @@ int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* str
 /* centroids k x c_T fp64, assignments r_T int32 (target order), losses */
 int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* loss,
                      int32_t n, int32_t* n_done, void* stream);
+/* assignments r_T int64 (target order) -- the reference's argmin dtype
+ * (trainers.py:232-236), widened on the device so the host receives them
+ * without a conversion pass */
+int fl_kmeans_assignments64(fl_kmeans* s, int64_t* assign, void* stream);
 int fl_kmeans_destroy(fl_kmeans* s);
 
 /* ---- Gaussian NMF, multiplicative updates (trainers.py:256-307) ----------

@@ -80,6 +80,7 @@ SIGNATURES = {
     "fl_kmeans_run": [_P, _I32, _P],
     "fl_kmeans_kernel_times": [_P, _I32, _P, _P],
     "fl_kmeans_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
+    "fl_kmeans_assignments64": [_P, _P, _P],
     "fl_kmeans_destroy": [_P],
     "fl_glm_path": [_P, C.POINTER(_I32), C.POINTER(_D)],
     "fl_gnmf_create": [_P, _I32, _P, _P, _D, _PP, _P],

@@ -742,6 +742,13 @@ __global__ void __launch_bounds__(256) k_km_reduce(const RedDesc* descs, int n, 
 
 __global__ void k_km_update(KmUpdateArgs u) { km_apply_update(u); }
 
+__global__ void k_km_assign_to_target64(const int32_t* __restrict__ a_dev,
+                                        const int32_t* __restrict__ perm, int64_t r_T,
+                                        int64_t* __restrict__ out) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < r_T) out[perm[p]] = (int64_t)a_dev[p];
+}
+
 __global__ void k_km_assign_to_target(const int32_t* __restrict__ a_dev,
                                       const int32_t* __restrict__ perm, int64_t r_T,
                                       int32_t* __restrict__ out) {
@@ -1267,6 +1274,21 @@ int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* l
     int m = std::min(n, nd);
     if (m > 0) FL_CUDA(cudaMemcpy(loss, s->loss_hist.p, (size_t)m * 8, cudaMemcpyDefault));
   }
+  return FL_OK;
+}
+
+int fl_kmeans_assignments64(fl_kmeans* s, int64_t* assign, void* stream) {
+  if (!s || !assign) return FL_ERR_ARG;
+  FL_CUDA(cudaSetDevice(s->t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* tmp = nullptr;
+  FL_CUDA(cudaMallocAsync((void**)&tmp, (size_t)s->t->r_T * 8 + 16, st));
+  k_km_assign_to_target64<<<(unsigned)ceil_div(s->t->r_T, 256), 256, 0, st>>>(
+      s->assign.as<int32_t>(), s->t->perm->as<int32_t>(), s->t->r_T, tmp);
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaMemcpyAsync(assign, tmp, (size_t)s->t->r_T * 8, cudaMemcpyDefault, st));
+  FL_CUDA(cudaFreeAsync(tmp, st));
+  FL_CUDA(cudaStreamSynchronize(st));
   return FL_OK;
 }
 

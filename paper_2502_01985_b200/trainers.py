@@ -327,13 +327,15 @@ class KMeansSession:
     def result(self, n: int):
         r_t, _ = self.h.shape
         cents = np.empty((self.k, self.c_T), dtype=np.float64)
-        assign = np.empty(r_t, dtype=np.int32)
+        assign = np.empty(r_t, dtype=np.int64)   # the reference's argmin dtype, widened on device
         loss = np.empty(max(n, 1), dtype=np.float64)
         done = C.c_int32()
         _lib.call("fl_kmeans_result", self.ptr, cents.ctypes.data_as(C.c_void_p),
-                  assign.ctypes.data_as(C.c_void_p), loss.ctypes.data_as(C.c_void_p), int(n),
+                  C.c_void_p(0), loss.ctypes.data_as(C.c_void_p), int(n),
                   C.byref(done), C.c_void_p(0))
-        return cents, assign.astype(np.int64), loss[:min(done.value, n)]
+        _lib.call("fl_kmeans_assignments64", self.ptr, assign.ctypes.data_as(C.c_void_p),
+                  C.c_void_p(0))
+        return cents, assign, loss[:min(done.value, n)]
 
     def close(self):
         if getattr(self, "ptr", None):
