@@ -249,8 +249,11 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   const int64_t gw = (int64_t)blockIdx.x * KM_WARPS + warp;
   const int64_t NW = (int64_t)gridDim.x * KM_WARPS;
   const int64_t base = a.nunits / NW, rem = a.nunits % NW;
-  const int64_t u0 = gw * base + min64(gw, rem);
-  const int64_t cnt = base + (gw < rem ? 1 : 0);
+  // row indices fit in 32 bits (fl_table_create caps r_T below INT32_MAX):
+  // 32-bit unit / row arithmetic in the unit loop
+  const int u0 = (int)(gw * base + min64(gw, rem));
+  const int cnt = (int)(base + (gw < rem ? 1 : 0));
+  const int r_T32 = (int)a.r_T;
   constexpr uint32_t F_BYTES = 32u * FP * 4u;
   // F tile + the 32 FKs of every source not in the async-copied FK ring
   const int npf = min(a.ng, KM_PF);
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   float* zs = ebuf;
   int32_t* fkr = fkr_all + warp * 3 * KM_PF * 32;
   uint64_t* wbar = bar[warp];
-  auto issue = [&](int s, int64_t unit) {
+  auto issue = [&](int s, int unit) {
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
     tma_load_2d(st, &tmF, 0, (int)(unit * 32), &wbar[s]);
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   // the prefetched sources' loops are unrolled: compile-time source indices
   // turn a.fk[d] / a.E[d] / a.rows[d] into constant-bank operands instead
   // of indexed parameter loads per unit
-  auto issue_fk = [&](int64_t unit, int slot) {
+  auto issue_fk = [&](int unit, int slot) {
 #pragma unroll
     for (int d = 0; d < KM_PF; d++)
       if (d < npf) cp_async4(fkr + (slot * KM_PF + d) * 32 + lane, a.fk[d] + unit * 32 + lane);
@@ -342,13 +345,13 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   int s = 0;            // stage slot and its mbarrier phase
   uint32_t ph = 0;
   int fslot = 0;        // FK ring slot of this unit
-  for (int64_t i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0),
+  for (int i = 0; i < cnt; i++, s = (s + 1 == a.nst) ? 0 : s + 1, ph ^= (s == 0),
                fslot = fslot == 2 ? 0 : fslot + 1) {
     mbar_wait(&wbar[s], ph);
     float* Fs = reinterpret_cast<float*>(wsm + (size_t)s * a.stage_bytes);
     const int32_t* fks_s = reinterpret_cast<const int32_t*>(wsm + (size_t)s * a.stage_bytes + F_BYTES);
-    const int64_t p0 = (u0 + i) * 32;
-    const bool valid = p0 + lane < a.r_T;
+    const int p0 = (u0 + i) * 32;
+    const bool valid = p0 + lane < r_T32;
     // E terms of every cluster: sum_d E_d[fk_d, j] (kept apart for the loss).
     // The first KM_PF sources were gathered into registers during the
     // previous unit; any further source is gathered here, before the screen
