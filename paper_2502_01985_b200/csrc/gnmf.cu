@@ -302,11 +302,14 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
   double* wp = a.wpart + gw * WP;
   for (int i = lane; i < WP; i += 32) wp[i] = 0.0;
   __syncwarp();
+  // W and F stream through once per pass: evict_first, so the per-warp fp64
+  // partials (flushed every GN_FLUSH units) and the G_d / Z_d rows stay in L2
+  const uint64_t pol_stream = l2_policy_evict_first();
   auto issue = [&](int s, int64_t unit) {
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
-    tma_load_2d(st, &tmW, 0, (int)(unit * 32), &wbar[s]);
-    tma_load_2d(st + a.off_f, &tmF, 0, (int)(unit * 32), &wbar[s]);
+    tma_load_2d_hint(st, &tmW, 0, (int)(unit * 32), &wbar[s], pol_stream);
+    tma_load_2d_hint(st + a.off_f, &tmF, 0, (int)(unit * 32), &wbar[s], pol_stream);
     if (has_sort) bulk_g2s(st + a.off_fk, a.fk[a.sort_g] + unit * 32, 128, &wbar[s]);
   };
   if (lane == 0)
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(GN_WARPS * 32, 1)
       __syncwarp();
       if (lane == 0) {
         fence_proxy_async();
-        tma_store_2d(&tmW, 0, (int)p0, Wt);
+        tma_store_2d_hint(&tmW, 0, (int)p0, Wt, pol_stream);
         bulk_commit();
       }
     }
