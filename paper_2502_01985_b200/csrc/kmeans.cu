@@ -263,10 +263,13 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   float* zs = ebuf;
   int32_t* fkr = fkr_all + warp * 3 * KM_PF * 32;
   uint64_t* wbar = bar[warp];
+  // F streams through once per pass: evict_first keeps the E_d rows and the
+  // I_d^T A counters L2-resident
+  const uint64_t pol_stream = l2_policy_evict_first();
   auto issue = [&](int s, int unit) {
     char* st = wsm + (size_t)s * a.stage_bytes;
     mbar_arrive_expect_tx(&wbar[s], tx);
-    tma_load_2d(st, &tmF, 0, (int)(unit * 32), &wbar[s]);
+    tma_load_2d_hint(st, &tmF, 0, (int)(unit * 32), &wbar[s], pol_stream);
 #pragma unroll
     for (int d = 0; d < MAX_GATHER; d++)   // FKs of the sources without an FK ring
       if (d >= npf && d < a.ng) bulk_g2s(st + F_BYTES + 128 * d, a.fk[d] + unit * 32, 128, &wbar[s]);
