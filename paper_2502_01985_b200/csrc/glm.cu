@@ -100,6 +100,7 @@ struct UpdateArgs {
   // reduction inputs (K3 last block)
   const double* part_fact;
   int nblk_fact;
+  double* red_fact;   // pf + 1: the fact partials, reduced early by K3's first CTAs
   const double* part_dim[MAX_GATHER];
   int nblk_dim[MAX_GATHER];
 };
@@ -492,35 +493,54 @@ __device__ void glm_apply_update(const UpdateArgs& u) {
   if (tid == 0) u.state->it = it + 1;
 }
 
+// the fact-pass partials are final once K3 passes its dependency wait: CTA
+// b (flat index) reduces elements b, b + #CTAs, ... of the pf + 1 with its
+// last warp, in parallel
+// with the S_d streaming, so the serial last-CTA step is left with the
+// dimension partials only
+__device__ void glm_reduce_fact_early(const UpdateArgs& u) {
+  if ((threadIdx.x >> 5) != (int)(blockDim.x >> 5) - 1) return;
+  const int nct = gridDim.x * gridDim.y;
+  for (int e = blockIdx.y * gridDim.x + blockIdx.x; e <= u.pf; e += nct) {
+    const double s = warp_sum_strided(u.part_fact + e, u.pf + 1, u.nblk_fact, threadIdx.x & 31);
+    if ((threadIdx.x & 31) == 0) u.red_fact[e] = s;
+  }
+}
+
 __device__ void glm_reduce_all(const UpdateArgs& u) {
-  // one warp per output element (fixed-order lane sums + a fixed xor tree:
-  // deterministic), so the ~300 partial loads of every element are in flight
-  // together instead of walking one chain per thread
+  // one warp per output element, two elements per step (fixed-order lane
+  // sums + a fixed xor tree: deterministic); the fact elements were reduced
+  // by glm_reduce_fact_early
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int c = tid; c <= u.c_T; c += blockDim.x) u.red[c] = 0.0;
   __syncthreads();
-  const int pf1 = u.pf + 1;
-  int total = pf1;
+  for (int e = tid; e <= u.pf; e += blockDim.x) {
+    const int dst = e == u.pf ? u.c_T : u.f_tcol[e];
+    if (dst >= 0) u.red[dst] = u.red_fact[e];
+  }
+  int total = 0;
   for (int d = 0; d < u.ng; d++) total += u.pitch[d];
-  for (int e = warp; e < total; e += nw) {
-    const double* base;
-    int stride, nblk, dst;
-    if (e < pf1) {
-      base = u.part_fact + e;
-      stride = pf1;
-      nblk = u.nblk_fact;
-      dst = e == u.pf ? u.c_T : u.f_tcol[e];
-    } else {
-      int c = e - pf1, d = 0;
-      while (c >= u.pitch[d]) c -= u.pitch[d++];
-      base = u.part_dim[d] + c;
-      stride = u.pitch[d];
-      nblk = u.nblk_dim[d];
-      dst = u.d_tcol[d][c];
+  auto locate = [&](int e, const double** base, int* stride, int* nblk, int* dst) {
+    int c = e, d = 0;
+    while (c >= u.pitch[d]) c -= u.pitch[d++];
+    *base = u.part_dim[d] + c;
+    *stride = u.pitch[d];
+    *nblk = u.nblk_dim[d];
+    *dst = u.d_tcol[d][c];
+  };
+  for (int e = 2 * warp; e < total; e += 2 * nw) {
+    const double *b0, *b1 = nullptr;
+    int st0, n0, dst0, st1 = 1, n1 = 0, dst1 = -1;
+    locate(e, &b0, &st0, &n0, &dst0);
+    if (e + 1 < total) locate(e + 1, &b1, &st1, &n1, &dst1);
+    if (dst0 < 0) n0 = 0;
+    if (dst1 < 0) n1 = 0;
+    double s0, s1;
+    warp_sum_strided2(b0, st0, n0, b1 ? b1 : b0, st1, n1, lane, &s0, &s1);
+    if (lane == 0) {
+      if (dst0 >= 0) u.red[dst0] = s0;
+      if (dst1 >= 0) u.red[dst1] = s1;
     }
-    if (dst < 0) continue;
-    const double s = warp_sum_strided(base, stride, nblk, lane);
-    if (lane == 0) u.red[dst] = s;
   }
   __syncthreads();
 }
@@ -553,8 +573,9 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u,
                  &bar[s]);
       }
     }
-    pdl_wait();      // bins / residuals of this iteration's fact pass are final
+    pdl_wait();      // bins / residuals / partials of this iteration's fact pass are final
     pdl_trigger();
+    glm_reduce_fact_early(u);
     __syncthreads();
     const int Gr = NTHREADS / c4;
     const bool pb = tid < Gr * c4;
@@ -620,7 +641,10 @@ __global__ void __launch_bounds__(NTHREADS) k_glm_dim_t(DimArgs a, UpdateArgs u,
       }
     }
   }
-  if (!active) pdl_wait();   // the last-CTA election below reads / writes shared state
+  if (!active) {   // the last-CTA election below reads / writes shared state
+    pdl_wait();
+    glm_reduce_fact_early(u);
+  }
   // last-block-done over the whole grid
   __threadfence();
   __syncthreads();
@@ -768,6 +792,7 @@ struct fl_glm {
   int loss_cap = 1 << 16;
   cudaGraphExec_t graph = nullptr;
   cudaGraphExec_t graph_n = nullptr;   // kGlmGraphIters iterations
+  DevBuf red_fact;                     // early-reduced fact partials
   cudaStream_t cap_stream = nullptr;
   int bins_rows = 0;
   bool use_fw = false;
@@ -1250,6 +1275,8 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
   ua.state = s->state.as<GlmState>();
   ua.part_fact = s->use_fw ? s->fw_part.as<double>() : s->part_fact.as<double>();
   ua.nblk_fact = s->use_fw ? s->nblk_fw : s->nblk_fact;
+  if ((rc = s->red_fact.alloc((size_t)(t->pf + 1) * 8))) return rc;
+  ua.red_fact = s->red_fact.as<double>();
   for (int d = 0; d < ng; d++) {
     ua.d_tcol[d] = t->g[d].d_tcol->as<int32_t>();
     ua.pitch[d] = t->g[d].pitch;

@@ -45,6 +45,48 @@ __device__ __forceinline__ double warp_sum_strided(const double* __restrict__ ba
   return s;
 }
 
+// two elements at once (same fixed order per element as warp_sum_strided):
+// twice the loads in flight for the serial last-CTA reductions
+__device__ __forceinline__ void warp_sum_strided2(const double* __restrict__ b0, int st0, int n0,
+                                                  const double* __restrict__ b1, int st1, int n1,
+                                                  int lane, double* s0, double* s1) {
+  constexpr int CH = 8;
+  double a0[CH], a1[CH];
+#pragma unroll
+  for (int c = 0; c < CH; c++) a0[c] = a1[c] = 0.0;
+  const int nmax = n0 > n1 ? n0 : n1;
+  int b = lane;
+  for (; b + 32 * (CH - 1) < nmax; b += 32 * CH) {
+    double v0[CH], v1[CH];
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+      const int bb = b + 32 * c;
+      v0[c] = bb < n0 ? b0[(int64_t)bb * st0] : 0.0;
+      v1[c] = bb < n1 ? b1[(int64_t)bb * st1] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+      a0[c] += v0[c];
+      a1[c] += v1[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CH - 1; c++) {
+    const int bb = b + 32 * c;
+    if (bb < n0) a0[c] += b0[(int64_t)bb * st0];
+    if (bb < n1) a1[c] += b1[(int64_t)bb * st1];
+  }
+  double r0 = ((a0[0] + a0[1]) + (a0[2] + a0[3])) + ((a0[4] + a0[5]) + (a0[6] + a0[7]));
+  double r1 = ((a1[0] + a1[1]) + (a1[2] + a1[3])) + ((a1[4] + a1[5]) + (a1[6] + a1[7]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+    r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+  }
+  *s0 = r0;
+  *s1 = r1;
+}
+
 __device__ __forceinline__ double warp_reduce_desc(const RedDesc& d, int lane) {
   return warp_sum_strided(d.base, d.stride, d.nblk, lane);
 }
