@@ -25,6 +25,47 @@ struct WarpCarry {
   double head_val, tail_val;
 };
 
+// Last CTA of a fact pass: segments that span warp ranges are stitched in a
+// fixed order from a shared-memory copy of the carry records (coalesced
+// 16-byte loads, all in flight together) instead of chained dependent L2
+// reads; the global records are walked directly when they do not fit.
+// Kept out of line so the streaming loop's register allocation is untouched.
+__device__ __noinline__ void stitch_carries(const WarpCarry* carry, int64_t NW, float* bins,
+                                            char* scratch, size_t scratch_bytes) {
+  if ((size_t)NW * sizeof(WarpCarry) <= scratch_bytes) {
+    const int4* src = reinterpret_cast<const int4*>(carry);
+    int4* dst = reinterpret_cast<int4*>(scratch);
+    const int64_t n16 = NW * (int64_t)(sizeof(WarpCarry) / 16);
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src + i);
+    __syncthreads();
+    const WarpCarry* cr = reinterpret_cast<const WarpCarry*>(scratch);
+    for (int64_t c = threadIdx.x; c < NW; c += blockDim.x) {
+      const int K = cr[c].tail_key;
+      if (K < 0) continue;
+      double total = cr[c].tail_val;
+      for (int64_t c2 = c + 1; c2 < NW; c2++) {
+        if (cr[c2].head_key != K) break;
+        total += cr[c2].head_val;
+        if (!cr[c2].through) break;
+      }
+      bins[K] = (float)total;
+    }
+  } else {
+    volatile const WarpCarry* cr = carry;   // records written by other CTAs
+    for (int64_t c = threadIdx.x; c < NW; c += blockDim.x) {
+      const int K = cr[c].tail_key;
+      if (K < 0) continue;
+      double total = cr[c].tail_val;
+      for (int64_t c2 = c + 1; c2 < NW; c2++) {
+        if (cr[c2].head_key != K) break;
+        total += cr[c2].head_val;
+        if (!cr[c2].through) break;
+      }
+      bins[K] = (float)total;
+    }
+  }
+}
+
 struct GlmFactWArgs {
   const float* F;
   int pf;
@@ -288,19 +329,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  if (has_sort) {
-    volatile WarpCarry* cr = a.carry;
-    for (int64_t c = threadIdx.x; c < NW; c += blockDim.x) {
-      int K = cr[c].tail_key;
-      if (K < 0) continue;
-      double total = cr[c].tail_val;
-      for (int64_t c2 = c + 1; c2 < NW; c2++) {
-        if (cr[c2].head_key != K) break;
-        total += cr[c2].head_val;
-        if (!cr[c2].through) break;
-      }
-      a.bins[K] = (float)total;
-    }
-  }
+  if (has_sort)
+    stitch_carries(a.carry, NW, a.bins, smem, (size_t)FW_WARPS * a.nst * a.stage_bytes);
   if (threadIdx.x == 0) a.state->done_fact = 0;
 }
