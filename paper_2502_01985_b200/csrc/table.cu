@@ -547,6 +547,14 @@ int fl_table_finalize(fl_table* t, void* stream) {
   // Identity-indicator sources are streamed for certain, so their chunks
   // start right away, overlapping the fanout analysis and the sort below.
   cudaStream_t cv = (cudaStream_t)t->cp_vals.get();
+  // every return path (errors included) waits for the value copies: the
+  // caller may release its host arrays as soon as finalize returns
+  struct CopyDrain {
+    cudaStream_t s;
+    ~CopyDrain() {
+      if (s) cudaStreamSynchronize(s);
+    }
+  } drain{cv};
   struct Chunk {
     int k;
     int64_t r0, nrows;
