@@ -521,6 +521,16 @@ int fl_table_finalize(fl_table* t, void* stream) {
   const PhaseTrace tr("fl_table_finalize");
   auto mark = [&](const char* what) { tr.mark(what); };
   FL_CUDA(cudaSetDevice(t->device));
+  // every return path (errors included) waits for the host-side copies (FKs
+  // from add_source, values from here): the caller may release its host
+  // arrays as soon as finalize returns
+  struct CopyDrain {
+    cudaStream_t a, b;
+    ~CopyDrain() {
+      if (a) cudaStreamSynchronize(a);
+      if (b) cudaStreamSynchronize(b);
+    }
+  } drain{(cudaStream_t)t->cp_idx.get(), (cudaStream_t)t->cp_vals.get()};
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t r_T = t->r_T, r_pad = t->r_pad;
   int rc;
@@ -547,14 +557,6 @@ int fl_table_finalize(fl_table* t, void* stream) {
   // Identity-indicator sources are streamed for certain, so their chunks
   // start right away, overlapping the fanout analysis and the sort below.
   cudaStream_t cv = (cudaStream_t)t->cp_vals.get();
-  // every return path (errors included) waits for the value copies: the
-  // caller may release its host arrays as soon as finalize returns
-  struct CopyDrain {
-    cudaStream_t s;
-    ~CopyDrain() {
-      if (s) cudaStreamSynchronize(s);
-    }
-  } drain{cv};
   struct Chunk {
     int k;
     int64_t r0, nrows;
