@@ -866,6 +866,9 @@ int fl_table_finalize(fl_table* t, void* stream) {
 int fl_table_destroy(fl_table* t) {
   if (!t) return FL_OK;
   cudaSetDevice(t->device);
+  // a table destroyed between add_source and finalize may still be copying
+  if (t->cp_idx) cudaStreamSynchronize((cudaStream_t)t->cp_idx.get());
+  if (t->cp_vals) cudaStreamSynchronize((cudaStream_t)t->cp_vals.get());
   delete t;
   return FL_OK;
 }
