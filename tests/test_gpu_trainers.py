@@ -413,3 +413,36 @@ def test_glm_wide_tables_vs_oracle(fl, model):
         res = fl.train(model, h, fl.TrainConfig(iterations=5, learning_rate=lr), y.reshape(-1, 1))
         assert max_rel(res.loss_history, want["loss_history"]) < TOL
         assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
+
+
+def test_glm_pdl_launch_is_bit_identical(tmp_path):
+    """The GLM iteration kernels are launched with programmatic dependent
+    launch (prologues overlap the previous kernel's tail).  The same fit with
+    FL_NO_PDL=1 (plain stream order) must give bit-identical weights and
+    losses: nothing before a kernel's griddepcontrol.wait may touch its
+    predecessor's outputs."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "fit.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.abspath(__file__))!r})\n"
+        "import paper_2502_01985_b200 as fl\n"
+        "from conftest import star_table\n"
+        "ft = star_table(21, 20_000, [(700, 9), (30, 4)], 11)\n"
+        "h = fl.TargetHandle.factorized(ft)\n"
+        "y = np.random.default_rng(2).integers(0, 2, 20_000).astype(np.float64).reshape(-1, 1)\n"
+        "r = fl.train('logreg', h, fl.TrainConfig(iterations=20, learning_rate=1e-4), y)\n"
+        "np.save(sys.argv[1], np.concatenate([r.parameters['w'].ravel(), np.asarray(r.loss_history)]))\n")
+    outs = []
+    for flag in (None, "1"):
+        env = dict(os.environ)
+        env.pop("FL_NO_PDL", None)
+        if flag:
+            env["FL_NO_PDL"] = flag
+        out = tmp_path / f"r{flag}.npy"
+        subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=300)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
