@@ -647,10 +647,12 @@ __device__ void km_apply_update(const KmUpdateArgs& u) {
 // fp32 within a tile, fp64 across tiles.  Each thread holds its share of the
 // NEXT tile in registers (float4 / int4 loads issued before the current
 // tile's math), so a CTA pays one load latency per kernel, not per tile.
-// Pitches up to 288 floats (KM_SUM_SL float4 slots per thread; cols <= 256
-// have pitch <= 260).
+// SL float4 prefetch slots per thread (SL * 256 >= 32 * pitch / 4) and U
+// work items (column x 8 clusters) per thread are template parameters, so a
+// narrow dimension (the common case) needs few registers and fits 3-4 CTAs
+// per SM.  Pitches up to 288 floats (SL = 9; cols <= 256 have pitch <= 260).
 constexpr int KM_SUM_SL = 9;
-template <int KP>
+template <int KP, int U, int SL>
 __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
@@ -667,11 +669,11 @@ __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
   const int tid = threadIdx.x;
   const float4* S4 = reinterpret_cast<const float4*>(a.S[d]);
   const int4* C4 = reinterpret_cast<const int4*>(a.cnt[d]);
-  float4 pv[KM_SUM_SL];
+  float4 pv[SL];
   int4 pc = make_int4(0, 0, 0, 0);
   auto load = [&](int64_t rb) {
 #pragma unroll
-    for (int sl = 0; sl < KM_SUM_SL; sl++) {
+    for (int sl = 0; sl < SL; sl++) {
       const int i = tid + sl * 256;
       const int r = i / pitch4, c4 = i - r * pitch4;
       pv[sl] = (i < nS4 && rb + r < r1) ? S4[(rb + r) * pitch4 + c4]
@@ -682,16 +684,16 @@ __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
       pc = rb + r < r1 ? C4[rb * Q4 + tid] : make_int4(0, 0, 0, 0);
     }
   };
-  double acc64[2][JB];
+  double acc64[U][JB];
 #pragma unroll
-  for (int u = 0; u < 2; u++)
+  for (int u = 0; u < U; u++)
 #pragma unroll
     for (int j = 0; j < JB; j++) acc64[u][j] = 0.0;
   if (r0 < r1) load(r0);
   for (int64_t rb = r0; rb < r1; rb += 32) {
     __syncthreads();   // the previous tile's math is done with ss / cs
 #pragma unroll
-    for (int sl = 0; sl < KM_SUM_SL; sl++) {
+    for (int sl = 0; sl < SL; sl++) {
       const int i = tid + sl * 256;
       if (i < nS4) {   // padding columns (c >= cols) are not stored
         const int r = i / pitch4, c = 4 * (i - r * pitch4);
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
     __syncthreads();
     if (rb + 32 < r1) load(rb + 32);   // in flight during this tile's math
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
+    for (int u = 0; u < U; u++) {
       const int w = tid + u * 256;
       if (w >= nwork) break;
       const int c = w % cols, jb = w / cols;
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(256) k_km_dim_sums(KmDimArgs a) {
     }
   }
 #pragma unroll
-  for (int u = 0; u < 2; u++) {
+  for (int u = 0; u < U; u++) {
     const int w = tid + u * 256;
     if (w >= nwork) break;
     const int c = w % cols, jb = w / cols;
@@ -767,10 +769,25 @@ static void km_dim_e_launch(int KP, dim3 g, size_t smem, cudaStream_t st, const 
   else if (KP == 16) k_km_dim_e<16><<<g, 256, smem, st>>>(a);
   else k_km_dim_e<32><<<g, 256, smem, st>>>(a);
 }
-static void km_dim_sums_launch(int KP, dim3 g, size_t smem, cudaStream_t st, const KmDimArgs& a) {
-  if (KP == 8) k_km_dim_sums<8><<<g, 256, smem, st>>>(a);
-  else if (KP == 16) k_km_dim_sums<16><<<g, 256, smem, st>>>(a);
-  else k_km_dim_sums<32><<<g, 256, smem, st>>>(a);
+template <int KP>
+static const void* km_dim_sums_ptr_kp(int U, int SL) {
+  if (U == 1) {
+    if (SL <= 3) return (const void*)k_km_dim_sums<KP, 1, 3>;
+    if (SL <= 5) return (const void*)k_km_dim_sums<KP, 1, 5>;
+    return (const void*)k_km_dim_sums<KP, 1, 9>;
+  }
+  if (SL <= 3) return (const void*)k_km_dim_sums<KP, 2, 3>;
+  if (SL <= 5) return (const void*)k_km_dim_sums<KP, 2, 5>;
+  return (const void*)k_km_dim_sums<KP, 2, 9>;
+}
+static const void* km_dim_sums_ptr(int KP, int U, int SL) {
+  return KP == 8 ? km_dim_sums_ptr_kp<8>(U, SL)
+                 : KP == 16 ? km_dim_sums_ptr_kp<16>(U, SL) : km_dim_sums_ptr_kp<32>(U, SL);
+}
+static cudaError_t km_dim_sums_launch(const void* fn, dim3 g, size_t smem, cudaStream_t st,
+                                      const KmDimArgs& a) {
+  void* args[] = {const_cast<KmDimArgs*>(&a)};
+  return cudaLaunchKernel(fn, g, dim3(256), args, smem, st);
 }
 
 // instantiation table: NT in {1,2,4} (k <= 8/16/32), KC in {1,2,3,4,6,8,12,16}
@@ -818,6 +835,7 @@ struct fl_kmeans {
   int nblk_fact = 0;
   size_t smem_fact = 0, smem_e = 0, smem_sum = 0;
   int grid_e = 1, grid_sum = 1, grid_red = 1, n_desc = 0;
+  const void* fn_sum = nullptr;   // k_km_dim_sums<KP, U, SL> chosen for the dimension widths
   DevBuf descs;
   DevBuf C64, C32, E, cnt, part_fact, part_w, part_dim, red, loss_hist, state, assign, done;
   int loss_cap = 1 << 16;
@@ -854,7 +872,7 @@ static int km_launch_iteration(fl_kmeans* s, cudaStream_t st, bool fuse_update,
   int rc = km_fact_run(s, st, write_assign);
   if (rc) return rc;
   if (s->da.ng > 0) {
-    km_dim_sums_launch(s->KP, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da);
+    FL_CUDA(km_dim_sums_launch(s->fn_sum, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da));
     FL_CHECK_LAUNCH();
   }
   k_km_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc, s->ua,
@@ -1078,6 +1096,16 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   int64_t max_rows = 1;
   size_t part_total = 0;
   s->grid_sum = 1;
+  int sum_u = 1, sum_sl = 1;
+  for (int d = 0; d < ng; d++) {
+    const GatherSrc& g = t->g[d];
+    if (g.cols * (KP / 8) > 256) sum_u = 2;
+    sum_sl = std::max(sum_sl, (int)ceil_div(32 * (g.pitch / 4), 256));
+  }
+  s->fn_sum = km_dim_sums_ptr(KP, sum_u, sum_sl);
+  int occ_sum = 2;
+  FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sum, s->fn_sum, 256, 0));
+  occ_sum = std::max(1, std::min(occ_sum, 4));
   for (int d = 0; d < ng; d++) {
     const GatherSrc& g = t->g[d];
     da.S[d] = g.S->as<float>();
@@ -1087,10 +1115,10 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.E[d] = const_cast<float*>(fa.E[d]);
     da.cnt[d] = fa.cnt[d];
-    // row ranges of >= 4 tiles, <= 2 CTAs per SM: the next tile is prefetched
-    // in registers, and fewer partials keep the final reduction short
+    // row ranges of >= 4 tiles, one wave of resident CTAs: the next tile is
+    // prefetched in registers, and few partials keep the final reduction short
     int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 128),
-                                                         (int64_t)t->sm_count * 2));
+                                                         (int64_t)t->sm_count * occ_sum));
     da.nblk[d] = nb;
     s->grid_sum = std::max(s->grid_sum, nb);
     max_cols = std::max(max_cols, g.cols);
@@ -1123,12 +1151,8 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   {
     const void* fe = KP == 8 ? (const void*)k_km_dim_e<8> : KP == 16 ? (const void*)k_km_dim_e<16>
                                                                      : (const void*)k_km_dim_e<32>;
-    const void* fs = KP == 8 ? (const void*)k_km_dim_sums<8>
-                             : KP == 16 ? (const void*)k_km_dim_sums<16> : (const void*)k_km_dim_sums<32>;
     FL_CUDA(cudaFuncSetAttribute(fe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(s->smem_e, 16)));
-    FL_CUDA(cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)s->smem_sum));
   }
 
   KmUpdateArgs& ua = s->ua;
@@ -1234,7 +1258,7 @@ int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* str
     if (rc) return rc;
     FL_CUDA(cudaEventRecord(ev[2], st));
     if (s->da.ng > 0) {
-      km_dim_sums_launch(s->KP, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da);
+      FL_CUDA(km_dim_sums_launch(s->fn_sum, dim3(s->grid_sum, s->da.ng), s->smem_sum, st, s->da));
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[3], st));
