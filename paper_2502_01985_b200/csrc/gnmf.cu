@@ -602,7 +602,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 // registers (loads issued before the current tile's math): one load latency
 // per CTA instead of one per tile.  Pitches up to 288 floats.
 constexpr int GN_P_SL = 9;
-template <int R>
+template <int R, int U, int SL>
 __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
   const int d = blockIdx.y;
   if (d >= a.ng || (int)blockIdx.x >= a.nblk[d]) return;
@@ -620,11 +620,11 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
   const int tid = threadIdx.x;
   const float4* S4 = reinterpret_cast<const float4*>(a.S[d]);
   const double2* Z2 = reinterpret_cast<const double2*>(a.Z[d]);
-  float4 pv[GN_P_SL];
+  float4 pv[SL];
   double2 pz[ZL];
   auto load = [&](int64_t rb) {
 #pragma unroll
-    for (int sl = 0; sl < GN_P_SL; sl++) {
+    for (int sl = 0; sl < SL; sl++) {
       const int i = tid + sl * 256;
       const int r = i / pitch4, c4 = i - r * pitch4;
       pv[sl] = (i < nS4 && rb + r < r1) ? S4[(rb + r) * pitch4 + c4]
@@ -637,16 +637,16 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
       pz[zl] = (i < 16 * R && rb + r < r1) ? Z2[rb * (R / 2) + i] : make_double2(0.0, 0.0);
     }
   };
-  double acc64[2][JB];
+  double acc64[U][JB];
 #pragma unroll
-  for (int u = 0; u < 2; u++)
+  for (int u = 0; u < U; u++)
 #pragma unroll
     for (int j = 0; j < JB; j++) acc64[u][j] = 0.0;
   if (r0 < r1) load(r0);
   for (int64_t rb = r0; rb < r1; rb += 32) {
     __syncthreads();   // the previous tile's math is done with ss / zs
 #pragma unroll
-    for (int sl = 0; sl < GN_P_SL; sl++) {
+    for (int sl = 0; sl < SL; sl++) {
       const int i = tid + sl * 256;
       if (i < nS4) {   // padding columns (c >= cols) are not stored
         const int r = i / pitch4, c = 4 * (i - r * pitch4);
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
     __syncthreads();
     if (rb + 32 < r1) load(rb + 32);   // in flight during this tile's math
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
+    for (int u = 0; u < U; u++) {
       const int w = tid + u * 256;
       if (w >= nwork) break;
       const int c = w % cols, jb = w / cols;
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_p(GnDimArgs a) {
     }
   }
 #pragma unroll
-  for (int u = 0; u < 2; u++) {
+  for (int u = 0; u < U; u++) {
     const int w = tid + u * 256;
     if (w >= nwork) break;
     const int c = w % cols, jb = w / cols;
@@ -702,10 +702,26 @@ static void gn_dim_g_launch(int R, dim3 g, size_t smem, cudaStream_t st, const G
   else if (R == 16) k_gnmf_dim_g<16><<<g, 256, smem, st>>>(a);
   else k_gnmf_dim_g<32><<<g, 256, smem, st>>>(a);
 }
-static void gn_dim_p_launch(int R, dim3 g, size_t smem, cudaStream_t st, const GnDimArgs& a) {
-  if (R == 8) k_gnmf_dim_p<8><<<g, 256, smem, st>>>(a);
-  else if (R == 16) k_gnmf_dim_p<16><<<g, 256, smem, st>>>(a);
-  else k_gnmf_dim_p<32><<<g, 256, smem, st>>>(a);
+// k_gnmf_dim_p<R, U, SL> for the dimension widths (few registers when narrow)
+template <int R>
+static const void* gn_dim_p_ptr_r(int U, int SL) {
+  if (U == 1) {
+    if (SL <= 3) return (const void*)k_gnmf_dim_p<R, 1, 3>;
+    if (SL <= 5) return (const void*)k_gnmf_dim_p<R, 1, 5>;
+    return (const void*)k_gnmf_dim_p<R, 1, 9>;
+  }
+  if (SL <= 3) return (const void*)k_gnmf_dim_p<R, 2, 3>;
+  if (SL <= 5) return (const void*)k_gnmf_dim_p<R, 2, 5>;
+  return (const void*)k_gnmf_dim_p<R, 2, 9>;
+}
+static const void* gn_dim_p_ptr(int R, int U, int SL) {
+  return R == 8 ? gn_dim_p_ptr_r<8>(U, SL) : R == 16 ? gn_dim_p_ptr_r<16>(U, SL)
+                                                     : gn_dim_p_ptr_r<32>(U, SL);
+}
+static cudaError_t gn_dim_p_launch(const void* fn, dim3 g, size_t smem, cudaStream_t st,
+                                   const GnDimArgs& a) {
+  void* args[] = {const_cast<GnDimArgs*>(&a)};
+  return cudaLaunchKernel(fn, g, dim3(256), args, smem, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -781,6 +797,7 @@ struct fl_gnmf {
   GnDimArgs da{};
   GnHArgs ha{};
   int nblk_fact = 0, grid_g = 1, grid_p = 1, grid_red = 1;
+  const void* fn_p = nullptr;   // k_gnmf_dim_p<R, U, SL> chosen for the dimension widths
   size_t smem_fact = 0, smem_g = 0, smem_p = 0, smem_h = 0;
   int stage_h = 0;   // k_gnmf_h stages H and G in shared memory
   DevBuf descs;
@@ -817,7 +834,7 @@ static int gn_products(fl_gnmf* s, cudaStream_t st, bool update) {
   gn_fact_any(s, update, st);
   FL_CHECK_LAUNCH();
   if (s->da.ng > 0) {
-    gn_dim_p_launch(s->R, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da);
+    FL_CUDA(gn_dim_p_launch(s->fn_p, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da));
     FL_CHECK_LAUNCH();
   }
   k_gnmf_reduce<<<s->grid_red, 256, 0, st>>>(s->descs.as<RedDesc>(), s->n_desc,
@@ -1005,6 +1022,15 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   int64_t max_rows = 1;
   size_t part_total = 0;
   s->grid_p = 1;
+  int p_u = 1, p_sl = 1;
+  for (int d = 0; d < ng; d++) {
+    if (t->g[d].cols * (R / 8) > 256) p_u = 2;
+    p_sl = std::max(p_sl, (int)ceil_div(32 * (t->g[d].pitch / 4), 256));
+  }
+  s->fn_p = gn_dim_p_ptr(R, p_u, p_sl);
+  int occ_p = 2;
+  FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, s->fn_p, 256, 0));
+  occ_p = std::max(1, std::min(occ_p, 4));
   for (int d = 0; d < ng; d++) {
     const GatherSrc& g = t->g[d];
     da.S[d] = g.S->as<float>();
@@ -1014,10 +1040,10 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
     da.tcol[d] = g.d_tcol->as<int32_t>();
     da.Gd[d] = const_cast<float*>(fa.Gd[d]);
     da.Z[d] = fa.Z[d];
-    // row ranges of >= 4 tiles, <= 2 CTAs per SM: the next tile is prefetched
-    // in registers, and fewer partials keep the final reduction short
+    // row ranges of >= 4 tiles, one wave of resident CTAs: the next tile is
+    // prefetched in registers, and few partials keep the final reduction short
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 128),
-                                                               (int64_t)t->sm_count * 2));
+                                                               (int64_t)t->sm_count * occ_p));
     da.nblk[d] = nb;
     s->grid_p = std::max(s->grid_p, nb);
     max_cols = std::max(max_cols, g.cols);
@@ -1050,11 +1076,8 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   {
     const void* fg = R == 8 ? (const void*)k_gnmf_dim_g<8> : R == 16 ? (const void*)k_gnmf_dim_g<16>
                                                                     : (const void*)k_gnmf_dim_g<32>;
-    const void* fp = R == 8 ? (const void*)k_gnmf_dim_p<8> : R == 16 ? (const void*)k_gnmf_dim_p<16>
-                                                                    : (const void*)k_gnmf_dim_p<32>;
     FL_CUDA(cudaFuncSetAttribute(fg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(s->smem_g, 16)));
-    (void)fp;
   }
   {
     std::vector<RedDesc> dv;
@@ -1173,7 +1196,7 @@ int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream)
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaEventRecord(ev[3], st));
     if (s->da.ng > 0) {
-      gn_dim_p_launch(s->R, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da);
+      FL_CUDA(gn_dim_p_launch(s->fn_p, dim3(s->grid_p, s->da.ng), s->smem_p, st, s->da));
       FL_CHECK_LAUNCH();
     }
     FL_CUDA(cudaEventRecord(ev[4], st));
