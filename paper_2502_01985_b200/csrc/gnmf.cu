@@ -186,13 +186,15 @@ __global__ void __launch_bounds__(256) k_gnmf_dim_g(GnDimArgs a) {
     for (int j = 0; j < R; j++) acc[j] = 0.f;
     const float4* sr = reinterpret_cast<const float4*>(a.S[d] + row * pitch);
     const int n4 = pitch / 4;
-    // batches of 8 independent float4 loads: one latency per batch
-    for (int c0 = 0; c0 < n4; c0 += 8) {
-      float4 vb[8];
+    // batches of independent float4 loads: one latency per batch (4 at R = 32,
+    // where the 32 accumulators already hold most of the registers)
+    constexpr int NB = R >= 32 ? 4 : 8;
+    for (int c0 = 0; c0 < n4; c0 += NB) {
+      float4 vb[NB];
 #pragma unroll
-      for (int u = 0; u < 8; u++) vb[u] = c0 + u < n4 ? sr[c0 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < NB; u++) vb[u] = c0 + u < n4 ? sr[c0 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < NB; u++) {
         if (c0 + u >= n4) break;
         const float vv[4] = {vb[u].x, vb[u].y, vb[u].z, vb[u].w};
 #pragma unroll
@@ -1061,8 +1063,18 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   int max_pitch = 4;
   for (auto& g : t->g) max_pitch = std::max(max_pitch, g.pitch);
   s->smem_g = (size_t)max_pitch * R * 4;
-  s->grid_g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows, 256),
-                                                          (int64_t)t->sm_count * 4));
+  {
+    const void* fg0 = R == 8 ? (const void*)k_gnmf_dim_g<8> : R == 16 ? (const void*)k_gnmf_dim_g<16>
+                                                                     : (const void*)k_gnmf_dim_g<32>;
+    FL_CUDA(cudaFuncSetAttribute(fg0, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(s->smem_g, 16)));
+    int occ_g = 2;
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, fg0, 256, s->smem_g));
+    occ_g = std::max(1, std::min(occ_g, 8));
+    // one wave of resident CTAs, thread per row (grid-stride)
+    s->grid_g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows, 256),
+                                                            (int64_t)t->sm_count * occ_g));
+  }
   s->smem_p = 0;   // static tiles
   for (auto& g : t->g)
     if (g.cols > 256 || g.cols * R / 8 > 512 || 32 * (g.pitch / 4) > GN_P_SL * 256) {
