@@ -231,7 +231,11 @@ def planted_star(seed, r_fact, dims, c_fact, k, noise=0.01):
 
 @pytest.mark.parametrize("k,dims,c_fact", [(16, [(3000, 30), (200, 5)], 20),
                                            (4, [(500, 9)], 12),
-                                           (24, [(4000, 7)], 5)])
+                                           (24, [(4000, 7)], 5),
+                                           # wide dimensions: two work items per thread and
+                                           # 3 / 5 prefetch slots in k_km_dim_sums
+                                           (16, [(600, 150)], 10),
+                                           (24, [(400, 70)], 6)])
 def test_kmeans_planted_star_vs_oracle(fl, k, dims, c_fact):
     ft = planted_star(21, 60_000, dims, c_fact, k)
     tab = oracle.OracleTable.from_ft(ft)
@@ -312,7 +316,11 @@ def test_gnmf_matches_reference(fl, name, model):
 
 @pytest.mark.parametrize("rank,dims,c_fact", [(32, [(2000, 50)], 20),
                                               (5, [(900, 11), (40, 3)], 12),
-                                              (12, [(30000, 6)], 7)])
+                                              (12, [(30000, 6)], 7),
+                                              # wide dimensions: two work items per thread and
+                                              # 3 / 9 prefetch slots in k_gnmf_dim_p
+                                              (32, [(800, 90)], 10),
+                                              (16, [(500, 220)], 8)])
 def test_gnmf_random_star_vs_oracle(fl, rank, dims, c_fact):
     ft = star_table(31, 40_000, dims, c_fact)
     tab = oracle.OracleTable.from_ft(ft)
