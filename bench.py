@@ -456,11 +456,20 @@ def main():
 
     import torch
     world, rank, local = dist_env()
+    # FL_BENCH_DIST_BACKEND=gloo: exercise the multi-rank path (sharding, per-
+    # iteration all-reduce, max-over-ranks timing) with several ranks sharing
+    # the GPUs of a smaller box -- a code-path check, not a performance number
+    backend = os.environ.get("FL_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2502_01985_b200 as fl
     from paper_2502_01985_b200 import _lib
     from paper_2502_01985_b200 import distributed as D
