@@ -595,6 +595,9 @@ def main():
     if world == 1 and not args.no_e2e and wl["model"] in ("linreg", "logreg", "kmeans"):
         sess.close()
         out["e2e"] = bench_e2e(torch, fl, wl, sh, hyper, args)
+    elif world > 1 and not args.no_e2e and wl["model"] in ("linreg", "logreg"):
+        sess.close()
+        out["e2e"] = bench_e2e_sharded(torch, fl, wl, sh, hyper, args, dist, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         per_iter_full, sample = cpu_measure(wl, 20.0, 3)
         out["cpu_baseline"] = {"value": 1.0 / per_iter_full, "unit": UNIT,
@@ -711,6 +714,59 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
             "note": ("one job through the public API from pinned host buffers: H2D of all "
                      "inputs + device layout (FK sort) + J iterations + D2H of the model and "
                      "losses, amortised per iteration; median of 5 jobs after a warm-up job")}
+
+
+def bench_e2e_sharded(torch, fl, wl, sh, hyper, args, dist, dev):
+    """e2e at N GPUs (GLM): every rank uploads its own shard from pinned host
+    buffers through the public API, runs `--e2e-iters` iterations of
+    partial -> all-reduce -> update and reads back w and the losses.  A job's
+    time is the max over ranks (barrier on both sides); median of 5 jobs."""
+    from paper_2502_01985_b200 import distributed as D
+    from paper_2502_01985_b200.trainers import GlmSession
+    maps, c_t = col_maps(wl)
+
+    def pinned(t):
+        p = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        p.copy_(t)
+        return p
+
+    host = [pinned(sh["fact"])] + [pinned(d) for d in sh["dims"]]
+    fks = [pinned(f) for f in sh["fks"]]
+    y_h = pinned(sh["y"])
+    torch.cuda.synchronize()
+    J = args.e2e_iters
+
+    def job(n):
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        h2 = fl.TargetHandle.from_arrays([t.numpy() for t in host],
+                                         [None] + [f.numpy() for f in fks], maps, sh["rows"], c_t)
+        s2 = GlmSession(h2, wl["model"], y_h.numpy(), hyper["learning_rate"])
+        D.run_sharded(s2, n, dist, dev)
+        w, losses = s2.result(n)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter() - t0
+        s2.close()
+        del h2
+        torch.cuda.empty_cache()
+        t = torch.tensor([t1], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    job(3)
+    runs = sorted(job(J) for _ in range(5))
+    t_job = runs[2]
+    h2d = sum(t.numel() * t.element_size() for t in host + fks) + y_h.numel() * y_h.element_size()
+    return {"value": J / t_job, "unit": UNIT, "h2d_bytes_per_step": h2d / J,
+            "d2h_bytes_per_step": 8 * (c_t + J) / J, "iterations_per_job": J,
+            "job_seconds": t_job, "jobs_seconds": runs,
+            "note": ("per rank: H2D of its shard from pinned host buffers + device layout + J "
+                     "iterations of partial / all-reduce / update + D2H of w and the losses; "
+                     "job time = max over ranks; median of 5 jobs after a warm-up job; "
+                     "h2d bytes are this rank's")}
 
 
 if __name__ == "__main__":
