@@ -142,6 +142,81 @@ __global__ void __launch_bounds__(256) k_tmm_partial(const float* __restrict__ A
     part[(int64_t)blockIdx.x * npair + i] = acc[i];
 }
 
+// Narrow A^T y (stream block with C4 float4 per row, CY <= 2 y columns): a
+// thread per row holds the row and its y values in registers (fp32 products,
+// fp64 every 64 rows), then a fixed-order block reduction -- the structure of
+// the GLM fact pass without the gathers.  part[block][a*CY + c] as above.
+template <int C4, int CY>
+__global__ void __launch_bounds__(256) k_tmm_narrow(const float4* __restrict__ F, int64_t rows,
+                                                    YView yv, const int32_t* __restrict__ perm,
+                                                    int64_t rows_per_block,
+                                                    double* __restrict__ part) {
+  constexpr int NP = C4 * 4 * CY;
+  __shared__ double wsum[8][NP];
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  const int64_t r1 = min64(rows, r0 + rows_per_block);
+  float acc[NP];
+  double acc64[NP];
+#pragma unroll
+  for (int i = 0; i < NP; i++) {
+    acc[i] = 0.f;
+    acc64[i] = 0.0;
+  }
+  int n = 0;
+  for (int64_t row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+    const int32_t tr = perm[row];
+    float yc[CY];
+#pragma unroll
+    for (int c = 0; c < CY; c++) yc[c] = tr >= 0 ? yv.at(tr, c) : 0.f;
+    float4 v[C4];
+#pragma unroll
+    for (int q = 0; q < C4; q++) v[q] = F[row * C4 + q];
+#pragma unroll
+    for (int q = 0; q < C4; q++) {
+      const float e4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; e++)
+#pragma unroll
+        for (int c = 0; c < CY; c++)
+          acc[(q * 4 + e) * CY + c] = fmaf(e4[e], yc[c], acc[(q * 4 + e) * CY + c]);
+    }
+    if (++n == 64) {
+#pragma unroll
+      for (int i = 0; i < NP; i++) {
+        acc64[i] += (double)acc[i];
+        acc[i] = 0.f;
+      }
+      n = 0;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NP; i++) {
+    double v = acc64[i] + (double)acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wsum[warp][i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wsum[w][i];
+    part[(int64_t)blockIdx.x * NP + i] = t;
+  }
+}
+
+template <int CY>
+static void tmm_narrow_launch(int c4, unsigned nb, cudaStream_t s, const float* F, int64_t rows,
+                              YView yv, const int32_t* perm, int64_t rpb, double* part) {
+  const float4* F4 = reinterpret_cast<const float4*>(F);
+  switch (c4) {
+#define TMN(C) case C: k_tmm_narrow<C, CY><<<nb, 256, 0, s>>>(F4, rows, yv, perm, rpb, part); break;
+    TMN(1) TMN(2) TMN(3) TMN(4) TMN(5) TMN(6) TMN(7) TMN(8)
+#undef TMN
+    default: break;
+  }
+}
+
 // bins[j, col] = sum over members m of group j (ascending target row) of y'(m, col)
 __global__ void k_group_bins(const int64_t* __restrict__ grp_ptr, const int32_t* __restrict__ grp_rows,
                              bool sorted, int64_t n_neg, int64_t rows, YView yv,
@@ -247,7 +322,15 @@ int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os
       set_error("tlmm: %d x %d output too wide for one pass", acols, cy);
       return FL_ERR_OP;
     }
-    if (bins) {
+    if (!bins && pitch == acols && acols % 4 == 0 && acols <= 32 && cy <= 2) {
+      // narrow stream block: thread-per-row kernel (registers, no staging)
+      if (cy == 1)
+        tmm_narrow_launch<1>(acols / 4, (unsigned)nb, s, A, rows, yv, t->perm->as<int32_t>(), rpb,
+                             part);
+      else
+        tmm_narrow_launch<2>(acols / 4, (unsigned)nb, s, A, rows, yv, t->perm->as<int32_t>(), rpb,
+                             part);
+    } else if (bins) {
       FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
       k_tmm_partial<true><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv, nullptr, bins,
