@@ -72,6 +72,83 @@ __global__ void k_lmm_main(const float* __restrict__ F, int pf, const int32_t* _
   out[(int64_t)perm[p] * c_x + col0 + col] = acc;
 }
 
+// Narrow T x (stream block of C4 float4 per row, NC <= 2 operand columns): a
+// thread per device row, the row loaded as float4s and both columns kept in
+// registers; same fmaf order as k_lmm_main, so results are identical.  The
+// result is written in DEVICE order (coalesced, dev[p*NC + c]) and put into
+// target order by k_lmm_unperm's gathered reads: 100M scattered 4-byte
+// writes (partial-sector read-modify-writes) cost more than the same number
+// of scattered reads.
+template <int C4, int NC>
+__global__ void __launch_bounds__(256) k_lmm_narrow(const float4* __restrict__ F,
+                                                    const int32_t* __restrict__ ftcol,
+                                                    const float* __restrict__ x, int c_x, int col0,
+                                                    GatherSet gs, int64_t r_T,
+                                                    float* __restrict__ dev) {
+  __shared__ float xf[C4 * 4 * NC];
+  for (int i = threadIdx.x; i < C4 * 4 * NC; i += blockDim.x) {
+    const int j = i / NC, col = i - j * NC;
+    const int tc = ftcol[j];
+    xf[i] = tc >= 0 ? x[(int64_t)tc * c_x + col0 + col] : 0.f;
+  }
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < r_T;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    float4 v[C4];
+#pragma unroll
+    for (int q = 0; q < C4; q++) v[q] = F[p * C4 + q];
+    float acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) acc[c] = 0.f;
+#pragma unroll
+    for (int q = 0; q < C4; q++) {
+      const float e4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; e++)
+#pragma unroll
+        for (int c = 0; c < NC; c++) acc[c] = fmaf(e4[e], xf[(q * 4 + e) * NC + c], acc[c]);
+    }
+    for (int d = 0; d < gs.n; d++) {
+      const int32_t fk = gs.fk[d][p];
+      if (fk >= 0) {
+#pragma unroll
+        for (int c = 0; c < NC; c++) acc[c] += gs.q[d][(int64_t)fk * NC + c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c++) dev[p * NC + c] = acc[c];
+  }
+}
+
+// out[t, col0 + c] = dev[iperm[t], c]
+template <int NC>
+__global__ void k_lmm_unperm(const float* __restrict__ dev, const int32_t* __restrict__ iperm,
+                             int64_t r_T, int c_x, int col0, float* __restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= r_T) return;
+  const int64_t p = iperm[t];
+#pragma unroll
+  for (int c = 0; c < NC; c++) out[t * c_x + col0 + c] = dev[p * NC + c];
+}
+
+template <int NC>
+static void lmm_narrow_launch(int c4, unsigned nb, cudaStream_t s, const float* F,
+                              const int32_t* ftcol, const float* x, int c_x, int col0,
+                              const GatherSet& gs, const int32_t* iperm, int64_t r_T, float* dev,
+                              float* out) {
+  const float4* F4 = reinterpret_cast<const float4*>(F);
+  switch (c4) {
+#define LMN(C)                                                                         \
+  case C:                                                                              \
+    k_lmm_narrow<C, NC><<<nb, 256, 0, s>>>(F4, ftcol, x, c_x, col0, gs, r_T, dev); \
+    break;
+    LMN(1) LMN(2) LMN(3) LMN(4) LMN(5) LMN(6) LMN(7) LMN(8)
+#undef LMN
+    default: break;
+  }
+  k_lmm_unperm<NC><<<gridn(r_T), 256, 0, s>>>(dev, iperm, r_T, c_x, col0, out);
+}
+
 
 // Per-block partial of A^T Y over a contiguous row range, A = row-major
 // (pitch) fp32 rows; Y rows either from a device-ordered fp64 buffer (bins)
@@ -294,10 +371,37 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
       gs.q[d] = q;
       gs.fk[d] = g.fk->as<int32_t>();
     }
-    size_t sm = (size_t)t->pf * ncol * 4;
-    k_lmm_main<<<gridn(t->r_T * ncol), 256, sm, s>>>(
-        t->F ? t->F->as<float>() : nullptr, t->pf, t->pf ? t->d_f_tcol->as<int32_t>() : nullptr,
-        x_dev, c_x, col0, ncol, gs, t->perm->as<int32_t>(), t->r_T, out_dev);
+    const float* F = t->F ? t->F->as<float>() : nullptr;
+    // narrow stream block: thread-per-row kernel, float4 row loads, device-
+    // order output + gathered unpermute.  Only past L2 (>= 8M rows by
+    // default): below that the scattered writes stay in L2 and the extra
+    // launch costs more than it saves (C1, 1M rows: 46 -> 51 us).
+    const char* mr = getenv("FL_LMM_NARROW_MIN_ROWS");
+    const int64_t min_rows = mr ? atoll(mr) : (int64_t)1 << 23;
+    if (F && t->pf % 4 == 0 && t->pf <= 32 && ncol <= 4 && t->r_T >= min_rows &&
+        !getenv("FL_NO_NARROW_LMM")) {
+      const unsigned nb = (unsigned)std::min<int64_t>(gridn(t->r_T), 8 * (int64_t)t->sm_count);
+      float* dev = nullptr;
+      FL_CUDA(cudaMallocAsync((void**)&dev, t->r_T * ncol * 4 + 16, s));
+      const int32_t* ftcol = t->d_f_tcol->as<int32_t>();
+      const int32_t* iperm = t->iperm->as<int32_t>();
+      switch (ncol) {
+#define LMC(NC)                                                                              \
+  case NC:                                                                                   \
+    lmm_narrow_launch<NC>(t->pf / 4, nb, s, F, ftcol, x_dev, c_x, col0, gs, iperm, t->r_T, dev, \
+                          out_dev);                                                          \
+    break;
+        LMC(1) LMC(2) LMC(3) LMC(4)
+#undef LMC
+        default: break;
+      }
+      FL_CUDA(cudaFreeAsync(dev, s));
+    } else {
+      size_t sm = (size_t)t->pf * ncol * 4;
+      k_lmm_main<<<gridn(t->r_T * ncol), 256, sm, s>>>(
+          F, t->pf, t->pf ? t->d_f_tcol->as<int32_t>() : nullptr, x_dev, c_x, col0, ncol, gs,
+          t->perm->as<int32_t>(), t->r_T, out_dev);
+    }
     FL_CHECK_LAUNCH();
     for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
   }

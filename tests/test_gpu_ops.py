@@ -199,3 +199,25 @@ def test_upload_paths_agree(fl, monkeypatch, chunk):
         m2 = sel_d[:r_fact] >= 0
         w2[m2, c_fact:] = dim[sel_d[:r_fact][m2]]
         assert np.array_equal(h2.materialize_dense(), w2), name + " identity"
+
+
+@pytest.mark.parametrize("c_fact,dims", [(20, [(1000, 50)]), (7, [(300, 9), (40, 5)]),
+                                         (29, [(997, 6)]), (3, [])])
+def test_narrow_lmm_matches_generic(fl, monkeypatch, c_fact, dims):
+    """The thread-per-row lmm (device-order output + gathered unpermute,
+    forced on here via FL_LMM_NARROW_MIN_ROWS=0) is bit-identical to the
+    generic kernel and matches the oracle, for 1-5 operand columns (5 takes
+    the generic kernel)."""
+    ft = star_table(11, 70_001, dims, c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    h = fl.TargetHandle.factorized(ft)
+    rng = np.random.default_rng(1)
+    monkeypatch.setenv("FL_LMM_NARROW_MIN_ROWS", "0")
+    for cx in (1, 2, 3, 4, 5):
+        x = rng.random((ft.c_T, cx)).astype(np.float32)
+        got = h.lmm(x)
+        monkeypatch.setenv("FL_NO_NARROW_LMM", "1")
+        generic = h.lmm(x)
+        monkeypatch.delenv("FL_NO_NARROW_LMM")
+        assert np.array_equal(got, generic), cx
+        assert rel(got, oracle.lmm(tab, x)) < RTOL

@@ -1,0 +1,58 @@
+"""Time the generic operators (lmm / transpose_lmm) at a bench workload's size.
+
+Usage: python tools/op_probe.py [workload]   (default c2)
+
+Compares the narrow thread-per-row lmm kernel against the generic one
+(FL_NO_NARROW_LMM=1) for 1-3 operand columns: outputs must be identical,
+times are CUDA-event medians over 10 calls.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.getcwd())
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2502_01985_b200 as fl  # noqa: E402
+
+
+def timed(fn, reps=10):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps)]
+    fn()
+    torch.cuda.synchronize()
+    for a, b in ev:
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return float(np.median([a.elapsed_time(b) for a, b in ev]))
+
+
+def main():
+    wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+    dev = torch.device("cuda")
+    sh = bench.make_shard(torch, wl, 0, 1, dev)
+    h = bench.build_handle(fl, wl, sh)
+    del sh
+    torch.cuda.empty_cache()
+    r, c = h.shape
+    g = torch.Generator(device=dev).manual_seed(0)
+    for cx in (1, 2, 3):
+        x = torch.rand((c, cx), device=dev, generator=g)
+        os.environ["FL_NO_NARROW_LMM"] = "1"
+        ref = h.lmm(x, traced=False).clone()
+        t_main = timed(lambda: h.lmm(x, traced=False))
+        os.environ.pop("FL_NO_NARROW_LMM")
+        out = h.lmm(x, traced=False)
+        same = bool(torch.equal(out, ref))
+        t_nar = timed(lambda: h.lmm(x, traced=False))
+        y = torch.rand((r, cx), device=dev, generator=g)
+        t_tl = timed(lambda: h.transpose_lmm(y, traced=False))
+        print(f"rows {r} cols {c} c_x {cx}: lmm generic {t_main:.3f} ms, narrow {t_nar:.3f} ms "
+              f"(identical={same}); transpose_lmm {t_tl:.3f} ms", flush=True)
+
+
+if __name__ == "__main__":
+    main()
