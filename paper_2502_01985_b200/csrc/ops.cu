@@ -156,6 +156,8 @@ static void lmm_narrow_launch(int c4, unsigned nb, cudaStream_t s, const float* 
 // 128-row chunks; each (a, y-column) pair is split over up to 8 row groups
 // (fp32 within a chunk, fp64 across chunks, groups combined in a fixed
 // order), so narrow outputs still use the whole CTA.  part[block][a*cy + c].
+// (y columns per pass are capped so na * ny <= blockDim: with 32+ A columns
+// and 9+ y columns the pairs past thread 255 were never computed.)
 constexpr int TM_RC = 128;
 constexpr int TM_AC = 40;    // A columns per pass
 constexpr int TM_YC = 16;    // y columns per pass
@@ -178,8 +180,10 @@ __global__ void __launch_bounds__(256) k_tmm_partial(const float* __restrict__ A
     const int nr = (int)min64(TM_RC, r1 - rb);
     for (int a0 = 0; a0 < acols; a0 += TM_AC) {
       const int na = min(TM_AC, acols - a0);
-      for (int y0 = 0; y0 < cy; y0 += TM_YC) {
-        const int ny = min(TM_YC, cy - y0);
+      // at most one (a, y-column) pair per thread: na * ny <= blockDim
+      const int ystep = min(TM_YC, max(1, (int)blockDim.x / na));
+      for (int y0 = 0; y0 < cy; y0 += ystep) {
+        const int ny = min(ystep, cy - y0);
         __syncthreads();
         for (int i = threadIdx.x; i < nr * na; i += blockDim.x) {
           const int r = i / na, c = i - r * na;
@@ -418,23 +422,38 @@ int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os
     int64_t nb = std::min<int64_t>(std::max<int64_t>(1, ceil_div(rows, 2048)), 4 * sms);
     int64_t rpb = round_up(ceil_div(rows, nb), 32);
     nb = ceil_div(rows, rpb);
+    if (!bins && pitch == acols && acols % 4 == 0 && acols <= 32 && cy <= 8) {
+      // narrow stream block: thread-per-row kernel (registers, no staging),
+      // one pass per pair of y columns (C2-size 3-column T^T y: 15.4 ms
+      // through k_tmm_partial's perm-staged tiles -> two streaming passes)
+      double* part = nullptr;
+      FL_CUDA(cudaMallocAsync((void**)&part, nb * acols * 2 * 8, s));
+      for (int c0 = 0; c0 < cy; c0 += 2) {
+        const int w = std::min(2, cy - c0);
+        const YView sub{yv.base + (int64_t)c0 * yv.sc, yv.sr, yv.sc};
+        if (w == 1)
+          tmm_narrow_launch<1>(acols / 4, (unsigned)nb, s, A, rows, sub, t->perm->as<int32_t>(),
+                               rpb, part);
+        else
+          tmm_narrow_launch<2>(acols / 4, (unsigned)nb, s, A, rows, sub, t->perm->as<int32_t>(),
+                               rpb, part);
+        FL_CHECK_LAUNCH();
+        k_reduce_partials<<<gridn(acols * w), 256, 0, s>>>(part, (int)nb, acols, w, tcol,
+                                                           out + c0 * os_c, os_t, os_c);
+        FL_CHECK_LAUNCH();
+      }
+      FL_CUDA(cudaFreeAsync(part, s));
+      return FL_OK;
+    }
     int npair = acols * cy;
-    double* part = nullptr;
-    FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
     size_t sm = (size_t)npair * 8;
     if (sm > 190 * 1024) {
       set_error("tlmm: %d x %d output too wide for one pass", acols, cy);
       return FL_ERR_OP;
     }
-    if (!bins && pitch == acols && acols % 4 == 0 && acols <= 32 && cy <= 2) {
-      // narrow stream block: thread-per-row kernel (registers, no staging)
-      if (cy == 1)
-        tmm_narrow_launch<1>(acols / 4, (unsigned)nb, s, A, rows, yv, t->perm->as<int32_t>(), rpb,
-                             part);
-      else
-        tmm_narrow_launch<2>(acols / 4, (unsigned)nb, s, A, rows, yv, t->perm->as<int32_t>(), rpb,
-                             part);
-    } else if (bins) {
+    double* part = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
+    if (bins) {
       FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
       k_tmm_partial<true><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv, nullptr, bins,

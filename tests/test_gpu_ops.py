@@ -221,3 +221,17 @@ def test_narrow_lmm_matches_generic(fl, monkeypatch, c_fact, dims):
         monkeypatch.delenv("FL_NO_NARROW_LMM")
         assert np.array_equal(got, generic), cx
         assert rel(got, oracle.lmm(tab, x)) < RTOL
+
+
+@pytest.mark.parametrize("c_fact", [20, 8, 32, 13])
+def test_transpose_lmm_widths_vs_oracle(fl, c_fact):
+    """T^T y for 1-9 y columns: the stream block takes the thread-per-row
+    kernel one column pair per pass (up to 8 columns, stream pitch <= 32),
+    wider y or stream blocks the staged generic kernel."""
+    ft = star_table(12, 60_003, [(900, 11), (31, 4)], c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    h = fl.TargetHandle.factorized(ft)
+    rng = np.random.default_rng(2)
+    for cy in range(1, 10):
+        y = rng.random((ft.r_T, cy)).astype(np.float32)
+        assert rel(h.transpose_lmm(y), oracle.transpose_lmm(tab, y)) < RTOL, cy
