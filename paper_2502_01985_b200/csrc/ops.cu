@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) k_tmm_partial(const float* __restrict__ A
           const int r = i / ny, c = i - r * ny;
           float v;
           if (BINS) v = (float)bins[(rb + r) * cy + y0 + c];
-          else v = yv.at(perm[rb + r], y0 + c);
+          else v = yv.at(perm ? perm[rb + r] : rb + r, y0 + c);
           ys[r * (TM_YC + 1) + c] = v;
         }
         __syncthreads();
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) k_tmm_narrow(const float4* __restrict__ F
   }
   int n = 0;
   for (int64_t row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
-    const int32_t tr = perm[row];
+    const int64_t tr = perm ? (int64_t)perm[row] : row;
     float yc[CY];
 #pragma unroll
     for (int c = 0; c < CY; c++) yc[c] = tr >= 0 ? yv.at(tr, c) : 0.f;
@@ -310,24 +310,40 @@ __global__ void k_group_bins(const int64_t* __restrict__ grp_ptr, const int32_t*
   double s = 0.0;
   for (int64_t m = m0; m < m1; m++) {
     int64_t p = sorted ? n_neg + m : (int64_t)grp_rows[m];
-    s += (double)yv.at(perm[p], col);
+    s += (double)yv.at(perm ? perm[p] : p, col);
   }
   bins[idx] = s;
+}
+
+// ydev[p*cy + c] = y(perm[p], c): the target-order operand read ONCE in
+// device order, so the stream pass and the group bins that follow both read
+// it sequentially instead of each gathering 4-byte values through perm.
+__global__ void k_gather_y_dev(YView yv, const int32_t* __restrict__ perm, int64_t rows, int cy,
+                               float* __restrict__ ydev) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * cy) return;
+  const int64_t p = idx / cy;
+  const int c = (int)(idx - p * cy);
+  const int32_t tr = perm[p];
+  ydev[idx] = tr >= 0 ? yv.at(tr, c) : 0.f;
 }
 
 // out[tcol[a] * os_t + col * os_c] += sum_b part[b][a*cy + col]  (fixed order)
 __global__ void k_reduce_partials(const double* __restrict__ part, int nblocks, int acols,
                                   int cy, const int32_t* __restrict__ tcol, double* __restrict__ out,
                                   int64_t os_t, int64_t os_c) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int npair = acols * cy;
+  // one warp per output pair: lanes stride the blocks, fixed xor tree
+  const int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int npair = acols * cy;
   if (i >= npair) return;
-  int a = i / cy, col = i - a * cy;
-  int tc = tcol[a];
-  if (tc < 0) return;
   double s = 0.0;
-  for (int b = 0; b < nblocks; b++) s += part[(int64_t)b * npair + i];
-  out[tc * os_t + col * os_c] += s;
+  for (int b = lane; b < nblocks; b += 32) s += part[(int64_t)b * npair + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int a = i / cy, col = i - a * cy;
+  const int tc = tcol[a];
+  if (lane == 0 && tc >= 0) out[tc * os_t + col * os_c] += s;
 }
 
 __global__ void k_fill(float* p, int64_t n, float v) {
@@ -413,9 +429,22 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
 }
 
 // generic T^T y with strided y view and strided fp64 output
-int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
+int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
                    cudaStream_t s) {
   const int sms = t->sm_count;
+  // With gathered sources there are two consumers of y in device order:
+  // gather it once (bit-identical values; perm == nullptr means "already in
+  // device order" to the kernels below).
+  YView yv = yv_in;
+  const int32_t* yperm = t->perm->as<int32_t>();
+  float* ydev = nullptr;
+  if (!t->g.empty() && t->r_T > 0 && !getenv("FL_NO_Y_DEVORDER")) {
+    FL_CUDA(cudaMallocAsync((void**)&ydev, t->r_T * cy * 4 + 16, s));
+    k_gather_y_dev<<<gridn(t->r_T * cy), 256, 0, s>>>(yv_in, yperm, t->r_T, cy, ydev);
+    FL_CHECK_LAUNCH();
+    yv = YView{ydev, cy, 1};
+    yperm = nullptr;
+  }
   auto launch_tmm = [&](const float* A, int pitch, int acols, int64_t rows, const double* bins,
                         const int32_t* tcol) -> int {
     if (rows <= 0 || acols <= 0) return FL_OK;
@@ -432,13 +461,13 @@ int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os
         const int w = std::min(2, cy - c0);
         const YView sub{yv.base + (int64_t)c0 * yv.sc, yv.sr, yv.sc};
         if (w == 1)
-          tmm_narrow_launch<1>(acols / 4, (unsigned)nb, s, A, rows, sub, t->perm->as<int32_t>(),
+          tmm_narrow_launch<1>(acols / 4, (unsigned)nb, s, A, rows, sub, yperm,
                                rpb, part);
         else
-          tmm_narrow_launch<2>(acols / 4, (unsigned)nb, s, A, rows, sub, t->perm->as<int32_t>(),
+          tmm_narrow_launch<2>(acols / 4, (unsigned)nb, s, A, rows, sub, yperm,
                                rpb, part);
         FL_CHECK_LAUNCH();
-        k_reduce_partials<<<gridn(acols * w), 256, 0, s>>>(part, (int)nb, acols, w, tcol,
+        k_reduce_partials<<<gridn((int64_t)acols * w * 32), 256, 0, s>>>(part, (int)nb, acols, w, tcol,
                                                            out + c0 * os_c, os_t, os_c);
         FL_CHECK_LAUNCH();
       }
@@ -462,11 +491,11 @@ int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os
       FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k_tmm_partial<false><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv,
-                                                         t->perm->as<int32_t>(), nullptr, cy, rpb,
+                                                         yperm, nullptr, cy, rpb,
                                                          part);
     }
     FL_CHECK_LAUNCH();
-    k_reduce_partials<<<gridn(npair), 256, 0, s>>>(part, (int)nb, acols, cy, tcol, out, os_t, os_c);
+    k_reduce_partials<<<gridn((int64_t)npair * 32), 256, 0, s>>>(part, (int)nb, acols, cy, tcol, out, os_t, os_c);
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaFreeAsync(part, s));
     return FL_OK;
@@ -481,12 +510,13 @@ int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os
     FL_CUDA(cudaMallocAsync((void**)&bins, g.rows * cy * 8 + 16, s));
     k_group_bins<<<gridn(g.rows * cy), 256, 0, s>>>(
         g.grp_ptr->as<int64_t>(), g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr, g.sorted,
-        g.n_neg, g.rows, yv, t->perm->as<int32_t>(), cy, bins);
+        g.n_neg, g.rows, yv, yperm, cy, bins);
     FL_CHECK_LAUNCH();
     rc = launch_tmm(g.S->as<float>(), g.pitch, g.cols, g.rows, bins, g.d_tcol->as<int32_t>());
     if (rc) return rc;
     FL_CUDA(cudaFreeAsync(bins, s));
   }
+  if (ydev) FL_CUDA(cudaFreeAsync(ydev, s));
   return FL_OK;
 }
 
