@@ -328,6 +328,14 @@ __global__ void k_gather_y_dev(YView yv, const int32_t* __restrict__ perm, int64
   ydev[idx] = tr >= 0 ? yv.at(tr, c) : 0.f;
 }
 
+// tmp[tr*w + c] = y(tr, c0 + c) for a column-strided view (rmm's x^T):
+// coalesced reads along each column, row-major chunk out.
+__global__ void k_view_rows(YView yv, int64_t rows, int c0, int w, float* __restrict__ tmp) {
+  const int64_t tr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tr >= rows) return;
+  for (int c = 0; c < w; c++) tmp[tr * w + c] = yv.at(tr, c0 + c);
+}
+
 // out[tcol[a] * os_t + col * os_c] += sum_b part[b][a*cy + col]  (fixed order)
 __global__ void k_reduce_partials(const double* __restrict__ part, int nblocks, int acols,
                                   int cy, const int32_t* __restrict__ tcol, double* __restrict__ out,
@@ -432,6 +440,35 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
 int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
                    cudaStream_t s) {
   const int sms = t->sm_count;
+  if (cy > 1 && yv_in.sc > yv_in.sr && t->r_T > 0 && !getenv("FL_NO_VIEW_ROWS")) {
+    // Column-strided y (rmm: x^T of a k x r_T row-major x).  Every device-
+    // order read of it would be one 32-byte sector per 4-byte value; make
+    // row-major 8-column chunks first (sequential on both sides), then run
+    // each chunk as an ordinary row-major T^T y.
+    constexpr int VW = 8;
+    float* tmp = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&tmp, t->r_T * VW * 4 + 16, s));
+    for (int c0 = 0; c0 < cy; c0 += VW) {
+      const int w = std::min(VW, cy - c0);
+      k_view_rows<<<gridn(t->r_T), 256, 0, s>>>(yv_in, t->r_T, c0, w, tmp);
+      FL_CHECK_LAUNCH();
+      const int rc = do_tlmm(t, YView{tmp, w, 1}, w, out + c0 * os_c, os_t, os_c, s);
+      if (rc) return rc;
+    }
+    FL_CUDA(cudaFreeAsync(tmp, s));
+    return FL_OK;
+  }
+  if (cy > 8 && !getenv("FL_NO_VIEW_ROWS")) {
+    // wide y: 8-column chunks, each through the narrow passes below (C2-size
+    // 32 columns: 67.8 ms in one staged pass -> 4 chunks)
+    for (int c0 = 0; c0 < cy; c0 += 8) {
+      const int w = std::min(8, cy - c0);
+      const int rc = do_tlmm(t, YView{yv_in.base + (int64_t)c0 * yv_in.sc, yv_in.sr, yv_in.sc}, w,
+                             out + c0 * os_c, os_t, os_c, s);
+      if (rc) return rc;
+    }
+    return FL_OK;
+  }
   // With gathered sources there are two consumers of y in device order:
   // gather it once (bit-identical values; perm == nullptr means "already in
   // device order" to the kernels below).

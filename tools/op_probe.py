@@ -54,5 +54,29 @@ def main():
               f"(identical={same}); transpose_lmm {t_tl:.3f} ms", flush=True)
 
 
+
+
+def wide(wl_name="c2"):
+    """Wider operands (generic kernels): lmm / transpose_lmm / rmm at 8 and 32 columns."""
+    wl = bench.WORKLOADS[wl_name]
+    dev = torch.device("cuda")
+    sh = bench.make_shard(torch, wl, 0, 1, dev)
+    h = bench.build_handle(fl, wl, sh)
+    del sh
+    torch.cuda.empty_cache()
+    r, c = h.shape
+    for k in (8, 32):
+        x = torch.rand((c, k), device=dev)
+        y = torch.rand((r, k), device=dev)
+        w = torch.rand((k, r), device=dev)
+        print(f"k {k}: lmm {timed(lambda: h.lmm(x, traced=False), 3):.2f} ms, "
+              f"transpose_lmm {timed(lambda: h.transpose_lmm(y, traced=False), 3):.2f} ms, "
+              f"rmm {timed(lambda: h.rmm(w, traced=False), 3):.2f} ms", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--wide" in sys.argv:
+        sys.argv.remove("--wide")
+        wide(sys.argv[1] if len(sys.argv) > 1 else "c2")
+    else:
+        main()
