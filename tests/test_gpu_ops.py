@@ -206,14 +206,14 @@ def test_upload_paths_agree(fl, monkeypatch, chunk):
 def test_narrow_lmm_matches_generic(fl, monkeypatch, c_fact, dims):
     """The thread-per-row lmm (device-order output + gathered unpermute,
     forced on here via FL_LMM_NARROW_MIN_ROWS=0) is bit-identical to the
-    generic kernel and matches the oracle, for 1-5 operand columns (5 takes
-    the generic kernel)."""
+    generic kernel and matches the oracle, for 1-9 and 20 operand columns
+    (more than 4 take the generic kernel)."""
     ft = star_table(11, 70_001, dims, c_fact)
     tab = oracle.OracleTable.from_ft(ft)
     h = fl.TargetHandle.factorized(ft)
     rng = np.random.default_rng(1)
     monkeypatch.setenv("FL_LMM_NARROW_MIN_ROWS", "0")
-    for cx in (1, 2, 3, 4, 5):
+    for cx in (1, 2, 3, 4, 5, 6, 7, 8, 9, 20):
         x = rng.random((ft.c_T, cx)).astype(np.float32)
         got = h.lmm(x)
         monkeypatch.setenv("FL_NO_NARROW_LMM", "1")
