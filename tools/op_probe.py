@@ -65,7 +65,7 @@ def wide(wl_name="c2"):
     del sh
     torch.cuda.empty_cache()
     r, c = h.shape
-    for k in (8, 32):
+    for k in [int(v) for v in os.environ.get("OP_KS", "8,32").split(",")]:
         x = torch.rand((c, k), device=dev)
         y = torch.rand((r, k), device=dev)
         w = torch.rand((k, r), device=dev)
