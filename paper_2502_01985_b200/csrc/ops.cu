@@ -120,6 +120,66 @@ __global__ void __launch_bounds__(256) k_lmm_narrow(const float4* __restrict__ F
   }
 }
 
+// Wider T x (5..32 operand columns, stream block of C4 float4 per row): a
+// warp per row at a time, lane = output column, grid-stride over rows.  The
+// thread's x column lives in registers (loaded once), the row is one
+// coalesced load broadcast by shuffle, and the target row is written as one
+// contiguous run.  k_lmm_main spends a thread, a 64-bit division and a
+// shared-memory refill of x per (row, column) block: ncu at C2-size k = 32
+// shows it issue-bound at 35.6G warp instructions.  Same fmaf order, so
+// results are identical.
+template <int C4>
+__global__ void __launch_bounds__(256) k_lmm_warp_rows(const float* __restrict__ F,
+                                                       const int32_t* __restrict__ ftcol,
+                                                       const float* __restrict__ x, int c_x,
+                                                       int col0, int ncol, GatherSet gs,
+                                                       const int32_t* __restrict__ perm,
+                                                       int64_t r_T, float* __restrict__ out) {
+  constexpr int PF = C4 * 4;
+  const int lane = threadIdx.x & 31;
+  const bool on = lane < ncol;
+  float xr[PF];
+#pragma unroll
+  for (int j = 0; j < PF; j++) {
+    const int tc = ftcol[j];
+    xr[j] = (on && tc >= 0) ? x[(int64_t)tc * c_x + col0 + lane] : 0.f;
+  }
+  // R rows per warp iteration, all loads issued before the arithmetic
+  // (one row at a time was latency-bound: ~37 ms flat in k at 100M rows)
+  constexpr int R = 8;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * R; p0 < r_T;
+       p0 += nw * R) {
+    float v[R], acc[R];
+    int32_t tr[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t p = p0 + r;
+      v[r] = (lane < PF && p < r_T) ? F[p * PF + lane] : 0.f;
+      tr[r] = p < r_T ? perm[p] : -1;
+      acc[r] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < PF; j++)
+#pragma unroll
+      for (int r = 0; r < R; r++) acc[r] = fmaf(__shfl_sync(0xffffffffu, v[r], j), xr[j], acc[r]);
+    for (int d = 0; d < gs.n; d++) {
+      int32_t fk[R];
+#pragma unroll
+      for (int r = 0; r < R; r++) fk[r] = p0 + r < r_T ? gs.fk[d][p0 + r] : -1;
+      float qv[R];
+#pragma unroll
+      for (int r = 0; r < R; r++) qv[r] = (fk[r] >= 0 && on) ? gs.q[d][(int64_t)fk[r] * ncol + lane] : 0.f;
+#pragma unroll
+      for (int r = 0; r < R; r++)
+        if (fk[r] >= 0) acc[r] += qv[r];
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++)
+      if (on && tr[r] >= 0) out[(int64_t)tr[r] * c_x + col0 + lane] = acc[r];
+  }
+}
+
 // out[t, col0 + c] = dev[iperm[t], c]
 template <int NC>
 __global__ void k_lmm_unperm(const float* __restrict__ dev, const int32_t* __restrict__ iperm,
@@ -424,6 +484,21 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
         default: break;
       }
       FL_CUDA(cudaFreeAsync(dev, s));
+    } else if (F && t->pf % 4 == 0 && t->pf <= 32 && ncol >= 16 && !getenv("FL_NO_NARROW_LMM")) {
+      const unsigned nb =
+          (unsigned)std::min<int64_t>(ceil_div(t->r_T, 64), 8 * (int64_t)t->sm_count);
+      const int32_t* ftcol = t->d_f_tcol->as<int32_t>();
+      const int32_t* perm = t->perm->as<int32_t>();
+      switch (t->pf / 4) {
+#define LMW(C)                                                                               \
+  case C:                                                                                    \
+    k_lmm_warp_rows<C><<<nb, 256, 0, s>>>(F, ftcol, x_dev, c_x, col0, ncol, gs, perm, t->r_T, \
+                                          out_dev);                                          \
+    break;
+        LMW(1) LMW(2) LMW(3) LMW(4) LMW(5) LMW(6) LMW(7) LMW(8)
+#undef LMW
+        default: break;
+      }
     } else {
       size_t sm = (size_t)t->pf * ncol * 4;
       k_lmm_main<<<gridn(t->r_T * ncol), 256, sm, s>>>(
