@@ -88,6 +88,10 @@ int fl_table_shape(const fl_table* t, int64_t* r_T, int32_t* c_T, int32_t* n_sou
  * sources; sort_source = user index of the sort source (-1 = none) */
 int fl_table_layout(const fl_table* t, int32_t* stream_cols, int32_t* stream_pitch,
                     int32_t* n_gather, int32_t* sort_source, int64_t* device_bytes);
+/* gathered source i (0 <= i < n_gather): user source index, r_d, c_d, row
+ * pitch (floats) and the number of target rows it matches (nnz of I_d) */
+int fl_table_gather_info(const fl_table* t, int32_t i, int32_t* src_index, int64_t* rows,
+                         int32_t* cols, int32_t* pitch, int64_t* matched);
 /* Device-derived selectors of source k in TARGET-row terms, for bit-exact
  * comparison with the reference's _build_selectors (ops.py:55-74).
  * ind_sel: r_T; group_indptr: r_k+1; group_rows: nnz(I_k).  Host or device

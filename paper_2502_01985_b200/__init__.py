@@ -20,10 +20,17 @@ from .trainers import (ConfigError, DivergenceError, TrainConfig, TrainResult,
 __version__ = "0.1.0"
 
 
-def materialize(ft, *, device: int = 0, check: bool = True) -> SparseMatrix:
-    """The join result T = sum_k I_k S_k M_k^T (reference `metadata.py:215-225`),
-    computed on the device; values are exact copies of the sources."""
-    return TargetHandle.factorized(ft, check=check, device=device).materialize_target()
+def materialize(ft, *, threads: int = 1, trace: OpTrace | None = None, check: bool = True,
+                device: int = 0) -> SparseMatrix:
+    """The join result T = sum_k I_k S_k M_k^T (reference `metadata.py:215-225`,
+    same signature), computed on the device; values are exact copies of the
+    sources.  `threads` is accepted for API parity (the GPU ignores it); the
+    join's work is recorded into `trace` when one is given."""
+    h = TargetHandle.factorized(ft, threads=threads, check=check, device=device)
+    out = h.materialize_target(traced=trace is not None)
+    if trace is not None:
+        trace.merge(h.trace)
+    return out
 
 
 __all__ = ["as_dense", "costmodel", "formats", "ConfigError", "DivergenceError", "FactorizedTable", "IndicatorMatrix",

@@ -54,6 +54,8 @@ SIGNATURES = {
     "fl_table_shape": [_P, C.POINTER(_I64), C.POINTER(_I32), C.POINTER(_I32)],
     "fl_table_layout": [_P, C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I32),
                         C.POINTER(_I32), C.POINTER(_I64)],
+    "fl_table_gather_info": [_P, _I32, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I32),
+                             C.POINTER(_I32), C.POINTER(_I64)],
     "fl_table_selectors": [_P, _I32, _P, _P, _P, _P],
     "fl_table_perm": [_P, _P, _P],
     "fl_lmm": [_P, _P, _I32, _P, _P],

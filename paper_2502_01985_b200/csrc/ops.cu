@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(256) k_lmm_narrow(const float4* __restrict__ F
   }
 }
 
-// Wider T x (5..32 operand columns, stream block of C4 float4 per row): a
+// Wider T x (16..32 operand columns per chunk -- the dispatch gate below --
+// stream block of C4 float4 per row): a
 // warp per row at a time, lane = output column, grid-stride over rows.  The
 // thread's x column lives in registers (loaded once), the row is one
 // coalesced load broadcast by shuffle, and the target row is written as one

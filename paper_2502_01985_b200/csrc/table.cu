@@ -905,6 +905,21 @@ int fl_table_layout(const fl_table* t, int32_t* stream_cols, int32_t* stream_pit
   return FL_OK;
 }
 
+int fl_table_gather_info(const fl_table* t, int32_t i, int32_t* src_index, int64_t* rows,
+                         int32_t* cols, int32_t* pitch, int64_t* matched) {
+  if (!t || !t->finalized || i < 0 || i >= (int)t->g.size()) {
+    set_error("fl_table_gather_info: bad table or gather index");
+    return FL_ERR_ARG;
+  }
+  const flb::GatherSrc& g = t->g[i];
+  if (src_index) *src_index = g.src_index;
+  if (rows) *rows = g.rows;
+  if (cols) *cols = g.cols;
+  if (pitch) *pitch = g.pitch;
+  if (matched) *matched = g.matched;
+  return FL_OK;
+}
+
 int fl_table_selectors(fl_table* t, int32_t k, int32_t* ind_sel, int64_t* group_indptr,
                        int32_t* group_rows, void* stream) {
   if (!t || !t->finalized || k < 0 || k >= (int)t->src.size()) {

@@ -144,13 +144,22 @@ def run_sharded(session, iterations: int, dist, device, group=None):
     """`iterations` x (partial -> all-reduce -> update) on one rank.  The
     session must expose partial(), update() and reduce_buffer()."""
     import torch
+
+    from .trainers import KMeansSession
     ptr, n = session.reduce_buffer()
     red = torch.as_tensor(DeviceBuffer(ptr, n), device=device)
     if getattr(session, "needs_prime", False):    # GNMF: products of W_0 first
         session.partial()
         all_reduce_(red, dist, group)
-    for _ in range(iterations):
-        session.partial()
+    # K-means: the last iteration writes the assignments it made against the
+    # centroids of that iteration (reference trainers.py:229-245 returns the
+    # final iteration's argmin, not one against the updated centroids)
+    assigns = isinstance(session, KMeansSession)
+    for it in range(iterations):
+        if assigns:
+            session.partial(write_assign=(it == iterations - 1))
+        else:
+            session.partial()
         all_reduce_(red, dist, group)
         session.update()
 

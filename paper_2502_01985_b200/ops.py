@@ -61,8 +61,20 @@ class DeviceTable:
         nb = C.c_int64()
         _lib.call("fl_table_layout", self.ptr, C.byref(sc), C.byref(sp), C.byref(ng),
                   C.byref(ss), C.byref(nb))
-        return {"stream_cols": sc.value, "stream_pitch": sp.value, "n_gather": ng.value,
-                "sort_source": ss.value, "device_bytes": nb.value}
+        lay = {"stream_cols": sc.value, "stream_pitch": sp.value, "n_gather": ng.value,
+               "sort_source": ss.value, "device_bytes": nb.value}
+        gathers = []
+        for i in range(ng.value):
+            si, rows, cols, pitch, matched = (C.c_int32(), C.c_int64(), C.c_int32(),
+                                              C.c_int32(), C.c_int64())
+            _lib.call("fl_table_gather_info", self.ptr, i, C.byref(si), C.byref(rows),
+                      C.byref(cols), C.byref(pitch), C.byref(matched))
+            gathers.append({"source": si.value, "rows": rows.value, "cols": cols.value,
+                            "pitch": pitch.value, "matched": matched.value})
+        lay["gathers"] = gathers
+        # one read of every dimension table (bytes), as the fused passes read them
+        lay["gather_bytes"] = sum(4 * g["rows"] * g["pitch"] for g in gathers)
+        return lay
 
     def perm(self) -> np.ndarray:
         out = np.empty(self.r_T, dtype=np.int32)
@@ -101,17 +113,26 @@ def upload_arrays(sources, ind_sels, col_maps, r_T: int, c_T: int, *,
     alive = []   # host buffers must outlive the asynchronous uploads (until finalize)
     for vals, sel, cmap in zip(sources, ind_sels, col_maps):
         if _is_torch(vals):
-            v_ptr, r_k, c_k = vals.data_ptr(), vals.shape[0], vals.shape[1]
-            keep = vals
+            import torch
+            if vals.dim() != 2:
+                raise ShapeError(f"source values must be 2-D, got {tuple(vals.shape)}")
+            keep = vals.to(torch.float32).contiguous()   # same cast as the numpy path
+            v_ptr, r_k, c_k = keep.data_ptr(), keep.shape[0], keep.shape[1]
         else:
             keep = np.ascontiguousarray(vals, dtype=np.float32)
             v_ptr, (r_k, c_k) = keep.ctypes.data, keep.shape
         if sel is None:           # identity indicator (r_k == r_T)
             s_keep, s_ptr = None, 0
         elif _is_torch(sel):
-            s_keep, s_ptr = sel, sel.data_ptr()
+            import torch
+            s_keep = sel.to(torch.int32).reshape(-1).contiguous()
+            if s_keep.numel() != int(r_T):
+                raise ShapeError(f"ind_sel must have r_T = {r_T} entries, got {s_keep.numel()}")
+            s_ptr = s_keep.data_ptr()
         else:
-            s_keep = np.ascontiguousarray(sel, dtype=np.int32)
+            s_keep = np.ascontiguousarray(sel, dtype=np.int32).reshape(-1)
+            if s_keep.size != int(r_T):
+                raise ShapeError(f"ind_sel must have r_T = {r_T} entries, got {s_keep.size}")
             s_ptr = s_keep.ctypes.data
         m_keep = np.ascontiguousarray(cmap, dtype=np.int32)
         _lib.check(lib.fl_table_add_source(ptr, int(r_k), int(c_k), C.c_void_p(v_ptr),
@@ -233,10 +254,17 @@ class TargetHandle:
 
     # -- algorithmic work of one pass over the device layout
     def _pass_cost(self, width: int) -> tuple[int, int]:
+        """(multiply-adds, algorithmic bytes read) of one factorized pass of
+        operand width `width`: the stream block and the FKs once per target
+        row, every dimension table once (its product is formed per dimension
+        row, then gathered per target row)."""
         lay = self._dev.layout()
         r_T = self._dev.r_T
         madds = width * r_T * lay["stream_cols"]
+        for g in lay["gathers"]:
+            madds += width * (g["rows"] * g["cols"] + g["matched"])
         rbytes = 4 * r_T * lay["stream_pitch"] + 4 * r_T * lay["n_gather"]
+        rbytes += lay["gather_bytes"]
         return madds, rbytes
 
     # -- operators

@@ -154,7 +154,11 @@ class GlmSession:
         self.c_T = h.shape[1]
         ptr = C.c_void_p()
         if _is_torch(y):
-            y_ptr, keep = C.c_void_p(y.data_ptr()), y
+            import torch
+            # the library reads uint8 labels (logreg) / fp32 targets (linreg)
+            keep = y.reshape(-1).to(torch.uint8 if model == "logreg" else torch.float32)
+            keep = keep.contiguous()
+            y_ptr = C.c_void_p(keep.data_ptr())
         else:
             dt = np.uint8 if model == "logreg" else np.float32
             keep = np.ascontiguousarray(np.asarray(y).reshape(-1), dtype=dt)
@@ -231,6 +235,19 @@ def _labels(y, r_t: int):
     return yd.reshape(-1)
 
 
+def _op_trace(t: TargetHandle, width: int, seconds: float) -> OpTrace:
+    """OpTrace of one operator call of operand width `width` over the device
+    layout: multiply-adds of the factorized product and the algorithmic bytes
+    of one pass (TargetHandle._pass_cost); the reference records the same
+    three counters per traced call (sparse.py:56-80, ops.py:159-204)."""
+    madds, rb = t._pass_cost(max(width, 1))
+    if width == 0:
+        madds = 0
+    tr = OpTrace()
+    tr.record(madds, rb, 4 * t.shape[0] * max(width, 1), seconds)
+    return tr
+
+
 def _log_glm_ops(t: TargetHandle, result: TrainResult, iterations: int, per_it: OpTrace):
     """Trace log in the reference's op vocabulary (trainers.py:151-157:
     one lmm and one transpose_lmm per iteration)."""
@@ -247,9 +264,13 @@ def _log_glm_ops(t: TargetHandle, result: TrainResult, iterations: int, per_it: 
 def _glm(model: str, t: TargetHandle, y, cfg: TrainConfig) -> TrainResult:
     r_t, c_t = t.shape
     yv = _labels(y, r_t)
-    if model == "logreg" and not _is_torch(yv):
-        nz = yv[yv != 0]
-        if nz.size and not np.all(nz == 1.0):
+    if model == "logreg":
+        # reference trainers.py:172-173 (checked for host and device labels)
+        if _is_torch(yv):
+            ok = bool(((yv == 0) | (yv == 1)).all())
+        else:
+            ok = bool(np.all((yv == 0) | (yv == 1)))
+        if not ok:
             raise ConfigError("logistic labels must be 0/1")
     s = GlmSession(t, model, yv, cfg.learning_rate)
     try:
@@ -395,11 +416,16 @@ def kmeans(t: TargetHandle, cfg: TrainConfig) -> TrainResult:
                         8 * (k * c_t + k + 1) * cfg.iterations, tm.seconds)
     result.wall_time = tm.seconds
     if t.trace_log is not None:
-        for name in ("rmm", "elementwise", "row_sum"):
-            t.trace_log.append((name, t.path, OpTrace()))
+        # the reference's op sequence (trainers.py:213-245): rmm (seed rows),
+        # elementwise square, row_sum, then lmm + transpose_lmm per iteration;
+        # each entry carries the device pass's algorithmic work, and the fused
+        # iteration's device time is split between its two products
+        for name, width in (("rmm", k), ("elementwise", 0), ("row_sum", 1)):
+            t.trace_log.append((name, t.path, _op_trace(t, width, 0.0)))
+        half = tm.seconds / (2 * cfg.iterations)
         for _ in range(cfg.iterations):
             for name in ("lmm", "transpose_lmm"):
-                t.trace_log.append((name, t.path, OpTrace()))
+                t.trace_log.append((name, t.path, _op_trace(t, k, half)))
     t.trace.merge(result.trace)
     return result
 
@@ -553,12 +579,21 @@ def gaussian_nmf(t: TargetHandle, cfg: TrainConfig) -> TrainResult:
         raise DivergenceError("gnmf", bad)
     result = TrainResult("gnmf", {"w": w, "h": h}, [float(v) for v in losses])
     result.wall_time = tm.seconds
-    result.trace.record(0, 0, 0, tm.seconds)
+    # per iteration: rmm (W^T T) and lmm (T H^T) of width r, fused in one pass
+    # that also reads and writes W (fp32 on the device)
+    per = _op_trace(t, r, 0.0)
+    w_bytes = 4 * r_t * r
+    result.trace.record(2 * per.multiply_add_count * cfg.iterations,
+                        (per.bytes_read + w_bytes) * cfg.iterations,
+                        (w_bytes + 8 * r * (c_t + r)) * cfg.iterations, tm.seconds)
     if t.trace_log is not None:
-        t.trace_log.append(("row_sum", t.path, OpTrace()))
+        # the reference's op sequence (trainers.py:270-301): row_sum, then
+        # rmm + lmm per iteration (the loss-only products are untraced)
+        t.trace_log.append(("row_sum", t.path, _op_trace(t, 1, 0.0)))
+        half = tm.seconds / (2 * cfg.iterations)
         for _ in range(cfg.iterations):
             for name in ("rmm", "lmm"):
-                t.trace_log.append((name, t.path, OpTrace()))
+                t.trace_log.append((name, t.path, _op_trace(t, r, half)))
     t.trace.merge(result.trace)
     return result
 

@@ -27,10 +27,21 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (CUDA) device")
 
 
+def pytest_collection_modifyitems(config, items):
+    """Skip gpu-marked tests on a host without a usable CUDA device."""
+    if has_gpu():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
 def golden_names():
     return sorted(os.path.basename(p)[:-4]
                   for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                  if os.path.basename(p) != "features.npz")
+                  if os.path.basename(p) != "features.npz"
+                  and not os.path.basename(p).startswith("cfg_"))
 
 
 class Golden(dict):

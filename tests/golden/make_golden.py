@@ -161,7 +161,16 @@ def ops_case(ft, seed):
     out["col_sum"] = h.col_sum().to_dense()
     out["sq_materialized"] = h.elementwise("square").materialize_target().to_dense()
     out["abs_lmm"] = h.elementwise("abs").lmm(SparseMatrix.from_dense(x)).to_dense()
+    # the rest of the registered maps (sparse.py:298-307): the mapped join and
+    # one product over the mapped table each
+    for func, scalar in EW_CASES:
+        m = h.elementwise(func, scalar)
+        out[f"ew_{func}_materialized"] = m.materialize_target().to_dense()
+        out[f"ew_{func}_lmm"] = m.lmm(SparseMatrix.from_dense(x)).to_dense()
     return out
+
+
+EW_CASES = (("scale", 2.5), ("divide", 3.0), ("expm1", None), ("logistic_centered", None))
 
 
 def trainer_case(ft, seed, models, iterations, k=3, rank=2):

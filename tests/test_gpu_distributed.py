@@ -90,10 +90,9 @@ def _worker(rank, world, port, out):
     h = fl.TargetHandle.from_arrays(ls, li, maps, plan.n_rows, c)
     cents0 = D.sharded_kmeans_seed(h, plan, r, 6, 4, dist)
     s = KMeansSession(h, 6, cents0)
-    D.run_sharded(s, 5, dist, dev)
-    s.partial(True)             # assignments of the final centroids' predecessor
+    D.run_sharded(s, 5, dist, dev)   # the last iteration writes its assignments
     cents, assign, loss = s.result(5)
-    res["kmeans"] = (cents0, plan.rows, assign)
+    res["kmeans"] = (cents0, plan.rows, assign, cents, loss)
     s.close()
     # ---- GNMF
     srcs, sels, maps, r, c = _data(seed=11)
@@ -145,18 +144,18 @@ def test_sharded_trainers_match_oracle():
     sel = np.zeros((6, r))
     sel[np.arange(6), pick] = 1.0
     for rank in range(world):
-        cents0, rows, assign = out[rank]["kmeans"]
+        cents0, rows, assign, cents, loss = out[rank]["kmeans"]
         assert np.array_equal(cents0, rops.rmm(tab, sel))
-    got = np.empty(r, dtype=np.int64)
+        cw = want["parameters"]["centroids"]
+        assert np.max(np.abs(cents - cw)) / np.max(np.abs(cw)) < TOL
+        wl = np.asarray(want["loss_history"])
+        assert np.max(np.abs(np.asarray(loss) - wl) / np.abs(wl)) < TOL
+    got = np.full(r, -1, dtype=np.int64)
     for rank in range(world):
-        _, rows, assign = out[rank]["kmeans"]
+        _, rows, assign, _, _ = out[rank]["kmeans"]
         got[rows] = assign
-    # the extra partial assigned with the final centroids: compare with the
-    # oracle's next assignment step
-    cen = want["parameters"]["centroids"]
-    sq = rops.row_sum(rops.elementwise(tab, "square"))
-    dist_ = sq - 2.0 * rops.lmm(tab, cen.T) + (cen ** 2).sum(axis=1)
-    assert np.array_equal(got, np.argmin(dist_, axis=1))
+    # the final iteration's assignments, as the reference returns them
+    assert np.array_equal(got, want["parameters"]["assignments"])
     # GNMF vs oracle with the same initial W, H
     srcs, sels, maps, r, c = _data(seed=11)
     tab = _oracle_table(srcs, sels, maps, r, c)

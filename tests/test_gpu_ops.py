@@ -66,6 +66,31 @@ def test_operators_match_reference(fl, name):
     assert rel(h.elementwise("abs").lmm(x).to_dense(), g["abs_lmm"]) < RTOL
 
 
+EW_CASES = (("scale", 2.5), ("divide", 3.0), ("expm1", None), ("logistic_centered", None),
+            ("square", None), ("abs", None))
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if n != "clusters"])
+@pytest.mark.parametrize("func,scalar", EW_CASES)
+def test_elementwise_maps_match_reference(fl, name, func, scalar):
+    """Every registered map (reference sparse.py:298-307) applied on the
+    device: the mapped join equals the reference's fp64 map rounded to fp32
+    (the device evaluates f in fp64 and stores fp32: relative 2^-24 per
+    value), and one product over the mapped table matches at RTOL."""
+    g = load_golden(name)
+    h = fl.TargetHandle.factorized(g.ft)
+    m = h.elementwise(func, scalar)
+    got = m.materialize_dense().astype(np.float64)
+    if func in ("square", "abs"):
+        want = g["sq_materialized"] if func == "square" else np.abs(g["materialized"])
+        assert np.array_equal(got, want)
+        return
+    want = g[f"ew_{func}_materialized"]
+    assert np.array_equal(got == 0, want == 0)          # f(0) = 0: structure kept
+    assert np.all(np.abs(got - want) <= 2.0 ** -24 * (1 + 1e-6) * np.abs(want))
+    assert rel(m.lmm(g["op_x"]), g[f"ew_{func}_lmm"]) < RTOL
+
+
 def test_spec_examples(fl):
     """test_factorized_ops.py:87-138: lmm(I)=T, rmm(I)=T, rmm(e_i)=row i,
     lmm(1)=rowSum, rmm(1)=colSum, tlmm(I)=T^T."""
@@ -206,14 +231,15 @@ def test_upload_paths_agree(fl, monkeypatch, chunk):
 def test_narrow_lmm_matches_generic(fl, monkeypatch, c_fact, dims):
     """The thread-per-row lmm (device-order output + gathered unpermute,
     forced on here via FL_LMM_NARROW_MIN_ROWS=0) is bit-identical to the
-    generic kernel and matches the oracle, for 1-9 and 20 operand columns
-    (more than 4 take the generic kernel)."""
+    generic kernel and matches the oracle, for 1-9, 15, 16, 20, 32 and 33
+    operand columns (1-4: thread-per-row kernel; 16-32 per chunk: the
+    warp-per-row kernel; 5-15 the generic kernel)."""
     ft = star_table(11, 70_001, dims, c_fact)
     tab = oracle.OracleTable.from_ft(ft)
     h = fl.TargetHandle.factorized(ft)
     rng = np.random.default_rng(1)
     monkeypatch.setenv("FL_LMM_NARROW_MIN_ROWS", "0")
-    for cx in (1, 2, 3, 4, 5, 6, 7, 8, 9, 20):
+    for cx in (1, 2, 3, 4, 5, 6, 7, 8, 9, 15, 16, 20, 32, 33):
         x = rng.random((ft.c_T, cx)).astype(np.float32)
         got = h.lmm(x)
         monkeypatch.setenv("FL_NO_NARROW_LMM", "1")

@@ -47,6 +47,19 @@ def test_operators_match_reference(name):
     assert rel(oracle.lmm(oracle.elementwise(tab, "abs"), g["op_x"]), g["abs_lmm"]) < 1e-12
 
 
+EW_CASES = (("scale", 2.5), ("divide", 3.0), ("expm1", None), ("logistic_centered", None))
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if n != "clusters"])
+@pytest.mark.parametrize("func,scalar", EW_CASES)
+def test_elementwise_maps_match_reference(name, func, scalar):
+    """The four maps beyond square / abs (reference sparse.py:298-307)."""
+    g = load_golden(name)
+    tab = oracle.elementwise(oracle.OracleTable.from_ft(g.ft), func, scalar)
+    assert np.array_equal(oracle.materialize(tab), g[f"ew_{func}_materialized"])
+    assert rel(oracle.lmm(tab, g["op_x"]), g[f"ew_{func}_lmm"]) < 1e-12
+
+
 def _trainer_cases():
     out = []
     for name in golden_names():
