@@ -277,7 +277,7 @@ def cpu_step_fn(wl, tab, rows):
                 r = p - y
             else:
                 r = z - y
-                _ = 0.5 * float(r.T @ r)
+                _ = 0.5 * (r.T @ r).item()
             state["w"] = state["w"] - 1e-9 * ops.transpose_lmm(tab, r)
         return step
     if model == "kmeans":
@@ -314,10 +314,14 @@ def cpu_step_fn(wl, tab, rows):
     return step
 
 
-def cpu_measure(wl, total_budget_s, n_steps, min_rows=100_000, max_rows=20_000_000):
-    """Time n_steps iterations of the oracle port on a bounded sample sized
-    to the budget; returns (seconds per iteration at the FULL workload size
-    by linear extrapolation in rows, sample description)."""
+def cpu_measure(wl, total_budget_s, n_steps, min_rows=100_000, max_rows=None, warmup=0):
+    """Time the oracle port (numpy, float64, host BLAS threads) for n_steps
+    iterations after `warmup` untimed ones.  The FULL workload is used when
+    its predicted time fits `total_budget_s` (same config, no
+    extrapolation); otherwise a row sample with the same tuple ratios sized
+    to the budget, and the per-iteration time is extrapolated linearly in
+    rows.  Returns (seconds per iteration at full size, total timed seconds
+    of the n_steps, sample description, full_scale flag)."""
     tr = wl["rows"] // wl["dims"][-1][0]
     cal = max(min_rows, 200_000)
     cal -= cal % tr
@@ -327,36 +331,122 @@ def cpu_measure(wl, total_budget_s, n_steps, min_rows=100_000, max_rows=20_000_0
     t0 = time.perf_counter()
     step()
     per_row = (time.perf_counter() - t0) / cal
-    rows = int(total_budget_s / max(n_steps, 1) / per_row)
-    rows = int(min(max(rows, min_rows), max_rows, wl["rows"]))
+    del tab, step
+    rows = int(total_budget_s / max(n_steps + warmup, 1) / per_row)
+    rows = int(min(max(rows, min_rows), max_rows or wl["rows"], wl["rows"]))
     rows -= rows % tr
+    full = rows == wl["rows"]
     tab = cpu_sample_table(wl, rows, seed=1)
     step = cpu_step_fn(wl, tab, rows)
+    for _ in range(warmup):
+        step()
     times = []
     for _ in range(n_steps):
         t0 = time.perf_counter()
         step()
         times.append(time.perf_counter() - t0)
     scale = wl["rows"] / rows
-    sample = (f"{rows} fact rows (1/{scale:g} of the workload, same tuple ratios), "
-              f"{n_steps} iterations of the oracle port (numpy, float64, host BLAS threads), "
-              "linear extrapolation in rows")
-    return float(np.median(times)) * scale, sample
+    if full:
+        sample = (f"the full workload ({rows} fact rows), {warmup} warm-up + {n_steps} timed "
+                  "iterations of the oracle port (numpy, float64, host BLAS threads)")
+    else:
+        sample = (f"{rows} fact rows (1/{scale:g} of the workload, same tuple ratios), "
+                  f"{n_steps} iterations of the oracle port (numpy, float64, host BLAS "
+                  "threads), linear extrapolation in rows")
+    return float(np.median(times)) * scale, float(sum(times)), sample, full
+
+
+def reference_package():
+    """The UNMODIFIED reference (`factorlearn`, numba kernels) installed with
+    `pip install --target baseline/_ref`; None if absent."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(p, "factorlearn")):
+        return None
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/fl_numba_cache")
+    try:
+        import factorlearn  # noqa: F401
+        from factorlearn import ops, trainers  # noqa: F401
+    except Exception:
+        return None
+    return sys.modules["factorlearn"]
+
+
+def reference_measure(wl, rows, iters, threads_list):
+    """The real reference timed on the host cores with its own bench protocol
+    (reference bench.py:136-145: one warm-up train(), then the median of 3
+    TrainResult.wall_time -- operator time only): `iters` iterations on a
+    `rows`-row sample of the workload (same tuple ratios; the full workload
+    when rows == wl["rows"]), for every thread count; iterations/s at the
+    workload size = iters / median, scaled linearly in rows for a sample."""
+    fl_ref = reference_package()
+    if fl_ref is None:
+        return None
+    from factorlearn.metadata import FactorizedTable, IndicatorMatrix, MappingMatrix
+    from factorlearn.ops import TargetHandle
+    from factorlearn.sparse import SparseMatrix
+    from factorlearn.trainers import TrainConfig, train
+    tab = cpu_sample_table(wl, rows, seed=2)
+    r_t, c_t = tab.r_T, tab.c_T
+    S, M, I = [], [], []
+    for src, sel, mst in zip(tab.sources, tab.ind_sel, tab.map_sel_t):
+        c_k = src.shape[1]
+        S.append(SparseMatrix.from_dense(src))
+        M.append(MappingMatrix(SparseMatrix.from_coo(c_t, c_k, mst, np.arange(c_k),
+                                                     np.ones(c_k))))
+        I.append(IndicatorMatrix(SparseMatrix.from_coo(r_t, src.shape[0], np.arange(r_t), sel,
+                                                       np.ones(r_t))))
+    ft = FactorizedTable(S, M, I, "inner", r_t, c_t)
+    del tab
+    rng = np.random.default_rng(3)
+    model = wl["model"]
+    y = None
+    if model == "linreg":
+        y = SparseMatrix.from_dense(rng.random((r_t, 1)))
+    elif model == "logreg":
+        y = SparseMatrix.from_dense(rng.integers(0, 2, (r_t, 1)).astype(np.float64))
+    cfg = dict(iterations=iters, learning_rate=1e-9, k_clusters=wl.get("k", 4),
+               rank=wl.get("rank", 2), seed=0)
+    per_thread = {}
+    for th in threads_list:
+        h = TargetHandle.factorized(ft, threads=th, check=False)
+        train(model, h, TrainConfig(**dict(cfg, iterations=1)), y)      # warm-up (+ JIT)
+        walls = sorted(train(model, h, TrainConfig(**cfg), y).wall_time for _ in range(3))
+        per_thread[th] = iters / walls[1] * rows / wl["rows"]
+    best = max(per_thread, key=per_thread.get)
+    full = rows == wl["rows"]
+    where = ("the full workload" if full else
+             f"a {rows}-row sample (1/{wl['rows'] / rows:g} of the fact rows, same tuple "
+             "ratios; linear extrapolation in rows)")
+    return {"value": per_thread[best], "unit": UNIT, "cores": best, "kind": "reference",
+            "sample": (f"the unmodified reference (factorlearn, numba; baseline/_ref) on {where}: "
+                       f"{iters} iterations per train(), one warm-up train() then the median "
+                       "wall_time of 3 (reference bench.py:136-145); best of threads "
+                       f"{list(threads_list)}"),
+            "per_threads": {str(k): v for k, v in per_thread.items()}}
 
 
 def run_reference(args, wl):
+    """--impl reference: the reference algorithm (oracle port, numpy float64,
+    all host BLAS threads) on the host cores, at the FULL workload size when
+    W + K iterations fit the time budget (C2: ~7.5 s per iteration on 16
+    cores), one iteration per step."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    per_iter_full, sample = cpu_measure(wl, 150.0, args.warmup + args.steps)
-    value = 1.0 / per_iter_full
+    per_iter_full, timed_s, sample, full = cpu_measure(wl, 420.0, args.steps,
+                                                       warmup=args.warmup)
+    value = args.steps / timed_s if full else 1.0 / per_iter_full
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_iter_full * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "parallelism": f"cpu x{cores} (numpy/BLAS)"},
+        "config": {"workload": wl["desc"], "fact_rows": wl["rows"],
+                   "dims": [list(d) for d in wl["dims"]], "same_config": full,
+                   "parallelism": f"cpu x{cores} (numpy/BLAS)"},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
@@ -599,14 +689,34 @@ def main():
         sess.close()
         out["e2e"] = bench_e2e_sharded(torch, fl, wl, sh, hyper, args, dist, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
-        per_iter_full, sample = cpu_measure(wl, 20.0, 3)
-        out["cpu_baseline"] = {"value": 1.0 / per_iter_full, "unit": UNIT,
-                               "cores": os.cpu_count() or 1, "kind": "port",
-                               "sample": sample}
+        out["cpu_baseline"] = cpu_baseline(wl)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def cpu_baseline(wl):
+    """The real reference on the host cores (kind "reference", bounded
+    sample: the full workload for C1, a 2M-row sample of the larger
+    configs); the oracle port when baseline/_ref is not installed."""
+    cores = os.cpu_count() or 1
+    rows = min(wl["rows"], 2_000_000 if wl["model"] in ("linreg", "logreg") else 1_000_000)
+    tr = wl["rows"] // wl["dims"][-1][0]
+    rows -= rows % tr
+    iters = 5 if rows == wl["rows"] else 2
+    try:
+        ref = reference_measure(wl, rows, iters, sorted({1, cores}))
+    except Exception as e:   # reported, never silently replaced by a GPU number
+        ref = {"error": f"{type(e).__name__}: {e}"}
+    if ref is not None and "error" not in ref:
+        return ref
+    per_iter_full, _, sample, _ = cpu_measure(wl, 20.0, 3, max_rows=20_000_000)
+    out = {"value": 1.0 / per_iter_full, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": sample}
+    if ref is not None:
+        out["reference_error"] = ref["error"]
+    return out
 
 
 def bench_materialized(torch, fl, h, y, gamma, wl, args, peak):
