@@ -530,6 +530,7 @@ def main():
     ap.add_argument("--no-materialized", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--density", type=float, default=None,
                     help="c2s: fraction of non-zero fact values (default 0.1)")
     args = ap.parse_args()
@@ -682,6 +683,10 @@ def main():
     if world == 1 and wl["model"] in ("linreg", "logreg") and not args.no_materialized:
         out["materialized"] = bench_materialized(torch, fl, h, sh["y"], hyper["learning_rate"],
                                                  wl, args, peak)
+    if world == 1 and not args.no_parity:
+        sess.close()
+        out["parity"] = bench_parity(torch, fl, wl, sh, h, hyper,
+                                     {"gnmf": 2}.get(wl["model"], 3))
     if world == 1 and not args.no_e2e and wl["model"] in ("linreg", "logreg", "kmeans"):
         sess.close()
         out["e2e"] = bench_e2e(torch, fl, wl, sh, hyper, args)
@@ -694,6 +699,85 @@ def main():
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def bench_parity(torch, fl, wl, sh, h, hyper, iters):
+    """Parity on the bench's OWN arrays: `iters` iterations of a fresh session
+    on the timed handle vs the oracle port (float64 numpy restatement of the
+    reference, pinned to the reference's goldens) on the same inputs copied
+    to the host.  Tolerance: the north star's 1e-4 relative; K-means
+    assignments must be identical."""
+    import oracle
+    from oracle import reference_ops as rops
+    from oracle import reference_trainers as rt
+    from paper_2502_01985_b200.trainers import GlmSession, GnmfSession, KMeansSession
+    t0 = time.perf_counter()
+    maps, c_t = col_maps(wl)
+    rows = sh["rows"]
+    srcs = [sh["fact"].cpu().numpy().astype(np.float64)] + \
+        [d.cpu().numpy().astype(np.float64) for d in sh["dims"]]
+    sels = [np.arange(rows, dtype=np.int64)] + [f.cpu().numpy().astype(np.int64)
+                                                for f in sh["fks"]]
+    tab = oracle.OracleTable(srcs, sels, [m.astype(np.int64) for m in maps], rows, c_t)
+
+    def mrel(a, b):
+        a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+        return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+    out = {"iterations": iters, "tolerance": 1e-4, "against": "oracle port, same arrays"}
+    model = wl["model"]
+    if model in ("linreg", "logreg"):
+        s = GlmSession(h, model, sh["y"], hyper["learning_rate"])
+        s.run(iters)
+        w, losses = s.result(iters)
+        s.close()
+        y = sh["y"].cpu().numpy().astype(np.float64)
+        want = rt.train(model, tab, iterations=iters, learning_rate=hyper["learning_rate"], y=y)
+        out["w_max_rel"] = mrel(w, want["parameters"]["w"].ravel())
+        out["loss_max_rel"] = mrel(losses, want["loss_history"])
+        out["ok"] = out["w_max_rel"] < 1e-4 and out["loss_max_rel"] < 1e-4
+    elif model == "kmeans":
+        k = wl["k"]
+        want = rt.kmeans(tab, iters, k, 0)
+        pick = np.sort(np.random.default_rng(0).choice(rows, size=k, replace=False))
+        sel = np.zeros((k, rows))
+        sel[np.arange(k), pick] = 1.0
+        s = KMeansSession(h, k, rops.rmm(tab, sel))
+        s.run(iters)
+        cents, assign, losses = s.result(iters)
+        s.close()
+        out["assign_mismatches"] = int(np.sum(assign != want["parameters"]["assignments"]))
+        out["centroids_max_rel"] = mrel(cents, want["parameters"]["centroids"])
+        out["loss_max_rel"] = mrel(losses, want["loss_history"])
+        out["ok"] = (out["assign_mismatches"] == 0 and out["centroids_max_rel"] < 1e-4
+                     and out["loss_max_rel"] < 1e-4)
+    else:
+        R = wl["rank"]
+        rng = np.random.default_rng(5)
+        w = rng.random((rows, R)) * 0.5
+        hh = rng.random((R, c_t)) * 0.5
+        t_sq = float(rops.row_sum(rops.elementwise(tab, "square")).sum())
+        s = GnmfSession(h, R, w, hh, t_sq)
+        s.run(iters)
+        W, H, losses = s.result(iters)
+        s.close()
+        want = []
+        for it in range(iters):        # reference trainers.py:284-301
+            p = rops.rmm(tab, w.T)
+            if it > 0:
+                want.append(t_sq - 2 * float((p * hh).sum())
+                            + float((w.T @ w * (hh @ hh.T)).sum()))
+            hh = hh * p / (w.T @ w @ hh + 1e-12)
+            q = rops.lmm(tab, hh.T)
+            w = w * q / (w @ (hh @ hh.T) + 1e-12)
+        p = rops.rmm(tab, w.T)
+        want.append(t_sq - 2 * float((p * hh).sum()) + float((w.T @ w * (hh @ hh.T)).sum()))
+        out["w_max_rel"] = mrel(W, w)
+        out["h_max_rel"] = mrel(H, hh)
+        out["loss_max_rel"] = mrel(losses, want)
+        out["ok"] = max(out["w_max_rel"], out["h_max_rel"], out["loss_max_rel"]) < 1e-4
+    out["seconds"] = time.perf_counter() - t0
+    return out
 
 
 def cpu_baseline(wl):
