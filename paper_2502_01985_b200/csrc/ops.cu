@@ -745,30 +745,4 @@ int fl_col_sum(fl_table* t, double* out, void* stream) {
   return finish_out(out, od, oo, (size_t)t->c_T, s);
 }
 
-int fl_crossprod(fl_table* t, double* out, void* stream) {
-  FL_REQUIRE_TABLE(t);
-  cudaStream_t s = (cudaStream_t)stream;
-  // T^T T: materialize in row panels and reuse the strided tlmm (panel of
-  // target columns as y).  O(r_T c_T^2) -- a reference-free extra operator.
-  const int64_t r_T = t->r_T;
-  const int c_T = t->c_T;
-  float* mat;
-  FL_CUDA(cudaMallocAsync((void**)&mat, (size_t)r_T * c_T * 4 + 16, s));
-  int rc = fl_materialize(t, mat, stream);
-  if (rc) return rc;
-  double* od;
-  bool oo;
-  rc = out_buffer(out, (size_t)c_T * c_T, s, &od, &oo);
-  if (rc) return rc;
-  FL_CUDA(cudaMemsetAsync(od, 0, (size_t)c_T * c_T * 8, s));
-  for (int c0 = 0; c0 < c_T; c0 += 32) {
-    int nc = std::min(32, c_T - c0);
-    // y'(t, col) = mat[t, c0 + col]; out[tc, c0 + col]
-    rc = do_tlmm(t, YView{mat + c0, c_T, 1}, nc, od + c0, c_T, 1, s);
-    if (rc) return rc;
-  }
-  FL_CUDA(cudaFreeAsync(mat, s));
-  return finish_out(out, od, oo, (size_t)c_T * c_T, s);
-}
-
 }  // extern "C"

@@ -128,11 +128,33 @@ def test_materialized_handle_matches(fl):
     assert rel(mh.rmm(g["op_w"]), g["rmm"]) < RTOL
 
 
-def test_crossprod(fl):
-    g = load_golden("star3")
+@pytest.mark.parametrize("name", golden_names())
+def test_crossprod_matches_dense(fl, name):
+    """Factorized T^T T (no materialization: F^T F, S_d^T diag(n_d) S_d and
+    S_d^T (I_d^T [F | I_e S_e]) blocks) against the dense product of the
+    reference's materialized join, for every golden table (inner / left /
+    outer joins, unions, 2-3 sources)."""
+    g = load_golden(name)
     h = fl.TargetHandle.factorized(g.ft)
     td = g["materialized"]
-    assert rel(h.crossprod(), td.T @ td) < RTOL
+    got = h.crossprod()
+    assert got.shape == (td.shape[1], td.shape[1])
+    assert rel(got, td.T @ td) < RTOL
+    assert np.allclose(got, got.T, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("dims,c_fact", [([(1000, 50)], 20), ([(300, 9), (40, 5)], 7),
+                                         ([(997, 37), (13, 3)], 29), ([], 45),
+                                         ([(50 + i, 2 + i) for i in range(10)], 6)])
+def test_crossprod_random_star_vs_oracle(fl, dims, c_fact):
+    """Wide tables (several 32-column output tiles), more gathered sources
+    than one grouped pass takes (10 > 8), and a fact-only table."""
+    ft = star_table(17, 50_003, dims, c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    td = oracle.materialize(tab)
+    h = fl.TargetHandle.factorized(ft)
+    got = h.crossprod()
+    assert rel(got, td.T @ td) < RTOL
 
 
 def test_shape_errors(fl):

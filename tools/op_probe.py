@@ -74,8 +74,38 @@ def wide(wl_name="c2"):
               f"rmm {timed(lambda: h.rmm(w, traced=False), 3):.2f} ms", flush=True)
 
 
+def crossprod(wl_name="c2"):
+    """Factorized T^T T at a workload's size: CUDA-event time (median of 5)
+    and the check against the dense product of the device-joined T
+    (fp64 torch matmul over 10M-row chunks)."""
+    wl = bench.WORKLOADS[wl_name]
+    dev = torch.device("cuda")
+    sh = bench.make_shard(torch, wl, 0, 1, dev)
+    h = bench.build_handle(fl, wl, sh)
+    del sh
+    torch.cuda.empty_cache()
+    r, c = h.shape
+    t_cp = timed(lambda: h.crossprod(traced=False), 5)
+    got = torch.as_tensor(h.crossprod(traced=False), device=dev)
+    T = torch.empty((r, c), device=dev, dtype=torch.float32)
+    h.materialize_dense(out=T)
+    want = torch.zeros((c, c), device=dev, dtype=torch.float64)
+    for r0 in range(0, r, 10_000_000):
+        blk = T[r0:r0 + 10_000_000].double()
+        want += blk.T @ blk
+    del T, blk
+    torch.cuda.empty_cache()
+    err = float((got - want).norm() / want.norm())
+    print(f"crossprod {wl_name}: rows {r} cols {c}: {t_cp:.3f} ms, rel err vs dense "
+          f"{err:.2e}", flush=True)
+
+
 if __name__ == "__main__":
-    if "--wide" in sys.argv:
+    if "--crossprod" in sys.argv:
+        sys.argv.remove("--crossprod")
+        for w in (sys.argv[1:] or ["c2", "c3"]):
+            crossprod(w)
+    elif "--wide" in sys.argv:
         sys.argv.remove("--wide")
         wide(sys.argv[1] if len(sys.argv) > 1 else "c2")
     else:
