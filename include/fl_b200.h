@@ -175,6 +175,10 @@ int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* l
  * without a conversion pass */
 int fl_kmeans_assignments64(fl_kmeans* s, int64_t* assign, void* stream);
 int fl_kmeans_destroy(fl_kmeans* s);
+/* which pass the session runs: 0 fused mma.sync, 1 fused tcgen05, 2 width-
+ * general (any k, width or number of sources; generic operators plus row
+ * kernels -- the composition of reference trainers.py:223-241) */
+int fl_kmeans_path(fl_kmeans* s, int32_t* path);
 
 /* ---- Gaussian NMF, multiplicative updates (trainers.py:256-307) ----------
  * w0: r_T x rank fp64 (target order), h0: rank x c_T fp64. */
@@ -193,6 +197,10 @@ int fl_gnmf_reduce_buffer(fl_gnmf* s, double** buf, int32_t* len);
 int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n,
                    int32_t* n_done, void* stream);
 int fl_gnmf_destroy(fl_gnmf* s);
+/* 0 fused mma.sync, 1 fused tcgen05, 2 width-general (any rank / width /
+ * number of sources; reference trainers.py:282-299 over the generic
+ * operators) */
+int fl_gnmf_path(fl_gnmf* s, int32_t* path);
 
 /* ---- diagnostics ---------------------------------------------------------
  * Known-answer test of the tcgen05 (5th-gen tensor core) operand layouts:

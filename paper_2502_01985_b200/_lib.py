@@ -84,6 +84,7 @@ SIGNATURES = {
     "fl_kmeans_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_kmeans_assignments64": [_P, _P, _P],
     "fl_kmeans_destroy": [_P],
+    "fl_kmeans_path": [_P, C.POINTER(_I32)],
     "fl_glm_path": [_P, C.POINTER(_I32), C.POINTER(_D)],
     "fl_gnmf_create": [_P, _I32, _P, _P, _D, _PP, _P],
     "fl_gnmf_run": [_P, _I32, _P],
@@ -92,6 +93,7 @@ SIGNATURES = {
     "fl_gnmf_reduce_buffer": [_P, C.POINTER(C.c_void_p), C.POINTER(_I32)],
     "fl_gnmf_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_gnmf_destroy": [_P],
+    "fl_gnmf_path": [_P, C.POINTER(_I32)],
     "fl_tc_selftest": [_I32, _P, _P, _P, _I32, _I32, _P],
 }
 

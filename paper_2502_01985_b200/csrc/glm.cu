@@ -925,11 +925,8 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     set_error("learning_rate must be > 0");
     return FL_ERR_CONFIG;
   }
-  if ((int)t->g.size() > MAX_GATHER) {
-    set_error("GLM supports <= %d gathered sources", MAX_GATHER);
-    return FL_ERR_OP;
-  }
-  bool wide = t->pf > 252;
+  // more than MAX_GATHER gathered sources: the width-general path below
+  bool wide = t->pf > 252 || (int)t->g.size() > MAX_GATHER;
   for (auto& g : t->g) wide |= (size_t)TILE * g.pitch * 4 * 2 > 200 * 1024;
   {
     const int yb0 = model == FL_MODEL_LOGREG ? 1 : 4;

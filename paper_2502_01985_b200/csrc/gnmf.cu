@@ -29,6 +29,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "generic.h"
 #include "mma_tf32.cuh"
 #include "reduce.cuh"
 #include "tc05.cuh"
@@ -809,6 +810,7 @@ struct fl_gnmf {
   bool primed = false;
   cudaGraphExec_t graph = nullptr;
   cudaStream_t cap_stream = nullptr;
+  GnGen* gen = nullptr;   // width-general session (generic.cu) when the fused pass does not apply
 };
 
 namespace flb {
@@ -855,8 +857,8 @@ static int gn_h(fl_gnmf* s, cudaStream_t st, bool update, bool loss) {
 
 extern "C" {
 
-int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0, double t_sq,
-                   fl_gnmf** out, void* stream) {
+static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const double* h0,
+                           double t_sq, fl_gnmf** out, void* stream) {
   if (!t || !t->finalized || !w0 || !h0 || !out) {
     set_error("fl_gnmf_create: bad arguments");
     return FL_ERR_ARG;
@@ -1143,12 +1145,51 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   return FL_OK;
 }
 
+// The fused pass when it applies (rank <= 32, streamed pitch <= 60, <= 8
+// gathered sources, dimension widths within its tiles); every other shape --
+// or FL_GN_GENERIC=1 -- runs the width-general session of generic.cu.
+int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0, double t_sq,
+                   fl_gnmf** out, void* stream) {
+  const char* fg = getenv("FL_GN_GENERIC");
+  const bool force = fg && atoi(fg) != 0;
+  if (!force) {
+    const int rc = gn_create_fused(t, rank, w0, h0, t_sq, out, stream);
+    if (rc != FL_ERR_OP) return rc;
+  }
+  if (!t || !t->finalized || !w0 || !h0 || !out) {
+    set_error("fl_gnmf_create: bad arguments");
+    return FL_ERR_ARG;
+  }
+  if (rank < 1 || rank > std::min<int64_t>(t->r_T, t->c_T)) {
+    set_error("rank = %d exceeds min(shape) = %lld", rank,
+              (long long)std::min<int64_t>(t->r_T, t->c_T));
+    return FL_ERR_CONFIG;
+  }
+  FL_CUDA(cudaSetDevice(t->device));
+  auto* s = new fl_gnmf();
+  std::unique_ptr<fl_gnmf> guard(s);
+  s->t = t;
+  s->rank = rank;
+  s->R = rank;
+  const int rc = gng_create(t, rank, w0, h0, t_sq, (cudaStream_t)stream, &s->gen);
+  if (rc) return rc;
+  *out = guard.release();
+  return FL_OK;
+}
+
+int fl_gnmf_path(fl_gnmf* s, int32_t* path) {
+  if (!s || !path) return FL_ERR_ARG;
+  *path = s->gen ? 2 : s->tc ? 1 : 0;
+  return FL_OK;
+}
+
 int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
   if (!s || iterations < 1) {
     set_error("iterations must be >= 1");
     return FL_ERR_CONFIG;
   }
   FL_CUDA(cudaSetDevice(s->t->device));
+  if (s->gen) return gng_run(s->gen, iterations, (cudaStream_t)stream);
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   if (!s->primed) {   // P_0 = W_0^T T, G_0 = W_0^T W_0
@@ -1185,12 +1226,29 @@ int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
 }
 
 int fl_gnmf_kernel_times(fl_gnmf* s, int32_t iters, float* ms_out, void* stream) {
-  if (!s || iters < 1 || !ms_out || !s->primed) {
+  if (!s || iters < 1 || !ms_out || (!s->primed && !s->gen)) {
     set_error("fl_gnmf_kernel_times: run at least one iteration first");
     return FL_ERR_ARG;
   }
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->gen) {   // one slot: the whole width-general iteration
+    cudaEvent_t e0, e1;
+    FL_CUDA(cudaEventCreate(&e0));
+    FL_CUDA(cudaEventCreate(&e1));
+    FL_CUDA(cudaEventRecord(e0, st));
+    const int rc = gng_run(s->gen, iters, st);
+    if (rc) return rc;
+    FL_CUDA(cudaEventRecord(e1, st));
+    FL_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FL_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int j = 0; j < 5; j++) ms_out[j] = 0.f;
+    ms_out[2] = ms / iters;
+    return FL_OK;
+  }
   cudaEvent_t ev[6];
   for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
   float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1232,6 +1290,7 @@ int fl_gnmf_partial(fl_gnmf* s, void* stream) {
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->gen) return gng_partial(s->gen, st);
   int rc;
   if (!s->primed) {   // products of W_0 only
     if ((rc = gn_h(s, st, false, false))) return rc;
@@ -1247,6 +1306,12 @@ int fl_gnmf_partial(fl_gnmf* s, void* stream) {
 
 int fl_gnmf_reduce_buffer(fl_gnmf* s, double** buf, int32_t* len) {
   if (!s || !buf || !len) return FL_ERR_ARG;
+  if (s->gen) {
+    int n = 0;
+    *buf = gng_red(s->gen, &n);
+    *len = n;
+    return FL_OK;
+  }
   *buf = s->red.as<double>();
   *len = s->R * s->t->c_T + s->R * s->R;
   return FL_OK;
@@ -1257,6 +1322,12 @@ int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n, in
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->gen) {
+    int nd = 0;
+    const int rc = gng_result(s->gen, w, h, loss, n, &nd, st);
+    if (n_done) *n_done = nd;
+    return rc;
+  }
   GnState hs{};
   FL_CUDA(cudaMemcpyAsync(&hs, s->state.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
@@ -1294,6 +1365,7 @@ int fl_gnmf_destroy(fl_gnmf* s) {
   cudaSetDevice(s->t->device);
   if (s->graph) cudaGraphExecDestroy(s->graph);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->gen) gng_destroy(s->gen);
   delete s;
   return FL_OK;
 }

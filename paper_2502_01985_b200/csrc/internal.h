@@ -185,8 +185,9 @@ struct YView {
 // generic operators (ops.cu), device operands, stream-ordered:
 //   out (r_T x c_x, target order) = T x;   out[tcol*os_t + col*os_c] += (T^T y)
 int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s);
+//   dev_order: y rows are in device order already (no perm gather)
 int do_tlmm(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
-            cudaStream_t s);
+            cudaStream_t s, bool dev_order = false);
 int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target,
                                        void* dst_dev, int elem_bytes, cudaStream_t s);
 int device_sm_count(int device);

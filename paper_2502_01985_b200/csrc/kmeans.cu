@@ -31,6 +31,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "generic.h"
 #include "mma_tf32.cuh"
 #include "reduce.cuh"
 #include "tc05.cuh"
@@ -841,6 +842,7 @@ struct fl_kmeans {
   int loss_cap = 1 << 16;
   cudaGraphExec_t graph = nullptr, graph_assign = nullptr;
   cudaStream_t cap_stream = nullptr;
+  KmGen* gen = nullptr;   // width-general session (generic.cu) when the fused pass does not apply
 };
 
 namespace flb {
@@ -899,8 +901,8 @@ static int km_graph(fl_kmeans* s, bool write_assign, cudaGraphExec_t* out) {
 
 extern "C" {
 
-int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans** out,
-                     void* stream) {
+static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_kmeans** out,
+                           void* stream) {
   if (!t || !t->finalized || !centroids0 || !out) {
     set_error("fl_kmeans_create: bad arguments");
     return FL_ERR_ARG;
@@ -1203,14 +1205,57 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   return FL_OK;
 }
 
+// The fused pass when it applies (k <= 32, streamed pitch <= 124, <= 8
+// gathered sources, dimension widths within its tiles); every other shape --
+// or FL_KM_GENERIC=1 -- runs the width-general session of generic.cu.
+int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans** out,
+                     void* stream) {
+  const char* fg = getenv("FL_KM_GENERIC");
+  const bool force = fg && atoi(fg) != 0;
+  if (!force) {
+    const int rc = km_create_fused(t, k, centroids0, out, stream);
+    if (rc != FL_ERR_OP) return rc;
+  }
+  if (!t || !t->finalized || !centroids0 || !out) {
+    set_error("fl_kmeans_create: bad arguments");
+    return FL_ERR_ARG;
+  }
+  if (k < 1 || k > t->r_T) {
+    set_error("k_clusters = %d exceeds row count %lld", k, (long long)t->r_T);
+    return FL_ERR_CONFIG;
+  }
+  FL_CUDA(cudaSetDevice(t->device));
+  auto* s = new fl_kmeans();
+  std::unique_ptr<fl_kmeans> guard(s);
+  s->t = t;
+  s->k = k;
+  const int rc = kmg_create(t, k, centroids0, (cudaStream_t)stream, &s->gen);
+  if (rc) return rc;
+  *out = guard.release();
+  return FL_OK;
+}
+
+int fl_kmeans_path(fl_kmeans* s, int32_t* path) {
+  if (!s || !path) return FL_ERR_ARG;
+  *path = s->gen ? 2 : s->tc ? 1 : 0;
+  return FL_OK;
+}
+
 int fl_kmeans_partial(fl_kmeans* s, int32_t write_assign, void* stream) {
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
+  if (s->gen) return kmg_partial(s->gen, (cudaStream_t)stream);
   return km_launch_iteration(s, (cudaStream_t)stream, false, write_assign != 0);
 }
 
 int fl_kmeans_reduce_buffer(fl_kmeans* s, double** buf, int32_t* len) {
   if (!s || !buf || !len) return FL_ERR_ARG;
+  if (s->gen) {
+    int n = 0;
+    *buf = kmg_red(s->gen, &n);
+    *len = n;
+    return FL_OK;
+  }
   *buf = s->red.as<double>();
   *len = s->k * s->t->c_T + s->k + 1;
   return FL_OK;
@@ -1219,6 +1264,7 @@ int fl_kmeans_reduce_buffer(fl_kmeans* s, double** buf, int32_t* len) {
 int fl_kmeans_update(fl_kmeans* s, void* stream) {
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
+  if (s->gen) return kmg_update(s->gen, (cudaStream_t)stream);
   k_km_update<<<1, 256, 0, (cudaStream_t)stream>>>(s->ua);
   FL_CHECK_LAUNCH();
   return FL_OK;
@@ -1230,6 +1276,7 @@ int fl_kmeans_run(fl_kmeans* s, int32_t iterations, void* stream) {
     return FL_ERR_CONFIG;
   }
   FL_CUDA(cudaSetDevice(s->t->device));
+  if (s->gen) return kmg_run(s->gen, iterations, (cudaStream_t)stream);
   int rc = km_graph(s, false, &s->graph);
   if (rc) return rc;
   rc = km_graph(s, true, &s->graph_assign);
@@ -1244,6 +1291,25 @@ int fl_kmeans_kernel_times(fl_kmeans* s, int32_t iters, float* ms_out, void* str
   if (!s || iters < 1 || !ms_out) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->gen) {   // one slot: the whole width-general iteration
+    cudaEvent_t e0, e1;
+    FL_CUDA(cudaEventCreate(&e0));
+    FL_CUDA(cudaEventCreate(&e1));
+    FL_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; i++) {
+      const int rc = kmg_partial(s->gen, st);
+      if (rc) return rc;
+    }
+    FL_CUDA(cudaEventRecord(e1, st));
+    FL_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FL_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ms_out[0] = ms_out[2] = ms_out[3] = 0.f;
+    ms_out[1] = ms / iters;
+    return FL_OK;
+  }
   cudaEvent_t ev[5];
   for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1283,6 +1349,12 @@ int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* l
   if (!s) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->gen) {
+    int nd = 0;
+    const int rc = kmg_result(s->gen, centroids, assign, nullptr, loss, n, &nd, st);
+    if (n_done) *n_done = nd;
+    return rc;
+  }
   KmState h{};
   FL_CUDA(cudaMemcpyAsync(&h, s->state.p, sizeof(h), cudaMemcpyDeviceToHost, st));
   if (centroids)
@@ -1311,6 +1383,7 @@ int fl_kmeans_assignments64(fl_kmeans* s, int64_t* assign, void* stream) {
   if (!s || !assign) return FL_ERR_ARG;
   FL_CUDA(cudaSetDevice(s->t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (s->gen) return kmg_result(s->gen, nullptr, nullptr, assign, nullptr, 0, nullptr, st);
   int64_t* tmp = nullptr;
   FL_CUDA(cudaMallocAsync((void**)&tmp, (size_t)s->t->r_T * 8 + 16, st));
   k_km_assign_to_target64<<<(unsigned)ceil_div(s->t->r_T, 256), 256, 0, st>>>(
@@ -1328,6 +1401,7 @@ int fl_kmeans_destroy(fl_kmeans* s) {
   if (s->graph) cudaGraphExecDestroy(s->graph);
   if (s->graph_assign) cudaGraphExecDestroy(s->graph_assign);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->gen) kmg_destroy(s->gen);
   delete s;
   return FL_OK;
 }

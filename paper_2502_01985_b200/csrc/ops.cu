@@ -48,7 +48,7 @@ __global__ void k_dim_q(const float* __restrict__ S, int pitch, int cols, int64_
 __global__ void k_lmm_main(const float* __restrict__ F, int pf, const int32_t* __restrict__ ftcol,
                            const float* __restrict__ x, int c_x, int col0, int ncol,
                            GatherSet gs, const int32_t* __restrict__ perm, int64_t r_T,
-                           float* __restrict__ out) {
+                           float* __restrict__ out, int accum) {
   extern __shared__ float xf[];  // pf x ncol
   for (int i = threadIdx.x; i < pf * ncol; i += blockDim.x) {
     int j = i / ncol, col = i - j * ncol;
@@ -69,7 +69,8 @@ __global__ void k_lmm_main(const float* __restrict__ F, int pf, const int32_t* _
     int32_t fk = gs.fk[d][p];
     if (fk >= 0) acc += gs.q[d][(int64_t)fk * ncol + col];
   }
-  out[(int64_t)perm[p] * c_x + col0 + col] = acc;
+  float* o = out + (int64_t)perm[p] * c_x + col0 + col;
+  *o = accum ? *o + acc : acc;   // accum: a further group of gathered sources
 }
 
 // Narrow T x (stream block of C4 float4 per row, NC <= 2 operand columns): a
@@ -437,11 +438,44 @@ int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target
 }
 
 // ---------------------------------------------------------------------------
-int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s) {
-  if ((int)t->g.size() > MAX_GATHER) {
-    set_error("lmm: at most %d gathered sources supported", MAX_GATHER);
-    return FL_ERR_OP;
+// More than MAX_GATHER gathered sources: the first group of MAX_GATHER rides
+// the stream pass, every further group adds its gathered rows in another
+// pass (same fp32 order per group; SURVEY.md a10 -- the reference takes any
+// number of sources, ops.py:227-233)
+static int do_lmm_many(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s) {
+  const int ng = (int)t->g.size();
+  for (int col0 = 0; col0 < c_x; col0 += CX_CHUNK) {
+    const int ncol = std::min(CX_CHUNK, c_x - col0);
+    for (int d0 = 0; d0 < ng; d0 += MAX_GATHER) {
+      GatherSet gs{};
+      gs.n = std::min(MAX_GATHER, ng - d0);
+      std::vector<float*> qs;
+      for (int d = 0; d < gs.n; d++) {
+        const GatherSrc& g = t->g[d0 + d];
+        float* q = nullptr;
+        FL_CUDA(cudaMallocAsync((void**)&q, g.rows * ncol * 4 + 16, s));
+        qs.push_back(q);
+        k_dim_q<<<gridn(g.rows * ncol), 256, (size_t)g.cols * ncol * 4, s>>>(
+            g.S->as<float>(), g.pitch, g.cols, g.rows, g.d_tcol->as<int32_t>(), x_dev, c_x, col0,
+            ncol, q);
+        FL_CHECK_LAUNCH();
+        gs.q[d] = q;
+        gs.fk[d] = g.fk->as<int32_t>();
+      }
+      const bool first = d0 == 0;
+      const int pf = first ? t->pf : 0;
+      k_lmm_main<<<gridn(t->r_T * ncol), 256, (size_t)pf * ncol * 4, s>>>(
+          pf ? t->F->as<float>() : nullptr, pf, pf ? t->d_f_tcol->as<int32_t>() : nullptr, x_dev,
+          c_x, col0, ncol, gs, t->perm->as<int32_t>(), t->r_T, out_dev, first ? 0 : 1);
+      FL_CHECK_LAUNCH();
+      for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
+    }
   }
+  return FL_OK;
+}
+
+int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_t s) {
+  if ((int)t->g.size() > MAX_GATHER) return do_lmm_many(t, x_dev, c_x, out_dev, s);
   for (int col0 = 0; col0 < c_x; col0 += CX_CHUNK) {
     int ncol = std::min(CX_CHUNK, c_x - col0);
     GatherSet gs{};
@@ -504,7 +538,7 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
       size_t sm = (size_t)t->pf * ncol * 4;
       k_lmm_main<<<gridn(t->r_T * ncol), 256, sm, s>>>(
           F, t->pf, t->pf ? t->d_f_tcol->as<int32_t>() : nullptr, x_dev, c_x, col0, ncol, gs,
-          t->perm->as<int32_t>(), t->r_T, out_dev);
+          t->perm->as<int32_t>(), t->r_T, out_dev, 0);
     }
     FL_CHECK_LAUNCH();
     for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
@@ -514,7 +548,7 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
 
 // generic T^T y with strided y view and strided fp64 output
 int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool dev_order) {
   const int sms = t->sm_count;
   if (cy > 1 && yv_in.sc > yv_in.sr && t->r_T > 0 && !getenv("FL_NO_VIEW_ROWS")) {
     // Column-strided y (rmm: x^T of a k x r_T row-major x).  Every device-
@@ -528,7 +562,7 @@ int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t
       const int w = std::min(VW, cy - c0);
       k_view_rows<<<gridn(t->r_T), 256, 0, s>>>(yv_in, t->r_T, c0, w, tmp);
       FL_CHECK_LAUNCH();
-      const int rc = do_tlmm(t, YView{tmp, w, 1}, w, out + c0 * os_c, os_t, os_c, s);
+      const int rc = do_tlmm(t, YView{tmp, w, 1}, w, out + c0 * os_c, os_t, os_c, s, dev_order);
       if (rc) return rc;
     }
     FL_CUDA(cudaFreeAsync(tmp, s));
@@ -540,7 +574,7 @@ int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t
     for (int c0 = 0; c0 < cy; c0 += 8) {
       const int w = std::min(8, cy - c0);
       const int rc = do_tlmm(t, YView{yv_in.base + (int64_t)c0 * yv_in.sc, yv_in.sr, yv_in.sc}, w,
-                             out + c0 * os_c, os_t, os_c, s);
+                             out + c0 * os_c, os_t, os_c, s, dev_order);
       if (rc) return rc;
     }
     return FL_OK;
@@ -549,9 +583,10 @@ int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t
   // gather it once (bit-identical values; perm == nullptr means "already in
   // device order" to the kernels below).
   YView yv = yv_in;
-  const int32_t* yperm = t->perm->as<int32_t>();
+  // dev_order: y is already in device row order (trainer-internal operands)
+  const int32_t* yperm = dev_order ? nullptr : t->perm->as<int32_t>();
   float* ydev = nullptr;
-  if (!t->g.empty() && t->r_T > 0 && !getenv("FL_NO_Y_DEVORDER")) {
+  if (!dev_order && !t->g.empty() && t->r_T > 0 && !getenv("FL_NO_Y_DEVORDER")) {
     FL_CUDA(cudaMallocAsync((void**)&ydev, t->r_T * cy * 4 + 16, s));
     k_gather_y_dev<<<gridn(t->r_T * cy), 256, 0, s>>>(yv_in, yperm, t->r_T, cy, ydev);
     FL_CHECK_LAUNCH();

@@ -338,6 +338,14 @@ class KMeansSession:
         _lib.call("fl_kmeans_reduce_buffer", self.ptr, C.byref(buf), C.byref(n))
         return buf.value, n.value
 
+    @property
+    def path(self) -> str:
+        """"fused" (mma.sync pass), "tcgen05" or "generic" (width-general
+        session: any k, width or number of gathered sources)."""
+        p = C.c_int32()
+        _lib.call("fl_kmeans_path", self.ptr, C.byref(p))
+        return ("fused", "tcgen05", "generic")[p.value]
+
     def kernel_times(self, iters: int, stream=None) -> list[float]:
         """Mean ms of [dim E, fact pass, dim sums, reduce + update]."""
         out = (C.c_float * 4)()
@@ -516,6 +524,14 @@ class GnmfSession:
         n = C.c_int32()
         _lib.call("fl_gnmf_reduce_buffer", self.ptr, C.byref(buf), C.byref(n))
         return buf.value, n.value
+
+    @property
+    def path(self) -> str:
+        """"fused" (mma.sync pass), "tcgen05" or "generic" (width-general
+        session: any rank, width or number of gathered sources)."""
+        p = C.c_int32()
+        _lib.call("fl_gnmf_path", self.ptr, C.byref(p))
+        return ("fused", "tcgen05", "generic")[p.value]
 
     def kernel_times(self, iters: int, stream=None) -> list[float]:
         """Mean ms of [H update, dim G, fact pass, dim P, reduce]."""
