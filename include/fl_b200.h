@@ -56,6 +56,7 @@ typedef struct fl_table fl_table;
 typedef struct fl_glm fl_glm;
 typedef struct fl_kmeans fl_kmeans;
 typedef struct fl_gnmf fl_gnmf;
+typedef struct fl_comm fl_comm;
 
 const char* fl_last_error(void);
 int fl_version(void);
@@ -201,6 +202,23 @@ int fl_gnmf_destroy(fl_gnmf* s);
  * number of sources; reference trainers.py:282-299 over the generic
  * operators) */
 int fl_gnmf_path(fl_gnmf* s, int32_t* path);
+
+/* ---- sharded sessions over NCCL (no reference counterpart:
+ * the reference is single-process) -----------------------------------------
+ * Rank 0 draws the id (fl_comm_unique_id), every rank receives it over the
+ * host-side process group and calls fl_comm_init.  NCCL is loaded at run
+ * time (the copy torch loaded, else libnccl.so.2; FL_NCCL_LIB overrides).
+ * With a communicator attached, fl_{glm,kmeans,gnmf}_run() executes
+ * partial -> in-place ncclAllReduce(sum) of the reduce buffer -> update per
+ * iteration, captured in CUDA graphs on the session's stream. */
+int fl_comm_unique_id(uint8_t* out, int32_t len);   /* len >= 128 */
+int fl_comm_init(const uint8_t* id, int32_t len, int32_t nranks, int32_t rank, int32_t device,
+                 fl_comm** out);
+int fl_comm_allreduce(fl_comm* c, double* buf, int64_t n, void* stream);
+int fl_comm_destroy(fl_comm* c);
+int fl_glm_set_comm(fl_glm* s, fl_comm* c);      /* c = NULL: back to single-GPU */
+int fl_kmeans_set_comm(fl_kmeans* s, fl_comm* c);
+int fl_gnmf_set_comm(fl_gnmf* s, fl_comm* c);
 
 /* ---- diagnostics ---------------------------------------------------------
  * Known-answer test of the tcgen05 (5th-gen tensor core) operand layouts:

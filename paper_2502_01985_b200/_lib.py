@@ -94,6 +94,13 @@ SIGNATURES = {
     "fl_gnmf_result": [_P, _P, _P, _P, _I32, C.POINTER(_I32), _P],
     "fl_gnmf_destroy": [_P],
     "fl_gnmf_path": [_P, C.POINTER(_I32)],
+    "fl_comm_unique_id": [_P, _I32],
+    "fl_comm_init": [_P, _I32, _I32, _I32, _I32, _PP],
+    "fl_comm_allreduce": [_P, _P, C.c_int64, _P],
+    "fl_comm_destroy": [_P],
+    "fl_glm_set_comm": [_P, _P],
+    "fl_kmeans_set_comm": [_P, _P],
+    "fl_gnmf_set_comm": [_P, _P],
     "fl_tc_selftest": [_I32, _P, _P, _P, _I32, _I32, _P],
 }
 

@@ -197,7 +197,10 @@ struct KmGen {
   int loss_cap = 1 << 16;
   DevBuf C64, C32, cF, E, gsrc, onehot, counts, lpart, red, loss_hist, assign;
   std::vector<int64_t> e_off;
+  fl_comm* comm = nullptr;
 };
+
+void kmg_set_comm(KmGen* s, fl_comm* c) { s->comm = c; }
 
 int kmg_create(fl_table* t, int k, const double* c0, cudaStream_t st, KmGen** out) {
   auto* s = new KmGen();
@@ -289,6 +292,11 @@ int kmg_update(KmGen* s, cudaStream_t st) {
 int kmg_run(KmGen* s, int iterations, cudaStream_t st) {
   for (int i = 0; i < iterations; i++) {
     int rc = kmg_partial(s, st);
+    if (!rc && s->comm) {
+      int n = 0;
+      double* red = kmg_red(s, &n);
+      rc = comm_allreduce(s->comm, red, (size_t)n, st);
+    }
     if (!rc) rc = kmg_update(s, st);
     if (rc) return rc;
   }
@@ -492,7 +500,10 @@ struct GnGen {
   int64_t rpb_g = 0;
   size_t smem_w = 0;
   DevBuf W, Q, H, Hn, Ht32, HH, HH32, red, gpart, loss_hist;
+  fl_comm* comm = nullptr;
 };
+
+void gng_set_comm(GnGen* s, fl_comm* c) { s->comm = c; }
 
 static unsigned gg_grid(int64_t n, int sms) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sms));
@@ -614,12 +625,21 @@ int gng_partial(GnGen* s, cudaStream_t st) {
 }
 
 int gng_run(GnGen* s, int iterations, cudaStream_t st) {
+  auto step = [&]() -> int {
+    int rc = gng_partial(s, st);
+    if (!rc && s->comm) {
+      int n = 0;
+      double* red = gng_red(s, &n);
+      rc = comm_allreduce(s->comm, red, (size_t)n, st);
+    }
+    return rc;
+  };
   for (int i = 0; i < iterations; i++) {
     if (!s->primed) {
-      int rc = gng_partial(s, st);
+      int rc = step();
       if (rc) return rc;
     }
-    int rc = gng_partial(s, st);
+    int rc = step();
     if (rc) return rc;
   }
   return FL_OK;

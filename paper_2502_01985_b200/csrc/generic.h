@@ -11,6 +11,7 @@ int kmg_partial(KmGen* s, cudaStream_t st);   // red = [sums | counts | loss] of
 int kmg_update(KmGen* s, cudaStream_t st);    // centroids from red, loss_hist[it++]
 int kmg_run(KmGen* s, int iterations, cudaStream_t st);
 double* kmg_red(KmGen* s, int* len);
+void kmg_set_comm(KmGen* s, fl_comm* c);   // run(): all-reduce between partial and update
 int kmg_result(KmGen* s, double* centroids, int32_t* assign, int64_t* assign64, double* loss,
                int n, int* n_done, cudaStream_t st);
 void kmg_destroy(KmGen* s);
@@ -21,6 +22,7 @@ int gng_create(fl_table* t, int rank, const double* w0, const double* h0, double
 int gng_partial(GnGen* s, cudaStream_t st);
 int gng_run(GnGen* s, int iterations, cudaStream_t st);
 double* gng_red(GnGen* s, int* len);
+void gng_set_comm(GnGen* s, fl_comm* c);
 int gng_result(GnGen* s, double* w, double* h, double* loss, int n, int* n_done, cudaStream_t st);
 void gng_destroy(GnGen* s);
 

@@ -804,6 +804,7 @@ struct fl_glm {
   bool unfused = false;
   DevBuf y_t, z, r, w32, lpart;
   int u_blocks = 0;
+  fl_comm* comm = nullptr;   // sharded run(): all-reduce of `red` between partial and update
 };
 
 namespace flb {
@@ -1310,6 +1311,30 @@ int fl_glm_update(fl_glm* s, void* stream) {
   return FL_OK;
 }
 
+// one iteration of run(): fused (single GPU), or partial -> all-reduce ->
+// update when a communicator is attached
+static int glm_iteration(fl_glm* s, cudaStream_t st) {
+  if (!s->comm) return glm_launch_iteration(s, st, true);
+  int rc = glm_launch_iteration(s, st, false);
+  if (!rc) rc = comm_allreduce(s->comm, s->red.as<double>(), (size_t)s->t->c_T + 1, st);
+  if (rc) return rc;
+  if (s->unfused) return glm_u_update(s, st);
+  k_glm_update<<<1, NTHREADS, 0, st>>>(s->ua);
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+int fl_glm_set_comm(fl_glm* s, fl_comm* c) {
+  if (!s) return FL_ERR_ARG;
+  if (s->comm != c) {   // graphs captured without / with another exchange
+    if (s->graph) cudaGraphExecDestroy(s->graph);
+    if (s->graph_n) cudaGraphExecDestroy(s->graph_n);
+    s->graph = s->graph_n = nullptr;
+  }
+  s->comm = c;
+  return FL_OK;
+}
+
 int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
   if (!s || iterations < 1) {
     set_error("iterations must be >= 1");
@@ -1319,7 +1344,7 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (s->unfused) {
     for (int i = 0; i < iterations; i++) {
-      int rc = glm_launch_iteration(s, st, true);
+      int rc = glm_iteration(s, st);
       if (rc) return rc;
     }
     return FL_OK;
@@ -1333,7 +1358,7 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
     cudaGraph_t g;
     FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = FL_OK;
-    for (int i = 0; i < n && rc == FL_OK; i++) rc = glm_launch_iteration(s, s->cap_stream, true);
+    for (int i = 0; i < n && rc == FL_OK; i++) rc = glm_iteration(s, s->cap_stream);
     cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
     if (rc) return rc;
     FL_CUDA(e);

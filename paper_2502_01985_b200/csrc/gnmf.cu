@@ -811,6 +811,7 @@ struct fl_gnmf {
   cudaGraphExec_t graph = nullptr;
   cudaStream_t cap_stream = nullptr;
   GnGen* gen = nullptr;   // width-general session (generic.cu) when the fused pass does not apply
+  fl_comm* comm = nullptr;  // sharded run(): all-reduce of `red` after every products pass
 };
 
 namespace flb {
@@ -851,6 +852,14 @@ static int gn_h(fl_gnmf* s, cudaStream_t st, bool update, bool loss) {
   k_gnmf_h<<<1, 256, s->smem_h, st>>>(s->ha, update ? 1 : 0, loss ? 1 : 0, s->stage_h);
   FL_CHECK_LAUNCH();
   return FL_OK;
+}
+
+// products, then (sharded) the all-reduce of [W^T T | W^T W]
+static int gn_products_x(fl_gnmf* s, cudaStream_t st, bool update) {
+  int rc = gn_products(s, st, update);
+  if (rc || !s->comm) return rc;
+  return comm_allreduce(s->comm, s->red.as<double>(),
+                        (size_t)s->R * s->t->c_T + (size_t)s->R * s->R, st);
 }
 
 }  // namespace flb
@@ -1177,6 +1186,17 @@ int fl_gnmf_create(fl_table* t, int32_t rank, const double* w0, const double* h0
   return FL_OK;
 }
 
+int fl_gnmf_set_comm(fl_gnmf* s, fl_comm* c) {
+  if (!s) return FL_ERR_ARG;
+  if (s->comm != c && s->graph) {
+    cudaGraphExecDestroy(s->graph);
+    s->graph = nullptr;
+  }
+  s->comm = c;
+  if (s->gen) gng_set_comm(s->gen, c);
+  return FL_OK;
+}
+
 int fl_gnmf_path(fl_gnmf* s, int32_t* path) {
   if (!s || !path) return FL_ERR_ARG;
   *path = s->gen ? 2 : s->tc ? 1 : 0;
@@ -1194,7 +1214,7 @@ int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
   int rc;
   if (!s->primed) {   // P_0 = W_0^T T, G_0 = W_0^T W_0
     if ((rc = gn_h(s, st, false, false))) return rc;   // fp32 copy of H_0
-    if ((rc = gn_products(s, st, false))) return rc;
+    if ((rc = gn_products_x(s, st, false))) return rc;
     s->primed = true;
   }
   if (!s->graph) {
@@ -1203,7 +1223,7 @@ int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
     FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
     // loss of the previous iteration is recorded by U when it > 0
     rc = gn_h(s, s->cap_stream, true, true);
-    if (!rc) rc = gn_products(s, s->cap_stream, true);
+    if (!rc) rc = gn_products_x(s, s->cap_stream, true);
     cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
     if (rc) return rc;
     FL_CUDA(e);
@@ -1217,7 +1237,7 @@ int fl_gnmf_run(fl_gnmf* s, int32_t iterations, void* stream) {
     if (h.it + i == 0) {
       // first iteration: no previous loss
       if ((rc = gn_h(s, st, true, false))) return rc;
-      if ((rc = gn_products(s, st, true))) return rc;
+      if ((rc = gn_products_x(s, st, true))) return rc;
     } else {
       FL_CUDA(cudaGraphLaunch(s->graph, st));
     }

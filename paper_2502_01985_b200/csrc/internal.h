@@ -165,7 +165,10 @@ struct fl_table {
   flb::Workspace ws;
 };
 
+struct fl_comm;
 namespace flb {
+// comm.cu: in-place fp64 sum over the communicator's ranks (ncclAllReduce)
+int comm_allreduce(fl_comm* c, double* buf, size_t n, cudaStream_t st);
 // tma.cu: 2-D fp32 TMA tensor map over a row-major [rows x cols] array with
 // `row_bytes` pitch; box = box_rows x box_cols (columns past `cols` are
 // zero-filled by the TMA unit).  swizzle_bytes in {0, 32, 64, 128}.

@@ -843,6 +843,7 @@ struct fl_kmeans {
   cudaGraphExec_t graph = nullptr, graph_assign = nullptr;
   cudaStream_t cap_stream = nullptr;
   KmGen* gen = nullptr;   // width-general session (generic.cu) when the fused pass does not apply
+  fl_comm* comm = nullptr;  // sharded run(): all-reduce of `red` between partial and update
 };
 
 namespace flb {
@@ -888,7 +889,18 @@ static int km_graph(fl_kmeans* s, bool write_assign, cudaGraphExec_t* out) {
   if (!s->cap_stream) FL_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
   cudaGraph_t g;
   FL_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
-  int rc = km_launch_iteration(s, s->cap_stream, true, write_assign);
+  int rc;
+  if (s->comm) {   // sharded: partial -> all-reduce -> update
+    rc = km_launch_iteration(s, s->cap_stream, false, write_assign);
+    if (!rc) rc = comm_allreduce(s->comm, s->red.as<double>(), (size_t)s->k * s->t->c_T + s->k + 1,
+                                 s->cap_stream);
+    if (!rc) {
+      k_km_update<<<1, 256, 0, s->cap_stream>>>(s->ua);
+      if (cudaGetLastError() != cudaSuccess) rc = FL_ERR_CUDA;
+    }
+  } else {
+    rc = km_launch_iteration(s, s->cap_stream, true, write_assign);
+  }
   cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
   if (rc) return rc;
   FL_CUDA(e);
@@ -1232,6 +1244,18 @@ int fl_kmeans_create(fl_table* t, int32_t k, const double* centroids0, fl_kmeans
   const int rc = kmg_create(t, k, centroids0, (cudaStream_t)stream, &s->gen);
   if (rc) return rc;
   *out = guard.release();
+  return FL_OK;
+}
+
+int fl_kmeans_set_comm(fl_kmeans* s, fl_comm* c) {
+  if (!s) return FL_ERR_ARG;
+  if (s->comm != c) {
+    if (s->graph) cudaGraphExecDestroy(s->graph);
+    if (s->graph_assign) cudaGraphExecDestroy(s->graph_assign);
+    s->graph = s->graph_assign = nullptr;
+  }
+  s->comm = c;
+  if (s->gen) kmg_set_comm(s->gen, c);
   return FL_OK;
 }
 

@@ -140,12 +140,66 @@ class DeviceBuffer:
                                          "data": (ptr, False), "version": 3}
 
 
-def run_sharded(session, iterations: int, dist, device, group=None):
+class NcclComm:
+    """The library's own NCCL communicator over the ranks of `group`
+    (`fl_comm_*`, include/fl_b200.h): rank 0 draws the unique id, the host
+    process group broadcasts it, every rank joins.  Attached to a session
+    (`session.set_comm`), the per-iteration all-reduce runs inside the
+    session's CUDA graphs."""
+
+    def __init__(self, dist, device: int, group=None):
+        import ctypes as C
+
+        from . import _lib
+        rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _lib.call("fl_comm_unique_id", buf, 128)
+        obj = [bytes(buf)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        self.ptr = C.c_void_p()
+        _lib.call("fl_comm_init", idb, 128, int(world), int(rank), int(device),
+                  C.byref(self.ptr))
+        self.rank, self.world, self.device = rank, world, device
+
+    def all_reduce(self, ptr: int, n: int, stream=None):
+        import ctypes as C
+
+        from . import _lib
+        _lib.call("fl_comm_allreduce", self.ptr, C.c_void_p(ptr), int(n),
+                  stream if stream is not None else C.c_void_p(0))
+
+    def close(self):
+        from . import _lib
+        if getattr(self, "ptr", None):
+            try:
+                _lib.load().fl_comm_destroy(self.ptr)
+            except Exception:
+                pass
+            self.ptr = None
+
+    def __del__(self):
+        self.close()
+
+
+def run_sharded(session, iterations: int, dist, device, group=None, comm=None):
     """`iterations` x (partial -> all-reduce -> update) on one rank.  The
-    session must expose partial(), update() and reduce_buffer()."""
+    session must expose partial(), update() and reduce_buffer().
+
+    comm: an `NcclComm` -- the session runs its iterations itself, the
+    all-reduce captured in its CUDA graphs next to the kernels (no host
+    round trip per iteration).  Without it the loop is host-driven and the
+    all-reduce goes through torch.distributed (any backend, e.g. gloo)."""
     import torch
 
     from .trainers import KMeansSession
+    if comm is not None:
+        session.set_comm(comm)
+        session.run(iterations)
+        return
     ptr, n = session.reduce_buffer()
     red = torch.as_tensor(DeviceBuffer(ptr, n), device=device)
     if getattr(session, "needs_prime", False):    # GNMF: products of W_0 first
@@ -164,6 +218,6 @@ def run_sharded(session, iterations: int, dist, device, group=None):
         session.update()
 
 
-__all__ = ["DeviceBuffer", "ShardPlan", "all_reduce_", "kmeans_seed_rows",
+__all__ = ["DeviceBuffer", "NcclComm", "ShardPlan", "all_reduce_", "kmeans_seed_rows",
            "local_seed_slots", "plan_shards", "run_sharded", "shard_arrays",
            "sharded_kmeans_seed"]

@@ -178,6 +178,13 @@ class GlmSession:
     def update(self, stream=None):
         _lib.call("fl_glm_update", self.ptr, stream if stream is not None else C.c_void_p(0))
 
+    def set_comm(self, comm):
+        """Attach an NCCL communicator (`distributed.NcclComm`, or None to
+        detach): run() then does partial -> all-reduce -> update per
+        iteration inside the session's CUDA graphs."""
+        _lib.call("fl_glm_set_comm", self.ptr, comm.ptr if comm is not None else C.c_void_p(0))
+        self.comm = comm
+
     def reduce_buffer(self) -> tuple[int, int]:
         buf = C.c_void_p()
         n = C.c_int32()
@@ -331,6 +338,13 @@ class KMeansSession:
 
     def update(self, stream=None):
         _lib.call("fl_kmeans_update", self.ptr, stream if stream is not None else C.c_void_p(0))
+
+    def set_comm(self, comm):
+        """Attach an NCCL communicator (`distributed.NcclComm`, or None to
+        detach): run() then does partial -> all-reduce -> update per
+        iteration inside the session's CUDA graphs."""
+        _lib.call("fl_kmeans_set_comm", self.ptr, comm.ptr if comm is not None else C.c_void_p(0))
+        self.comm = comm
 
     def reduce_buffer(self) -> tuple[int, int]:
         buf = C.c_void_p()
@@ -518,6 +532,13 @@ class GnmfSession:
 
     def update(self, stream=None):
         """The H update runs at the start of the next partial()."""
+
+    def set_comm(self, comm):
+        """Attach an NCCL communicator (`distributed.NcclComm`, or None to
+        detach): run() then does partial -> all-reduce -> update per
+        iteration inside the session's CUDA graphs."""
+        _lib.call("fl_gnmf_set_comm", self.ptr, comm.ptr if comm is not None else C.c_void_p(0))
+        self.comm = comm
 
     def reduce_buffer(self) -> tuple[int, int]:
         buf = C.c_void_p()
