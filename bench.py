@@ -519,6 +519,9 @@ def algorithmic_bytes(wl, rows, dims_local, layout):
     return fact, fact + dimb
 
 
+_COMM = None   # the NCCL communicator of a multi-GPU run (main)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
@@ -576,11 +579,17 @@ def main():
     if args.workload == "c1":
         flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB
 
+    # NCCL: the library's own communicator, the all-reduce captured in the
+    # session's CUDA graphs (gloo: host-driven loop through torch.distributed)
+    comm = D.NcclComm(dist, local) if (world > 1 and backend == "nccl") else None
+    global _COMM
+    _COMM = comm
+
     def run(n):
         if world == 1:
             sess.run(n)
         else:
-            D.run_sharded(sess, n, dist, dev)
+            D.run_sharded(sess, n, dist, dev, comm=comm)
 
     run(args.warmup)
     torch.cuda.synchronize()
@@ -661,7 +670,9 @@ def main():
             "l2": ("working set < L2: 256 MB L2 flush between iterations, each timed alone"
                    if flush_buf is not None else "inputs >> L2 126 MB (no flush needed)"),
             "parallelism": (f"dp{world}: fact rows sharded by FK range of the largest "
-                            "dimension; one NCCL all-reduce of the reduce buffer per iteration")
+                            "dimension; one all-reduce of the reduce buffer per iteration"
+                            + (" (ncclAllReduce captured in the session CUDA graphs)"
+                               if comm is not None else f" ({backend}, host-driven)"))
                            if world > 1 else "single GPU",
             "sm_count": info["sm_count"],
         },
@@ -939,7 +950,7 @@ def bench_e2e_sharded(torch, fl, wl, sh, hyper, args, dist, dev):
         h2 = fl.TargetHandle.from_arrays([t.numpy() for t in host],
                                          [None] + [f.numpy() for f in fks], maps, sh["rows"], c_t)
         s2 = GlmSession(h2, wl["model"], y_h.numpy(), hyper["learning_rate"])
-        D.run_sharded(s2, n, dist, dev)
+        D.run_sharded(s2, n, dist, dev, comm=_COMM)
         w, losses = s2.result(n)
         torch.cuda.synchronize()
         t1 = time.perf_counter() - t0
