@@ -172,6 +172,20 @@ def make_shard(torch, wl, rank, world, device, seed=1234):
     fk0 = fk0[torch.randperm(rows, generator=g, device=device)]
     dims, fks = [], []
     if k:
+        # the reference's K-means seed rows (trainers.py:209-210, seed 0) get
+        # one planted cluster each, so Lloyd converges to the planted
+        # clusters: no cluster is split, no row sits on a split boundary,
+        # and assignments are decided by margins far above fp32 rounding
+        from paper_2502_01985_b200.distributed import kmeans_seed_rows
+        pick = kmeans_seed_rows(wl["rows"], k, 0)
+        lo = rows * rank
+        mine = np.nonzero((pick >= lo) & (pick < lo + rows))[0]
+        if mine.size:
+            at = torch.as_tensor(pick[mine] - lo, device=device)
+            want = torch.as_tensor(mine, device=device)
+            cur = (fk0[at] + d0) % k
+            new = fk0[at] + (want - cur) % k
+            fk0[at] = torch.where(new >= d1 - d0, new - k, new)
         grep = torch.Generator(device=device)
         grep.manual_seed(seed)          # replicated centres
         lab = (fk0 + d0) % k

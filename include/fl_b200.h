@@ -229,6 +229,12 @@ int fl_gnmf_set_comm(fl_gnmf* s, fl_comm* c);
  * {A LBO, A SBO, B LBO, B SBO} overriding mode 1 (-1 keeps the default). */
 int fl_tc_selftest(int32_t mode, const float* A, const float* B, float* D, int32_t K, int32_t N,
                    const int32_t* lbo_sbo);
+/* MN-major tf32 operand probe (csrc/tc_probe.cu): mode 0 dumps a 32 x 32
+ * fp32 tile as TMA lays it out with the 128B / 32-byte-atom swizzle; modes
+ * 1 / 2 compute D[128 x N] = A[128 x K] B[K x N] with A / B read MN-major in
+ * that layout.  params = {LBO, SBO, descriptor layout} (NULL: 16, 1024, 1). */
+int fl_tc_probe(int32_t mode, const float* A, const float* B, float* D, float* dump, int32_t K,
+                int32_t N, const int32_t* params);
 
 #ifdef __cplusplus
 }

@@ -169,6 +169,9 @@ struct fl_comm;
 namespace flb {
 // comm.cu: in-place fp64 sum over the communicator's ranks (ncclAllReduce)
 int comm_allreduce(fl_comm* c, double* buf, size_t n, cudaStream_t st);
+// swizzle code for make_tmap_2d: 128B swizzle with 32-byte atoms (the smem
+// layout of MN-major tf32 tcgen05 operands, descriptor layout 1)
+constexpr int kSwz128Atom32 = 1032;
 // tma.cu: 2-D fp32 TMA tensor map over a row-major [rows x cols] array with
 // `row_bytes` pitch; box = box_rows x box_cols (columns past `cols` are
 // zero-filled by the TMA unit).  swizzle_bytes in {0, 32, 64, 128}.

@@ -19,7 +19,7 @@
 namespace flb {
 namespace tc {
 
-enum Layout : uint64_t { kInterleave = 0, kSw128 = 2, kSw64 = 4, kSw32 = 6 };
+enum Layout : uint64_t { kInterleave = 0, kSw128B32 = 1, kSw128 = 2, kSw64 = 4, kSw32 = 6 };
 
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                               Layout layout) {

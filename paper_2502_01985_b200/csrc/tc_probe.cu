@@ -1,0 +1,152 @@
+// Layout probe for MN-major tf32 tcgen05 operands (diagnostics, not a hot
+// path).  kind::tf32 accepts MN-major shared-memory operands only in the
+// "128B swizzle with 32-byte atoms" layout (descriptor layout 1), which TMA
+// produces with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.  The row-contracting
+// products of the fused trainers (K-means one-hot^T [F|1], GNMF [W|F]^T W)
+// read their row-major tiles as MN-major operands in that layout, so no
+// transposed copy is needed.  This probe:
+//   mode 0: TMA-loads a 32 x 32 fp32 tile with that swizzle and dumps the raw
+//           shared-memory bytes (the physical layout the epilogues write);
+//   mode 1: D[128 x N] = A B with A MN-major: A^T given row-major [K x 128],
+//           TMA-loaded as 4 groups of 32 columns; B K-major interleave;
+//   mode 2: D[128 x N] = A B with B MN-major: B given row-major [K x N],
+//           TMA-loaded as N/32 groups; A K-major interleave.
+// Descriptor LBO / SBO / layout are parameters so candidates can be checked.
+#include <vector>
+
+#include "internal.h"
+#include "tc05.cuh"
+
+namespace flb {
+
+__global__ void __launch_bounds__(128) k_tc_probe(int mode, const __grid_constant__ CUtensorMap tm,
+                                                  const float* __restrict__ A,
+                                                  const float* __restrict__ B,
+                                                  float* __restrict__ D, float* __restrict__ dump,
+                                                  int K, int N, int lbo, int sbo, int layout) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar, mbar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  char* Ts = sm;                      // TMA-loaded operand (<= 4 groups x K x 128 B)
+  float* Is = reinterpret_cast<float*>(sm + 65536);   // interleave operand
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int groups = mode == 0 ? 1 : mode == 1 ? 4 : N / 32;
+  const int rows = mode == 0 ? 32 : K;
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(groups * rows * 128));
+    for (int g = 0; g < groups; g++) tma_load_2d(Ts + g * rows * 128, &tm, 32 * g, 0, &bar);
+  }
+  // interleave operand: mode 1 -> B[K x N] (N rows of K), mode 2 -> A[128 x K]
+  if (mode == 1)
+    for (int i = tid; i < K * N; i += blockDim.x) {
+      const int k = i / N, n = i - k * N;
+      Is[(k / 4) * N * 4 + n * 4 + (k & 3)] = B[i];
+    }
+  if (mode == 2)
+    for (int i = tid; i < 128 * K; i += blockDim.x) {
+      const int m = i / K, k = i - m * K;
+      Is[(k / 4) * 512 + m * 4 + (k & 3)] = A[i];
+    }
+  tc::fence_smem_to_async();
+  mbar_wait(&bar, 0);
+  if (mode == 0) {
+    for (int i = tid; i < 32 * 32; i += blockDim.x) dump[i] = reinterpret_cast<float*>(Ts)[i];
+    return;
+  }
+  __syncthreads();
+  if (warp == 0) tc::alloc(&tbase, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t t0 = smem_u32(Ts), i0 = smem_u32(Is);
+    const uint32_t idesc = tc::idesc_tf32(128, N, mode == 1, mode == 2);
+    for (int kk = 0; kk < K / 8; kk++) {
+      uint64_t ad, bd;
+      const uint64_t mn = tc::smem_desc(t0 + kk * 1024, (uint32_t)lbo, (uint32_t)sbo,
+                                        (tc::Layout)layout);
+      if (mode == 1) {
+        ad = mn;
+        bd = tc::smem_desc(i0 + kk * 2 * N * 16, N * 16, 128, tc::kInterleave);
+      } else {
+        ad = tc::smem_desc(i0 + kk * 2 * 2048, 2048, 128, tc::kInterleave);
+        bd = mn;
+      }
+      tc::mma_tf32(tmem, ad, bd, idesc, kk > 0);
+    }
+    tc::commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  tc::fence_after();
+  for (int c = 0; c < N; c += 16) {
+    uint32_t r[16];
+    tc::ld16(tmem + ((uint32_t)(32 * warp) << 16) + c, r);
+    tc::wait_ld();
+    for (int j = 0; j < 16; j++) D[(32 * warp + lane) * N + c + j] = __uint_as_float(r[j]);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 256);
+}
+
+}  // namespace flb
+
+using namespace flb;
+
+// params = {lbo, sbo, layout}; mode 0: A = the 32 x 32 tile, dump = 1024 floats
+extern "C" int fl_tc_probe(int32_t mode, const float* A, const float* B, float* D, float* dump,
+                           int32_t K, int32_t N, const int32_t* params) {
+  if (mode < 0 || mode > 2 || (mode > 0 && (K < 8 || K > 64 || (K & 7) || N < 32 || N > 128 ||
+                                            (N & 31)))) {
+    set_error("fl_tc_probe: unsupported shape (mode %d, K %d, N %d)", mode, K, N);
+    return FL_ERR_ARG;
+  }
+  float *dA = nullptr, *dB = nullptr, *dD = nullptr, *dT = nullptr;
+  const size_t na = mode == 0 ? 32 * 32 : (size_t)128 * K, nb = mode == 0 ? 1 : (size_t)K * N;
+  FL_CUDA(cudaMalloc(&dA, na * 4));
+  FL_CUDA(cudaMalloc(&dB, nb * 4));
+  FL_CUDA(cudaMalloc(&dD, (size_t)128 * 128 * 4));
+  FL_CUDA(cudaMalloc(&dT, 32 * 32 * 4));
+  FL_CUDA(cudaMemcpy(dA, A, na * 4, cudaMemcpyDefault));
+  if (mode > 0) FL_CUDA(cudaMemcpy(dB, B, nb * 4, cudaMemcpyDefault));
+  CUtensorMap tm;
+  int rc;
+  if (mode == 0) rc = make_tmap_2d(&tm, dA, 32, 32, 128, 32, 32, kSwz128Atom32);
+  else if (mode == 1) {
+    // A^T row-major [K x 128] is the host's A transposed: upload it that way
+    float* at = nullptr;
+    FL_CUDA(cudaMalloc(&at, na * 4));
+    std::vector<float> h((size_t)128 * K);
+    for (int m = 0; m < 128; m++)
+      for (int k = 0; k < K; k++) h[(size_t)k * 128 + m] = A[(size_t)m * K + k];
+    FL_CUDA(cudaMemcpy(at, h.data(), na * 4, cudaMemcpyHostToDevice));
+    cudaFree(dA);
+    dA = at;
+    rc = make_tmap_2d(&tm, dA, (uint64_t)K, 128, 512, (uint32_t)K, 32, kSwz128Atom32);
+  } else {
+    rc = make_tmap_2d(&tm, dB, (uint64_t)K, (uint64_t)N, (uint64_t)N * 4, (uint32_t)K, 32,
+                      kSwz128Atom32);
+  }
+  if (rc) return rc;
+  const size_t smem = 1024 + 65536 + 65536;
+  FL_CUDA(cudaFuncSetAttribute(k_tc_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_tc_probe<<<1, 128, smem>>>(mode, tm, dA, dB, dD, dT, K, N, params ? params[0] : 16,
+                               params ? params[1] : 1024, params ? params[2] : 1);
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaDeviceSynchronize());
+  if (mode == 0) FL_CUDA(cudaMemcpy(dump, dT, 32 * 32 * 4, cudaMemcpyDefault));
+  else FL_CUDA(cudaMemcpy(D, dD, (size_t)128 * N * 4, cudaMemcpyDefault));
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dD);
+  cudaFree(dT);
+  return FL_OK;
+}

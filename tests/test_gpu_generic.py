@@ -33,6 +33,40 @@ def _cases(model):
     return out
 
 
+def planted_seeded(seed, r_fact, dims, c_fact, k, train_seed, noise=0.01):
+    """planted_star with the reference's K-means seed rows (trainers.py:209-
+    210: sorted rng.choice of k target rows) placed one per planted cluster,
+    so Lloyd converges to the planted clusters and every row's nearest and
+    second-nearest centroids are far apart (assignments are then identical
+    for any correct implementation, fp32 or fp64)."""
+    from paper_2502_01985_b200.metadata import FactorizedTable, block_mapping, fk_indicator
+    from paper_2502_01985_b200.sparse import SparseMatrix
+    rng = np.random.default_rng(seed)
+    lab = rng.integers(0, k, r_fact)
+    pick = np.sort(np.random.default_rng(train_seed).choice(r_fact, size=k, replace=False))
+    lab[pick] = np.arange(k)
+    c_t = c_fact + sum(c for _, c in dims)
+    cen = rng.random((k, c_fact))
+    fact = (cen[lab] + noise * rng.standard_normal((r_fact, c_fact))).astype(np.float32)
+    srcs = [SparseMatrix.from_dense(fact.astype(np.float64))]
+    maps = [block_mapping(c_t, c_fact, 0)]
+    inds = [fk_indicator(r_fact, r_fact, np.arange(r_fact))]
+    off = c_fact
+    for r_d, c_d in dims:
+        dlab = np.arange(r_d) % k
+        dim = (rng.random((k, c_d))[dlab] + noise * rng.standard_normal((r_d, c_d))).astype(np.float32)
+        fk = np.empty(r_fact, dtype=np.int64)
+        for j in range(k):
+            rows = np.nonzero(dlab == j)[0]
+            mine = np.nonzero(lab == j)[0]
+            fk[mine] = rows[rng.integers(0, rows.size, mine.size)]
+        srcs.append(SparseMatrix.from_dense(dim.astype(np.float64)))
+        maps.append(block_mapping(c_t, c_d, off))
+        inds.append(fk_indicator(r_fact, r_d, fk))
+        off += c_d
+    return FactorizedTable(srcs, maps, inds, "inner", r_fact, c_t)
+
+
 def _km_path(fl, ft, k):
     from paper_2502_01985_b200.trainers import KMeansSession, kmeans_init
     h = fl.TargetHandle.factorized(ft)
@@ -76,7 +110,7 @@ def test_kmeans_generic_forced_matches_reference(fl, name, monkeypatch):
     (48, [(500, 300)], 12),                     # k > 32 and a 300-column dimension
 ])
 def test_kmeans_width_general_vs_oracle(fl, k, dims, c_fact):
-    ft = planted_star(23, 30_000, dims, c_fact, k)
+    ft = planted_seeded(23, 30_000, dims, c_fact, k, 4)
     assert _km_path(fl, ft, k) == "generic"
     tab = oracle.OracleTable.from_ft(ft)
     want = rt.kmeans(tab, 5, k, 4)
@@ -88,7 +122,7 @@ def test_kmeans_width_general_vs_oracle(fl, k, dims, c_fact):
 
 
 def test_kmeans_generic_deterministic(fl):
-    ft = planted_star(29, 20_000, [(700, 13)], 10, 36)
+    ft = planted_seeded(29, 20_000, [(700, 13)], 10, 36, 2)
     h = fl.TargetHandle.factorized(ft)
     cfg = fl.TrainConfig(iterations=4, k_clusters=36, seed=2)
     a = fl.train("kmeans", h, cfg)
