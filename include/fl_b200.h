@@ -176,9 +176,11 @@ int fl_kmeans_result(fl_kmeans* s, double* centroids, int32_t* assign, double* l
  * without a conversion pass */
 int fl_kmeans_assignments64(fl_kmeans* s, int64_t* assign, void* stream);
 int fl_kmeans_destroy(fl_kmeans* s);
-/* which pass the session runs: 0 fused mma.sync, 1 fused tcgen05, 2 width-
- * general (any k, width or number of sources; generic operators plus row
- * kernels -- the composition of reference trainers.py:223-241) */
+/* which pass the session runs: 0 fused mma.sync, 1 fused tcgen05 (K-major,
+ * opt-in), 2 width-general (any k, width or number of sources; generic
+ * operators plus row kernels -- the composition of reference
+ * trainers.py:223-241), 3 fused tcgen05 with MN-major row-contraction
+ * operands (the default for <= 28 streamed columns) */
 int fl_kmeans_path(fl_kmeans* s, int32_t* path);
 
 /* ---- Gaussian NMF, multiplicative updates (trainers.py:256-307) ----------

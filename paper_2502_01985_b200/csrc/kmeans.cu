@@ -610,6 +610,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
 }
 
 #include "kmeans_tc.cuh"
+#include "kmeans_t5.cuh"
 
 __global__ void k_km_block(const float* __restrict__ F, int pf, int64_t r_pad, int C4P,
                            float* __restrict__ Fb) {
@@ -842,6 +843,11 @@ struct fl_kmeans {
   int loss_cap = 1 << 16;
   cudaGraphExec_t graph = nullptr, graph_assign = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // tcgen05 pass with MN-major row-contraction operands (kmeans_t5.cuh)
+  bool t5 = false;
+  CUtensorMap tmF5;
+  KmT5Args t5a{};
+  K5Geom k5g{};
   KmGen* gen = nullptr;   // width-general session (generic.cu) when the fused pass does not apply
   fl_comm* comm = nullptr;  // sharded run(): all-reduce of `red` between partial and update
 };
@@ -849,7 +855,15 @@ struct fl_kmeans {
 namespace flb {
 
 static int km_fact_run(fl_kmeans* s, cudaStream_t st, bool write_assign) {
-  if (s->tc) {
+  if (s->t5) {
+    KmT5Args ta = s->t5a;
+    ta.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
+    const size_t smem = s->k5g.total + 1024;
+    if (s->KP == 16)
+      k_km_t5<16><<<s->nblk_fact, K5_THREADS, smem, st>>>(s->tmF5, ta, s->k5g);
+    else
+      k_km_t5<32><<<s->nblk_fact, K5_THREADS, smem, st>>>(s->tmF5, ta, s->k5g);
+  } else if (s->tc) {
     KmTcArgs ta = s->ta;
     ta.assign = write_assign ? s->assign.as<int32_t>() : nullptr;
     if (s->KP == 16)
@@ -954,6 +968,18 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
   if (s->tc) {
     s->KP = std::max(16, NT * 8);
     s->SC = (s->C4P + 1) * 4;
+  }
+  // default: the tcgen05 pass with MN-major row-contraction operands
+  // (kmeans_t5.cuh) for <= 28 streamed columns; FL_KM_T5=0 selects the
+  // per-warp mma.sync pass
+  {
+    const char* e5 = getenv("FL_KM_T5");
+    const bool on = e5 && atoi(e5) != 0;   // opt-in until validated on the B200
+    if (!s->tc && on && t->pf <= 28 && k <= 32) {
+      s->t5 = true;
+      s->KP = std::max(16, NT * 8);
+      s->SC = K5_SC;
+    }
   }
   const int KP = s->KP, SC = s->SC, MT = (NT + 1) / 2;
   const int ng = (int)t->g.size();
@@ -1093,11 +1119,44 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
     ta.assign = nullptr;
     ta.SC = SC;
   }
+  if (s->t5) {
+    s->k5g = k5_geom(KP, ng);
+    const size_t smem5 = s->k5g.total + 1024;
+    if (smem5 > 227 * 1024) {
+      set_error("fused K-means (tcgen05): shared memory budget exceeded (%zu bytes)", smem5);
+      return FL_ERR_OP;
+    }
+    if ((rc = make_tmap_2d(&s->tmF5, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
+                           (uint64_t)t->pf * 4, K5_TILE, 32, 128)))
+      return rc;
+    const void* k5 = KP == 16 ? (const void*)k_km_t5<16> : (const void*)k_km_t5<32>;
+    FL_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+    const int64_t ntiles = t->r_pad / K5_TILE;
+    s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+    KmT5Args& ta = s->t5a;
+    ta.pf = t->pf;
+    ta.c_T = c_T;
+    ta.k = k;
+    ta.r_T = t->r_T;
+    ta.ntiles = ntiles;
+    ta.ng = ng;
+    ta.sort_g = t->sort_g;
+    for (int d = 0; d < ng; d++) {
+      ta.fk[d] = fa.fk[d];
+      ta.E[d] = fa.E[d];
+      ta.cnt[d] = fa.cnt[d];
+      ta.rows[d] = fa.rows[d];
+    }
+    ta.C32 = s->C32.as<float>();
+    ta.f_tcol = t->d_f_tcol->as<int32_t>();
+    ta.assign = nullptr;
+  }
   if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (KP * SC + 1) * 8))) return rc;
   if ((rc = s->part_w.alloc((size_t)s->nblk_fact * KM_WARPS * MT * 16 * SC * 8))) return rc;
   fa.part_w = s->part_w.as<double>();
   fa.part = s->part_fact.as<double>();
   s->ta.part = fa.part;
+  s->t5a.part = fa.part;
 
   // ---- dimension kernels
   KmDimArgs& da = s->da;
@@ -1261,7 +1320,7 @@ int fl_kmeans_set_comm(fl_kmeans* s, fl_comm* c) {
 
 int fl_kmeans_path(fl_kmeans* s, int32_t* path) {
   if (!s || !path) return FL_ERR_ARG;
-  *path = s->gen ? 2 : s->tc ? 1 : 0;
+  *path = s->gen ? 2 : s->tc ? 1 : s->t5 ? 3 : 0;
   return FL_OK;
 }
 

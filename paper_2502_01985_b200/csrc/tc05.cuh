@@ -11,8 +11,14 @@
 //       K groups.
 //   K-major SWIZZLE_128B: rows of 128B, 8-row atoms of 1024B (SBO), chunk
 //       index XOR row%8; a K step of 8 tf32 advances the start by 32B.
-//   MN-major SWIZZLE_128B: 32 MN elements per 128B row, K rows 128B apart,
-//       8-row atoms at SBO; LBO = stride between 32-element MN groups.
+//   MN-major SWIZZLE_128B_BASE32B (layout 1, the only MN-major form kind::tf32
+//       takes): 32 MN elements per 128B row, K rows 128B apart, 32-byte
+//       granule g of row r stored at g ^ (r % 4); LBO = stride between
+//       32-element MN groups, SBO = stride between 4-row K groups (512 B for
+//       contiguous rows); a K step of 8 advances the start by 1024 B.
+//       Measured with fl_tc_probe (profiles/r02_tc_probe.txt), as is the
+//       fact that kind::tf32 TRUNCATES fp32 operand bits below the tf32
+//       mantissa (an fp32 tile is its own tf32 "hi" part).
 #pragma once
 #include <stdint.h>
 

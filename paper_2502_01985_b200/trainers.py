@@ -354,11 +354,13 @@ class KMeansSession:
 
     @property
     def path(self) -> str:
-        """"fused" (mma.sync pass), "tcgen05" or "generic" (width-general
-        session: any k, width or number of gathered sources)."""
+        """"tcgen05_mn" (default fused pass: tcgen05 screen and MN-major
+        row contraction), "fused" (per-warp mma.sync pass), "tcgen05" (opt-in
+        K-major variant) or "generic" (width-general session: any k, width or
+        number of gathered sources)."""
         p = C.c_int32()
         _lib.call("fl_kmeans_path", self.ptr, C.byref(p))
-        return ("fused", "tcgen05", "generic")[p.value]
+        return ("fused", "tcgen05", "generic", "tcgen05_mn")[p.value]
 
     def kernel_times(self, iters: int, stream=None) -> list[float]:
         """Mean ms of [dim E, fact pass, dim sums, reduce + update]."""

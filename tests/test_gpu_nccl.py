@@ -72,14 +72,16 @@ def _worker(rank, world, port, out):
             pair.append(s.result(7) + (path,))
             s.close()
         res[f"kmeans{k}"] = pair
-    for rank_ in (5, 40):   # fused / generic
+    ft_w = star_table(63, 30_000, [(500, 40)], 10)   # c_T = 50: room for rank 40
+    for rank_, gft in ((5, ft), (40, ft_w)):   # fused / generic
+        hg = fl.TargetHandle.factorized(gft)
         g = np.random.default_rng(7)
-        w0 = g.random((ft.r_T, rank_)) * 0.2
-        h0 = g.random((rank_, ft.c_T)) * 0.2
-        t_sq = float((fl.TargetHandle.factorized(ft).materialize_dense().astype(np.float64) ** 2).sum())
+        w0 = g.random((gft.r_T, rank_)) * 0.2
+        h0 = g.random((rank_, gft.c_T)) * 0.2
+        t_sq = float((hg.materialize_dense().astype(np.float64) ** 2).sum())
         pair = []
         for use in (False, True):
-            s = GnmfSession(h, rank_, w0, h0, t_sq)
+            s = GnmfSession(hg, rank_, w0, h0, t_sq)
             path = s.path
             if use:
                 D.run_sharded(s, 6, dist, torch.device("cuda", 0), comm=comm)
@@ -105,11 +107,11 @@ def test_nccl_captured_iterations_bit_identical():
         assert len(l1) == int(key[6:])
     for k in (6, 40):
         (c0, a0, l0, p0), (c1, a1, l1, p1) = res[f"kmeans{k}"]
-        assert p0 == p1 == ("fused" if k == 6 else "generic")
+        assert p0 == p1 and (p0 == "generic") == (k == 40)
         assert np.array_equal(c0, c1) and np.array_equal(a0, a1) and np.array_equal(l0, l1)
         assert len(l1) == 7
     for r in (5, 40):
         (w0, h0, l0, p0), (w1, h1, l1, p1) = res[f"gnmf{r}"]
-        assert p0 == p1 == ("fused" if r == 5 else "generic")
+        assert p0 == p1 and (p0 == "generic") == (r == 40)
         assert np.array_equal(w0, w1) and np.array_equal(h0, h1) and np.array_equal(l0, l1)
         assert len(l1) == 6

@@ -28,7 +28,51 @@ def tf32_round(x):
     return u.astype(np.uint32).view(np.float32)
 
 
+def one(mode, K, N, lbo, sbo, lay):
+    """one MN-major MMA check (run in its own process: a bad descriptor
+    faults and poisons the CUDA context)"""
+    rng = np.random.default_rng(K * 1000 + N)
+    A = (rng.integers(-8, 9, (128, K)) / 4).astype(np.float32)
+    B = (rng.integers(-8, 9, (K, N)) / 4).astype(np.float32)
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    D = np.zeros((128, N), dtype=np.float32)
+    prm = np.array([lbo, sbo, lay], dtype=np.int32)
+    _lib.call("fl_tc_probe", mode, ptr(A), ptr(B), ptr(D), None, K, N, ptr(prm))
+    err = float(np.max(np.abs(D - want)))
+    print(f" mode {mode} K {K} N {N} lbo {lbo} sbo {sbo} layout {lay}: max err {err:.3g}"
+          f" {'OK' if err == 0 else ''}", flush=True)
+
+
+def truncation():
+    rng = np.random.default_rng(5)
+    K, N = 32, 32
+    A = rng.random((128, K)).astype(np.float32) + 1.0
+    Bm = np.eye(K, N, dtype=np.float32)
+    D = np.zeros((128, N), dtype=np.float32)
+    _lib.call("fl_tc_selftest", 0, ptr(A), ptr(Bm), ptr(D), K, N, None)
+    print(" exact fp32:", float(np.max(np.abs(D - A))),
+          " truncated:", float(np.max(np.abs(D - tf32_trunc(A)))),
+          " rounded:", float(np.max(np.abs(D - tf32_round(A)))), flush=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "one":
+        one(*(int(v) for v in sys.argv[2:8]))
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "trunc":
+        truncation()
+        return
+    import subprocess
+    print("== kind::tf32 treatment of fp32 operand bits (selftest mode 0)", flush=True)
+    subprocess.run([sys.executable, __file__, "trunc"], timeout=120)
+    print("== MN-major candidates", flush=True)
+    for K in (16, 32):
+        for mode, N in ((1, 32), (2, 32), (1, 64), (2, 64)):
+            grp = K * 128
+            for lbo, sbo in ((grp, 512), (512, grp), (grp, 1024), (1024, grp), (grp, 128),
+                             (128, grp), (grp, 256), (256, grp)):
+                subprocess.run([sys.executable, __file__, "one", str(mode), str(K), str(N),
+                                str(lbo), str(sbo), "1"], timeout=120)
     lib = _lib.load()
     print("== mode 0: TMA 128B/32B-atom swizzle layout of a 32 x 32 fp32 tile")
     tile = np.arange(1024, dtype=np.float32)
@@ -41,37 +85,6 @@ def main():
         src_cols = row % 32
         print(f" smem row {r}: src row {sorted(set(src_rows.tolist()))} cols "
               f"{src_cols.tolist()}")
-
-    rng = np.random.default_rng(0)
-    for K in (16, 32):
-        A = (rng.integers(-8, 9, (128, K)) / 4).astype(np.float32)
-        for mode, N in ((1, 32), (1, 64), (2, 32), (2, 64)):
-            B = (rng.integers(-8, 9, (K, N)) / 4).astype(np.float32)
-            want = A.astype(np.float64) @ B.astype(np.float64)
-            cands = [(K * 128, 1024, 1), (1024, K * 128, 1), (16, 1024, 1), (K * 128, 1024, 2),
-                     (1024, K * 128, 2)]
-            for lbo, sbo, lay in cands:
-                D = np.zeros((128, N), dtype=np.float32)
-                prm = np.array([lbo, sbo, lay], dtype=np.int32)
-                try:
-                    _lib.call("fl_tc_probe", mode, ptr(A), ptr(B), ptr(D), None, K, N, ptr(prm))
-                except Exception as e:      # noqa: BLE001
-                    print(f" mode {mode} K {K} N {N} lbo {lbo} sbo {sbo} layout {lay}: ERROR {e}")
-                    continue
-                err = float(np.max(np.abs(D - want)))
-                print(f" mode {mode} K {K} N {N} lbo {lbo} sbo {sbo} layout {lay}: "
-                      f"max err {err:.3g} {'OK' if err == 0 else ''}")
-
-    print("== kind::tf32 treatment of fp32 operand bits (selftest mode 0)")
-    K, N = 32, 32
-    A = rng.random((128, K)).astype(np.float32) + 1.0
-    Bm = np.eye(K, N, dtype=np.float32)
-    D = np.zeros((128, N), dtype=np.float32)
-    _lib.call("fl_tc_selftest", 0, ptr(A), ptr(Bm), ptr(D), K, N, None)
-    print(" exact fp32:", float(np.max(np.abs(D - A))),
-          " truncated:", float(np.max(np.abs(D - tf32_trunc(A)))),
-          " rounded:", float(np.max(np.abs(D - tf32_round(A)))))
-
 
 if __name__ == "__main__":
     main()
