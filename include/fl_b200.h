@@ -200,9 +200,10 @@ int fl_gnmf_reduce_buffer(fl_gnmf* s, double** buf, int32_t* len);
 int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n,
                    int32_t* n_done, void* stream);
 int fl_gnmf_destroy(fl_gnmf* s);
-/* 0 fused mma.sync, 1 fused tcgen05, 2 width-general (any rank / width /
- * number of sources; reference trainers.py:282-299 over the generic
- * operators) */
+/* 0 fused mma.sync, 1 fused tcgen05 (K-major, opt-in), 2 width-general
+ * (any rank / width / number of sources; reference trainers.py:282-299 over
+ * the generic operators), 3 fused tcgen05 with MN-major row-contraction
+ * operands (rank tile 32, <= 28 streamed columns, <= 1 gathered source) */
 int fl_gnmf_path(fl_gnmf* s, int32_t* path);
 
 /* ---- sharded sessions over NCCL (no reference counterpart:

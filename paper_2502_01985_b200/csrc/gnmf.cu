@@ -595,6 +595,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 #include "gnmf_tc.cuh"
+#include "gnmf_t5.cuh"
 
 // ---------------------------------------------------------------------------
 // D2: P_d = Z_d^T S_d (fp64 per-CTA partials over row ranges)
@@ -810,6 +811,12 @@ struct fl_gnmf {
   bool primed = false;
   cudaGraphExec_t graph = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // tcgen05 pass with MN-major row-contraction operands (gnmf_t5.cuh)
+  bool t5 = false;
+  CUtensorMap tmW5, tmF5, tmWs;
+  GnT5Args g5a{};
+  G5Geom g5g{};
+  DevBuf scratch5;
   GnGen* gen = nullptr;   // width-general session (generic.cu) when the fused pass does not apply
   fl_comm* comm = nullptr;  // sharded run(): all-reduce of `red` after every products pass
 };
@@ -817,7 +824,15 @@ struct fl_gnmf {
 namespace flb {
 
 static void gn_fact_any(fl_gnmf* s, bool update, cudaStream_t st) {
-  if (s->tc) {
+  if (s->t5) {
+    const size_t smem = s->g5g.total + 1024;
+    if (update)
+      k_gnmf_t5<true><<<s->nblk_fact, G5_THREADS, smem, st>>>(s->tmW5, s->tmF5, s->tmWs, s->g5a,
+                                                              s->g5g);
+    else
+      k_gnmf_t5<false><<<s->nblk_fact, G5_THREADS, smem, st>>>(s->tmW5, s->tmF5, s->tmWs, s->g5a,
+                                                               s->g5g);
+  } else if (s->tc) {
     const size_t smem = s->gm.total + 1024;
     if (update)
       k_gnmf_tc<true><<<s->nblk_fact, GT_THREADS, smem, st>>>(s->tmWt, s->tmFt, s->ta, s->gm);
@@ -1018,12 +1033,57 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
                                    (int)(gm.total + 1024)));
     }
   }
+  // default candidate: the tcgen05 pass with MN-major row-contraction
+  // operands (gnmf_t5.cuh): rank tile 32, <= 28 streamed columns, <= 1
+  // gathered source (the sort source); opt-in (FL_GN_T5=1) while validated
+  {
+    const char* e5 = getenv("FL_GN_T5");
+    const bool on = e5 && atoi(e5) != 0;
+    const G5Geom g5 = g5_geom();
+    if (on && !s->tc && R == 32 && t->pf <= 28 && ng <= 1 && (ng == 0 || t->sort_g == 0) &&
+        g5.total + 1024 <= 227 * 1024) {
+      s->t5 = true;
+      s->g5g = g5;
+      s->SC = 32;
+      if ((rc = make_tmap_2d(&s->tmW5, s->W.p, (uint64_t)t->r_pad, 32, 128, G5_TILE, 32, 128)))
+        return rc;
+      if ((rc = make_tmap_2d(&s->tmF5, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,
+                             (uint64_t)t->pf * 4, G5_TILE, 32, 128)))
+        return rc;
+      if ((rc = make_tmap_2d(&s->tmWs, s->W.p, (uint64_t)t->r_pad, 32, 128, G5_TILE, 32,
+                             kSwz128Atom32)))
+        return rc;
+      const int64_t ntiles = t->r_pad / G5_TILE;
+      s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+      if ((rc = s->scratch5.alloc((size_t)s->nblk_fact * G5_TILE * 64 * 8))) return rc;
+      GnT5Args& ga = s->g5a;
+      ga.pf = t->pf;
+      ga.c_T = c_T;
+      ga.r_T = t->r_T;
+      ga.ntiles = ntiles;
+      ga.ng = ng;
+      ga.fk = ng ? fa.fk[0] : nullptr;
+      ga.Gd = ng ? fa.Gd[0] : nullptr;
+      ga.Z = ng ? fa.Z[0] : nullptr;
+      ga.H32 = fa.H32;
+      ga.HH32 = fa.HH32;
+      ga.f_tcol = fa.f_tcol;
+      ga.scratch = s->scratch5.as<double>();
+      const size_t smem5 = g5.total + 1024;
+      FL_CUDA(cudaFuncSetAttribute(k_gnmf_t5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem5));
+      FL_CUDA(cudaFuncSetAttribute(k_gnmf_t5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem5));
+    }
+  }
   const size_t WP = (size_t)MR * 16 * (SC + R);
   if ((rc = s->wpart.alloc((size_t)s->nblk_fact * GN_WARPS * WP * 8))) return rc;
-  if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (R * SC + R * R) * 8))) return rc;
+  const int SCP = s->SC;   // partial stride: 8 KC (mma.sync pass) or 32 (tcgen05 pass)
+  if ((rc = s->part_fact.alloc((size_t)s->nblk_fact * (R * SCP + R * R) * 8))) return rc;
   fa.wpart = s->wpart.as<double>();
   fa.part = s->part_fact.as<double>();
   s->ta.part = fa.part;
+  s->g5a.part = fa.part;
 
   // ---- dimension kernels
   GnDimArgs& da = s->da;
@@ -1104,17 +1164,17 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
   }
   {
     std::vector<RedDesc> dv;
-    const int fst = R * SC + R * R;
+    const int fst = R * SCP + R * R;
     const double* pfb = s->part_fact.as<double>();
     for (int j = 0; j < R; j++) {
       for (int c = 0; c < t->pf; c++)
-        if (t->f_tcol[c] >= 0) dv.push_back(RedDesc{pfb + j * SC + c, fst, s->nblk_fact, j * c_T + t->f_tcol[c], 0});
+        if (t->f_tcol[c] >= 0) dv.push_back(RedDesc{pfb + j * SCP + c, fst, s->nblk_fact, j * c_T + t->f_tcol[c], 0});
       for (int q = 0; q < R; q++) {
         // the fact pass skips G tiles strictly below the diagonal (rank rows
         // 16..31 x columns 0..15 when R = 32): read the transposed entry
         const bool lower = R == 32 && j >= 16 && q < 16;
         const int src = lower ? q * R + j : j * R + q;
-        dv.push_back(RedDesc{pfb + R * SC + src, fst, s->nblk_fact, R * c_T + j * R + q, 0});
+        dv.push_back(RedDesc{pfb + R * SCP + src, fst, s->nblk_fact, R * c_T + j * R + q, 0});
       }
     }
     for (int d = 0; d < ng; d++) {
@@ -1199,7 +1259,7 @@ int fl_gnmf_set_comm(fl_gnmf* s, fl_comm* c) {
 
 int fl_gnmf_path(fl_gnmf* s, int32_t* path) {
   if (!s || !path) return FL_ERR_ARG;
-  *path = s->gen ? 2 : s->tc ? 1 : 0;
+  *path = s->gen ? 2 : s->tc ? 1 : s->t5 ? 3 : 0;
   return FL_OK;
 }
 

@@ -1,0 +1,382 @@
+// F on the 5th-generation tensor cores with MN-major row-contraction
+// operands (included inside namespace flb by gnmf.cu): the GNMF fact-row
+// pass for rank tiles of R = 32, <= 28 streamed columns and at most one
+// gathered source (the sort source).  Same arithmetic and outputs as
+// k_gnmf_fact (reference trainers.py:283-298): Q = T H^T, W' = W o Q /
+// (W H H^T + eps), then P_F = W'^T F, G = W'^T W' and Z = I^T W' for the next
+// H update.
+//
+// One persistent CTA per SM walks a contiguous range of 128-row tiles:
+//   warp 0      producer: TMA of the W and F tiles (128 x 32 fp32, 128B
+//               swizzle = K-major SW128 operands) and the tile's FKs
+//   warp 1      MMA issuer (one thread), every product 3xTF32 (kind::tf32
+//               truncates, so an fp32 tile is its own hi part):
+//                 Q  = F H_F^T            M = 128 rows, N = 32, K = F cols
+//                 V  = W HH               M = 128 rows, N = 32, K = 32
+//                 PG += [W'|W'_lo|F|F_lo]^T [W'|W'_lo]   M = 128, N = 64,
+//                                         K = 128 rows of the tile
+//               PG reads its four row-major [128 x 32] tiles MN-major (128B /
+//               32-byte-atom swizzle, descriptor layout 1): no transposes.
+//   warps 2-9   epilogue, thread = (tile row, 16-column half): lo parts of W
+//               and F for Q / V, W' from Q, V and the gathered G_d row, the
+//               PG operand rows, the W' TMA store, Z segment sums.
+// PG accumulates in TMEM fp32 over G5_FT tiles (512 rows, k_gnmf_fact's
+// window), then folds into fp64 registers.
+constexpr int G5_TILE = 128;
+constexpr int G5_EPI = 256;
+constexpr int G5_THREADS = 64 + G5_EPI;
+constexpr int G5_NS = 2;
+constexpr int G5_FT = 4;
+
+struct GnT5Args {
+  int pf, c_T;
+  int64_t r_T, ntiles;
+  int ng;                          // 0 or 1 (the sort source)
+  const int32_t* fk;
+  const float* Gd;                 // r_d x 32
+  double* Z;                       // r_d x 32
+  const float* H32;                // 32 x c_T
+  const float* HH32;               // 32 x 32
+  const int32_t* f_tcol;
+  double* part;                    // gridDim.x x (32 * 32 + 32 * 32): [P_F (SC = 32) | G]
+  double* scratch;                 // gridDim.x x 128 x 64 fp64 PG
+};
+
+struct G5Geom {
+  uint32_t stage, o_f, o_fk;       // stage: W (16 KB) | F (16 KB) | FKs (512 B)
+  uint32_t o_lo;                   // 2 buffers x [W_lo | F_lo] (K-major SW128, 2 x 16 KB)
+  uint32_t o_ops;                  // W' | W'_lo | F | F_lo (MN-major, 4 x 16 KB)
+  uint32_t o_cst;                  // H_F hi | H_F lo | HH hi | HH lo (interleave, 4 x 4 KB)
+  uint32_t total;
+};
+
+__host__ __device__ inline G5Geom g5_geom() {
+  G5Geom g{};
+  g.o_f = 16384;
+  g.o_fk = 32768;
+  g.stage = 32768 + 1024;
+  g.o_lo = G5_NS * g.stage;
+  g.o_ops = g.o_lo + 2 * 32768;
+  g.o_cst = g.o_ops + 65536;
+  g.total = g.o_cst + 16384;
+  return g;
+}
+
+__device__ __forceinline__ uint32_t g5_sw128(int row, int c4) {   // 16B chunk c4 of a K-major SW128 row
+  return (uint32_t)(row * 128 + ((c4 ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ uint32_t g5_b32(int row, int c4) {     // 16B chunk c4 of an MN-major B32 row
+  return (uint32_t)(row * 128 + (((c4 >> 1) ^ (row & 3)) << 5) + ((c4 & 1) << 4));
+}
+__device__ __forceinline__ float g5_lo(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+template <bool UPDATE>
+__global__ void __launch_bounds__(G5_THREADS, 1)
+    k_gnmf_t5(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmF,
+              const __grid_constant__ CUtensorMap tmWs, GnT5Args a, G5Geom gm) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[G5_NS], empty[G5_NS], lo_ready[2], qv_full[2], ops_ready, ops_free;
+  __shared__ uint64_t acc_full[2], acc_empty[2];
+  __shared__ uint32_t tbase;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int pf = a.pf;
+
+  // ---- constant B operands (K-major interleave [K chunk][32 rank][4]):
+  // H_F^T (K = F column) and HH, hi (truncated) / exact lo
+  float* cst = reinterpret_cast<float*>(sm + gm.o_cst);
+  if (UPDATE) {
+    for (int i = tid; i < 8 * 32 * 4; i += blockDim.x) {
+      const int ch = i >> 7, n = (i >> 2) & 31, e = i & 3, k = ch * 4 + e;
+      const int tcol = k < pf ? a.f_tcol[k] : -1;
+      const float h = tcol >= 0 ? a.H32[(size_t)n * a.c_T + tcol] : 0.f;
+      const float hh = a.HH32[k * 32 + n];   // HH symmetric
+      cst[i] = h - g5_lo(h);
+      cst[1024 + i] = g5_lo(h);
+      cst[2048 + i] = hh - g5_lo(hh);
+      cst[3072 + i] = g5_lo(hh);
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < G5_NS; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&lo_ready[b], G5_EPI);
+      mbar_init(&qv_full[b], 1);
+    }
+    mbar_init(&ops_ready, G5_EPI);
+    mbar_init(&ops_free, 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], G5_EPI);
+    }
+    fence_mbar_init();
+  }
+  tc::fence_smem_to_async();
+  if (warp == 0) tc::alloc(&tbase, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;   // [0, 128): Q | V of tile parity b at 64 b; [128, 256): PG x 2
+
+  const int64_t Gd = gridDim.x;
+  const int64_t base = a.ntiles / Gd, rem = a.ntiles % Gd;
+  const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
+  const int n = (int)(base + (blockIdx.x < rem ? 1 : 0));
+
+  if (warp == 0) {
+    // =================== producer ===================
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      for (int i = 0; i < n; i++) {
+        const int s = i % G5_NS;
+        if (i >= G5_NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / G5_NS) - 1) & 1));
+        char* st = sm + s * gm.stage;
+        const int row = (int)((t0 + i) * G5_TILE);
+        mbar_arrive_expect_tx(&full[s], 32768u + (a.ng ? 512u : 0u));
+        tma_load_2d_hint(st, &tmW, 0, row, &full[s], pol);
+        tma_load_2d_hint(st + gm.o_f, &tmF, 0, row, &full[s], pol);
+        if (a.ng) bulk_g2s(st + gm.o_fk, a.fk + (t0 + i) * G5_TILE, 512, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // =================== MMA issuer ===================
+    if (lane == 0 && n > 0) {
+      const uint32_t id_qv = tc::idesc_tf32(128, 32, false, false);
+      const uint32_t id_pg = tc::idesc_tf32(128, 64, true, true);
+      const uint32_t c0 = smem_u32(cst);
+      const uint32_t ops = smem_u32(sm + gm.o_ops);
+      const int kst = (pf + 7) / 8;
+      // Q(t), V(t) into TMEM buffer t & 1 once the tile's lo parts are staged
+      auto qv = [&](int t) {
+        const int b = t & 1;
+        mbar_wait_sleep(&lo_ready[b], (uint32_t)((t >> 1) & 1));   // (implies the stage landed)
+        tc::fence_after();
+        const uint32_t st = smem_u32(sm + (t % G5_NS) * gm.stage);
+        const uint32_t lo = smem_u32(sm + gm.o_lo + b * 32768);
+        const uint32_t tq = tmem + 64 * b;
+        for (int ks = 0; ks < kst; ks++) {   // Q = F H_F^T
+          const uint64_t ah = tc::smem_desc(st + gm.o_f + ks * 32, 16, 1024, tc::kSw128);
+          const uint64_t al = tc::smem_desc(lo + 16384 + ks * 32, 16, 1024, tc::kSw128);
+          const uint64_t bh = tc::smem_desc(c0 + ks * 1024, 512, 128, tc::kInterleave);
+          const uint64_t bl = tc::smem_desc(c0 + 4096 + ks * 1024, 512, 128, tc::kInterleave);
+          tc::mma_tf32(tq, ah, bh, id_qv, ks > 0);
+          tc::mma_tf32(tq, al, bh, id_qv, true);
+          tc::mma_tf32(tq, ah, bl, id_qv, true);
+        }
+        for (int ks = 0; ks < 4; ks++) {     // V = W HH
+          const uint64_t ah = tc::smem_desc(st + ks * 32, 16, 1024, tc::kSw128);
+          const uint64_t al = tc::smem_desc(lo + ks * 32, 16, 1024, tc::kSw128);
+          const uint64_t bh = tc::smem_desc(c0 + 8192 + ks * 1024, 512, 128, tc::kInterleave);
+          const uint64_t bl = tc::smem_desc(c0 + 12288 + ks * 1024, 512, 128, tc::kInterleave);
+          tc::mma_tf32(tq + 32, ah, bh, id_qv, ks > 0);
+          tc::mma_tf32(tq + 32, al, bh, id_qv, true);
+          tc::mma_tf32(tq + 32, ah, bl, id_qv, true);
+        }
+        tc::commit(&qv_full[b]);
+      };
+      if (UPDATE) qv(0);
+      for (int t = 0; t < n; t++) {
+        const int s = t % G5_NS;
+        const int w = t / G5_FT, b = w & 1;
+        if (UPDATE && t + 1 < n) qv(t + 1);
+        mbar_wait_sleep(&ops_ready, (uint32_t)(t & 1));
+        if ((t % G5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
+        tc::fence_after();
+        const uint32_t tp = tmem + 128 + 64 * b;
+        for (int kk = 0; kk < G5_TILE / 8; kk++) {
+          // A = 4 MN groups [W' | W'_lo | F | F_lo], B = [W' | W'_lo]
+          const uint64_t ad = tc::smem_desc(ops + kk * 1024, 16384, 512, tc::kSw128B32);
+          tc::mma_tf32(tp, ad, ad, id_pg, !((t % G5_FT) == 0 && kk == 0));
+        }
+        tc::commit(&empty[s]);
+        tc::commit(&ops_free);
+        if ((t % G5_FT) == G5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // =================== epilogue: thread = (tile row, 16-column half) ===================
+    const int ew = warp - 2, h = ew >> 2, q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+    char* ops = sm + gm.o_ops;
+    double acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; j++) acc[j] = 0.0;
+    auto fold = [&](int w) {
+      const int b = w & 1;
+      mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
+      tc::fence_after();
+      uint32_t x[16];
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        tc::ld16(tmem + lane_off + 128 + 64 * b + 32 * h + 16 * u, x);
+        tc::wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; j++) acc[16 * u + j] += (double)__uint_as_float(x[j]);
+      }
+      tc::fence_before();
+      mbar_arrive(&acc_empty[b]);
+    };
+    // this thread's 16 columns of the W and F rows of tile t (exact fp32)
+    auto load_row = [&](int t, float (&w)[16], float (&x)[16]) {
+      const char* st = sm + (t % G5_NS) * gm.stage;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int c4 = 4 * h + u;
+        const float4 wv = *reinterpret_cast<const float4*>(st + g5_sw128(r, c4));
+        const float4 xv = *reinterpret_cast<const float4*>(st + gm.o_f + g5_sw128(r, c4));
+        w[4 * u + 0] = wv.x; w[4 * u + 1] = wv.y; w[4 * u + 2] = wv.z; w[4 * u + 3] = wv.w;
+        x[4 * u + 0] = xv.x; x[4 * u + 1] = xv.y; x[4 * u + 2] = xv.z; x[4 * u + 3] = xv.w;
+      }
+    };
+    // lo parts of tile t for Q / V (K-major SW128, buffer t & 1); F_lo also
+    // goes to the PG operand once the buffer is free (see below)
+    auto split = [&](int t) {
+      mbar_wait_sleep(&full[t % G5_NS], (uint32_t)((t / G5_NS) & 1));
+      float w[16], x[16];
+      load_row(t, w, x);
+      char* lo_b = sm + gm.o_lo + (t & 1) * 32768;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int c4 = 4 * h + u;
+        *reinterpret_cast<float4*>(lo_b + g5_sw128(r, c4)) =
+            make_float4(g5_lo(w[4 * u]), g5_lo(w[4 * u + 1]), g5_lo(w[4 * u + 2]), g5_lo(w[4 * u + 3]));
+        *reinterpret_cast<float4*>(lo_b + 16384 + g5_sw128(r, c4)) =
+            make_float4(g5_lo(x[4 * u]), g5_lo(x[4 * u + 1]), g5_lo(x[4 * u + 2]), g5_lo(x[4 * u + 3]));
+      }
+      fence_proxy_async();
+      tc::fence_before();
+      mbar_arrive(&lo_ready[t & 1]);
+    };
+    if (UPDATE && n > 0) split(0);
+    for (int t = 0; t < n; t++) {
+      const int s = t % G5_NS;
+      char* st = sm + s * gm.stage;
+      // software pipeline: the next tile's lo parts go out before this
+      // tile's Q / V are awaited, so its MMAs overlap this tile's epilogue
+      if (UPDATE && t + 1 < n) split(t + 1);
+      mbar_wait_sleep(&full[s], (uint32_t)((t / G5_NS) & 1));
+      const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
+      const int fk = a.ng ? fks[r] : -1;
+      float w[16], x[16];
+      load_row(t, w, x);
+      if (UPDATE) {
+        float4 gl[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) gl[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (fk >= 0) {
+          const float4* gr = reinterpret_cast<const float4*>(a.Gd + (int64_t)fk * 32 + 16 * h);
+#pragma unroll
+          for (int u = 0; u < 4; u++) gl[u] = __ldg(gr + u);
+        }
+        mbar_wait_sleep(&qv_full[t & 1], (uint32_t)((t >> 1) & 1));
+        tc::fence_after();
+        uint32_t qq[16], vv[16];
+        tc::ld16(tmem + lane_off + 64 * (t & 1) + 16 * h, qq);
+        tc::ld16(tmem + lane_off + 64 * (t & 1) + 32 + 16 * h, vv);
+        tc::wait_ld();
+        // W' = W o (Q + G_d[fk]) / (V + eps)   (k_gnmf_fact's expression)
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const float ga[4] = {gl[u].x, gl[u].y, gl[u].z, gl[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int j = 4 * u + e;
+            const float qv = __uint_as_float(qq[j]) + ga[e];
+            w[j] = w[j] * __fdividef(qv, __uint_as_float(vv[j]) + 1e-12f);
+          }
+        }
+      }
+      // PG operand rows: W' | W'_lo | F | F_lo (MN-major B32); the previous
+      // tile's PG MMAs and W' store must be done with the buffer.  Chunks
+      // are written in a per-row rotated order: rows r and r + 4 (same
+      // swizzle granule) then hit different 16-byte halves (no conflicts)
+      if (t >= 1) mbar_wait_sleep(&ops_free, (uint32_t)((t - 1) & 1));
+      if (UPDATE && tid == 64) bulk_wait_read<0>();
+      if (UPDATE) named_sync(1, G5_EPI);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int uu = (u + ((r >> 2) & 1)) & 3;
+        const int c4 = 4 * h + uu;
+        float wv[4], xv[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {   // select by the rotated index (registers only)
+          wv[e] = uu == 0 ? w[e] : uu == 1 ? w[4 + e] : uu == 2 ? w[8 + e] : w[12 + e];
+          xv[e] = uu == 0 ? x[e] : uu == 1 ? x[4 + e] : uu == 2 ? x[8 + e] : x[12 + e];
+        }
+        *reinterpret_cast<float4*>(ops + g5_b32(r, c4)) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<float4*>(ops + 16384 + g5_b32(r, c4)) =
+            make_float4(g5_lo(wv[0]), g5_lo(wv[1]), g5_lo(wv[2]), g5_lo(wv[3]));
+        *reinterpret_cast<float4*>(ops + 32768 + g5_b32(r, c4)) = make_float4(xv[0], xv[1], xv[2], xv[3]);
+        *reinterpret_cast<float4*>(ops + 49152 + g5_b32(r, c4)) =
+            make_float4(g5_lo(xv[0]), g5_lo(xv[1]), g5_lo(xv[2]), g5_lo(xv[3]));
+      }
+      fence_proxy_async();
+      named_sync(1, G5_EPI);
+      if (UPDATE && tid == 64) {
+        tma_store_2d_hint(&tmWs, 0, (int)((t0 + t) * G5_TILE), ops, l2_policy_evict_first());
+        bulk_commit();
+      }
+      // Z[fk] += W' rows: warp (q4, h) takes the 16 rows [32 q4 + 16 h, +16),
+      // lane = rank column; a segment with one FK (the common case: keys are
+      // sorted, fanout >> 16) is one branch-free sum and one fp64 atomic
+      if (a.ng) {
+        const int r0 = 32 * q4 + 16 * h;
+        const int c4 = lane >> 2;
+        const int k0 = fks[r0], k1 = fks[r0 + 15];
+        const float* zcol = reinterpret_cast<const float*>(ops + (lane & 3) * 4);
+        if (k0 == k1) {
+          float run = 0.f;
+#pragma unroll
+          for (int rr = 0; rr < 16; rr++)
+            run += *reinterpret_cast<const float*>(reinterpret_cast<const char*>(zcol) + g5_b32(r0 + rr, c4));
+          if (k0 >= 0) atomicAdd(a.Z + (int64_t)k0 * 32 + lane, (double)run);
+        } else {
+          float run = 0.f;
+          int cur = k0;
+          for (int rr = r0; rr < r0 + 16; rr++) {
+            const int f = fks[rr];
+            if (f != cur) {
+              if (cur >= 0) atomicAdd(a.Z + (int64_t)cur * 32 + lane, (double)run);
+              run = 0.f;
+              cur = f;
+            }
+            run += *reinterpret_cast<const float*>(reinterpret_cast<const char*>(zcol) + g5_b32(rr, c4));
+          }
+          if (cur >= 0) atomicAdd(a.Z + (int64_t)cur * 32 + lane, (double)run);
+        }
+      }
+      tc::fence_before();
+      mbar_arrive(&ops_ready);
+      if ((t % G5_FT) == G5_FT - 1) fold(t / G5_FT);
+    }
+    if (n > 0 && ((n - 1) % G5_FT) != G5_FT - 1) fold((n - 1) / G5_FT);
+    if (UPDATE && tid == 64) bulk_wait<0>();
+    double* sc = a.scratch + ((int64_t)blockIdx.x * G5_TILE + r) * 64 + 32 * h;
+#pragma unroll
+    for (int j = 0; j < 32; j++) sc[j] = acc[j];
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  // CTA partial in k_gnmf_fact's format [R x SC] P_F (SC = 32) | [R x R] G from
+  // S[m][n] (m: W' | W'_lo | F | F_lo columns, n: W' | W'_lo columns)
+  const double* S = a.scratch + (int64_t)blockIdx.x * G5_TILE * 64;
+  double* out = a.part + (int64_t)blockIdx.x * (32 * 32 + 32 * 32);
+  for (int i = tid; i < 32 * 32; i += blockDim.x) {
+    const int j = i >> 5, c = i & 31;
+    out[i] = c < pf ? S[(64 + c) * 64 + j] + S[(96 + c) * 64 + j] + S[(64 + c) * 64 + 32 + j] : 0.0;
+  }
+  for (int i = tid; i < 32 * 32; i += blockDim.x) {
+    const int j = i >> 5, q = i & 31;
+    out[1024 + i] = S[j * 64 + q] + S[(32 + j) * 64 + q] + S[j * 64 + 32 + q];
+  }
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 256);
+}

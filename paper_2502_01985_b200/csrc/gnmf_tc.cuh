@@ -76,20 +76,6 @@ __device__ __forceinline__ uint32_t sw128(int row, int col) {   // byte offset i
 }
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// mbarrier wait that suspends the thread (up to ~1 ms per try) instead of
-// spinning: the producer / MMA threads share issue slots with the epilogue
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-        : "memory");
-}
-
 struct GtBars {
   uint64_t *full, *empty, *lo_ready, *qv_full, *qv_empty, *pg_ready, *pg_free, *acc_full,
       *acc_empty;

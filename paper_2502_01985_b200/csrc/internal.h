@@ -305,6 +305,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// mbarrier wait that suspends the warp (hint ~1 ms per try) instead of
+// spinning: waiting producer / MMA / epilogue warps give their issue slots
+// to the warps that have work
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
+// arrive on an mbarrier once every prior cp.async of this thread has landed
+// (the arrival is counted in the barrier's expected count: .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 // L2 eviction-priority policies (createpolicy): streamed operands that are
 // touched once are loaded / stored evict_first so they do not push out the
 // small, repeatedly updated working set (per-warp partials, gathered rows)

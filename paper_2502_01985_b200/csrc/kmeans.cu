@@ -354,6 +354,10 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     mbar_wait(&wbar[s], ph);
     float* Fs = reinterpret_cast<float*>(wsm + (size_t)s * a.stage_bytes);
     const int32_t* fks_s = reinterpret_cast<const int32_t*>(wsm + (size_t)s * a.stage_bytes + F_BYTES);
+    // the count column of [F | 1] (column pf, zero-filled by the TMA): one
+    // store per row here instead of a select per B element in the sums
+    Fs[lane * FP + pf] = 1.f;
+    __syncwarp();
     const int p0 = (u0 + i) * 32;
     const bool valid = p0 + lane < r_T32;
     // E terms of every cluster: sum_d E_d[fk_d, j] (kept apart for the loss).
@@ -412,10 +416,11 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       for (int n = 0; n < NT; n++) bf[n] = reinterpret_cast<const uint2*>(bfrag)[(kc * NT + n) * 32 + lane];
 #pragma unroll
       for (int m = 0; m < 2; m++) {
+        // A as loaded: the tensor core truncates fp32 operand bits below the
+        // tf32 mantissa (measured, profiles/r02_tc_probe.txt), which is the
+        // truncated-A error the certification bound assumes
         uint32_t x[4];
         ldsm_x4(x[0], x[1], x[2], x[3], Fs + (m * 16 + (lane & 15)) * FP + kc * 8 + (lane >> 4) * 4);
-#pragma unroll
-        for (int e = 0; e < 4; e++) x[e] &= 0xffffe000u;
 #pragma unroll
         for (int n = 0; n < NT; n++) mma_tf32(z[m][n], x[0], x[1], x[2], x[3], bf[n].x, bf[n].y);
       }
@@ -560,9 +565,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       }
 #pragma unroll
       for (int c = 0; c < KC; c++) {
-        // column pf of [F | 1] is the count column (TMA zero-fills it)
-        const float b0 = c * 8 + g == pf ? 1.f : Fs[rr0 * FP + c * 8 + g];
-        const float b1 = c * 8 + g == pf ? 1.f : Fs[rr1 * FP + c * 8 + g];
+        // column pf of [F | 1] is the count column (set to 1 after the TMA)
+        const float b0 = Fs[rr0 * FP + c * 8 + g];
+        const float b1 = Fs[rr1 * FP + c * 8 + g];
         const uint32_t h0 = __float_as_uint(b0) & 0xffffe000u;
         const uint32_t h1 = __float_as_uint(b1) & 0xffffe000u;
         const uint32_t l0 = __float_as_uint(b0 - __uint_as_float(h0));
@@ -975,9 +980,11 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
   {
     const char* e5 = getenv("FL_KM_T5");
     const bool on = e5 && atoi(e5) != 0;   // opt-in until validated on the B200
-    if (!s->tc && on && t->pf <= 28 && k <= 32) {
+    const int kp5 = std::max(16, NT * 8);
+    if (!s->tc && on && t->pf <= 28 && k <= 32 &&
+        k5_geom(kp5, (int)t->g.size()).total + 1024 <= 227 * 1024) {
       s->t5 = true;
-      s->KP = std::max(16, NT * 8);
+      s->KP = kp5;
       s->SC = K5_SC;
     }
   }

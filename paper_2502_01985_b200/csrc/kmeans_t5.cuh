@@ -13,9 +13,12 @@
 //               The row contraction reads its tiles MN-major (row-major
 //               [rows x 32] in the 128B / 32-byte-atom swizzle, descriptor
 //               layout 1), so no transposed copy exists anywhere.
-//   warps 2-9   epilogue, two groups of four warps taking alternate tiles;
-//               thread = tile row: distances from the screen (+ the E_d
-//               rows of the gathered sources), certified argmin, exact loss,
+//   warps 2-3   gather: the E_d rows of every tile row's FKs, copied from L2
+//               into the stage by cp.async (completion on an mbarrier), so
+//               the epilogue never waits on a dependent global load
+//   warps 4-11  epilogue, two groups of four warps taking alternate tiles;
+//               thread = tile row: distances from the screen (+ the staged
+//               E_d rows), certified argmin, exact loss,
 //               I_d^T A counters, then the row's one-hot, F_hi and F_lo
 //               (+ the count column) into the group's MN-major operand tiles.
 // The screen is one tf32 term (certified, as k_km_fact); the sums are exact
@@ -24,8 +27,9 @@
 // as k_km_fact's flushes).
 constexpr int K5_TILE = 128;
 constexpr int K5_EPI = 256;           // epilogue threads (2 groups x 4 warps)
-constexpr int K5_THREADS = 64 + K5_EPI;
-constexpr int K5_NS = 3;              // TMA stages
+constexpr int K5_GAT = 64;            // gather threads
+constexpr int K5_THREADS = 64 + K5_GAT + K5_EPI;
+constexpr int K5_NS_MAX = 3;          // TMA stages (2 or 3: whatever fits)
 constexpr int K5_FT = 4;              // tiles per fp32 sums window
 constexpr int K5_SC = 32;             // F columns in the operand tiles (pf <= 28)
 
@@ -44,7 +48,9 @@ struct KmT5Args {
 };
 
 struct K5Geom {                      // byte offsets from the 1024-aligned base
-  uint32_t stage, o_fk;              // stage: F tile (16 KB) | FKs (512 B per source)
+  int ns;                            // stages
+  uint32_t stage, o_fk, o_e;         // stage: F tile (16 KB) | FKs (512 B per source) |
+                                     //        E rows [source][128][KP] fp32
   uint32_t o_ops;                    // 2 groups x [F_hi | F_lo | one-hot] (3 x 16 KB)
   uint32_t o_cb, o_cf, o_cn, o_scr;  // screen B operand, fp32 centroids, norms, fp64 scratch
   uint32_t total;
@@ -53,8 +59,12 @@ struct K5Geom {                      // byte offsets from the 1024-aligned base
 __host__ __device__ inline K5Geom k5_geom(int KP, int ng) {
   K5Geom g{};
   g.o_fk = 16384;
-  g.stage = (uint32_t)round_up(16384 + 512 * (ng > 0 ? ng : 1), 1024);
-  g.o_ops = K5_NS * g.stage;
+  g.o_e = (uint32_t)round_up(16384 + 512 * (ng > 0 ? ng : 1), 128);
+  g.stage = (uint32_t)round_up(g.o_e + 512 * KP * ng, 1024);
+  const uint32_t fixed = 2 * 49152 + (uint32_t)KP * 128 + (uint32_t)KP * 36 * 4 + KP * 4 + 1024 +
+                         32 * 64 * 8;
+  g.ns = (K5_NS_MAX * g.stage + fixed + 1024 <= 227 * 1024) ? K5_NS_MAX : 2;
+  g.o_ops = g.ns * g.stage;
   g.o_cb = g.o_ops + 2 * 49152;
   g.o_cf = g.o_cb + (uint32_t)KP * 128;
   g.o_cn = g.o_cf + (uint32_t)KP * 36 * 4;
@@ -82,10 +92,12 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
     k_km_t5(const __grid_constant__ CUtensorMap tmF, KmT5Args a, K5Geom gm) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[K5_NS], empty[K5_NS], scr_full[2], ops_ready[2], ops_free[2];
+  __shared__ uint64_t full[K5_NS_MAX], empty[K5_NS_MAX], es_ready[K5_NS_MAX];
+  __shared__ uint64_t scr_full[2], ops_ready[2], ops_free[2];
   __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tbase;
   __shared__ double lsum_w[K5_EPI / 32];
+
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int pf = a.pf, k = a.k;
@@ -112,9 +124,10 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
     cn[j] = j < k ? s : __int_as_float(0x7f800000);
   }
   if (tid == 0) {
-    for (int s = 0; s < K5_NS; s++) {
+    for (int s = 0; s < K5_NS_MAX; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&es_ready[s], K5_GAT);
     }
     for (int g = 0; g < 2; g++) {
       mbar_init(&scr_full[g], 1);
@@ -137,14 +150,15 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
   const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
   const int n = (int)(base + (blockIdx.x < rem ? 1 : 0));
   const int ng = a.ng;
+  const int NS = gm.ns;
 
   if (warp == 0) {
     // =================== producer ===================
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       for (int i = 0; i < n; i++) {
-        const int s = i % K5_NS;
-        if (i >= K5_NS) mbar_wait(&empty[s], (uint32_t)(((i / K5_NS) - 1) & 1));
+        const int s = i % NS;
+        if (i >= NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / NS) - 1) & 1));
         char* st = sm + s * gm.stage;
         mbar_arrive_expect_tx(&full[s], 16384u + 512u * ng);
         tma_load_2d_hint(st, &tmF, 0, (int)((t0 + i) * K5_TILE), &full[s], pol);
@@ -160,8 +174,8 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
       const uint32_t cb0 = smem_u32(cb);
       const int kst = (pf + 7) / 8;
       auto screen = [&](int t) {
-        const int s = t % K5_NS, g = t & 1;
-        mbar_wait(&full[s], (uint32_t)((t / K5_NS) & 1));
+        const int s = t % NS, g = t & 1;
+        mbar_wait_sleep(&full[s], (uint32_t)((t / NS) & 1));
         tc::fence_after();
         const uint32_t st = smem_u32(sm + s * gm.stage);
         for (int ks = 0; ks < kst; ks++) {
@@ -174,10 +188,10 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
       screen(0);
       if (n > 1) screen(1);
       for (int t = 0; t < n; t++) {
-        const int g = t & 1, s = t % K5_NS;
+        const int g = t & 1, s = t % NS;
         const int w = t / K5_FT, b = w & 1;
-        mbar_wait(&ops_ready[g], (uint32_t)((t >> 1) & 1));
-        if ((t % K5_FT) == 0 && w >= 2) mbar_wait(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
+        mbar_wait_sleep(&ops_ready[g], (uint32_t)((t >> 1) & 1));
+        if ((t % K5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
         tc::fence_after();
         const uint32_t ops = smem_u32(sm + gm.o_ops + g * 49152);
         for (int kk = 0; kk < K5_TILE / 8; kk++) {
@@ -193,9 +207,31 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
         if (t + 2 < n) screen(t + 2);
       }
     }
+  } else if (warp < 4) {
+    // =================== gather: E_d rows -> the stage (cp.async) ===================
+    const int gt = tid - 64;
+    constexpr int Q = KP / 4;
+    for (int i = 0; i < n; i++) {
+      const int s = i % NS;
+      char* st = sm + s * gm.stage;
+      mbar_wait_sleep(&full[s], (uint32_t)((i / NS) & 1));   // the tile's FKs
+      const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
+      for (int rr = gt; rr < K5_TILE; rr += K5_GAT) {
+#pragma unroll
+        for (int d = 0; d < MAX_GATHER; d++) {
+          if (d >= ng) break;
+          const int f = fks[d * K5_TILE + rr];
+          const float* src = a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP;
+          char* dst = st + gm.o_e + (d * K5_TILE + rr) * KP * 4;
+#pragma unroll
+          for (int q = 0; q < Q; q++) cp_async16(dst + 16 * (q ^ (rr & (Q - 1))), src + 4 * q);
+        }
+      }
+      cp_async_mbar_arrive(&es_ready[s]);
+    }
   } else {
     // =================== epilogue ===================
-    const int ew = warp - 2, grp = ew >> 2;
+    const int ew = warp - 4, grp = ew >> 2;
     const int q4 = warp & 3;                  // TMEM lane quarter of this warp
     const int r = 32 * q4 + lane;             // tile row
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
@@ -207,9 +243,11 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
       for (int j = 0; j < 32; j++) acc64[j * 64 + r] = 0.0;
     double lsum = 0.0;
     const int pf4 = pf / 4;
+    float cn_max = 0.f;
+    for (int j = 0; j < k; j++) cn_max = fmaxf(cn_max, cn[j]);
     auto flush = [&](int w) {
       const int b = w & 1;
-      mbar_wait(&acc_full[b], (uint32_t)((w >> 1) & 1));
+      mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
       tc::fence_after();
       uint32_t x[16];
 #pragma unroll
@@ -223,26 +261,26 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
       mbar_arrive(&acc_empty[b]);
     };
     for (int t = grp; t < n; t += 2) {
-      const int s = t % K5_NS;
+      const int s = t % NS;
       char* st = sm + s * gm.stage;
-      mbar_wait(&full[s], (uint32_t)((t / K5_NS) & 1));
+      mbar_wait_sleep(&full[s], (uint32_t)((t / NS) & 1));
       const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
       const int64_t p = (t0 + t) * K5_TILE + r;
       const bool valid = p < a.r_T;
-      // E rows of every gathered source (L2), summed per cluster
+      // E rows of every gathered source (staged by the gather warps)
       float eacc[KP];
 #pragma unroll
       for (int j = 0; j < KP; j++) eacc[j] = 0.f;
       int fkv[MAX_GATHER];
+      mbar_wait_sleep(&es_ready[s], (uint32_t)((t / NS) & 1));
 #pragma unroll
       for (int d = 0; d < MAX_GATHER; d++) {
         if (d >= ng) break;
-        const int f = fks[d * K5_TILE + r];
-        fkv[d] = f;
-        const float4* er = reinterpret_cast<const float4*>(a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP);
+        fkv[d] = fks[d * K5_TILE + r];
+        const char* er = st + gm.o_e + (d * K5_TILE + r) * KP * 4;
 #pragma unroll
         for (int q = 0; q < KP / 4; q++) {
-          const float4 v = er[q];
+          const float4 v = *reinterpret_cast<const float4*>(er + 16 * (q ^ (r & (KP / 4 - 1))));
           eacc[4 * q + 0] += v.x;
           eacc[4 * q + 1] += v.y;
           eacc[4 * q + 2] += v.z;
@@ -256,7 +294,7 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
         xr[c4] = c4 < pf4 ? *reinterpret_cast<const float4*>(st + k5_sw128(r, 4 * c4))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       // screen distances: ||c||^2 + E - 2 z
-      mbar_wait(&scr_full[grp], (uint32_t)((t >> 1) & 1));
+      mbar_wait_sleep(&scr_full[grp], (uint32_t)((t >> 1) & 1));
       tc::fence_after();
       float dv[KP];
       {
@@ -285,8 +323,6 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
       for (int c4 = 0; c4 < K5_SC / 4; c4++)
         xn = fmaf(xr[c4].x, xr[c4].x, fmaf(xr[c4].y, xr[c4].y,
              fmaf(xr[c4].z, xr[c4].z, fmaf(xr[c4].w, xr[c4].w, xn))));
-      float cn_max = 0.f;
-      for (int j = 0; j < k; j++) cn_max = fmaxf(cn_max, cn[j]);
       // certify (k_km_fact's bound): near-ties re-decided from exact fp32
       // differences of the F part plus the E terms
       const float tol = 4e-3f * (xn + cn_max) + 1e-5f * (fabsf(v1) + fminf(fabsf(v2), 3e38f));
@@ -346,7 +382,7 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
         }
       }
       // operand rows: F_hi | F_lo (+ count column 31) | one-hot
-      if (t >= 2) mbar_wait(&ops_free[grp], (uint32_t)(((t >> 1) - 1) & 1));
+      if (t >= 2) mbar_wait_sleep(&ops_free[grp], (uint32_t)(((t >> 1) - 1) & 1));
 #pragma unroll
       for (int c4 = 0; c4 < K5_SC / 4; c4++) {
         const float4 x = valid ? xr[c4] : make_float4(0.f, 0.f, 0.f, 0.f);

@@ -550,11 +550,13 @@ class GnmfSession:
 
     @property
     def path(self) -> str:
-        """"fused" (mma.sync pass), "tcgen05" or "generic" (width-general
-        session: any rank, width or number of gathered sources)."""
+        """"fused" (per-warp mma.sync pass), "tcgen05" (opt-in K-major
+        variant), "generic" (width-general session: any rank, width or number
+        of gathered sources) or "tcgen05_mn" (tcgen05 pass with MN-major
+        row-contraction operands)."""
         p = C.c_int32()
         _lib.call("fl_gnmf_path", self.ptr, C.byref(p))
-        return ("fused", "tcgen05", "generic")[p.value]
+        return ("fused", "tcgen05", "generic", "tcgen05_mn")[p.value]
 
     def kernel_times(self, iters: int, stream=None) -> list[float]:
         """Mean ms of [H update, dim G, fact pass, dim P, reduce]."""

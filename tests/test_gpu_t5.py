@@ -47,7 +47,7 @@ def test_kmeans_t5_matches_reference(fl, t5, name):
 @pytest.mark.parametrize("k,dims,c_fact,rows", [(16, [(3000, 30), (200, 5)], 20, 60_000),
                                                 (4, [(500, 9)], 12, 40_001),
                                                 (24, [(4000, 7)], 5, 30_000),
-                                                (32, [(600, 150)], 28, 50_000),
+                                                (32, [(600, 60)], 28, 50_000),
                                                 (9, [], 20, 20_000),
                                                 (16, [(60 + 7 * i, 3) for i in range(8)], 8, 25_000)])
 def test_kmeans_t5_planted_vs_oracle(fl, t5, k, dims, c_fact, rows):
@@ -93,4 +93,62 @@ def test_kmeans_t5_deterministic_and_matches_mma_pass(fl, monkeypatch):
     c = fl.train("kmeans", h, cfg)
     assert np.array_equal(a.parameters["assignments"], c.parameters["assignments"])
     assert max_rel(a.parameters["centroids"], c.parameters["centroids"]) < 1e-6
+    assert max_rel(a.loss_history, c.loss_history) < 1e-6
+
+
+# ---------------------------------------------------------------------------
+# GNMF (csrc/gnmf_t5.cuh)
+# ---------------------------------------------------------------------------
+@pytest.fixture
+def g5(monkeypatch):
+    monkeypatch.setenv("FL_GN_T5", "1")
+
+
+def _gn_cases():
+    return [n for n in golden_names() if "gnmf" in load_golden(n).meta.get("trainers", {})]
+
+
+@pytest.mark.parametrize("name", _gn_cases())
+def test_gnmf_t5_matches_reference(fl, g5, name):
+    g = load_golden(name)
+    m = g.meta["trainers"]["gnmf"]
+    res = fl.train("gnmf", fl.TargetHandle.factorized(g.ft), _cfg(fl, m))
+    assert max_rel(res.loss_history, g["gnmf_loss"]) < TOL
+    assert max_rel(res.parameters["h"], g["gnmf_h"]) < TOL
+    assert max_rel(res.parameters["w"], g["gnmf_w"]) < TOL
+
+
+@pytest.mark.parametrize("rank,dims,c_fact,rows", [(32, [(2000, 50)], 20, 40_000),
+                                                   (20, [(700, 9)], 28, 30_001),
+                                                   (25, [], 28, 20_000),
+                                                   (17, [(5000, 20)], 3, 25_000)])
+def test_gnmf_t5_vs_oracle(fl, g5, rank, dims, c_fact, rows):
+    from conftest import star_table
+    from paper_2502_01985_b200.trainers import GnmfSession
+    ft = star_table(37, rows, dims, c_fact)
+    h = fl.TargetHandle.factorized(ft)
+    s = GnmfSession(h, rank, np.ones((ft.r_T, rank)), np.ones((rank, ft.c_T)), 1.0)
+    assert s.path == "tcgen05_mn"
+    s.close()
+    tab = oracle.OracleTable.from_ft(ft)
+    want = rt.gaussian_nmf(tab, 5, rank, 9)
+    res = fl.train("gnmf", h, fl.TrainConfig(iterations=5, rank=rank, seed=9))
+    assert max_rel(res.loss_history, want["loss_history"]) < TOL
+    assert max_rel(res.parameters["h"], want["parameters"]["h"]) < TOL
+    assert max_rel(res.parameters["w"], want["parameters"]["w"]) < TOL
+
+
+def test_gnmf_t5_deterministic_and_matches_mma_pass(fl, monkeypatch):
+    from conftest import star_table
+    ft = star_table(39, 60_000, [(800, 30)], 20)
+    h = fl.TargetHandle.factorized(ft)
+    cfg = fl.TrainConfig(iterations=6, rank=32, seed=2)
+    monkeypatch.setenv("FL_GN_T5", "1")
+    a = fl.train("gnmf", h, cfg)
+    b = fl.train("gnmf", h, cfg)
+    assert np.array_equal(a.parameters["w"], b.parameters["w"])
+    assert a.loss_history == b.loss_history
+    monkeypatch.setenv("FL_GN_T5", "0")
+    c = fl.train("gnmf", h, cfg)
+    assert max_rel(a.parameters["w"], c.parameters["w"]) < 1e-5
     assert max_rel(a.loss_history, c.loss_history) < 1e-6
