@@ -466,8 +466,23 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_glm_fact(GlmFactArgs a) {
   if (tid == 0) a.state->done_fact = 0;
 }
 
+__device__ void glm_apply_update(const UpdateArgs& u);
 #include "glm_fact_warp.cuh"
 #include "glm_fact_csr.cuh"
+
+// solo iteration check: the widest dimension-row range one fact-pass CTA
+// references (it must fit the CTA's q staging, FW_QCAP entries)
+__global__ void k_glm_solo_span(const int32_t* __restrict__ fks, int64_t n_neg, int64_t r_T,
+                                int64_t nunits, int rw, int nblk, int* __restrict__ out) {
+  const int64_t NW = (int64_t)nblk * FW_WARPS;
+  const int64_t base = nunits / NW, rem = nunits % NW;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x) {
+    const int64_t cw0 = (int64_t)b * FW_WARPS, cw1 = cw0 + FW_WARPS;
+    const int64_t cu0 = cw0 * base + min64(cw0, rem), cu1 = cw1 * base + min64(cw1, rem);
+    const int64_t rlo = max64(cu0 * rw, n_neg), rhi = min64(cu1 * rw, r_T) - 1;
+    if (rlo <= rhi) atomicMax(out, fks[rhi] - fks[rlo] + 1);
+  }
+}
 // auto-selection threshold of the CSR pass: it must beat the dense pass,
 // which streams F at the HBM roofline (profiles/r01_glm_csr.txt)
 constexpr double kCsrAutoDensity = 0.0;
@@ -665,7 +680,8 @@ __global__ void k_glm_update(UpdateArgs u) { glm_apply_update(u); }
 
 namespace flb {
 template <int MODEL, int C4>
-static void launch_fw(const GlmFactWArgs& a, int grid, size_t smem, cudaStream_t st, bool pdl) {
+static void launch_fw(const GlmFactWArgs& a, const UpdateArgs& u, int grid, size_t smem,
+                      cudaStream_t st, bool pdl) {
   constexpr int RPL = C4 <= 7 ? 2 : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -677,7 +693,7 @@ static void launch_fw(const GlmFactWArgs& a, int grid, size_t smem, cudaStream_t
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = (pdl && std::getenv("FL_NO_PDL") == nullptr) ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k_glm_fact_w<MODEL, C4, RPL>, a);
+  cudaLaunchKernelEx(&cfg, k_glm_fact_w<MODEL, C4, RPL>, a, u);
 }
 template <int MODEL, int C4>
 static const void* fw_ptr() {
@@ -693,9 +709,9 @@ static const void* fw_kernel(int model, int c4) {
 #undef FW_PTR
   return nullptr;
 }
-static void fw_launch(int model, int c4, const GlmFactWArgs& a, int grid, size_t smem,
-                      cudaStream_t st, bool pdl = false) {
-#define FW_LAUNCH(M, C) if (c4 == C) { launch_fw<M, C>(a, grid, smem, st, pdl); return; }
+static void fw_launch(int model, int c4, const GlmFactWArgs& a, const UpdateArgs& u, int grid,
+                      size_t smem, cudaStream_t st, bool pdl = false) {
+#define FW_LAUNCH(M, C) if (c4 == C) { launch_fw<M, C>(a, u, grid, smem, st, pdl); return; }
   if (model == 0) { FW_CASES(0, FW_LAUNCH) } else { FW_CASES(1, FW_LAUNCH) }
 #undef FW_LAUNCH
 }
@@ -796,6 +812,8 @@ struct fl_glm {
   cudaStream_t cap_stream = nullptr;
   int bins_rows = 0;
   bool use_fw = false;
+  bool solo = false;       // one-kernel iteration (glm_fact_warp.cuh, solo)
+  DevBuf solo_part, solo_span;
   GlmFactWArgs fw{};
   int nblk_fw = 0;
   size_t smem_fw = 0;
@@ -883,6 +901,13 @@ static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
     if (rc) return rc;
     return fuse_update ? glm_u_update(s, st) : FL_OK;
   }
+  if (s->solo) {   // one kernel: q, fact pass, gradient, reduction (+ update)
+    GlmFactWArgs fw = s->fw;
+    fw.fuse_update = fuse_update ? 1 : 0;
+    fw_launch(s->model, s->t->pf / 4, fw, s->ua, s->nblk_fw, s->smem_fw, st, true);
+    FL_CHECK_LAUNCH();
+    return FL_OK;
+  }
   fl_table* t = s->t;
   // the sort source's bins are zeroed by k_glm_dim_q (after its PDL wait)
   if (s->da.ng > 0) {
@@ -895,7 +920,7 @@ static int glm_launch_iteration(fl_glm* s, cudaStream_t st, bool fuse_update) {
     else
       k_glm_fact_csr<1><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
   } else if (s->use_fw)
-    fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st, true);
+    fw_launch(s->model, s->t->pf / 4, s->fw, s->ua, s->nblk_fw, s->smem_fw, st, true);
   else if (s->model == FL_MODEL_LINREG)
     k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
   else
@@ -1283,6 +1308,44 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     ua.nblk_dim[d] = da.nblk[d];
   }
   trace.mark("dim geometry");
+  // solo iteration (one kernel per GD step): the only gathered source is the
+  // sort source, its rows are <= FW_SOLO_PITCH wide, and every fact-pass
+  // CTA references <= FW_QCAP of its rows.  FL_GLM_SOLO=0 disables it.
+  {
+    const char* e = getenv("FL_GLM_SOLO");
+    const bool off = e && atoi(e) == 0;
+    if (!off && s->use_fw && !s->use_csr && ng == 1 && t->sort_g == 0 &&
+        t->g[0].pitch <= FW_SOLO_PITCH) {
+      const int rw = 32 * (c4 <= 7 ? 2 : 1);
+      if ((rc = s->solo_span.alloc(16))) return rc;
+      FL_CUDA(cudaMemsetAsync(s->solo_span.p, 0, 4, st));
+      k_glm_solo_span<<<(unsigned)ceil_div(s->nblk_fw, 256), 256, 0, st>>>(
+          t->g[0].fk->as<int32_t>(), t->g[0].n_neg, t->r_T, s->fw.nunits, rw, s->nblk_fw,
+          s->solo_span.as<int>());
+      FL_CHECK_LAUNCH();
+      int span = 0;
+      FL_CUDA(cudaMemcpyAsync(&span, s->solo_span.p, 4, cudaMemcpyDeviceToHost, st));
+      FL_CUDA(cudaStreamSynchronize(st));
+      const size_t extra = (size_t)FW_QCAP * 4 + (size_t)FW_WARPS * FW_LCAP * sizeof(SoloRec) +
+                           (size_t)FW_WARPS * FW_SOLO_PITCH * 8;
+      const size_t smem_solo = s->smem_fw + extra;
+      if (span <= FW_QCAP && smem_solo <= 227 * 1024) {
+        const void* kfw = fw_kernel(model, c4);
+        FL_CUDA(cudaFuncSetAttribute(kfw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_solo));
+        if ((rc = s->solo_part.alloc((size_t)s->nblk_fw * t->g[0].pitch * 8))) return rc;
+        GlmFactWArgs& fw = s->fw;
+        fw.solo = 1;
+        fw.S0 = t->g[0].S->as<float>();
+        fw.pitch0 = t->g[0].pitch;
+        fw.w0d = da.w[0];
+        fw.n_neg0 = t->g[0].n_neg;
+        fw.part_d = s->solo_part.as<double>();
+        s->smem_fw = smem_solo;
+        s->solo = true;
+      }
+    }
+  }
   FL_CUDA(cudaStreamSynchronize(st));
   trace.mark("done");
   *out = guard.release();
@@ -1420,6 +1483,25 @@ int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
     cudaEventDestroy(e1);
     return FL_OK;
   }
+  if (s->solo) {   // [0, the one kernel, 0]
+    cudaEvent_t e0, e1;
+    FL_CUDA(cudaEventCreate(&e0));
+    FL_CUDA(cudaEventCreate(&e1));
+    FL_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; i++) {
+      const int rc = glm_launch_iteration(s, st, true);
+      if (rc) return rc;
+    }
+    FL_CUDA(cudaEventRecord(e1, st));
+    FL_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FL_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ms_out[0] = ms_out[2] = 0.f;
+    ms_out[1] = ms / iters;
+    return FL_OK;
+  }
   cudaEvent_t ev[4];
   for (auto& e : ev) FL_CUDA(cudaEventCreate(&e));
   float acc[3] = {0.f, 0.f, 0.f};
@@ -1437,7 +1519,7 @@ int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream) {
       else
         k_glm_fact_csr<1><<<s->nblk_fw, FW_WARPS * 32, s->smem_csr, st>>>(s->csr);
     } else if (s->use_fw)
-      fw_launch(s->model, s->t->pf / 4, s->fw, s->nblk_fw, s->smem_fw, st);
+      fw_launch(s->model, s->t->pf / 4, s->fw, s->ua, s->nblk_fw, s->smem_fw, st);
     else if (s->model == FL_MODEL_LINREG)
       k_glm_fact<0><<<s->nblk_fact, NTHREADS, s->smem_fact, st>>>(s->fa);
     else

@@ -16,6 +16,9 @@
 
 constexpr int FW_WARPS = 8;        // warps per CTA
 constexpr int FW_FLUSH = 16;       // stages between fp32 -> fp64 flushes
+constexpr int FW_LCAP = 32;        // solo: segment records per warp before a gradient flush
+constexpr int FW_QCAP = 4096;      // solo: q entries per CTA (dimension rows it references)
+constexpr int FW_SOLO_PITCH = 64;  // solo: widest sort-source row
 // narrow rows (C4 <= 7) run two CTAs (16 warps) per SM: the pass is
 // latency-bound at one CTA (ncu r01: 12.5% warps active, issue 39%)
 __host__ __device__ constexpr int fw_min_blocks(int c4) { return c4 <= 7 ? 2 : 1; }
@@ -82,10 +85,52 @@ struct GlmFactWArgs {
   GlmState* state;
   uint32_t stage_bytes, off_y, off_fk;
   int nst;
+  // solo iteration: the only gathered source is the sort source, so each CTA
+  // computes the q_d entries its rows reference (a contiguous dimension-row
+  // range) in its prologue, and turns its segment sums into that source's
+  // gradient partial S_d^T bins (linear in the bins, so warp- and CTA-
+  // boundary segments need no stitching); the last CTA reduces and updates.
+  // One kernel per GD iteration (dim_q / dim_t are not launched).
+  int solo, fuse_update;
+  const float* S0;           // sort source values, r_0 x pitch0
+  int pitch0;
+  const float* w0d;          // fp32 w of the sort source's columns (pitch0)
+  int64_t n_neg0;            // device rows without a match (FK -1, at the front)
+  double* part_d;            // gridDim.x x pitch0
 };
 
+struct SoloRec {
+  int key;
+  float v;
+};
+
+// the last CTA of a solo iteration: red = sum over CTAs of [grad_F | loss]
+// and of the sort source's gradient partials (fixed order), then the update
+__device__ __noinline__ void glm_solo_reduce(const GlmFactWArgs& a, const UpdateArgs& u, int pf) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int c = tid; c <= u.c_T; c += blockDim.x) u.red[c] = 0.0;
+  __syncthreads();
+  const int nb = gridDim.x;
+  for (int e = warp; e <= pf + a.pitch0; e += nw) {
+    double v;
+    int dst;
+    if (e <= pf) {
+      v = warp_sum_strided(a.part + e, pf + 1, nb, lane);
+      dst = e == pf ? u.c_T : u.f_tcol[e];
+    } else {
+      const int c = e - pf - 1;
+      v = warp_sum_strided(a.part_d + c, a.pitch0, nb, lane);
+      dst = u.d_tcol[a.sort_g][c];
+    }
+    if (lane == 0 && dst >= 0) u.red[dst] = v;
+  }
+  __syncthreads();
+  if (a.fuse_update) glm_apply_update(u);
+}
+
 template <int MODEL, int C4, int RPL>
-__global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w(GlmFactWArgs a) {
+__global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
+    k_glm_fact_w(GlmFactWArgs a, UpdateArgs u) {
   constexpr int RW = 32 * RPL;               // rows per warp stage
   constexpr bool W_REG = C4 <= 9;            // w in registers (else smem broadcast)
   extern __shared__ __align__(128) char smem[];
@@ -132,7 +177,53 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
   pdl_trigger();
   for (int j = threadIdx.x; j < C4; j += blockDim.x)
     w_s[j] = reinterpret_cast<const float4*>(a.wF)[j];
+  // solo: q_d of the dimension rows this CTA's rows reference
+  char* solo_sm = smem + (size_t)FW_WARPS * a.nst * a.stage_bytes;
+  float* q_s = reinterpret_cast<float*>(solo_sm);
+  SoloRec* rec = reinterpret_cast<SoloRec*>(q_s + FW_QCAP) + warp * FW_LCAP;
+  int k_lo = 0;
+  if (a.solo) {
+    const int64_t cw0 = (int64_t)blockIdx.x * FW_WARPS, cw1 = cw0 + FW_WARPS;
+    const int64_t cu0 = cw0 * base + min64(cw0, rem), cu1 = cw1 * base + min64(cw1, rem);
+    const int64_t rlo = max64(cu0 * RW, a.n_neg0), rhi = min64(cu1 * RW, a.r_T) - 1;
+    int nq = 0;
+    if (rlo <= rhi) {
+      k_lo = fks[rlo];
+      nq = fks[rhi] - k_lo + 1;
+    }
+    const int p4 = a.pitch0 / 4;
+    const float4* w04 = reinterpret_cast<const float4*>(a.w0d);
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+      const float4* sr = reinterpret_cast<const float4*>(a.S0 + (int64_t)(k_lo + i) * a.pitch0);
+      float z = 0.f;
+      for (int j = 0; j < p4; j++) {
+        const float4 v = sr[j], ww = w04[j];
+        z = fmaf(v.x, ww.x, z);
+        z = fmaf(v.y, ww.y, z);
+        z = fmaf(v.z, ww.z, z);
+        z = fmaf(v.w, ww.w, z);
+      }
+      q_s[i] = z;
+    }
+  }
   __syncthreads();
+  // solo: this warp's share of the sort source's gradient, sum_seg v S_d[key]
+  double gd[FW_SOLO_PITCH / 32] = {0.0, 0.0};
+  int ln = 0;   // records pending in rec[]
+  auto solo_flush = [&]() {
+    __syncwarp();
+    for (int e = 0; e < ln; e++) {
+      const SoloRec rr = rec[e];
+      const float* sr = a.S0 + (int64_t)rr.key * a.pitch0;
+#pragma unroll
+      for (int m = 0; m < FW_SOLO_PITCH / 32; m++) {
+        const int c = lane + 32 * m;
+        if (c < a.pitch0) gd[m] += (double)rr.v * (double)__ldg(sr + c);
+      }
+    }
+    __syncwarp();
+    ln = 0;
+  };
   float4 w[W_REG ? C4 : 1];
   if (W_REG) {
 #pragma unroll
@@ -145,6 +236,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
     int k0 = fks[W0];
     if (k0 >= 0 && fks[W0 - 1] == k0) head_key = k0;
   }
+  if (a.solo) head_key = -1;   // linear: a partial first segment is emitted as is
   bool head_open = head_key >= 0;
   float head_val = 0.f;
   int ck = -1;          // running segment key (warp uniform)
@@ -192,7 +284,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
       float gq = 0.f;
       for (int d = 0; d < a.ng; d++) {
         int32_t fk = (d == a.sort_g) ? key : a.fk[d][p];
-        if (fk >= 0) gq += __ldg(a.q[d] + fk);
+        if (fk >= 0) gq += (a.solo && d == a.sort_g) ? q_s[fk - k_lo] : __ldg(a.q[d] + fk);
       }
       float4 x[C4];
 #pragma unroll
@@ -250,23 +342,35 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
         // rows continuing the running segment (keys are non-decreasing)
         if (key >= 0 && key == ck) v += cv;
         const int k0 = __shfl_sync(0xffffffffu, key, 0);
-        if (ck >= 0 && k0 != ck) {              // running segment is complete
-          if (head_open && ck == head_key) {
-            head_val = cv;
-            head_open = false;
-          } else if (lane == 0) {
-            a.bins[ck] = cv;
-          }
-        }
         const int kn = __shfl_down_sync(0xffffffffu, key, 1);
         const bool end = lane < 31 && key >= 0 && kn != key;
-        const bool eh = end && head_open && key == head_key;
-        const unsigned bm = __ballot_sync(0xffffffffu, eh);
-        if (bm) {
-          head_val = __shfl_sync(0xffffffffu, v, __ffs(bm) - 1);
-          head_open = false;
+        if (a.solo) {
+          // completed segments -> records (fixed order: running one first,
+          // then by lane); flushed into the gradient when the list fills
+          const bool run_done = ck >= 0 && k0 != ck;
+          const unsigned em = __ballot_sync(0xffffffffu, end);
+          const int m = __popc(em) + (run_done ? 1 : 0);
+          if (ln + m > FW_LCAP) solo_flush();
+          if (run_done && lane == 0) rec[ln] = SoloRec{ck, cv};
+          if (end) rec[ln + (run_done ? 1 : 0) + __popc(em & ((1u << lane) - 1u))] = SoloRec{key, v};
+          ln += m;
+        } else {
+          if (ck >= 0 && k0 != ck) {              // running segment is complete
+            if (head_open && ck == head_key) {
+              head_val = cv;
+              head_open = false;
+            } else if (lane == 0) {
+              a.bins[ck] = cv;
+            }
+          }
+          const bool eh = end && head_open && key == head_key;
+          const unsigned bm = __ballot_sync(0xffffffffu, eh);
+          if (bm) {
+            head_val = __shfl_sync(0xffffffffu, v, __ffs(bm) - 1);
+            head_open = false;
+          }
+          if (end && !eh) a.bins[key] = v;
         }
-        if (end && !eh) a.bins[key] = v;
         ck = __shfl_sync(0xffffffffu, key, 31);
         cv = __shfl_sync(0xffffffffu, v, 31);
       }
@@ -280,8 +384,18 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
   }
   flush();
 
+  // solo: the running segment is emitted as is; the warp's gradient share
+  // goes to shared memory for the CTA's fixed-order sum
+  if (a.solo) {
+    if (ck >= 0) {
+      if (ln + 1 > FW_LCAP) solo_flush();
+      if (lane == 0) rec[ln] = SoloRec{ck, cv};
+      ln += 1;
+    }
+    solo_flush();
+  }
   // warp range end: running segment -> carry record
-  if (has_sort) {
+  if (has_sort && !a.solo) {
     WarpCarry c;
     c.head_key = -1;
     c.tail_key = -1;
@@ -322,6 +436,20 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
       for (int w2 = 0; w2 < FW_WARPS; w2++) sum += lsum[w2];
     out[t] = sum;
   }
+  if (a.solo) {
+    double* gsd = reinterpret_cast<double*>(rec + FW_LCAP * (FW_WARPS - warp));   // past all lists
+#pragma unroll
+    for (int m = 0; m < FW_SOLO_PITCH / 32; m++) {
+      const int c = lane + 32 * m;
+      if (c < a.pitch0) gsd[warp * FW_SOLO_PITCH + c] = gd[m];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < a.pitch0; c += blockDim.x) {
+      double sum = 0.0;
+      for (int w2 = 0; w2 < FW_WARPS; w2++) sum += gsd[w2 * FW_SOLO_PITCH + c];
+      a.part_d[(int64_t)blockIdx.x * a.pitch0 + c] = sum;
+    }
+  }
   // last CTA stitches the segments that span warp ranges (fixed order)
   __threadfence();
   __syncthreads();
@@ -329,7 +457,10 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1)) k_glm_fact_w
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  if (has_sort)
+  if (a.solo) {
+    glm_solo_reduce(a, u, C4 * 4);
+  } else if (has_sort) {
     stitch_carries(a.carry, NW, a.bins, smem, (size_t)FW_WARPS * a.nst * a.stage_bytes);
+  }
   if (threadIdx.x == 0) a.state->done_fact = 0;
 }

@@ -25,8 +25,9 @@
 constexpr int G5_TILE = 128;
 constexpr int G5_EPI = 256;
 constexpr int G5_THREADS = 64 + G5_EPI;
-constexpr int G5_NS = 2;
+constexpr int G5_NS = 3;
 constexpr int G5_FT = 4;
+constexpr int G5_PD = 6;              // tiles prefetched into L2 ahead of the TMA loads
 
 struct GnT5Args {
   int pf, c_T;
@@ -44,7 +45,7 @@ struct GnT5Args {
 
 struct G5Geom {
   uint32_t stage, o_f, o_fk;       // stage: W (16 KB) | F (16 KB) | FKs (512 B)
-  uint32_t o_lo;                   // 2 buffers x [W_lo | F_lo] (K-major SW128, 2 x 16 KB)
+  uint32_t o_lo;                   // W_lo | F_lo (K-major SW128, 2 x 16 KB)
   uint32_t o_ops;                  // W' | W'_lo | F | F_lo (MN-major, 4 x 16 KB)
   uint32_t o_cst;                  // H_F hi | H_F lo | HH hi | HH lo (interleave, 4 x 4 KB)
   uint32_t total;
@@ -56,7 +57,7 @@ __host__ __device__ inline G5Geom g5_geom() {
   g.o_fk = 32768;
   g.stage = 32768 + 1024;
   g.o_lo = G5_NS * g.stage;
-  g.o_ops = g.o_lo + 2 * 32768;
+  g.o_ops = g.o_lo + 32768;
   g.o_cst = g.o_ops + 65536;
   g.total = g.o_cst + 16384;
   return g;
@@ -133,8 +134,17 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     // =================== producer ===================
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
+      for (int i = 0; i < G5_PD && i < n; i++) {
+        tma_prefetch_2d(&tmW, 0, (int)((t0 + i) * G5_TILE));
+        tma_prefetch_2d(&tmF, 0, (int)((t0 + i) * G5_TILE));
+      }
       for (int i = 0; i < n; i++) {
         const int s = i % G5_NS;
+        if (i + G5_PD < n) {
+          tma_prefetch_2d(&tmW, 0, (int)((t0 + i + G5_PD) * G5_TILE));
+          tma_prefetch_2d(&tmF, 0, (int)((t0 + i + G5_PD) * G5_TILE));
+          if (a.ng) bulk_prefetch_l2(a.fk + (t0 + i + G5_PD) * G5_TILE, 512);
+        }
         if (i >= G5_NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / G5_NS) - 1) & 1));
         char* st = sm + s * gm.stage;
         const int row = (int)((t0 + i) * G5_TILE);
@@ -158,7 +168,7 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         mbar_wait_sleep(&lo_ready[b], (uint32_t)((t >> 1) & 1));   // (implies the stage landed)
         tc::fence_after();
         const uint32_t st = smem_u32(sm + (t % G5_NS) * gm.stage);
-        const uint32_t lo = smem_u32(sm + gm.o_lo + b * 32768);
+        const uint32_t lo = smem_u32(sm + gm.o_lo);
         const uint32_t tq = tmem + 64 * b;
         for (int ks = 0; ks < kst; ks++) {   // Q = F H_F^T
           const uint64_t ah = tc::smem_desc(st + gm.o_f + ks * 32, 16, 1024, tc::kSw128);
@@ -189,9 +199,13 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         if ((t % G5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
         tc::fence_after();
         const uint32_t tp = tmem + 128 + 64 * b;
+        // A = 4 MN groups [W' | W'_lo | F | F_lo], B = [W' | W'_lo]; a K step
+        // of 8 rows advances the start address by 1024 B (64 in the 16-byte
+        // address field)
+        const uint64_t ad0 = tc::smem_desc(ops, 16384, 512, tc::kSw128B32);
+#pragma unroll
         for (int kk = 0; kk < G5_TILE / 8; kk++) {
-          // A = 4 MN groups [W' | W'_lo | F | F_lo], B = [W' | W'_lo]
-          const uint64_t ad = tc::smem_desc(ops + kk * 1024, 16384, 512, tc::kSw128B32);
+          const uint64_t ad = ad0 + (uint64_t)(kk * 64);
           tc::mma_tf32(tp, ad, ad, id_pg, !((t % G5_FT) == 0 && kk == 0));
         }
         tc::commit(&empty[s]);
@@ -237,18 +251,20 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     };
     // lo parts of tile t for Q / V (K-major SW128, buffer t & 1); F_lo also
     // goes to the PG operand once the buffer is free (see below)
+    float4 flo_next[4];   // F_lo of the tile split last (reused for its PG operand)
     auto split = [&](int t) {
       mbar_wait_sleep(&full[t % G5_NS], (uint32_t)((t / G5_NS) & 1));
       float w[16], x[16];
       load_row(t, w, x);
-      char* lo_b = sm + gm.o_lo + (t & 1) * 32768;
+      char* lo_b = sm + gm.o_lo;
 #pragma unroll
       for (int u = 0; u < 4; u++) {
         const int c4 = 4 * h + u;
         *reinterpret_cast<float4*>(lo_b + g5_sw128(r, c4)) =
             make_float4(g5_lo(w[4 * u]), g5_lo(w[4 * u + 1]), g5_lo(w[4 * u + 2]), g5_lo(w[4 * u + 3]));
-        *reinterpret_cast<float4*>(lo_b + 16384 + g5_sw128(r, c4)) =
-            make_float4(g5_lo(x[4 * u]), g5_lo(x[4 * u + 1]), g5_lo(x[4 * u + 2]), g5_lo(x[4 * u + 3]));
+        flo_next[u] = make_float4(g5_lo(x[4 * u]), g5_lo(x[4 * u + 1]), g5_lo(x[4 * u + 2]),
+                                  g5_lo(x[4 * u + 3]));
+        *reinterpret_cast<float4*>(lo_b + 16384 + g5_sw128(r, c4)) = flo_next[u];
       }
       fence_proxy_async();
       tc::fence_before();
@@ -258,14 +274,13 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     for (int t = 0; t < n; t++) {
       const int s = t % G5_NS;
       char* st = sm + s * gm.stage;
-      // software pipeline: the next tile's lo parts go out before this
-      // tile's Q / V are awaited, so its MMAs overlap this tile's epilogue
-      if (UPDATE && t + 1 < n) split(t + 1);
       mbar_wait_sleep(&full[s], (uint32_t)((t / G5_NS) & 1));
       const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
       const int fk = a.ng ? fks[r] : -1;
       float w[16], x[16];
-      load_row(t, w, x);
+      float4 flo[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) flo[u] = flo_next[u];
       if (UPDATE) {
         float4 gl[4];
 #pragma unroll
@@ -281,6 +296,12 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         tc::ld16(tmem + lane_off + 64 * (t & 1) + 16 * h, qq);
         tc::ld16(tmem + lane_off + 64 * (t & 1) + 32 + 16 * h, vv);
         tc::wait_ld();
+        tc::fence_before();
+        // software pipeline: Q / V(t) are done with the lo buffer, so the
+        // next tile's lo parts go out now and its MMAs overlap the rest of
+        // this tile's epilogue
+        if (t + 1 < n) split(t + 1);
+        load_row(t, w, x);
         // W' = W o (Q + G_d[fk]) / (V + eps)   (k_gnmf_fact's expression)
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -292,30 +313,25 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
             w[j] = w[j] * __fdividef(qv, __uint_as_float(vv[j]) + 1e-12f);
           }
         }
+      } else {
+        load_row(t, w, x);
       }
       // PG operand rows: W' | W'_lo | F | F_lo (MN-major B32); the previous
-      // tile's PG MMAs and W' store must be done with the buffer.  Chunks
-      // are written in a per-row rotated order: rows r and r + 4 (same
-      // swizzle granule) then hit different 16-byte halves (no conflicts)
+      // tile's PG MMAs and W' store must be done with the buffer
       if (t >= 1) mbar_wait_sleep(&ops_free, (uint32_t)((t - 1) & 1));
       if (UPDATE && tid == 64) bulk_wait_read<0>();
       if (UPDATE) named_sync(1, G5_EPI);
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        const int uu = (u + ((r >> 2) & 1)) & 3;
-        const int c4 = 4 * h + uu;
-        float wv[4], xv[4];
-#pragma unroll
-        for (int e = 0; e < 4; e++) {   // select by the rotated index (registers only)
-          wv[e] = uu == 0 ? w[e] : uu == 1 ? w[4 + e] : uu == 2 ? w[8 + e] : w[12 + e];
-          xv[e] = uu == 0 ? x[e] : uu == 1 ? x[4 + e] : uu == 2 ? x[8 + e] : x[12 + e];
-        }
-        *reinterpret_cast<float4*>(ops + g5_b32(r, c4)) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        const int c4 = 4 * h + u;
+        const float4 wv = make_float4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+        const float4 xv = make_float4(x[4 * u], x[4 * u + 1], x[4 * u + 2], x[4 * u + 3]);
+        *reinterpret_cast<float4*>(ops + g5_b32(r, c4)) = wv;
         *reinterpret_cast<float4*>(ops + 16384 + g5_b32(r, c4)) =
-            make_float4(g5_lo(wv[0]), g5_lo(wv[1]), g5_lo(wv[2]), g5_lo(wv[3]));
-        *reinterpret_cast<float4*>(ops + 32768 + g5_b32(r, c4)) = make_float4(xv[0], xv[1], xv[2], xv[3]);
+            make_float4(g5_lo(wv.x), g5_lo(wv.y), g5_lo(wv.z), g5_lo(wv.w));
+        *reinterpret_cast<float4*>(ops + 32768 + g5_b32(r, c4)) = xv;
         *reinterpret_cast<float4*>(ops + 49152 + g5_b32(r, c4)) =
-            make_float4(g5_lo(xv[0]), g5_lo(xv[1]), g5_lo(xv[2]), g5_lo(xv[3]));
+            UPDATE ? flo[u] : make_float4(g5_lo(xv.x), g5_lo(xv.y), g5_lo(xv.z), g5_lo(xv.w));
       }
       fence_proxy_async();
       named_sync(1, G5_EPI);
@@ -354,9 +370,12 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       }
       tc::fence_before();
       mbar_arrive(&ops_ready);
-      if ((t % G5_FT) == G5_FT - 1) fold(t / G5_FT);
+      // fold a finished window one tile late: its MMAs complete while the
+      // next tile's epilogue runs (the PG accumulator is double-buffered)
+      if ((t % G5_FT) == 0 && t >= G5_FT) fold(t / G5_FT - 1);
     }
-    if (n > 0 && ((n - 1) % G5_FT) != G5_FT - 1) fold((n - 1) / G5_FT);
+    // the loop folded windows 0 .. wl - 1; the last one is left
+    if (n > 0) fold((n - 1) / G5_FT);
     if (UPDATE && tid == 64) bulk_wait<0>();
     double* sc = a.scratch + ((int64_t)blockIdx.x * G5_TILE + r) * 64 + 32 * h;
 #pragma unroll

@@ -384,6 +384,19 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, int co
       : "memory");
 }
 
+// L2 prefetch of a 2-D TMA box / a 1-D bulk range (no shared memory, no
+// completion): a producer runs these PD tiles ahead of its loads so the
+// loads hit L2 and more HBM traffic is in flight than the stages hold
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int col, int row) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(col), "r"(row)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // TMA 2-D tile store shared -> global (bulk-group completion)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int col, int row,
                                              const void* src) {

@@ -32,6 +32,7 @@ constexpr int K5_THREADS = 64 + K5_GAT + K5_EPI;
 constexpr int K5_NS_MAX = 3;          // TMA stages (2 or 3: whatever fits)
 constexpr int K5_FT = 4;              // tiles per fp32 sums window
 constexpr int K5_SC = 32;             // F columns in the operand tiles (pf <= 28)
+constexpr int K5_PD = 8;              // tiles prefetched into L2 ahead of the TMA loads
 
 struct KmT5Args {
   int pf, c_T, k;
@@ -156,8 +157,13 @@ __global__ void __launch_bounds__(K5_THREADS, 1)
     // =================== producer ===================
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
+      for (int i = 0; i < K5_PD && i < n; i++) tma_prefetch_2d(&tmF, 0, (int)((t0 + i) * K5_TILE));
       for (int i = 0; i < n; i++) {
         const int s = i % NS;
+        if (i + K5_PD < n) {
+          tma_prefetch_2d(&tmF, 0, (int)((t0 + i + K5_PD) * K5_TILE));
+          for (int d = 0; d < ng; d++) bulk_prefetch_l2(a.fk[d] + (t0 + i + K5_PD) * K5_TILE, 512);
+        }
         if (i >= NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / NS) - 1) & 1));
         char* st = sm + s * gm.stage;
         mbar_arrive_expect_tx(&full[s], 16384u + 512u * ng);

@@ -49,7 +49,7 @@ def test_kmeans_t5_matches_reference(fl, t5, name):
                                                 (24, [(4000, 7)], 5, 30_000),
                                                 (32, [(600, 60)], 28, 50_000),
                                                 (9, [], 20, 20_000),
-                                                (16, [(60 + 7 * i, 3) for i in range(8)], 8, 25_000)])
+                                                (16, [(60 + 7 * i, 3) for i in range(4)], 8, 25_000)])
 def test_kmeans_t5_planted_vs_oracle(fl, t5, k, dims, c_fact, rows):
     from paper_2502_01985_b200.trainers import KMeansSession, kmeans_init
     ft = planted_seeded(21, rows, dims, c_fact, k, 3)

@@ -454,3 +454,35 @@ def test_glm_pdl_launch_is_bit_identical(tmp_path):
         subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=300)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("model", ["linreg", "logreg"])
+@pytest.mark.parametrize("dims,rows", [([(1000, 50)], 100_000), ([(30, 7)], 70_000),
+                                       ([(60_000, 13)], 120_000)])
+def test_glm_solo_iteration_vs_three_kernel_path(fl, model, dims, rows, monkeypatch):
+    """The one-kernel GLM iteration (sort source only: q_d staged per CTA,
+    the dimension gradient from the segment sums, reduction + update by the
+    last CTA) against the three-kernel path and the oracle."""
+    from paper_2502_01985_b200.trainers import GlmSession
+    ft = star_table(71, rows, dims, 20)
+    tab = oracle.OracleTable.from_ft(ft)
+    rng = np.random.default_rng(4)
+    y = (rng.random(ft.r_T) if model == "linreg" else rng.integers(0, 2, ft.r_T)).astype(np.float64)
+    lr = rt.safe_learning_rate(tab)
+    want = rt.train(model, tab, iterations=9, learning_rate=lr, y=y)
+    h = fl.TargetHandle.factorized(ft)
+    got = {}
+    for solo in ("1", "0"):
+        monkeypatch.setenv("FL_GLM_SOLO", solo)
+        s = GlmSession(h, model, y, lr)
+        s.run(9)
+        got[solo] = s.result(9)
+        s.close()
+        w, loss = got[solo]
+        assert max_rel(loss, want["loss_history"]) < TOL
+        assert max_rel(w, want["parameters"]["w"].ravel()) < TOL
+    assert max_rel(got["1"][0], got["0"][0]) < 1e-5
+    monkeypatch.setenv("FL_GLM_SOLO", "1")
+    a = fl.train(model, h, fl.TrainConfig(iterations=5, learning_rate=lr), y.reshape(-1, 1))
+    b = fl.train(model, h, fl.TrainConfig(iterations=5, learning_rate=lr), y.reshape(-1, 1))
+    assert np.array_equal(a.parameters["w"], b.parameters["w"]) and a.loss_history == b.loss_history
