@@ -693,7 +693,8 @@ static void launch_fw(const GlmFactWArgs& a, const UpdateArgs& u, int grid, size
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = (pdl && std::getenv("FL_NO_PDL") == nullptr) ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k_glm_fact_w<MODEL, C4, RPL>, a, u);
+  (void)u;
+  cudaLaunchKernelEx(&cfg, k_glm_fact_w<MODEL, C4, RPL>, a);
 }
 template <int MODEL, int C4>
 static const void* fw_ptr() {
@@ -813,7 +814,7 @@ struct fl_glm {
   int bins_rows = 0;
   bool use_fw = false;
   bool solo = false;       // one-kernel iteration (glm_fact_warp.cuh, solo)
-  DevBuf solo_part, solo_span;
+  DevBuf solo_part, solo_span, ua_dev;
   GlmFactWArgs fw{};
   int nblk_fw = 0;
   size_t smem_fw = 0;
@@ -1329,7 +1330,11 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
       const size_t extra = (size_t)FW_QCAP * 4 + (size_t)FW_WARPS * FW_LCAP * sizeof(SoloRec) +
                            (size_t)FW_WARPS * FW_SOLO_PITCH * 8;
       const size_t smem_solo = s->smem_fw + extra;
-      if (span <= FW_QCAP && smem_solo <= 227 * 1024) {
+      // a CTA stages its q rows before streaming: worth it while that
+      // prologue is short (C1: 34 rows per CTA, one kernel instead of three);
+      // at C2 (3.4K rows, 700 KB per CTA) the separate dim kernels win
+      const int span_max = e ? FW_QCAP : 512;   // FL_GLM_SOLO=1 forces up to FW_QCAP
+      if (span <= span_max && smem_solo <= 227 * 1024) {
         const void* kfw = fw_kernel(model, c4);
         FL_CUDA(cudaFuncSetAttribute(kfw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_solo));
@@ -1341,6 +1346,9 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         fw.w0d = da.w[0];
         fw.n_neg0 = t->g[0].n_neg;
         fw.part_d = s->solo_part.as<double>();
+        if ((rc = s->ua_dev.alloc(sizeof(UpdateArgs)))) return rc;
+        FL_CUDA(cudaMemcpy(s->ua_dev.p, &ua, sizeof(UpdateArgs), cudaMemcpyHostToDevice));
+        fw.up = s->ua_dev.as<UpdateArgs>();
         s->smem_fw = smem_solo;
         s->solo = true;
       }

@@ -97,6 +97,7 @@ struct GlmFactWArgs {
   const float* w0d;          // fp32 w of the sort source's columns (pitch0)
   int64_t n_neg0;            // device rows without a match (FK -1, at the front)
   double* part_d;            // gridDim.x x pitch0
+  const UpdateArgs* up;      // the session's update arguments (device copy: no param copies)
 };
 
 struct SoloRec {
@@ -105,32 +106,39 @@ struct SoloRec {
 };
 
 // the last CTA of a solo iteration: red = sum over CTAs of [grad_F | loss]
-// and of the sort source's gradient partials (fixed order), then the update
-__device__ __noinline__ void glm_solo_reduce(const GlmFactWArgs& a, const UpdateArgs& u, int pf) {
+// and of the sort source's gradient partials (fixed order), then the update.
+// Arguments are plain pointers / scalars and the update arguments live in
+// global memory: nothing forces a local copy of a kernel parameter struct.
+__device__ __noinline__ void glm_solo_reduce(const double* __restrict__ part,
+                                             const double* __restrict__ part_d, int pf, int pitch0,
+                                             int sort_g, int fuse_update, const UpdateArgs* u) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int c = tid; c <= u.c_T; c += blockDim.x) u.red[c] = 0.0;
+  const int c_T = u->c_T;
+  double* red = u->red;
+  for (int c = tid; c <= c_T; c += blockDim.x) red[c] = 0.0;
   __syncthreads();
   const int nb = gridDim.x;
-  for (int e = warp; e <= pf + a.pitch0; e += nw) {
+  const int32_t* dt = u->d_tcol[sort_g];
+  for (int e = warp; e <= pf + pitch0; e += nw) {
     double v;
     int dst;
     if (e <= pf) {
-      v = warp_sum_strided(a.part + e, pf + 1, nb, lane);
-      dst = e == pf ? u.c_T : u.f_tcol[e];
+      v = warp_sum_strided(part + e, pf + 1, nb, lane);
+      dst = e == pf ? c_T : u->f_tcol[e];
     } else {
       const int c = e - pf - 1;
-      v = warp_sum_strided(a.part_d + c, a.pitch0, nb, lane);
-      dst = u.d_tcol[a.sort_g][c];
+      v = warp_sum_strided(part_d + c, pitch0, nb, lane);
+      dst = dt[c];
     }
-    if (lane == 0 && dst >= 0) u.red[dst] = v;
+    if (lane == 0 && dst >= 0) red[dst] = v;
   }
   __syncthreads();
-  if (a.fuse_update) glm_apply_update(u);
+  if (fuse_update) glm_apply_update(*u);
 }
 
 template <int MODEL, int C4, int RPL>
 __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
-    k_glm_fact_w(GlmFactWArgs a, UpdateArgs u) {
+    k_glm_fact_w(GlmFactWArgs a) {
   constexpr int RW = 32 * RPL;               // rows per warp stage
   constexpr bool W_REG = C4 <= 9;            // w in registers (else smem broadcast)
   extern __shared__ __align__(128) char smem[];
@@ -458,7 +466,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
   if (!is_last) return;
   __threadfence();
   if (a.solo) {
-    glm_solo_reduce(a, u, C4 * 4);
+    glm_solo_reduce(a.part, a.part_d, C4 * 4, a.pitch0, a.sort_g, a.fuse_update, a.up);
   } else if (has_sort) {
     stitch_carries(a.carry, NW, a.bins, smem, (size_t)FW_WARPS * a.nst * a.stage_bytes);
   }

@@ -17,13 +17,15 @@
 //                                         K = 128 rows of the tile
 //               PG reads its four row-major [128 x 32] tiles MN-major (128B /
 //               32-byte-atom swizzle, descriptor layout 1): no transposes.
-//   warps 2-9   epilogue, thread = (tile row, 16-column half): lo parts of W
+//   warps 2-17  epilogue, thread = (tile row, 8-column group): lo parts of W
 //               and F for Q / V, W' from Q, V and the gathered G_d row, the
 //               PG operand rows, the W' TMA store, Z segment sums.
 // PG accumulates in TMEM fp32 over G5_FT tiles (512 rows, k_gnmf_fact's
 // window), then folds into fp64 registers.
 constexpr int G5_TILE = 128;
-constexpr int G5_EPI = 256;
+constexpr int G5_CPT = 8;             // W / Q / V columns per epilogue thread
+constexpr int G5_HG = 32 / G5_CPT;    // epilogue threads per row
+constexpr int G5_EPI = 128 * G5_HG;
 constexpr int G5_THREADS = 64 + G5_EPI;
 constexpr int G5_NS = 3;
 constexpr int G5_FT = 4;
@@ -214,22 +216,23 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       }
     }
   } else {
-    // =================== epilogue: thread = (tile row, 16-column half) ===================
+    // =================== epilogue: thread = (tile row, G5_CPT-column group) ===================
     const int ew = warp - 2, h = ew >> 2, q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
     char* ops = sm + gm.o_ops;
-    double acc[32];
+    constexpr int FC = 64 / G5_HG;   // PG columns this thread folds
+    double acc[FC];
 #pragma unroll
-    for (int j = 0; j < 32; j++) acc[j] = 0.0;
+    for (int j = 0; j < FC; j++) acc[j] = 0.0;
     auto fold = [&](int w) {
       const int b = w & 1;
       mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
       tc::fence_after();
       uint32_t x[16];
 #pragma unroll
-      for (int u = 0; u < 2; u++) {
-        tc::ld16(tmem + lane_off + 128 + 64 * b + 32 * h + 16 * u, x);
+      for (int u = 0; u < FC / 16; u++) {
+        tc::ld16(tmem + lane_off + 128 + 64 * b + FC * h + 16 * u, x);
         tc::wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; j++) acc[16 * u + j] += (double)__uint_as_float(x[j]);
@@ -237,12 +240,13 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       tc::fence_before();
       mbar_arrive(&acc_empty[b]);
     };
-    // this thread's 16 columns of the W and F rows of tile t (exact fp32)
-    auto load_row = [&](int t, float (&w)[16], float (&x)[16]) {
+    constexpr int NU = G5_CPT / 4;   // 16-byte chunks per thread
+    // this thread's G5_CPT columns of the W and F rows of tile t (exact fp32)
+    auto load_row = [&](int t, float (&w)[G5_CPT], float (&x)[G5_CPT]) {
       const char* st = sm + (t % G5_NS) * gm.stage;
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int c4 = 4 * h + u;
+      for (int u = 0; u < NU; u++) {
+        const int c4 = NU * h + u;
         const float4 wv = *reinterpret_cast<const float4*>(st + g5_sw128(r, c4));
         const float4 xv = *reinterpret_cast<const float4*>(st + gm.o_f + g5_sw128(r, c4));
         w[4 * u + 0] = wv.x; w[4 * u + 1] = wv.y; w[4 * u + 2] = wv.z; w[4 * u + 3] = wv.w;
@@ -251,15 +255,15 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     };
     // lo parts of tile t for Q / V (K-major SW128, buffer t & 1); F_lo also
     // goes to the PG operand once the buffer is free (see below)
-    float4 flo_next[4];   // F_lo of the tile split last (reused for its PG operand)
+    float4 flo_next[NU];   // F_lo of the tile split last (reused for its PG operand)
     auto split = [&](int t) {
       mbar_wait_sleep(&full[t % G5_NS], (uint32_t)((t / G5_NS) & 1));
-      float w[16], x[16];
+      float w[G5_CPT], x[G5_CPT];
       load_row(t, w, x);
       char* lo_b = sm + gm.o_lo;
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int c4 = 4 * h + u;
+      for (int u = 0; u < NU; u++) {
+        const int c4 = NU * h + u;
         *reinterpret_cast<float4*>(lo_b + g5_sw128(r, c4)) =
             make_float4(g5_lo(w[4 * u]), g5_lo(w[4 * u + 1]), g5_lo(w[4 * u + 2]), g5_lo(w[4 * u + 3]));
         flo_next[u] = make_float4(g5_lo(x[4 * u]), g5_lo(x[4 * u + 1]), g5_lo(x[4 * u + 2]),
@@ -277,24 +281,25 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       mbar_wait_sleep(&full[s], (uint32_t)((t / G5_NS) & 1));
       const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
       const int fk = a.ng ? fks[r] : -1;
-      float w[16], x[16];
-      float4 flo[4];
+      float w[G5_CPT], x[G5_CPT];
+      float4 flo[NU];
 #pragma unroll
-      for (int u = 0; u < 4; u++) flo[u] = flo_next[u];
+      for (int u = 0; u < NU; u++) flo[u] = flo_next[u];
       if (UPDATE) {
-        float4 gl[4];
+        float4 gl[NU];
 #pragma unroll
-        for (int u = 0; u < 4; u++) gl[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < NU; u++) gl[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (fk >= 0) {
-          const float4* gr = reinterpret_cast<const float4*>(a.Gd + (int64_t)fk * 32 + 16 * h);
+          const float4* gr = reinterpret_cast<const float4*>(a.Gd + (int64_t)fk * 32 + G5_CPT * h);
 #pragma unroll
-          for (int u = 0; u < 4; u++) gl[u] = __ldg(gr + u);
+          for (int u = 0; u < NU; u++) gl[u] = __ldg(gr + u);
         }
         mbar_wait_sleep(&qv_full[t & 1], (uint32_t)((t >> 1) & 1));
         tc::fence_after();
-        uint32_t qq[16], vv[16];
-        tc::ld16(tmem + lane_off + 64 * (t & 1) + 16 * h, qq);
-        tc::ld16(tmem + lane_off + 64 * (t & 1) + 32 + 16 * h, vv);
+        uint32_t qq[G5_CPT], vv[G5_CPT];
+        static_assert(G5_CPT == 8, "TMEM loads are 8 columns wide");
+        tc::ld8(tmem + lane_off + 64 * (t & 1) + G5_CPT * h, qq);
+        tc::ld8(tmem + lane_off + 64 * (t & 1) + 32 + G5_CPT * h, vv);
         tc::wait_ld();
         tc::fence_before();
         // software pipeline: Q / V(t) are done with the lo buffer, so the
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         load_row(t, w, x);
         // W' = W o (Q + G_d[fk]) / (V + eps)   (k_gnmf_fact's expression)
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < NU; u++) {
           const float ga[4] = {gl[u].x, gl[u].y, gl[u].z, gl[u].w};
 #pragma unroll
           for (int e = 0; e < 4; e++) {
@@ -321,17 +326,29 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       if (t >= 1) mbar_wait_sleep(&ops_free, (uint32_t)((t - 1) & 1));
       if (UPDATE && tid == 64) bulk_wait_read<0>();
       if (UPDATE) named_sync(1, G5_EPI);
+      static_assert(NU == 2, "the conflict-free store order below pairs two chunks");
+      {
+        // rows r and r + 4 share a 32-byte swizzle granule: odd row quads
+        // store the thread's two 16-byte chunks in swapped order, so the
+        // eight rows of a store phase hit all 32 banks once (no conflicts)
+        const bool sw = (r >> 2) & 1;
+        float4 wq[2], wl[2], xq[2], xl[2];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int c4 = 4 * h + u;
-        const float4 wv = make_float4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
-        const float4 xv = make_float4(x[4 * u], x[4 * u + 1], x[4 * u + 2], x[4 * u + 3]);
-        *reinterpret_cast<float4*>(ops + g5_b32(r, c4)) = wv;
-        *reinterpret_cast<float4*>(ops + 16384 + g5_b32(r, c4)) =
-            make_float4(g5_lo(wv.x), g5_lo(wv.y), g5_lo(wv.z), g5_lo(wv.w));
-        *reinterpret_cast<float4*>(ops + 32768 + g5_b32(r, c4)) = xv;
-        *reinterpret_cast<float4*>(ops + 49152 + g5_b32(r, c4)) =
-            UPDATE ? flo[u] : make_float4(g5_lo(xv.x), g5_lo(xv.y), g5_lo(xv.z), g5_lo(xv.w));
+        for (int u = 0; u < 2; u++) {
+          wq[u] = make_float4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+          wl[u] = make_float4(g5_lo(wq[u].x), g5_lo(wq[u].y), g5_lo(wq[u].z), g5_lo(wq[u].w));
+          xq[u] = make_float4(x[4 * u], x[4 * u + 1], x[4 * u + 2], x[4 * u + 3]);
+          xl[u] = UPDATE ? flo[u] : make_float4(g5_lo(xq[u].x), g5_lo(xq[u].y), g5_lo(xq[u].z), g5_lo(xq[u].w));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          const int uu = sw ? 1 - u : u;
+          const uint32_t o = g5_b32(r, NU * h + uu);
+          *reinterpret_cast<float4*>(ops + o) = sw ? wq[1 - u] : wq[u];
+          *reinterpret_cast<float4*>(ops + 16384 + o) = sw ? wl[1 - u] : wl[u];
+          *reinterpret_cast<float4*>(ops + 32768 + o) = sw ? xq[1 - u] : xq[u];
+          *reinterpret_cast<float4*>(ops + 49152 + o) = sw ? xl[1 - u] : xl[u];
+        }
       }
       fence_proxy_async();
       named_sync(1, G5_EPI);
@@ -339,24 +356,25 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         tma_store_2d_hint(&tmWs, 0, (int)((t0 + t) * G5_TILE), ops, l2_policy_evict_first());
         bulk_commit();
       }
-      // Z[fk] += W' rows: warp (q4, h) takes the 16 rows [32 q4 + 16 h, +16),
+      // Z[fk] += W' rows: warp (q4, h) takes the ZR rows [32 q4 + ZR h, +ZR),
       // lane = rank column; a segment with one FK (the common case: keys are
-      // sorted, fanout >> 16) is one branch-free sum and one fp64 atomic
+      // sorted, fanout >> ZR) is one branch-free sum and one fp64 atomic
       if (a.ng) {
-        const int r0 = 32 * q4 + 16 * h;
+        constexpr int ZR = 32 / G5_HG;
+        const int r0 = 32 * q4 + ZR * h;
         const int c4 = lane >> 2;
-        const int k0 = fks[r0], k1 = fks[r0 + 15];
+        const int k0 = fks[r0], k1 = fks[r0 + ZR - 1];
         const float* zcol = reinterpret_cast<const float*>(ops + (lane & 3) * 4);
         if (k0 == k1) {
           float run = 0.f;
 #pragma unroll
-          for (int rr = 0; rr < 16; rr++)
+          for (int rr = 0; rr < ZR; rr++)
             run += *reinterpret_cast<const float*>(reinterpret_cast<const char*>(zcol) + g5_b32(r0 + rr, c4));
           if (k0 >= 0) atomicAdd(a.Z + (int64_t)k0 * 32 + lane, (double)run);
         } else {
           float run = 0.f;
           int cur = k0;
-          for (int rr = r0; rr < r0 + 16; rr++) {
+          for (int rr = r0; rr < r0 + ZR; rr++) {
             const int f = fks[rr];
             if (f != cur) {
               if (cur >= 0) atomicAdd(a.Z + (int64_t)cur * 32 + lane, (double)run);
@@ -377,9 +395,9 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     // the loop folded windows 0 .. wl - 1; the last one is left
     if (n > 0) fold((n - 1) / G5_FT);
     if (UPDATE && tid == 64) bulk_wait<0>();
-    double* sc = a.scratch + ((int64_t)blockIdx.x * G5_TILE + r) * 64 + 32 * h;
+    double* sc = a.scratch + ((int64_t)blockIdx.x * G5_TILE + r) * 64 + FC * h;
 #pragma unroll
-    for (int j = 0; j < 32; j++) sc[j] = acc[j];
+    for (int j = 0; j < FC; j++) sc[j] = acc[j];
   }
   tc::fence_before();
   __syncthreads();
