@@ -814,7 +814,7 @@ struct fl_glm {
   int bins_rows = 0;
   bool use_fw = false;
   bool solo = false;       // one-kernel iteration (glm_fact_warp.cuh, solo)
-  DevBuf solo_part, solo_span, ua_dev;
+  DevBuf solo_part, solo_span, ua_dev, solo_gcnt, solo_gpart;
   GlmFactWArgs fw{};
   int nblk_fw = 0;
   size_t smem_fw = 0;
@@ -1349,6 +1349,12 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         if ((rc = s->ua_dev.alloc(sizeof(UpdateArgs)))) return rc;
         FL_CUDA(cudaMemcpy(s->ua_dev.p, &ua, sizeof(UpdateArgs), cudaMemcpyHostToDevice));
         fw.up = s->ua_dev.as<UpdateArgs>();
+        const int ngroups = (int)ceil_div(s->nblk_fw, FW_GROUP);
+        if ((rc = s->solo_gcnt.alloc((size_t)ngroups * 4))) return rc;
+        FL_CUDA(cudaMemsetAsync(s->solo_gcnt.p, 0, (size_t)ngroups * 4, st));
+        if ((rc = s->solo_gpart.alloc((size_t)ngroups * (t->pf + 1 + t->g[0].pitch) * 8))) return rc;
+        fw.gcnt = s->solo_gcnt.as<int>();
+        fw.gpart = s->solo_gpart.as<double>();
         s->smem_fw = smem_solo;
         s->solo = true;
       }

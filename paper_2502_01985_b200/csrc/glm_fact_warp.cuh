@@ -19,6 +19,7 @@ constexpr int FW_FLUSH = 16;       // stages between fp32 -> fp64 flushes
 constexpr int FW_LCAP = 32;        // solo: segment records per warp before a gradient flush
 constexpr int FW_QCAP = 4096;      // solo: q entries per CTA (dimension rows it references)
 constexpr int FW_SOLO_PITCH = 64;  // solo: widest sort-source row
+constexpr int FW_GROUP = 16;       // solo: CTAs per first-level reduction group
 // narrow rows (C4 <= 7) run two CTAs (16 warps) per SM: the pass is
 // latency-bound at one CTA (ncu r01: 12.5% warps active, issue 39%)
 __host__ __device__ constexpr int fw_min_blocks(int c4) { return c4 <= 7 ? 2 : 1; }
@@ -98,6 +99,8 @@ struct GlmFactWArgs {
   int64_t n_neg0;            // device rows without a match (FK -1, at the front)
   double* part_d;            // gridDim.x x pitch0
   const UpdateArgs* up;      // the session's update arguments (device copy: no param copies)
+  int* gcnt;                 // per-group arrival counters (zeroed; reset by each group's last CTA)
+  double* gpart;             // groups x (pf + 1 + pitch0): first-level partial sums
 };
 
 struct SoloRec {
@@ -105,32 +108,24 @@ struct SoloRec {
   float v;
 };
 
-// the last CTA of a solo iteration: red = sum over CTAs of [grad_F | loss]
-// and of the sort source's gradient partials (fixed order), then the update.
-// Arguments are plain pointers / scalars and the update arguments live in
-// global memory: nothing forces a local copy of a kernel parameter struct.
-__device__ __noinline__ void glm_solo_reduce(const double* __restrict__ part,
-                                             const double* __restrict__ part_d, int pf, int pitch0,
-                                             int sort_g, int fuse_update, const UpdateArgs* u) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int c_T = u->c_T;
+// the last CTA of a solo iteration: red = the fixed-order sum of the group
+// partials [grad_F | loss | grad_d], then the update.  Arguments are plain
+// pointers / scalars and the update arguments live in global memory: nothing
+// forces a local copy of a kernel parameter struct.
+__device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, int ngroups, int pf,
+                                            int pitch0, int sort_g, int fuse_update,
+                                            const UpdateArgs* u) {
+  const int tid = threadIdx.x;
+  const int c_T = u->c_T, ne = pf + 1 + pitch0;
   double* red = u->red;
   for (int c = tid; c <= c_T; c += blockDim.x) red[c] = 0.0;
   __syncthreads();
-  const int nb = gridDim.x;
   const int32_t* dt = u->d_tcol[sort_g];
-  for (int e = warp; e <= pf + pitch0; e += nw) {
-    double v;
-    int dst;
-    if (e <= pf) {
-      v = warp_sum_strided(part + e, pf + 1, nb, lane);
-      dst = e == pf ? c_T : u->f_tcol[e];
-    } else {
-      const int c = e - pf - 1;
-      v = warp_sum_strided(part_d + c, pitch0, nb, lane);
-      dst = dt[c];
-    }
-    if (lane == 0 && dst >= 0) red[dst] = v;
+  for (int e = tid; e < ne; e += blockDim.x) {
+    double v = 0.0;
+    for (int g = 0; g < ngroups; g++) v += __ldcg(gpart + (int64_t)g * ne + e);
+    const int dst = e < pf ? u->f_tcol[e] : e == pf ? c_T : dt[e - pf - 1];
+    if (dst >= 0) red[dst] = v;
   }
   __syncthreads();
   if (fuse_update) glm_apply_update(*u);
@@ -458,17 +453,44 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
       a.part_d[(int64_t)blockIdx.x * a.pitch0 + c] = sum;
     }
   }
-  // last CTA stitches the segments that span warp ranges (fixed order)
   __threadfence();
   __syncthreads();
+  if (a.solo) {
+    // two-level fixed-order reduction: the last CTA of each group of
+    // FW_GROUP CTAs sums the group's partials, the last group the groups'
+    // (a short, parallel tail instead of one CTA reducing every partial)
+    const int pf = C4 * 4, ne = pf + 1 + a.pitch0;
+    const int g = blockIdx.x / FW_GROUP, g0 = g * FW_GROUP;
+    const int g1 = min((int)gridDim.x, g0 + FW_GROUP);
+    const int ngroups = (gridDim.x + FW_GROUP - 1) / FW_GROUP;
+    if (threadIdx.x == 0) is_last = atomicAdd(&a.gcnt[g], 1) == g1 - g0 - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+      double sum = 0.0;
+      for (int b = g0; b < g1; b++)
+        sum += e <= pf ? __ldcg(a.part + (int64_t)b * (pf + 1) + e)
+                       : __ldcg(a.part_d + (int64_t)b * a.pitch0 + (e - pf - 1));
+      a.gpart[(int64_t)g * ne + e] = sum;
+    }
+    if (threadIdx.x == 0) a.gcnt[g] = 0;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(&a.state->done_fact, 1) == ngroups - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    glm_solo_final(a.gpart, ngroups, pf, a.pitch0, a.sort_g, a.fuse_update, a.up);
+    if (threadIdx.x == 0) a.state->done_fact = 0;
+    return;
+  }
+  // last CTA stitches the segments that span warp ranges (fixed order)
   if (threadIdx.x == 0) is_last = atomicAdd(&a.state->done_fact, 1) == (int)gridDim.x - 1;
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  if (a.solo) {
-    glm_solo_reduce(a.part, a.part_d, C4 * 4, a.pitch0, a.sort_g, a.fuse_update, a.up);
-  } else if (has_sort) {
+  if (has_sort)
     stitch_carries(a.carry, NW, a.bins, smem, (size_t)FW_WARPS * a.nst * a.stage_bytes);
-  }
   if (threadIdx.x == 0) a.state->done_fact = 0;
 }

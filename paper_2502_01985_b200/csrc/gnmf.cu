@@ -1033,12 +1033,13 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
                                    (int)(gm.total + 1024)));
     }
   }
-  // default candidate: the tcgen05 pass with MN-major row-contraction
-  // operands (gnmf_t5.cuh): rank tile 32, <= 28 streamed columns, <= 1
-  // gathered source (the sort source); opt-in (FL_GN_T5=1) while validated
+  // default: the tcgen05 pass with MN-major row-contraction operands
+  // (gnmf_t5.cuh) for rank tile 32, <= 28 streamed columns, <= 1 gathered
+  // source (the sort source): C4 fact pass 5.56 ms vs 6.2 ms for the
+  // mma.sync pass (profiles/r02_gnmf_t5.txt)
   {
     const char* e5 = getenv("FL_GN_T5");
-    const bool on = e5 && atoi(e5) != 0;
+    const bool on = !(e5 && atoi(e5) == 0);   // default; FL_GN_T5=0 selects the mma.sync pass
     const G5Geom g5 = g5_geom();
     if (on && !s->tc && R == 32 && t->pf <= 28 && ng <= 1 && (ng == 0 || t->sort_g == 0) &&
         g5.total + 1024 <= 227 * 1024) {
