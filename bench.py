@@ -646,6 +646,10 @@ def main():
              "gnmf": ["h_update", "dim_g", "fact_pass", "dim_p", "reduce"]}[wl["model"]]
     kernel = {"linreg": "k_glm_fact_w", "logreg": "k_glm_fact_w", "kmeans": "k_km_fact",
               "gnmf": "k_gnmf_fact"}[wl["model"]]
+    if wl["model"] in ("kmeans", "gnmf") and getattr(sess, "path", None) in ("tcgen05_mn", "generic"):
+        kernel = {("kmeans", "tcgen05_mn"): "k_km_t5", ("gnmf", "tcgen05_mn"): "k_gnmf_t5",
+                  ("kmeans", "generic"): "k_kg_fact (width-general)",
+                  ("gnmf", "generic"): "generic GNMF iteration"}[(wl["model"], sess.path)]
     lay = h.layout
     d0, d1 = sh["dim0"]
     dims_local = [(d1 - d0, wl["dims"][0][1])] + list(wl["dims"][1:])
@@ -669,6 +673,8 @@ def main():
         if pj.get("rows") == sh["rows"]:
             traffic = pj.get("dram_bytes_per_launch")
     launches_per_step = {"linreg": 3, "logreg": 3, "kmeans": 4, "gnmf": 5}[wl["model"]]
+    if wl["model"] in ("linreg", "logreg") and sess.path[0] == "solo":
+        launches_per_step = 1
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

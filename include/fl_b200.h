@@ -149,7 +149,8 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream);
  * (K1 includes the bins memset).  Advances the model like fl_glm_run. */
 /* Which fact pass the session runs: 0 CTA tiles, 1 per-warp TMA pipelines
  * (dense stream block), 2 CSR stream block (sparse F),
- * 3 generic operators.  stream_density: measured nonzero density of the
+ * 3 generic operators, 4 solo (the dense per-warp pass with the sort source's
+ * q and gradient folded in: one kernel per iteration).  stream_density: measured nonzero density of the
  * real stream columns (1.0 when not measured). */
 int fl_glm_path(fl_glm* s, int32_t* path, double* stream_density);
 int fl_glm_kernel_times(fl_glm* s, int32_t iters, float* ms_out, void* stream);

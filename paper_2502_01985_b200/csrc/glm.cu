@@ -1457,7 +1457,7 @@ int fl_glm_path(fl_glm* s, int32_t* path, double* stream_density) {
     set_error("fl_glm_path: null session");
     return FL_ERR_ARG;
   }
-  if (path) *path = s->unfused ? 3 : s->use_csr ? 2 : s->use_fw ? 1 : 0;
+  if (path) *path = s->unfused ? 3 : s->use_csr ? 2 : s->solo ? 4 : s->use_fw ? 1 : 0;
   if (stream_density) {
     if (s->csr_density < 0.0) {
       if (s->unfused || s->t->nf == 0) {

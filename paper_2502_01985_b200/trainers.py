@@ -199,7 +199,7 @@ class GlmSession:
         p = C.c_int32()
         dens = C.c_double()
         _lib.call("fl_glm_path", self.ptr, C.byref(p), C.byref(dens))
-        return ("cta_tiles", "warp_tma", "csr", "generic")[p.value], dens.value
+        return ("cta_tiles", "warp_tma", "csr", "generic", "solo")[p.value], dens.value
 
     def kernel_times(self, iters: int, stream=None) -> list[float]:
         """Mean ms of [dim q, fact pass, dim t + update] over `iters` iterations
