@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "tc05.cuh"
 
 namespace flb {
 
@@ -437,6 +438,8 @@ int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target
   return FL_OK;
 }
 
+#include "lmm_t5.cuh"
+
 // ---------------------------------------------------------------------------
 // More than MAX_GATHER gathered sources: the first group of MAX_GATHER rides
 // the stream pass, every further group adds its gathered rows in another
@@ -495,6 +498,47 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
       gs.fk[d] = g.fk->as<int32_t>();
     }
     const float* F = t->F ? t->F->as<float>() : nullptr;
+    // tcgen05 pass (lmm_t5.cuh) for >= 8 operand columns over a narrow
+    // stream block past L2 (FL_LMM_T5_MIN_ROWS, default 8M rows; FL_NO_LMM_T5
+    // disables it): F x_F on the tensor cores, the epilogue writes rows
+    {
+      const char* mr5 = getenv("FL_LMM_T5_MIN_ROWS");
+      const int64_t min5 = mr5 ? atoll(mr5) : (int64_t)1 << 23;
+      if (F && t->pf <= 28 && ncol >= 8 && t->r_T >= min5 && !getenv("FL_NO_LMM_T5")) {
+        const L5Geom g5 = l5_geom(gs.n);
+        CUtensorMap tm;
+        int rc = make_tmap_2d(&tm, F, (uint64_t)t->r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,
+                              L5_TILE, 32, 128);
+        if (rc) return rc;
+        static bool attr_set = false;
+        if (!attr_set) {
+          FL_CUDA(cudaFuncSetAttribute(k_lmm_t5, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(l5_geom(MAX_GATHER).total + 1024)));
+          attr_set = true;
+        }
+        LmT5Args la{};
+        la.pf = t->pf;
+        la.c_x = c_x;
+        la.col0 = col0;
+        la.ncol = ncol;
+        la.r_T = t->r_T;
+        la.ntiles = t->r_pad / L5_TILE;
+        la.ng = gs.n;
+        for (int d = 0; d < gs.n; d++) {
+          la.fk[d] = gs.fk[d];
+          la.q[d] = gs.q[d];
+        }
+        la.x = x_dev;
+        la.f_tcol = t->d_f_tcol->as<int32_t>();
+        la.perm = t->perm->as<int32_t>();
+        la.out = out_dev;
+        const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(la.ntiles, t->sm_count));
+        k_lmm_t5<<<nb, L5_THREADS, g5.total + 1024, s>>>(tm, la, g5);
+        FL_CHECK_LAUNCH();
+        for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
+        continue;
+      }
+    }
     // narrow stream block: thread-per-row kernel, float4 row loads, device-
     // order output + gathered unpermute.  Only past L2 (>= 8M rows by
     // default): below that the scattered writes stay in L2 and the extra

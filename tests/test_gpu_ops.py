@@ -283,3 +283,21 @@ def test_transpose_lmm_widths_vs_oracle(fl, c_fact):
     for cy in range(1, 10):
         y = rng.random((ft.r_T, cy)).astype(np.float32)
         assert rel(h.transpose_lmm(y), oracle.transpose_lmm(tab, y)) < RTOL, cy
+
+
+@pytest.mark.parametrize("c_fact,dims", [(20, [(2000, 30)]), (12, [(500, 7), (40, 3)]),
+                                         (28, []), (5, [(3000, 9)])])
+def test_lmm_tcgen05_vs_oracle(fl, monkeypatch, c_fact, dims):
+    """The tcgen05 lmm (csrc/lmm_t5.cuh: F x_F as a 3xTF32 tcgen05 MMA per
+    128-row tile, gathered q_d rows added in the epilogue, rows written at
+    their target positions), forced on here (FL_LMM_T5_MIN_ROWS=0), for
+    8-40 operand columns (chunks of 32, ragged last chunk, odd widths)."""
+    monkeypatch.setenv("FL_LMM_T5_MIN_ROWS", "0")
+    ft = star_table(13, 50_001, dims, c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    h = fl.TargetHandle.factorized(ft)
+    rng = np.random.default_rng(2)
+    for cx in (8, 13, 16, 32, 33, 40):
+        x = rng.random((ft.c_T, cx)).astype(np.float32)
+        got = h.lmm(x)
+        assert rel(got, oracle.lmm(tab, x)) < RTOL, cx
