@@ -33,6 +33,7 @@ struct L5Geom {
   uint32_t stage, o_fk;             // stage: F (16 KB) | FKs (512 B per source)
   uint32_t o_lo;                    // 2 x F_lo (K-major SW128, 16 KB)
   uint32_t o_cst;                   // x_F hi | lo (interleave [8][32][4], 2 x 4 KB)
+  uint32_t o_stg;                   // 2 x [128 rows x 33] fp32 output staging
   uint32_t total;
 };
 
@@ -42,7 +43,8 @@ __host__ __device__ inline L5Geom l5_geom(int ng) {
   g.stage = (uint32_t)round_up(16384 + 512 * (ng > 0 ? ng : 1), 1024);
   g.o_lo = L5_NS * g.stage;
   g.o_cst = g.o_lo + 2 * 16384;
-  g.total = g.o_cst + 8192;
+  g.o_stg = g.o_cst + 8192;
+  g.total = g.o_stg + 2 * L5_TILE * 33 * 4;
   return g;
 }
 
@@ -148,7 +150,6 @@ __global__ void __launch_bounds__(L5_THREADS, 1)
       tc::fence_before();
       mbar_arrive(&lo_ready[t & 1]);
     };
-    const bool vec = (a.c_x % 4) == 0 && (a.col0 % 4) == 0;
     if (n > 0) split(0);
     for (int t = 0; t < n; t++) {
       const int s = t % L5_NS;
@@ -178,23 +179,19 @@ __global__ void __launch_bounds__(L5_THREADS, 1)
       // the stage (F tile, FKs) is consumed: F_lo of the next tile, then release
       if (t + 1 < n) split(t + 1);
       mbar_arrive(&empty[s]);
-      if (valid) {
-        // F x_F + sum_d q_d (k_lmm_main's order: the F product first)
-        float o[16];
+      // F x_F + sum_d q_d into the staging tile (pitch 33: conflict-free),
+      // then every warp writes 16 whole rows, lane = column: one coalesced
+      // 128-byte store per target row instead of two scattered halves
+      float* stg = reinterpret_cast<float*>(sm + gm.o_stg) + (t & 1) * (L5_TILE * 33);
 #pragma unroll
-        for (int j = 0; j < 16; j++) o[j] = __uint_as_float(z[j]) + acc[j];
-        float* orow = a.out + (int64_t)a.perm[p] * a.c_x + a.col0 + c_lo;
-        const int nc = min(16, a.ncol - c_lo);
-        if (vec && nc == 16) {
-#pragma unroll
-          for (int u = 0; u < 4; u++)
-            reinterpret_cast<float4*>(orow)[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; j++)
-            if (j < nc) orow[j] = o[j];
-        }
+      for (int j = 0; j < 16; j++) stg[r * 33 + c_lo + j] = __uint_as_float(z[j]) + acc[j];
+      named_sync(1, L5_EPI);
+      for (int rr = ew * 16; rr < ew * 16 + 16; rr++) {
+        const int64_t pr = (t0 + t) * L5_TILE + rr;
+        if (pr < a.r_T && lane < a.ncol)
+          a.out[(int64_t)a.perm[pr] * a.c_x + a.col0 + lane] = stg[rr * 33 + lane];
       }
+      (void)valid;
     }
   }
   tc::fence_before();

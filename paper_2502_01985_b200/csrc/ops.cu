@@ -438,6 +438,9 @@ int launch_gather_rows_to_device_order(const fl_table* t, const void* src_target
   return FL_OK;
 }
 
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 #include "lmm_t5.cuh"
 
 // ---------------------------------------------------------------------------
