@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "tc05.cuh"
 
 namespace flb {
 namespace {
@@ -241,6 +242,34 @@ int gram(fl_table* t, const float* A, int pa, int acols, const float* B, int pb,
   return FL_OK;
 }
 
+#include "gram_t5.cuh"
+
+// F^T F through k_fgram_t5 (stream block <= 28 columns)
+int fgram_t5(fl_table* t, double* out, cudaStream_t s) {
+  const R5Geom gm = r5_geom();
+  CUtensorMap tm;
+  int rc = make_tmap_2d(&tm, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,
+                        R5_TILE, 32, kSwz128Atom32);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA(cudaFuncSetAttribute(k_fgram_t5, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(gm.total + 1024)));
+    attr = true;
+  }
+  const int64_t ntiles = t->r_pad / R5_TILE;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+  double* part = nullptr;
+  FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * t->pf * t->pf * 8, s));
+  k_fgram_t5<<<nb, R5_THREADS, gm.total + 1024, s>>>(tm, t->pf, ntiles, gm, part);
+  FL_CHECK_LAUNCH();
+  k_fgram_reduce<<<(unsigned)ceil_div((int64_t)t->pf * t->pf * 32, 256), 256, 0, s>>>(
+      part, nb, t->pf, t->d_f_tcol->as<int32_t>(), t->c_T, out);
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaFreeAsync(part, s));
+  return FL_OK;
+}
+
 }  // namespace
 }  // namespace flb
 
@@ -261,9 +290,13 @@ extern "C" int fl_crossprod(fl_table* t, double* out, void* stream) {
   FL_CUDA(cudaMemsetAsync(od, 0, (size_t)c_T * c_T * 8, s));
   const float* F = t->F ? t->F->as<float>() : nullptr;
   const int32_t* ftcol = t->pf ? t->d_f_tcol->as<int32_t>() : nullptr;
-  // F x F
+  // F x F: tcgen05 Gram with MN-major operands for <= 28 streamed columns
+  // (FL_NO_GRAM_T5=1: the SIMT tile Gram)
   if (t->pf > 0) {
-    rc = gram(t, F, t->pf, t->pf, F, t->pf, t->pf, t->r_T, nullptr, ftcol, ftcol, false, od, s);
+    if (t->pf <= 28 && !getenv("FL_NO_GRAM_T5"))
+      rc = fgram_t5(t, od, s);
+    else
+      rc = gram(t, F, t->pf, t->pf, F, t->pf, t->pf, t->r_T, nullptr, ftcol, ftcol, false, od, s);
     if (rc) return rc;
   }
   const int ng = (int)t->g.size();

@@ -1,0 +1,167 @@
+// F^T F on the 5th-generation tensor cores (included inside namespace flb by
+// crossprod.cu): the stream-block Gram of the factorized crossprod for
+// stream blocks of <= 28 columns.  Per 128-row tile ONE M = 128, N = 64 MMA
+// chain over the tile's rows computes [F | F_lo]^T [F | F_lo] with both
+// operands read MN-major from row-major tiles (128B / 32-byte-atom swizzle,
+// descriptor layout 1, tc05.cuh): the TMA tile is its own tf32 hi part (the
+// tensor core truncates), F_lo is written next to it by the split warps, and
+// G = hi hi + lo hi + hi lo (3xTF32).  TMEM accumulates 512 rows in fp32,
+// then folds into fp64 (the k_gram window); per-CTA partials are reduced in
+// CTA order.  Bound: one read of F (HBM).
+constexpr int R5_TILE = 128;
+constexpr int R5_NS = 4;
+constexpr int R5_FT = 4;
+constexpr int R5_THREADS = 64 + 128;
+
+struct R5Geom {
+  uint32_t stage;   // F (16 KB) | F_lo (16 KB)
+  uint32_t o_acc;   // fp64 [64 cols][64 lanes]
+  uint32_t total;   // + 32 KB past the last stage (the M = 128 A operand reads groups 2, 3)
+};
+
+__host__ __device__ inline R5Geom r5_geom() {
+  R5Geom g{};
+  g.stage = 32768;
+  g.o_acc = R5_NS * g.stage + 32768;
+  g.total = g.o_acc + 64 * 64 * 8;
+  return g;
+}
+
+__device__ __forceinline__ uint32_t r5_b32(int row, int c4) {
+  return (uint32_t)(row * 128 + (((c4 >> 1) ^ (row & 3)) << 5) + ((c4 & 1) << 4));
+}
+__device__ __forceinline__ float r5_lo(float v) {
+  return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+}
+
+// part[cta][i * pf + j] = sum over the CTA's rows of F[r][i] F[r][j]
+__global__ void __launch_bounds__(R5_THREADS, 1)
+    k_fgram_t5(const __grid_constant__ CUtensorMap tmF, int pf, int64_t ntiles, R5Geom gm,
+               double* __restrict__ part) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[R5_NS], empty[R5_NS], lo_ready[R5_NS], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* acc = reinterpret_cast<double*>(sm + gm.o_acc);   // [col][lane]
+  for (int i = tid; i < 64 * 64; i += blockDim.x) acc[i] = 0.0;
+  // the M = 128 operand reads 32 KB past the last stage into rows of D that
+  // are never used; keep that memory finite
+  for (int i = tid; i < 8192; i += blockDim.x)
+    reinterpret_cast<float*>(sm + R5_NS * gm.stage)[i] = 0.f;
+  if (tid == 0) {
+    for (int s = 0; s < R5_NS; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&lo_ready[s], 128);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 64);
+    }
+    fence_mbar_init();
+  }
+  tc::fence_smem_to_async();
+  if (warp == 0) tc::alloc(&tbase, 128);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  const int64_t G = gridDim.x;
+  const int64_t base = ntiles / G, rem = ntiles % G;
+  const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
+  const int n = (int)(base + (blockIdx.x < rem ? 1 : 0));
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      for (int i = 0; i < n; i++) {
+        const int s = i % R5_NS;
+        if (i >= R5_NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / R5_NS) - 1) & 1));
+        mbar_arrive_expect_tx(&full[s], 16384u);
+        tma_load_2d_hint(sm + s * gm.stage, &tmF, 0, (int)((t0 + i) * R5_TILE), &full[s], pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n > 0) {
+      const uint32_t id = tc::idesc_tf32(128, 64, true, true);
+      for (int t = 0; t < n; t++) {
+        const int s = t % R5_NS, w = t / R5_FT, b = w & 1;
+        mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / R5_NS) & 1));
+        if ((t % R5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
+        tc::fence_after();
+        const uint64_t d0 = tc::smem_desc(smem_u32(sm + s * gm.stage), 16384, 512, tc::kSw128B32);
+#pragma unroll
+        for (int kk = 0; kk < R5_TILE / 8; kk++) {
+          const uint64_t d = d0 + (uint64_t)(kk * 64);
+          tc::mma_tf32(tmem + 64 * b, d, d, id, !((t % R5_FT) == 0 && kk == 0));
+        }
+        tc::commit(&empty[s]);
+        if ((t % R5_FT) == R5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
+      }
+    }
+  } else {
+    const int q4 = warp & 3, r = 32 * q4 + lane;
+    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+    const bool folder = q4 < 2;   // TMEM lanes 0..63: rows [F | F_lo] of the Gram
+    auto fold = [&](int w) {
+      const int b = w & 1;
+      mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
+      tc::fence_after();
+      uint32_t x[16];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        tc::ld16(tmem + lane_off + 64 * b + 16 * u, x);
+        tc::wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; j++) acc[(16 * u + j) * 64 + r] += (double)__uint_as_float(x[j]);
+      }
+      tc::fence_before();
+      mbar_arrive(&acc_empty[b]);
+    };
+    const int sw = (r >> 2) & 1;   // rows r, r + 4 share a granule: swap chunk halves
+    for (int t = 0; t < n; t++) {
+      const int s = t % R5_NS;
+      char* st = sm + s * gm.stage;
+      mbar_wait_sleep(&full[s], (uint32_t)((t / R5_NS) & 1));
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const uint32_t o = r5_b32(r, c ^ sw);
+        const float4 v = *reinterpret_cast<const float4*>(st + o);
+        *reinterpret_cast<float4*>(st + 16384 + o) =
+            make_float4(r5_lo(v.x), r5_lo(v.y), r5_lo(v.z), r5_lo(v.w));
+      }
+      fence_proxy_async();
+      tc::fence_before();
+      mbar_arrive(&lo_ready[s]);
+      if (folder && (t % R5_FT) == 0 && t >= R5_FT) fold(t / R5_FT - 1);
+    }
+    if (folder && n > 0) fold((n - 1) / R5_FT);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  // G[i][j] = D[i][j] + D[32 + i][j] + D[i][32 + j]  (hi hi + lo hi + hi lo)
+  double* out = part + (int64_t)blockIdx.x * pf * pf;
+  for (int e = tid; e < pf * pf; e += blockDim.x) {
+    const int i = e / pf, j = e - i * pf;
+    out[e] = acc[j * 64 + i] + acc[j * 64 + 32 + i] + acc[(32 + j) * 64 + i];
+  }
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 128);
+}
+
+// out[tcol[i], tcol[j]] += sum over CTAs (CTA order) of part[.][i * pf + j]
+__global__ void k_fgram_reduce(const double* __restrict__ part, int nb, int pf,
+                               const int32_t* __restrict__ tcol, int c_T, double* __restrict__ out) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)pf * pf) return;
+  const int e = (int)w, i = e / pf, j = e - i * pf;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += part[(int64_t)b * pf * pf + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int ti = tcol[i], tj = tcol[j];
+  if (lane == 0 && ti >= 0 && tj >= 0) out[(int64_t)ti * c_T + tj] += s;
+}

@@ -501,13 +501,16 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
       gs.fk[d] = g.fk->as<int32_t>();
     }
     const float* F = t->F ? t->F->as<float>() : nullptr;
-    // tcgen05 pass (lmm_t5.cuh) for >= 8 operand columns over a narrow
-    // stream block past L2 (FL_LMM_T5_MIN_ROWS, default 8M rows; FL_NO_LMM_T5
-    // disables it): F x_F on the tensor cores, the epilogue writes rows
+    // tcgen05 pass (lmm_t5.cuh, opt-in FL_LMM_T5=1) for >= 8 operand columns
+    // over a narrow stream block past L2 (FL_LMM_T5_MIN_ROWS, default 8M
+    // rows): F x_F on the tensor cores, the epilogue writes whole rows.  It
+    // is bound by the scattered target-order row writes like the row-wise
+    // kernels and measured slower at C2 size (k = 32: 13.3 vs 12.5 ms)
     {
       const char* mr5 = getenv("FL_LMM_T5_MIN_ROWS");
       const int64_t min5 = mr5 ? atoll(mr5) : (int64_t)1 << 23;
-      if (F && t->pf <= 28 && ncol >= 8 && t->r_T >= min5 && !getenv("FL_NO_LMM_T5")) {
+      const char* on5 = getenv("FL_LMM_T5");   // opt-in: measured slower
+      if (on5 && atoi(on5) != 0 && F && t->pf <= 28 && ncol >= 8 && t->r_T >= min5) {
         const L5Geom g5 = l5_geom(gs.n);
         CUtensorMap tm;
         int rc = make_tmap_2d(&tm, F, (uint64_t)t->r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,

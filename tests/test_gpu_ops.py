@@ -290,8 +290,9 @@ def test_transpose_lmm_widths_vs_oracle(fl, c_fact):
 def test_lmm_tcgen05_vs_oracle(fl, monkeypatch, c_fact, dims):
     """The tcgen05 lmm (csrc/lmm_t5.cuh: F x_F as a 3xTF32 tcgen05 MMA per
     128-row tile, gathered q_d rows added in the epilogue, rows written at
-    their target positions), forced on here (FL_LMM_T5_MIN_ROWS=0), for
+    their target positions), forced on here (FL_LMM_T5=1, FL_LMM_T5_MIN_ROWS=0), for
     8-40 operand columns (chunks of 32, ragged last chunk, odd widths)."""
+    monkeypatch.setenv("FL_LMM_T5", "1")
     monkeypatch.setenv("FL_LMM_T5_MIN_ROWS", "0")
     ft = star_table(13, 50_001, dims, c_fact)
     tab = oracle.OracleTable.from_ft(ft)
@@ -301,3 +302,19 @@ def test_lmm_tcgen05_vs_oracle(fl, monkeypatch, c_fact, dims):
         x = rng.random((ft.c_T, cx)).astype(np.float32)
         got = h.lmm(x)
         assert rel(got, oracle.lmm(tab, x)) < RTOL, cx
+
+
+@pytest.mark.parametrize("c_fact,dims", [(20, [(2000, 30)]), (28, []), (3, [(500, 7), (40, 3)])])
+def test_crossprod_tcgen05_gram_matches_simt(fl, monkeypatch, c_fact, dims):
+    """F^T F of the crossprod on tcgen05 (csrc/gram_t5.cuh: [F | F_lo]^T
+    [F | F_lo] read MN-major per 128-row tile) against the SIMT tile Gram
+    (FL_NO_GRAM_T5=1) and the dense product."""
+    ft = star_table(19, 90_001, dims, c_fact)
+    tab = oracle.OracleTable.from_ft(ft)
+    td = oracle.materialize(tab)
+    h = fl.TargetHandle.factorized(ft)
+    got = h.crossprod()
+    monkeypatch.setenv("FL_NO_GRAM_T5", "1")
+    simt = h.crossprod()
+    assert rel(got, td.T @ td) < RTOL
+    assert rel(got, simt) < 1e-6
