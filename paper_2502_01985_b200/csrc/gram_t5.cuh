@@ -5,12 +5,13 @@
 // operands read MN-major from row-major tiles (128B / 32-byte-atom swizzle,
 // descriptor layout 1, tc05.cuh): the TMA tile is its own tf32 hi part (the
 // tensor core truncates), F_lo is written next to it by the split warps, and
-// G = hi hi + lo hi + hi lo (3xTF32).  TMEM accumulates 512 rows in fp32,
-// then folds into fp64 (the k_gram window); per-CTA partials are reduced in
-// CTA order.  Bound: one read of F (HBM).
+// G = hi hi + lo hi + hi lo (3xTF32).  TMEM accumulates one tile (128 rows)
+// in fp32, folded into fp64 every tile (a 512-row window left a 1e-6
+// relative deviation from the fp64 Gram at C2 size); per-CTA partials are
+// reduced in CTA order.  Bound: one read of F (HBM).
 constexpr int R5_TILE = 128;
 constexpr int R5_NS = 4;
-constexpr int R5_FT = 4;
+constexpr int R5_FT = 1;              // fold every tile: fp32 TMEM sums over 128 rows only
 constexpr int R5_THREADS = 64 + 128;
 
 struct R5Geom {
