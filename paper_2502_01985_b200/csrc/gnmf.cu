@@ -1070,6 +1070,7 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
       ga.HH32 = fa.HH32;
       ga.f_tcol = fa.f_tcol;
       ga.scratch = s->scratch5.as<double>();
+      if (const char* dg = getenv("FL_GN5_DIAG")) ga.diag = atoi(dg);   // timing experiments
       const size_t smem5 = g5.total + 1024;
       FL_CUDA(cudaFuncSetAttribute(k_gnmf_t5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem5));

@@ -35,6 +35,7 @@ struct GnT5Args {
   int pf, c_T;
   int64_t r_T, ntiles;
   int ng;                          // 0 or 1 (the sort source)
+  int diag;                        // timing experiments only (FL_GN5_DIAG): 1 no Z sums, 2 no PG MMA
   const int32_t* fk;
   const float* Gd;                 // r_d x 32
   double* Z;                       // r_d x 32
@@ -205,10 +206,12 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         // of 8 rows advances the start address by 1024 B (64 in the 16-byte
         // address field)
         const uint64_t ad0 = tc::smem_desc(ops, 16384, 512, tc::kSw128B32);
+        if (!(a.diag & 2)) {
 #pragma unroll
-        for (int kk = 0; kk < G5_TILE / 8; kk++) {
-          const uint64_t ad = ad0 + (uint64_t)(kk * 64);
-          tc::mma_tf32(tp, ad, ad, id_pg, !((t % G5_FT) == 0 && kk == 0));
+          for (int kk = 0; kk < G5_TILE / 8; kk++) {
+            const uint64_t ad = ad0 + (uint64_t)(kk * 64);
+            tc::mma_tf32(tp, ad, ad, id_pg, !((t % G5_FT) == 0 && kk == 0));
+          }
         }
         tc::commit(&empty[s]);
         tc::commit(&ops_free);
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       // Z[fk] += W' rows: warp (q4, h) takes the ZR rows [32 q4 + ZR h, +ZR),
       // lane = rank column; a segment with one FK (the common case: keys are
       // sorted, fanout >> ZR) is one branch-free sum and one fp64 atomic
-      if (a.ng) {
+      if (a.ng && !(a.diag & 1)) {
         constexpr int ZR = 32 / G5_HG;
         const int r0 = 32 * q4 + ZR * h;
         const int c4 = lane >> 2;
