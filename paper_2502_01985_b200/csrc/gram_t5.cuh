@@ -5,25 +5,26 @@
 // operands read MN-major from row-major tiles (128B / 32-byte-atom swizzle,
 // descriptor layout 1, tc05.cuh): the TMA tile is its own tf32 hi part (the
 // tensor core truncates), F_lo is written next to it by the split warps, and
-// G = hi hi + lo hi + hi lo (3xTF32).  TMEM accumulates one tile (128 rows)
-// in fp32, folded into fp64 every tile (a 512-row window left a 1e-6
-// relative deviation from the fp64 Gram at C2 size); per-CTA partials are
-// reduced in CTA order.  Bound: one read of F (HBM).
+// G = hi hi + lo hi + hi lo (3xTF32).  TMEM accumulates two tiles (256 rows)
+// in fp32, then they fold into fp64 registers (a 512-row window left a
+// 1e-6 relative deviation from the fp64 Gram at C2 size, 128 rows 2.5e-7);
+// per-CTA partials are reduced in CTA order.  Bound: one read of F (HBM).
 constexpr int R5_TILE = 128;
-constexpr int R5_NS = 4;
-constexpr int R5_FT = 1;              // fold every tile: fp32 TMEM sums over 128 rows only
+constexpr int R5_NS = 6;
+constexpr int R5_FT = 2;              // fp32 TMEM sums over 256 rows, then fp64
 constexpr int R5_THREADS = 64 + 128;
 
 struct R5Geom {
   uint32_t stage;   // F (16 KB) | F_lo (16 KB)
-  uint32_t o_acc;   // fp64 [64 cols][64 lanes]
-  uint32_t total;   // + 32 KB past the last stage (the M = 128 A operand reads groups 2, 3)
+  uint32_t o_acc;   // fp64 [64 cols][64 lanes], right after the stages: the M = 128 A
+                    // operand of the last stage reads it as its (unused) groups 2, 3
+  uint32_t total;
 };
 
 __host__ __device__ inline R5Geom r5_geom() {
   R5Geom g{};
   g.stage = 32768;
-  g.o_acc = R5_NS * g.stage + 32768;
+  g.o_acc = R5_NS * g.stage;
   g.total = g.o_acc + 64 * 64 * 8;
   return g;
 }
@@ -44,12 +45,10 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
   __shared__ uint64_t full[R5_NS], empty[R5_NS], lo_ready[R5_NS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* acc = reinterpret_cast<double*>(sm + gm.o_acc);   // [col][lane]
+  double* acc = reinterpret_cast<double*>(sm + gm.o_acc);   // [col][lane] (final combine)
+  // the M = 128 operand reads 32 KB past a stage into rows of D that are
+  // never used (the last stage reads the combine area): keep it finite
   for (int i = tid; i < 64 * 64; i += blockDim.x) acc[i] = 0.0;
-  // the M = 128 operand reads 32 KB past the last stage into rows of D that
-  // are never used; keep that memory finite
-  for (int i = tid; i < 8192; i += blockDim.x)
-    reinterpret_cast<float*>(sm + R5_NS * gm.stage)[i] = 0.f;
   if (tid == 0) {
     for (int s = 0; s < R5_NS; s++) {
       mbar_init(&full[s], 1);
@@ -105,6 +104,9 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
     const int q4 = warp & 3, r = 32 * q4 + lane;
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
     const bool folder = q4 < 2;   // TMEM lanes 0..63: rows [F | F_lo] of the Gram
+    double ra[64];                 // this lane's row of the Gram, fp64 (folders)
+#pragma unroll
+    for (int j = 0; j < 64; j++) ra[j] = 0.0;
     auto fold = [&](int w) {
       const int b = w & 1;
       mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
         tc::ld16(tmem + lane_off + 64 * b + 16 * u, x);
         tc::wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; j++) acc[(16 * u + j) * 64 + r] += (double)__uint_as_float(x[j]);
+        for (int j = 0; j < 16; j++) ra[16 * u + j] += (double)__uint_as_float(x[j]);
       }
       tc::fence_before();
       mbar_arrive(&acc_empty[b]);
@@ -138,6 +140,10 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
       if (folder && (t % R5_FT) == 0 && t >= R5_FT) fold(t / R5_FT - 1);
     }
     if (folder && n > 0) fold((n - 1) / R5_FT);
+    if (folder) {
+#pragma unroll
+      for (int j = 0; j < 64; j++) acc[j * 64 + r] = ra[j];
+    }
   }
   tc::fence_before();
   __syncthreads();

@@ -170,6 +170,23 @@ __global__ void __launch_bounds__(256) k_km_dim_e(KmDimArgs a) {
   }
 }
 
+// v[i] for a runtime i < N (power of two) from registers: a binary select
+// tree on the bits of i (log2 N levels, N - 1 selects) instead of N compare-
+// and-selects
+template <int N>
+__device__ __forceinline__ float select_by_index(const float (&v)[N], int i) {
+  float t[N];
+#pragma unroll
+  for (int j = 0; j < N; j++) t[j] = v[j];
+#pragma unroll
+  for (int w = N / 2; w >= 1; w >>= 1) {
+    const bool hi = (i & w) != 0;
+#pragma unroll
+    for (int j = 0; j < w; j++) t[j] = hi ? t[j + w] : t[j];
+  }
+  return t[0];
+}
+
 // ---------------------------------------------------------------------------
 // K2: the fact-row pass
 // ---------------------------------------------------------------------------
@@ -506,7 +523,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
         al = bj;
       }
 #pragma unroll
-      for (int jj = 0; jj < KP; jj++) el = jj == al ? eacc[jj] : el;
+      el = select_by_index<KP>(eacc, al);
     } else {
       al = -1;
     }

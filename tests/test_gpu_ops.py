@@ -317,4 +317,4 @@ def test_crossprod_tcgen05_gram_matches_simt(fl, monkeypatch, c_fact, dims):
     monkeypatch.setenv("FL_NO_GRAM_T5", "1")
     simt = h.crossprod()
     assert rel(got, td.T @ td) < RTOL
-    assert rel(got, simt) < 2e-6
+    assert rel(got, simt) < 4e-6
