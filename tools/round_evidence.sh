@@ -10,15 +10,15 @@ out=gpurun_out/ev
 mkdir -p $out
 NCU="ncu --clock-control none"
 if [ "$what" = bench ] || [ "$what" = all ]; then
-  timeout 600 python bench.py > $out/bench_c2.json 2> $out/bench_c2.err
+  timeout 900 python bench.py > $out/bench_c2.json 2> $out/bench_c2.err
   for w in c1 c3 c4; do
-    timeout 600 python bench.py --workload $w > $out/bench_$w.json 2> $out/bench_$w.err
+    timeout 900 python bench.py --workload $w > $out/bench_$w.json 2> $out/bench_$w.err
   done
   timeout 600 python bench.py --workload c2s --no-e2e --no-cpu --no-parity > $out/bench_c2s.json 2> $out/bench_c2s.err
-  timeout 600 python bench.py --impl reference > $out/bench_reference_c2.json 2> $out/bench_reference_c2.err
+  timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $out/bench_reference_c2.json 2> $out/bench_reference_c2.err
 fi
 if [ "$what" = launches ] || [ "$what" = all ]; then
-  for w in c2 c3 c4; do
+  for w in c1 c2 c3 c4; do
     timeout 900 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $out/launches_$w.csv \
       python bench.py --workload $w --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity --no-materialized > /dev/null 2>&1
   done
@@ -26,9 +26,16 @@ fi
 if [ "$what" = full ] || [ "$what" = all ]; then
   timeout 900 $NCU --set full --import-source on -k regex:k_glm_fact_w -s 4 -c 1 -o $out/full_c2_fact \
     python bench.py --workload c2 --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity --no-materialized > /dev/null 2>&1
+  timeout 900 $NCU --set full --import-source on -k regex:k_glm_fact_w -s 6 -c 1 -o $out/full_c1_fact \
+    python bench.py --workload c1 --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity --no-materialized > /dev/null 2>&1
   timeout 900 $NCU --set full --import-source on -k regex:k_km_fact -s 4 -c 1 -o $out/full_c3_fact \
     python bench.py --workload c3 --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity > /dev/null 2>&1
-  timeout 900 $NCU --set full --import-source on -k regex:k_gnmf_fact -s 4 -c 1 -o $out/full_c4_fact \
+  timeout 900 $NCU --set full --import-source on -k regex:k_gnmf_t5 -s 4 -c 1 -o $out/full_c4_fact \
     python bench.py --workload c4 --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity > /dev/null 2>&1
 fi
 ls -la $out
+if [ "$what" = ops ]; then
+  timeout 900 $NCU --set full --import-source on -k regex:k_fgram_t5 -s 1 -c 1 -o $out/full_fgram \
+    python tools/op_probe.py --crossprod c2 > /dev/null 2>&1
+  ls -la $out
+fi
