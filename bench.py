@@ -718,7 +718,7 @@ def main():
         sess.close()
         out["parity"] = bench_parity(torch, fl, wl, sh, h, hyper,
                                      {"gnmf": 2}.get(wl["model"], 3))
-    if world == 1 and not args.no_e2e and wl["model"] in ("linreg", "logreg", "kmeans"):
+    if world == 1 and not args.no_e2e:
         sess.close()
         out["e2e"] = bench_e2e(torch, fl, wl, sh, hyper, args)
     elif world > 1 and not args.no_e2e and wl["model"] in ("linreg", "logreg"):
@@ -873,9 +873,10 @@ def bench_materialized(torch, fl, h, y, gamma, wl, args, peak):
 
 def bench_e2e(torch, fl, wl, sh, hyper, args):
     """End to end through the public API from pinned HOST buffers: upload
-    (fact, dims, FKs, labels), device layout derivation, `--e2e-iters`
-    iterations and the read-back of the model and the loss history."""
-    from paper_2502_01985_b200.trainers import GlmSession, KMeansSession
+    (fact, dims, FKs, labels; GNMF: W_0, H_0), device layout derivation,
+    `--e2e-iters` iterations and the read-back of the model (GNMF: W and H)
+    and the loss history."""
+    from paper_2502_01985_b200.trainers import GlmSession, GnmfSession, KMeansSession
     maps, c_t = col_maps(wl)
 
     def pinned(t):
@@ -886,6 +887,12 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
     host = [pinned(sh["fact"])] + [pinned(d) for d in sh["dims"]]
     fks = [pinned(f) for f in sh["fks"]]
     y_h = pinned(sh["y"]) if sh["y"] is not None else None
+    w0_h = h0_h = None
+    if wl["model"] == "gnmf":
+        g = torch.Generator()
+        g.manual_seed(7)
+        w0_h = pinned(torch.rand((sh["rows"], wl["rank"]), generator=g, dtype=torch.float64) * 0.5)
+        h0_h = pinned(torch.rand((wl["rank"], c_t), generator=g, dtype=torch.float64) * 0.5)
     torch.cuda.synchronize()
 
     def job(J):
@@ -906,6 +913,21 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
             t_r = time.perf_counter()
             w, losses = s2.result(J)
             d2h = 8 * (c_t + J)
+        elif wl["model"] == "gnmf":
+            # t_sq through the public API (square, row_sum) as gaussian_nmf
+            # does; W_0 / H_0 are inputs (pinned fp64, counted in h2d)
+            from paper_2502_01985_b200.sparse import as_dense
+            sq = h2.elementwise("square", traced=False)
+            t_sq = float(as_dense(sq.row_sum(traced=False)).sum())
+            del sq
+            s2 = GnmfSession(h2, wl["rank"], w0_h.numpy(), h0_h.numpy(), t_sq)
+            torch.cuda.synchronize()
+            t_s = time.perf_counter()
+            s2.run(J)
+            torch.cuda.synchronize()
+            t_r = time.perf_counter()
+            w, hh, losses = s2.result(J)
+            d2h = w.nbytes + hh.nbytes + 8 * J
         else:
             from paper_2502_01985_b200.trainers import kmeans_init
             s2 = KMeansSession(h2, wl["k"], kmeans_init(h2, wl["k"], 0))
@@ -927,8 +949,8 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
     in_order = [job(J) for _ in range(7)]      # median of seven timed jobs (robust to
     runs = sorted(in_order)                    # the host stalls some boxes show)
     t_job, t_up, d2h, phases = runs[3]
-    h2d = sum(t.numel() * t.element_size() for t in host + fks) + (
-        y_h.numel() * y_h.element_size() if y_h is not None else 0)
+    h2d = sum(t.numel() * t.element_size() for t in host + fks + [
+        x for x in (y_h, w0_h, h0_h) if x is not None])
     return {"value": J / t_job, "unit": UNIT, "h2d_bytes_per_step": h2d / J,
             "d2h_bytes_per_step": d2h / J, "iterations_per_job": J,
             "job_seconds": t_job, "upload_layout_seconds": t_up,
