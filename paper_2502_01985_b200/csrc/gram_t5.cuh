@@ -1,23 +1,33 @@
 // F^T F on the 5th-generation tensor cores (included inside namespace flb by
 // crossprod.cu): the stream-block Gram of the factorized crossprod for
-// stream blocks of <= 28 columns.  Per 128-row tile ONE M = 128, N = 64 MMA
-// chain over the tile's rows computes [F | F_lo]^T [F | F_lo] with both
-// operands read MN-major from row-major tiles (128B / 32-byte-atom swizzle,
+// stream blocks of <= 28 columns.  Per 128-row tile ONE M = 128, N = 32 MMA
+// chain over the tile's rows computes D = [F | F_lo]^T F with both operands
+// read MN-major from row-major tiles (128B / 32-byte-atom swizzle,
 // descriptor layout 1, tc05.cuh): the TMA tile is its own tf32 hi part (the
-// tensor core truncates), F_lo is written next to it by the split warps, and
-// G = hi hi + lo hi + hi lo (3xTF32).  TMEM accumulates two tiles (256 rows)
-// in fp32, then they fold into fp64 registers (a 512-row window left a
-// 1e-6 relative deviation from the fp64 Gram at C2 size, 128 rows 2.5e-7);
-// per-CTA partials are reduced in CTA order.  Bound: one read of F (HBM).
+// tensor core truncates) and F_lo is written next to it by the split warps.
+// 3xTF32 needs hi^T hi + lo^T hi + hi^T lo; the last term is the transpose
+// of the second, so D's two 32-row halves give the Gram as
+// G = D_hh + D_lh + D_lh^T at half the MMA work of an N = 64 chain.  TMEM
+// accumulates two tiles (256 rows) in fp32, then dedicated fold warps move
+// them into fp64 registers (a 512-row window left a 1e-6 relative deviation
+// from the fp64 Gram at C2 size, 128 rows 2.5e-7); per-CTA partials are
+// reduced in CTA order.  Bound: one read of F (HBM).
+//
+//   warp 0     producer (TMA of the F tile)
+//   warp 1     MMA issuer (one thread)
+//   warps 2-5  split: F_lo of each tile (thread = tile row)
+//   warps 8-9  fold: TMEM lanes 0..63 (rows of D) into fp64 registers
+//   warps 6-7  idle (TMEM lane quadrants 2, 3 hold no used rows of D)
 constexpr int R5_TILE = 128;
 constexpr int R5_NS = 6;
 constexpr int R5_FT = 2;              // fp32 TMEM sums over 256 rows, then fp64
-constexpr int R5_THREADS = 64 + 128;
+constexpr int R5_THREADS = 320;
 
 struct R5Geom {
   uint32_t stage;   // F (16 KB) | F_lo (16 KB)
-  uint32_t o_acc;   // fp64 [64 cols][64 lanes], right after the stages: the M = 128 A
-                    // operand of the last stage reads it as its (unused) groups 2, 3
+  uint32_t o_acc;   // fp64 [32 cols][64 lanes] (+ zero pad to 32 KB), right after the
+                    // stages: the M = 128 A operand of the last stage reads it as its
+                    // (unused) groups 2, 3
   uint32_t total;
 };
 
@@ -57,12 +67,12 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 64);
+      mbar_init(&acc_empty[b], 64);   // the two fold warps
     }
     fence_mbar_init();
   }
   tc::fence_smem_to_async();
-  if (warp == 0) tc::alloc(&tbase, 128);
+  if (warp == 0) tc::alloc(&tbase, 64);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -84,7 +94,7 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && n > 0) {
-      const uint32_t id = tc::idesc_tf32(128, 64, true, true);
+      const uint32_t id = tc::idesc_tf32(128, 32, true, true);
       for (int t = 0; t < n; t++) {
         const int s = t % R5_NS, w = t / R5_FT, b = w & 1;
         mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / R5_NS) & 1));
@@ -94,34 +104,14 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < R5_TILE / 8; kk++) {
           const uint64_t d = d0 + (uint64_t)(kk * 64);
-          tc::mma_tf32(tmem + 64 * b, d, d, id, !((t % R5_FT) == 0 && kk == 0));
+          tc::mma_tf32(tmem + 32 * b, d, d, id, !((t % R5_FT) == 0 && kk == 0));
         }
         tc::commit(&empty[s]);
         if ((t % R5_FT) == R5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
       }
     }
-  } else {
-    const int q4 = warp & 3, r = 32 * q4 + lane;
-    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
-    const bool folder = q4 < 2;   // TMEM lanes 0..63: rows [F | F_lo] of the Gram
-    double ra[64];                 // this lane's row of the Gram, fp64 (folders)
-#pragma unroll
-    for (int j = 0; j < 64; j++) ra[j] = 0.0;
-    auto fold = [&](int w) {
-      const int b = w & 1;
-      mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
-      tc::fence_after();
-      uint32_t x[16];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        tc::ld16(tmem + lane_off + 64 * b + 16 * u, x);
-        tc::wait_ld();
-#pragma unroll
-        for (int j = 0; j < 16; j++) ra[16 * u + j] += (double)__uint_as_float(x[j]);
-      }
-      tc::fence_before();
-      mbar_arrive(&acc_empty[b]);
-    };
+  } else if (warp >= 2 && warp < 6) {
+    const int r = 32 * (warp & 3) + lane;
     const int sw = (r >> 2) & 1;   // rows r, r + 4 share a granule: swap chunk halves
     for (int t = 0; t < n; t++) {
       const int s = t % R5_NS;
@@ -137,25 +127,44 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
       fence_proxy_async();
       tc::fence_before();
       mbar_arrive(&lo_ready[s]);
-      if (folder && (t % R5_FT) == 0 && t >= R5_FT) fold(t / R5_FT - 1);
     }
-    if (folder && n > 0) fold((n - 1) / R5_FT);
-    if (folder) {
+  } else if (warp >= 8) {
+    const int q4 = warp & 3, r = 32 * q4 + lane;   // q4 = 0, 1: rows 0..63 of D
+    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+    double ra[32];                 // this lane's row of D, fp64
 #pragma unroll
-      for (int j = 0; j < 64; j++) acc[j * 64 + r] = ra[j];
+    for (int j = 0; j < 32; j++) ra[j] = 0.0;
+    const int nw = n > 0 ? (n - 1) / R5_FT + 1 : 0;
+    for (int w = 0; w < nw; w++) {
+      const int b = w & 1;
+      mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
+      tc::fence_after();
+      uint32_t x0[16], x1[16];
+      tc::ld16(tmem + lane_off + 32 * b, x0);
+      tc::ld16(tmem + lane_off + 32 * b + 16, x1);
+      tc::wait_ld();
+      tc::fence_before();
+      mbar_arrive(&acc_empty[b]);
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        ra[j] += (double)__uint_as_float(x0[j]);
+        ra[16 + j] += (double)__uint_as_float(x1[j]);
+      }
     }
+#pragma unroll
+    for (int j = 0; j < 32; j++) acc[j * 64 + r] = ra[j];
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  // G[i][j] = D[i][j] + D[32 + i][j] + D[i][32 + j]  (hi hi + lo hi + hi lo)
+  // G[i][j] = D[i][j] + D[32 + i][j] + D[32 + j][i]  (hi hi + lo hi + (lo hi)^T)
   double* out = part + (int64_t)blockIdx.x * pf * pf;
   for (int e = tid; e < pf * pf; e += blockDim.x) {
     const int i = e / pf, j = e - i * pf;
-    out[e] = acc[j * 64 + i] + acc[j * 64 + 32 + i] + acc[(32 + j) * 64 + i];
+    out[e] = acc[j * 64 + i] + acc[j * 64 + 32 + i] + acc[i * 64 + 32 + j];
   }
   __syncthreads();
-  if (warp == 0) tc::dealloc(tmem, 128);
+  if (warp == 0) tc::dealloc(tmem, 64);
 }
 
 // out[tcol[i], tcol[j]] += sum over CTAs (CTA order) of part[.][i * pf + j]

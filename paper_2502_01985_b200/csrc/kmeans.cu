@@ -69,6 +69,7 @@ struct KmFactArgs {
   double* part_w;                // gridDim.x x KM_WARPS x (MT * 16 * SC): per-warp sums
   uint32_t stage_bytes;          // 32 x FP fp32 TMA tile | 32 int32 sort-source FK
   int nst;
+  int diag;                      // timing experiments only (FL_KM_DIAG): 1 no sums, 2 no loss
 };
 
 struct KmDimArgs {
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       cp_async_commit();
     }
     // ---- loss (direct differences), I_d^T A counters, assignments
-    if (valid) {
+    if (valid && !(a.diag & 2)) {
       const float4* cr = reinterpret_cast<const float4*>(cf + al * CFP);
       float l = el;
 #pragma unroll
@@ -564,6 +565,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
     if (a.assign && valid) a.assign[p0 + lane] = al;
     // ---- sums_F | counts = one-hot^T [F | 1]: 2-term tf32 split of F (hi =
     // truncated mantissa, lo = exact remainder), one-hot exact
+    if (!(a.diag & 1))
 #pragma unroll
     for (int kb = 0; kb < 4; kb++) {
       // k index t <-> row kb*8 + 2t, t + 4 <-> row kb*8 + 2t + 1: with the
@@ -1061,6 +1063,7 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
   fa.C32 = s->C32.as<float>();
   fa.f_tcol = t->d_f_tcol->as<int32_t>();
   fa.assign = nullptr;
+  if (const char* dg = getenv("FL_KM_DIAG")) fa.diag = atoi(dg);   // timing experiments
   const int FP = SC + 4, ZP = KP + 4;
   fa.stage_bytes = (uint32_t)round_up(32 * FP * 4 + 128 * ng, 128);
   if ((rc = make_tmap_2d(&s->tmF, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,

@@ -596,9 +596,72 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
   return FL_OK;
 }
 
+#include "tmm_t5.cuh"
+
+static int tlmm_impl(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
+                     cudaStream_t s, bool dev_order, bool with_f);
+
+// F^T y through k_tmm_t5 for 3..32 operand columns (tmm_t5.cuh): y laid out
+// once as YD (device order, 32-column rows), then one tensor-core pass; the
+// gathered sources read YD in device order
+static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
+                        cudaStream_t s, bool dev_order) {
+  const int64_t r_T = t->r_T, r_pad = t->r_pad;
+  float* yd = nullptr;
+  FL_CUDA(cudaMallocAsync((void**)&yd, (size_t)r_pad * 32 * 4, s));
+  if (r_pad > r_T) FL_CUDA(cudaMemsetAsync(yd + r_T * 32, 0, (size_t)(r_pad - r_T) * 32 * 4, s));
+  const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(r_T, 32), 16 * (int64_t)t->sm_count);
+  if (yv.sc > yv.sr)
+    k_ydev32_cols<<<gb, 256, 0, s>>>(yv, cy, r_T, dev_order ? nullptr : t->iperm->as<int32_t>(), yd);
+  else
+    k_ydev32_rows<<<gb, 256, 0, s>>>(yv, cy, r_T, dev_order ? nullptr : t->perm->as<int32_t>(), yd);
+  FL_CHECK_LAUNCH();
+  CUtensorMap tmF, tmY;
+  int rc = make_tmap_2d(&tmF, t->F->p, (uint64_t)r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,
+                        M5_TILE, 32, kSwz128Atom32);
+  if (rc) return rc;
+  rc = make_tmap_2d(&tmY, yd, (uint64_t)r_pad, 32, 128, M5_TILE, 32, kSwz128Atom32);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA(cudaFuncSetAttribute(k_tmm_t5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M5_SMEM));
+    attr = true;
+  }
+  const int64_t ntiles = r_pad / M5_TILE;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+  double* part = nullptr;
+  FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * t->pf * cy * 8, s));
+  k_tmm_t5<<<nb, M5_THREADS, M5_SMEM, s>>>(tmF, tmY, t->pf, cy, ntiles, part);
+  FL_CHECK_LAUNCH();
+  k_reduce_partials<<<gridn((int64_t)t->pf * cy * 32), 256, 0, s>>>(
+      part, nb, t->pf, cy, t->d_f_tcol->as<int32_t>(), out, os_t, os_c);
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaFreeAsync(part, s));
+  rc = FL_OK;
+  if (!t->g.empty()) rc = tlmm_impl(t, YView{yd, 32, 1}, cy, out, os_t, os_c, s, true, false);
+  FL_CUDA(cudaFreeAsync(yd, s));
+  return rc;
+}
+
+static int tmm_t5_min_cols() {
+  static const int v = [] {
+    const char* e = getenv("FL_TMM_T5_MIN");
+    return e ? atoi(e) : 3;
+  }();
+  return v;
+}
+
 // generic T^T y with strided y view and strided fp64 output
 int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
-                   cudaStream_t s, bool dev_order) {
+            cudaStream_t s, bool dev_order) {
+  if (t->pf > 0 && t->pf <= 28 && cy >= tmm_t5_min_cols() && cy <= 32 && t->r_T > 0 &&
+      t->r_T <= (int64_t)INT32_MAX - M5_TILE && !getenv("FL_NO_TMM_T5"))
+    return tlmm_wide_t5(t, yv_in, cy, out, os_t, os_c, s, dev_order);
+  return tlmm_impl(t, yv_in, cy, out, os_t, os_c, s, dev_order, true);
+}
+
+static int tlmm_impl(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
+                     cudaStream_t s, bool dev_order, bool with_f) {
   const int sms = t->sm_count;
   if (cy > 1 && yv_in.sc > yv_in.sr && t->r_T > 0 && !getenv("FL_NO_VIEW_ROWS")) {
     // Column-strided y (rmm: x^T of a k x r_T row-major x).  Every device-
@@ -612,7 +675,7 @@ int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t
       const int w = std::min(VW, cy - c0);
       k_view_rows<<<gridn(t->r_T), 256, 0, s>>>(yv_in, t->r_T, c0, w, tmp);
       FL_CHECK_LAUNCH();
-      const int rc = do_tlmm(t, YView{tmp, w, 1}, w, out + c0 * os_c, os_t, os_c, s, dev_order);
+      const int rc = tlmm_impl(t, YView{tmp, w, 1}, w, out + c0 * os_c, os_t, os_c, s, dev_order, with_f);
       if (rc) return rc;
     }
     FL_CUDA(cudaFreeAsync(tmp, s));
@@ -623,8 +686,8 @@ int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t
     // 32 columns: 67.8 ms in one staged pass -> 4 chunks)
     for (int c0 = 0; c0 < cy; c0 += 8) {
       const int w = std::min(8, cy - c0);
-      const int rc = do_tlmm(t, YView{yv_in.base + (int64_t)c0 * yv_in.sc, yv_in.sr, yv_in.sc}, w,
-                             out + c0 * os_c, os_t, os_c, s, dev_order);
+      const int rc = tlmm_impl(t, YView{yv_in.base + (int64_t)c0 * yv_in.sc, yv_in.sr, yv_in.sc},
+                               w, out + c0 * os_c, os_t, os_c, s, dev_order, with_f);
       if (rc) return rc;
     }
     return FL_OK;
@@ -699,7 +762,7 @@ int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t
     return FL_OK;
   };
   int rc;
-  if (t->pf > 0) {
+  if (t->pf > 0 && with_f) {
     rc = launch_tmm(t->F->as<float>(), t->pf, t->pf, t->r_T, nullptr, t->d_f_tcol->as<int32_t>());
     if (rc) return rc;
   }

@@ -1,0 +1,205 @@
+// Stream-block part of a WIDE T^T y on the 5th-generation tensor cores
+// (included inside namespace flb by ops.cu): F^T Y for stream blocks of
+// <= 28 columns and 3..32 operand columns -- the op-level transpose_lmm
+// (reference ops.py:237-253) and rmm = (T^T x^T)^T (ops.py:219-235 via the
+// strided view), which before took one F pass per pair of operand columns.
+//
+// Y is first laid out as YD[r_pad x 32] fp32 in DEVICE row order (operand
+// columns past c_y and the padding rows are zero; k_ydev32_*).  Then per
+// 128-row tile ONE M = 128, N = 64 MMA chain over the tile's rows computes
+//     D = [F | F_lo | Y | Y_lo]^T [Y | Y_lo]
+// with both operands read MN-major straight from the row-major TMA tiles
+// (128B / 32-byte-atom swizzle, descriptor layout 1, tc05.cuh); the tiles are
+// their own tf32 hi parts (the tensor core truncates), the lo parts are
+// written next to them by the split warps, and
+//     F^T Y = D[F][Y] + D[F_lo][Y] + D[F][Y_lo]          (3xTF32)
+// (rows 64..127 of D -- Y^T Y -- are a by-product of the M = 128 shape and
+// unused).  TMEM accumulates two tiles (256 rows) in fp32; dedicated fold
+// warps move them into fp64 registers; per-CTA partials are reduced in CTA
+// order by k_reduce_partials.  Bytes: F (4 pf) + YD (128) per row, read once.
+//
+//   warp 0     producer (TMA of the F and Y tiles)
+//   warp 1     MMA issuer (one thread)
+//   warps 2-5  split: F_lo and Y_lo of each tile (thread = tile row)
+//   warps 8-9  fold: TMEM lanes 0..63 (the F / F_lo rows of D)
+//   warps 6-7  idle (TMEM lane quadrants 2, 3 hold the unused Y rows of D)
+constexpr int M5_TILE = 128;
+constexpr int M5_NS = 3;
+constexpr int M5_FT = 2;
+constexpr int M5_THREADS = 320;
+constexpr uint32_t M5_STAGE = 65536;   // F | F_lo | Y | Y_lo, 16 KB each
+constexpr uint32_t M5_SMEM = M5_NS * M5_STAGE + 1024;
+
+__device__ __forceinline__ uint32_t m5_b32(int row, int c4) {
+  return (uint32_t)(row * 128 + (((c4 >> 1) ^ (row & 3)) << 5) + ((c4 & 1) << 4));
+}
+__device__ __forceinline__ float m5_lo(float v) {
+  return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+}
+
+// part[cta][i * cy + c] = sum over the CTA's rows of F[r][i] Y[r][c]
+__global__ void __launch_bounds__(M5_THREADS, 1)
+    k_tmm_t5(const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmY,
+             int pf, int cy, int64_t ntiles, double* __restrict__ part) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[M5_NS], empty[M5_NS], lo_ready[M5_NS], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < M5_NS; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&lo_ready[s], 128);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 64);   // the two fold warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::alloc(&tbase, 128);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  const int64_t G = gridDim.x;
+  const int64_t base = ntiles / G, rem = ntiles % G;
+  const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
+  const int n = (int)(base + (blockIdx.x < rem ? 1 : 0));
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      for (int i = 0; i < n; i++) {
+        const int s = i % M5_NS;
+        if (i >= M5_NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / M5_NS) - 1) & 1));
+        char* st = sm + s * M5_STAGE;
+        mbar_arrive_expect_tx(&full[s], 32768u);
+        tma_load_2d_hint(st, &tmF, 0, (int)((t0 + i) * M5_TILE), &full[s], pol);
+        tma_load_2d_hint(st + 32768, &tmY, 0, (int)((t0 + i) * M5_TILE), &full[s], pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n > 0) {
+      const uint32_t id = tc::idesc_tf32(128, 64, true, true);
+      for (int t = 0; t < n; t++) {
+        const int s = t % M5_NS, w = t / M5_FT, b = w & 1;
+        mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / M5_NS) & 1));
+        if ((t % M5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
+        tc::fence_after();
+        const uint32_t st = smem_u32(sm + s * M5_STAGE);
+        const uint64_t a0 = tc::smem_desc(st, 16384, 512, tc::kSw128B32);
+        const uint64_t b0 = tc::smem_desc(st + 32768, 16384, 512, tc::kSw128B32);
+#pragma unroll
+        for (int kk = 0; kk < M5_TILE / 8; kk++)
+          tc::mma_tf32(tmem + 64 * b, a0 + (uint64_t)(kk * 64), b0 + (uint64_t)(kk * 64), id,
+                       !((t % M5_FT) == 0 && kk == 0));
+        tc::commit(&empty[s]);
+        if ((t % M5_FT) == M5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
+      }
+    }
+  } else if (warp >= 2 && warp < 6) {
+    const int r = 32 * (warp & 3) + lane;
+    const int sw = (r >> 2) & 1;   // rows r, r + 4 share a granule: swap chunk halves
+    for (int t = 0; t < n; t++) {
+      const int s = t % M5_NS;
+      char* st = sm + s * M5_STAGE;
+      mbar_wait_sleep(&full[s], (uint32_t)((t / M5_NS) & 1));
+#pragma unroll
+      for (int h = 0; h < 2; h++) {   // F, then Y
+        char* src = st + h * 32768;
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+          const uint32_t o = m5_b32(r, c ^ sw);
+          const float4 v = *reinterpret_cast<const float4*>(src + o);
+          *reinterpret_cast<float4*>(src + 16384 + o) =
+              make_float4(m5_lo(v.x), m5_lo(v.y), m5_lo(v.z), m5_lo(v.w));
+        }
+      }
+      fence_proxy_async();
+      tc::fence_before();
+      mbar_arrive(&lo_ready[s]);
+    }
+  } else if (warp >= 8) {
+    const int q4 = warp & 3, r = 32 * q4 + lane;   // q4 = 0, 1: rows 0..63 of D
+    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+    double ra[64];
+#pragma unroll
+    for (int j = 0; j < 64; j++) ra[j] = 0.0;
+    const int nw = n > 0 ? (n - 1) / M5_FT + 1 : 0;
+    for (int w = 0; w < nw; w++) {
+      const int b = w & 1;
+      mbar_wait_sleep(&acc_full[b], (uint32_t)((w >> 1) & 1));
+      tc::fence_after();
+#pragma unroll
+      for (int u = 0; u < 4; u += 2) {
+        uint32_t x0[16], x1[16];
+        tc::ld16(tmem + lane_off + 64 * b + 16 * u, x0);
+        tc::ld16(tmem + lane_off + 64 * b + 16 * u + 16, x1);
+        tc::wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          ra[16 * u + j] += (double)__uint_as_float(x0[j]);
+          ra[16 * u + 16 + j] += (double)__uint_as_float(x1[j]);
+        }
+      }
+      tc::fence_before();
+      mbar_arrive(&acc_empty[b]);
+    }
+    // all MMAs are complete (the last acc_full): stage 0 is free for the
+    // combine area acc[col][row] (fp64 64 x 64 = 32 KB)
+    double* acc = reinterpret_cast<double*>(sm);
+#pragma unroll
+    for (int j = 0; j < 64; j++) acc[j * 64 + r] = ra[j];
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  // (F^T Y)[i][c] = D[i][c] + D[32 + i][c] + D[i][32 + c]
+  const double* acc = reinterpret_cast<const double*>(sm);
+  double* out = part + (int64_t)blockIdx.x * pf * cy;
+  for (int e = tid; e < pf * cy; e += blockDim.x) {
+    const int i = e / cy, c = e - i * cy;
+    out[e] = acc[c * 64 + i] + acc[c * 64 + 32 + i] + acc[(32 + c) * 64 + i];
+  }
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 128);
+}
+
+// YD[iperm[t]][c] = y(t, c) for a column-strided y view (rmm's x^T): each
+// block transposes 32 target rows through shared memory -- coalesced reads
+// along the columns of x, one 128-byte row write per device row
+__global__ void __launch_bounds__(256) k_ydev32_cols(YView yv, int cy, int64_t r_T,
+                                                     const int32_t* __restrict__ iperm,
+                                                     float* __restrict__ yd) {
+  __shared__ float tile[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t t0 = blockIdx.x * 32LL; t0 < r_T; t0 += gridDim.x * 32LL) {
+    const int64_t tr = t0 + lane;
+    for (int c = warp; c < 32; c += 8)
+      tile[lane][c] = (c < cy && tr < r_T) ? yv.at(tr, c) : 0.f;
+    __syncthreads();
+    for (int rr = warp; rr < 32; rr += 8) {
+      const int64_t t = t0 + rr;
+      if (t < r_T) {
+        const int64_t p = iperm ? (int64_t)iperm[t] : t;
+        yd[p * 32 + lane] = tile[rr][lane];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// YD[p][c] = y(perm[p], c) for a row-major y view (warp per device row);
+// perm == nullptr: y is in device order already
+__global__ void __launch_bounds__(256) k_ydev32_rows(YView yv, int cy, int64_t r_T,
+                                                     const int32_t* __restrict__ perm,
+                                                     float* __restrict__ yd) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < r_T;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t tr = perm ? (int64_t)perm[p] : p;
+    yd[p * 32 + lane] = lane < cy ? yv.at(tr, lane) : 0.f;
+  }
+}

@@ -318,3 +318,29 @@ def test_crossprod_tcgen05_gram_matches_simt(fl, monkeypatch, c_fact, dims):
     simt = h.crossprod()
     assert rel(got, td.T @ td) < RTOL
     assert rel(got, simt) < 4e-6
+
+
+@pytest.mark.parametrize("c_fact,dims,sort_fk", [(20, [(2000, 30)], False), (28, [], False),
+                                                 (13, [(500, 7), (40, 3)], False),
+                                                 (3, [(3000, 9)], True)])
+def test_wide_tlmm_rmm_tcgen05_vs_oracle(fl, monkeypatch, c_fact, dims, sort_fk):
+    """Wide T^T y and rmm through the tcgen05 pass (csrc/tmm_t5.cuh: y laid
+    out once in device order, [F | F_lo | Y | Y_lo]^T [Y | Y_lo] per 128-row
+    tile) for 3..32 operand columns, against the oracle and against the
+    per-column-pair SIMT passes (FL_NO_TMM_T5=1); 33 columns stays on the
+    chunked path."""
+    ft = star_table(23, 70_001, dims, c_fact, sort_fk=sort_fk)
+    tab = oracle.OracleTable.from_ft(ft)
+    h = fl.TargetHandle.factorized(ft)
+    rng = np.random.default_rng(4)
+    for cy in (3, 5, 9, 16, 31, 32, 33):
+        y = rng.random((ft.r_T, cy)).astype(np.float32)
+        w = rng.random((cy, ft.r_T)).astype(np.float32)
+        got_t = h.transpose_lmm(y)
+        got_r = h.rmm(w)
+        assert rel(got_t, oracle.transpose_lmm(tab, y)) < RTOL, cy
+        assert rel(got_r, oracle.rmm(tab, w)) < RTOL, cy
+        monkeypatch.setenv("FL_NO_TMM_T5", "1")
+        assert rel(got_t, h.transpose_lmm(y)) < 4e-6, cy
+        assert rel(got_r, h.rmm(w)) < 4e-6, cy
+        monkeypatch.delenv("FL_NO_TMM_T5")
