@@ -184,10 +184,10 @@ __global__ void k_group_rows_sum(const int64_t* __restrict__ grp_ptr,
       double s = 0.0;
       if (c < w && src >= 0) {
         int64_t m = m0;
-        for (; m + 4 <= m1; m += 4) {   // four independent loads in flight
-          float v[4];
+        for (; m + 8 <= m1; m += 8) {   // eight independent loads in flight
+          float v[8];
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
+          for (int u = 0; u < 8; u++) {
             const int64_t p = sorted ? n_neg + m + u : (int64_t)grp_rows[m + u];
             if (src == 0) {
               v[u] = F[p * pf + cc];
@@ -198,7 +198,7 @@ __global__ void k_group_rows_sum(const int64_t* __restrict__ grp_ptr,
             }
           }
 #pragma unroll
-          for (int u = 0; u < 4; u++) s += (double)v[u];
+          for (int u = 0; u < 8; u++) s += (double)v[u];
         }
         for (; m < m1; m++) {
           const int64_t p = sorted ? n_neg + m : (int64_t)grp_rows[m];
@@ -224,9 +224,10 @@ int gram(fl_table* t, const float* A, int pa, int acols, const float* B, int pb,
   if (rows <= 0 || acols <= 0 || bcols <= 0) return FL_OK;
   const int nta = (acols + GT - 1) / GT, ntb = (bcols + GT - 1) / GT;
   const int ntiles = nta * ntb;
-  // ~4 CTAs per SM over all tiles; row chunks are whole staged tiles
+  // ~8 CTAs per SM over all tiles (the staged loop is latency-bound); row
+  // chunks are whole staged tiles
   int64_t nb = std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 4 * GROWS),
-                                                      (4 * (int64_t)t->sm_count + ntiles - 1) / ntiles));
+                                                      (8 * (int64_t)t->sm_count + ntiles - 1) / ntiles));
   const int64_t rpc = round_up(ceil_div(rows, nb), GROWS);
   nb = ceil_div(rows, rpc);
   double* part = nullptr;
@@ -261,7 +262,9 @@ int fgram_t5(fl_table* t, double* out, cudaStream_t s) {
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
   double* part = nullptr;
   FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * t->pf * t->pf * 8, s));
-  k_fgram_t5<<<nb, R5_THREADS, gm.total + 1024, s>>>(tm, t->pf, ntiles, gm, part);
+  const char* m6 = getenv("FL_GRAM_M64");
+  k_fgram_t5<<<nb, R5_THREADS, gm.total + 1024, s>>>(tm, t->pf, ntiles, gm, part,
+                                                     (m6 && atoi(m6)) ? 1 : 0);
   FL_CHECK_LAUNCH();
   k_fgram_reduce<<<(unsigned)ceil_div((int64_t)t->pf * t->pf * 32, 256), 256, 0, s>>>(
       part, nb, t->pf, t->d_f_tcol->as<int32_t>(), t->c_T, out);

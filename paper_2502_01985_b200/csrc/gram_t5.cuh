@@ -16,12 +16,16 @@
 //   warp 0     producer (TMA of the F tile)
 //   warp 1     MMA issuer (one thread)
 //   warps 2-5  split: F_lo of each tile (thread = tile row)
-//   warps 8-9  fold: TMEM lanes 0..63 (rows of D) into fp64 registers
-//   warps 6-7  idle (TMEM lane quadrants 2, 3 hold no used rows of D)
+//   warps 8-11 fold: the 64 used rows of D into fp64 registers
+//   warps 6-7  idle
+// m64 selects the M = 64 MMA shape (A = [F | F_lo] exactly, half the shared-
+// memory operand reads of M = 128, whose groups 2, 3 are padding): D row i
+// then sits in TMEM lane 32 (i / 16) + i % 16 (16 lanes per warp quadrant)
+// instead of lane i.
 constexpr int R5_TILE = 128;
 constexpr int R5_NS = 6;
 constexpr int R5_FT = 2;              // fp32 TMEM sums over 256 rows, then fp64
-constexpr int R5_THREADS = 320;
+constexpr int R5_THREADS = 384;
 
 struct R5Geom {
   uint32_t stage;   // F (16 KB) | F_lo (16 KB)
@@ -49,7 +53,7 @@ __device__ __forceinline__ float r5_lo(float v) {
 // part[cta][i * pf + j] = sum over the CTA's rows of F[r][i] F[r][j]
 __global__ void __launch_bounds__(R5_THREADS, 1)
     k_fgram_t5(const __grid_constant__ CUtensorMap tmF, int pf, int64_t ntiles, R5Geom gm,
-               double* __restrict__ part) {
+               double* __restrict__ part, int m64) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[R5_NS], empty[R5_NS], lo_ready[R5_NS], acc_full[2], acc_empty[2];
@@ -59,6 +63,9 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
   // the M = 128 operand reads 32 KB past a stage into rows of D that are
   // never used (the last stage reads the combine area): keep it finite
   for (int i = tid; i < 64 * 64; i += blockDim.x) acc[i] = 0.0;
+  // F_lo columns past pf are never written by the split: keep them zero
+  for (int i = tid; i < R5_NS * 4096; i += blockDim.x)
+    reinterpret_cast<float*>(sm + (i >> 12) * gm.stage + 16384)[i & 4095] = 0.f;
   if (tid == 0) {
     for (int s = 0; s < R5_NS; s++) {
       mbar_init(&full[s], 1);
@@ -67,7 +74,7 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 64);   // the two fold warps
+      mbar_init(&acc_empty[b], m64 ? 128 : 64);   // the fold warps
     }
     fence_mbar_init();
   }
@@ -94,7 +101,7 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && n > 0) {
-      const uint32_t id = tc::idesc_tf32(128, 32, true, true);
+      const uint32_t id = tc::idesc_tf32(m64 ? 64 : 128, 32, true, true);
       for (int t = 0; t < n; t++) {
         const int s = t % R5_NS, w = t / R5_FT, b = w & 1;
         mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / R5_NS) & 1));
@@ -113,12 +120,14 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
   } else if (warp >= 2 && warp < 6) {
     const int r = 32 * (warp & 3) + lane;
     const int sw = (r >> 2) & 1;   // rows r, r + 4 share a granule: swap chunk halves
+    const int nc4 = (pf + 3) >> 2;
     for (int t = 0; t < n; t++) {
       const int s = t % R5_NS;
       char* st = sm + s * gm.stage;
       mbar_wait_sleep(&full[s], (uint32_t)((t / R5_NS) & 1));
 #pragma unroll
       for (int c = 0; c < 8; c++) {
+        if ((c ^ sw) >= nc4) continue;
         const uint32_t o = r5_b32(r, c ^ sw);
         const float4 v = *reinterpret_cast<const float4*>(st + o);
         *reinterpret_cast<float4*>(st + 16384 + o) =
@@ -128,10 +137,12 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
       tc::fence_before();
       mbar_arrive(&lo_ready[s]);
     }
-  } else if (warp >= 8) {
-    const int q4 = warp & 3, r = 32 * q4 + lane;   // q4 = 0, 1: rows 0..63 of D
+  } else if (warp >= 8 && (m64 || warp < 10)) {
+    const int q4 = warp & 3;
+    // row of D held by this lane (-1: an unused TMEM lane)
+    const int r = m64 ? (lane < 16 ? 16 * q4 + lane : -1) : 32 * q4 + lane;
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
-    double ra[32];                 // this lane's row of D, fp64
+    double ra[32];
 #pragma unroll
     for (int j = 0; j < 32; j++) ra[j] = 0.0;
     const int nw = n > 0 ? (n - 1) / R5_FT + 1 : 0;
@@ -151,8 +162,10 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
         ra[16 + j] += (double)__uint_as_float(x1[j]);
       }
     }
+    if (r >= 0) {
 #pragma unroll
-    for (int j = 0; j < 32; j++) acc[j * 64 + r] = ra[j];
+      for (int j = 0; j < 32; j++) acc[j * 64 + r] = ra[j];
+    }
   }
   tc::fence_before();
   __syncthreads();

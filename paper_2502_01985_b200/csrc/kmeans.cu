@@ -70,6 +70,7 @@ struct KmFactArgs {
   uint32_t stage_bytes;          // 32 x FP fp32 TMA tile | 32 int32 sort-source FK
   int nst;
   int diag;                      // timing experiments only (FL_KM_DIAG): 1 no sums, 2 no loss
+  int npf_max;                   // gathered sources on the async-copy E prefetch (<= KM_PF_MAX)
 };
 
 struct KmDimArgs {
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
   const int r_T32 = (int)a.r_T;
   constexpr uint32_t F_BYTES = 32u * FP * 4u;
   // F tile + the 32 FKs of every source not in the async-copied FK ring
-  const int npf = min(a.ng, KM_PF);
+  const int npf = min(a.ng, a.npf_max);
   const uint32_t tx = F_BYTES + 128u * (a.ng - npf);
   char* wsm = stages + (size_t)warp * a.nst * a.stage_bytes;
   float* ebuf = ebuf_all + warp * EW;   // [KM_PF][32][KP] E rows; also the z transpose scratch
@@ -403,8 +404,9 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       __syncwarp();   // the scratch is reused for the distance transpose
     }
 #pragma unroll
-    for (int d = KM_PF; d < MAX_GATHER; d++) {
+    for (int d = 0; d < MAX_GATHER; d++) {
       if (d >= a.ng) break;
+      if (d < npf) continue;
       const int f = fks_s[d * 32 + lane];
       const float4* er = reinterpret_cast<const float4*>(a.E[d] + (f >= 0 ? (int64_t)f : a.rows[d]) * KP);
 #pragma unroll
@@ -1064,6 +1066,8 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
   fa.f_tcol = t->d_f_tcol->as<int32_t>();
   fa.assign = nullptr;
   if (const char* dg = getenv("FL_KM_DIAG")) fa.diag = atoi(dg);   // timing experiments
+  fa.npf_max = KM_PF_MAX;
+  if (const char* pe = getenv("FL_KM_PF")) fa.npf_max = std::max(0, std::min(KM_PF_MAX, atoi(pe)));
   const int FP = SC + 4, ZP = KP + 4;
   fa.stage_bytes = (uint32_t)round_up(32 * FP * 4 + 128 * ng, 128);
   if ((rc = make_tmap_2d(&s->tmF, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf,

@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(256) k_lmm_warp_rows(const float* __restrict__
                                                        const float* __restrict__ x, int c_x,
                                                        int col0, int ncol, GatherSet gs,
                                                        const int32_t* __restrict__ perm,
-                                                       int64_t r_T, float* __restrict__ out) {
+                                                       int64_t r_T, float* __restrict__ out,
+                                                       int o_pitch, int o_col0) {
   constexpr int PF = C4 * 4;
   const int lane = threadIdx.x & 31;
   const bool on = lane < ncol;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(256) k_lmm_warp_rows(const float* __restrict__
     for (int r = 0; r < R; r++) {
       const int64_t p = p0 + r;
       v[r] = (lane < PF && p < r_T) ? F[p * PF + lane] : 0.f;
-      tr[r] = p < r_T ? perm[p] : -1;
+      tr[r] = p < r_T ? (perm ? perm[p] : (int32_t)p) : -1;   // perm null: device order out
       acc[r] = 0.f;
     }
 #pragma unroll
@@ -179,7 +180,24 @@ __global__ void __launch_bounds__(256) k_lmm_warp_rows(const float* __restrict__
     }
 #pragma unroll
     for (int r = 0; r < R; r++)
-      if (on && tr[r] >= 0) out[(int64_t)tr[r] * c_x + col0 + lane] = acc[r];
+      if (on && tr[r] >= 0) out[(int64_t)tr[r] * o_pitch + o_col0 + lane] = acc[r];
+  }
+}
+
+// out[t, col0 + c] = dev[iperm[t], c] for ncol <= 32 columns: warp per
+// target row, one contiguous row read (random) and one row write
+// (sequential).  Scattered row WRITES cost ~2x scattered row reads on the
+// B200 (tools/scatter_probe.py), so wide lmm outputs are produced in device
+// order and gathered into target order here.
+__global__ void __launch_bounds__(256) k_rows_unperm(const float* __restrict__ dev, int ncol,
+                                                     const int32_t* __restrict__ iperm,
+                                                     int64_t r_T, int c_x, int col0,
+                                                     float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < r_T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t p = iperm[t];
+    if (lane < ncol) out[t * c_x + col0 + lane] = dev[p * ncol + lane];
   }
 }
 
@@ -573,16 +591,36 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
       const unsigned nb =
           (unsigned)std::min<int64_t>(ceil_div(t->r_T, 64), 8 * (int64_t)t->sm_count);
       const int32_t* ftcol = t->d_f_tcol->as<int32_t>();
-      const int32_t* perm = t->perm->as<int32_t>();
+      // scattered row writes straight from the pass; FL_LMM_UNPERM=1: device-
+      // order rows + a row gather into target order (measured slower: the
+      // pass is issue-bound either way, C2 k = 32 12.5 -> 21.0 ms)
+      const char* up = getenv("FL_LMM_UNPERM");
+      const bool unperm = up && atoi(up) == 1;
+      const int32_t* perm = unperm ? nullptr : t->perm->as<int32_t>();
+      float* dst = out_dev;
+      int dc = c_x, d0 = col0;
+      if (unperm) {
+        FL_CUDA(cudaMallocAsync((void**)&dst, t->r_T * ncol * 4 + 16, s));
+        dc = ncol;
+        d0 = 0;
+      }
       switch (t->pf / 4) {
-#define LMW(C)                                                                               \
-  case C:                                                                                    \
+#define LMW(C)                                                                                 \
+  case C:                                                                                      \
     k_lmm_warp_rows<C><<<nb, 256, 0, s>>>(F, ftcol, x_dev, c_x, col0, ncol, gs, perm, t->r_T, \
-                                          out_dev);                                          \
+                                          dst, dc, d0);                                        \
     break;
         LMW(1) LMW(2) LMW(3) LMW(4) LMW(5) LMW(6) LMW(7) LMW(8)
 #undef LMW
         default: break;
+      }
+      if (unperm) {
+        FL_CHECK_LAUNCH();
+        const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(t->r_T, 8), 16 * (int64_t)t->sm_count);
+        k_rows_unperm<<<gb, 256, 0, s>>>(dst, ncol, t->iperm->as<int32_t>(), t->r_T, c_x, col0,
+                                         out_dev);
+        FL_CHECK_LAUNCH();
+        FL_CUDA(cudaFreeAsync(dst, s));
       }
     } else {
       size_t sm = (size_t)t->pf * ncol * 4;
@@ -601,9 +639,38 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
 static int tlmm_impl(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
                      cudaStream_t s, bool dev_order, bool with_f);
 
-// F^T y through k_tmm_t5 for 3..32 operand columns (tmm_t5.cuh): y laid out
-// once as YD (device order, 32-column rows), then one tensor-core pass; the
-// gathered sources read YD in device order
+// S_d^T bins (bins = I_d^T y, r_d x cy fp64) into out: per-CTA partials
+// (k_tmm_partial) reduced in CTA order
+static int tlmm_bins_product(fl_table* t, const GatherSrc& g, const double* bins, int cy,
+                             double* out, int64_t os_t, int64_t os_c, cudaStream_t s) {
+  if (g.rows <= 0 || g.cols <= 0) return FL_OK;
+  int64_t nb = std::min<int64_t>(std::max<int64_t>(1, ceil_div(g.rows, 2048)), 4 * t->sm_count);
+  const int64_t rpb = round_up(ceil_div(g.rows, nb), 32);
+  nb = ceil_div(g.rows, rpb);
+  const int npair = g.cols * cy;
+  const size_t sm = (size_t)npair * 8;
+  double* part = nullptr;
+  FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
+  FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm));
+  k_tmm_partial<true><<<(unsigned)nb, 256, sm, s>>>(g.S->as<float>(), g.pitch, g.cols, g.rows,
+                                                    YView{nullptr, 0, 0}, nullptr, bins, cy, rpb,
+                                                    part);
+  FL_CHECK_LAUNCH();
+  k_reduce_partials<<<gridn((int64_t)npair * 32), 256, 0, s>>>(part, (int)nb, g.cols, cy,
+                                                               g.d_tcol->as<int32_t>(), out, os_t,
+                                                               os_c);
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaFreeAsync(part, s));
+  return FL_OK;
+}
+
+// T^T y for 3..32 operand columns with the stream block on tcgen05
+// (tmm_t5.cuh): y laid out once as YD (device order, 32-column rows; a
+// column-strided view -- rmm's x^T -- is first transposed in target order,
+// sequential on both sides, then gathered by rows), one tensor-core pass
+// over F and YD, then per gathered source the group sums of YD (warp per
+// group, k_group_bins' ascending fp64 order) and the S_d^T bins product
 static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
                         cudaStream_t s, bool dev_order) {
   const int64_t r_T = t->r_T, r_pad = t->r_pad;
@@ -611,10 +678,22 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
   FL_CUDA(cudaMallocAsync((void**)&yd, (size_t)r_pad * 32 * 4, s));
   if (r_pad > r_T) FL_CUDA(cudaMemsetAsync(yd + r_T * 32, 0, (size_t)(r_pad - r_T) * 32 * 4, s));
   const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(r_T, 32), 16 * (int64_t)t->sm_count);
-  if (yv.sc > yv.sr)
-    k_ydev32_cols<<<gb, 256, 0, s>>>(yv, cy, r_T, dev_order ? nullptr : t->iperm->as<int32_t>(), yd);
-  else
-    k_ydev32_rows<<<gb, 256, 0, s>>>(yv, cy, r_T, dev_order ? nullptr : t->perm->as<int32_t>(), yd);
+  const int32_t* perm = dev_order ? nullptr : t->perm->as<int32_t>();
+  if (yv.sc > yv.sr && yv.sr == 1) {
+    // column-strided (rmm's x^T): transpose in target order, then gather rows
+    float* xt = yd;
+    if (perm) FL_CUDA(cudaMallocAsync((void**)&xt, (size_t)r_T * 32 * 4, s));
+    k_xt32<<<(unsigned)std::min<int64_t>(ceil_div(r_T, 128), 8 * (int64_t)t->sm_count), 256, 0, s>>>(
+        yv, cy, r_T, xt);
+    FL_CHECK_LAUNCH();
+    if (perm) {
+      k_ydev32_rows<<<gb, 256, 0, s>>>(YView{xt, 32, 1}, 32, r_T, perm, yd);
+      FL_CHECK_LAUNCH();
+      FL_CUDA(cudaFreeAsync(xt, s));
+    }
+  } else {
+    k_ydev32_rows<<<gb, 256, 0, s>>>(yv, cy, r_T, perm, yd);
+  }
   FL_CHECK_LAUNCH();
   CUtensorMap tmF, tmY;
   int rc = make_tmap_2d(&tmF, t->F->p, (uint64_t)r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,
@@ -637,16 +716,26 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
       part, nb, t->pf, cy, t->d_f_tcol->as<int32_t>(), out, os_t, os_c);
   FL_CHECK_LAUNCH();
   FL_CUDA(cudaFreeAsync(part, s));
-  rc = FL_OK;
-  if (!t->g.empty()) rc = tlmm_impl(t, YView{yd, 32, 1}, cy, out, os_t, os_c, s, true, false);
+  for (auto& g : t->g) {
+    double* bins = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&bins, g.rows * cy * 8 + 16, s));
+    k_group_bins32<<<(unsigned)std::min<int64_t>(ceil_div(g.rows, 8), 32 * (int64_t)t->sm_count),
+                     256, 0, s>>>(g.grp_ptr->as<int64_t>(),
+                                  g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr, g.sorted,
+                                  g.n_neg, g.rows, yd, cy, bins);
+    FL_CHECK_LAUNCH();
+    rc = tlmm_bins_product(t, g, bins, cy, out, os_t, os_c, s);
+    if (rc) return rc;
+    FL_CUDA(cudaFreeAsync(bins, s));
+  }
   FL_CUDA(cudaFreeAsync(yd, s));
-  return rc;
+  return FL_OK;
 }
 
 static int tmm_t5_min_cols() {
   static const int v = [] {
     const char* e = getenv("FL_TMM_T5_MIN");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 6;
   }();
   return v;
 }
@@ -654,9 +743,11 @@ static int tmm_t5_min_cols() {
 // generic T^T y with strided y view and strided fp64 output
 int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
             cudaStream_t s, bool dev_order) {
-  if (t->pf > 0 && t->pf <= 28 && cy >= tmm_t5_min_cols() && cy <= 32 && t->r_T > 0 &&
-      t->r_T <= (int64_t)INT32_MAX - M5_TILE && !getenv("FL_NO_TMM_T5"))
-    return tlmm_wide_t5(t, yv_in, cy, out, os_t, os_c, s, dev_order);
+  bool wide = t->pf > 0 && t->pf <= 28 && cy >= tmm_t5_min_cols() && cy <= 32 && t->r_T > 0 &&
+              t->r_T <= (int64_t)INT32_MAX - M5_TILE && !getenv("FL_NO_TMM_T5");
+  for (const auto& g : t->g)
+    if ((size_t)g.cols * cy * 8 > 190 * 1024) wide = false;   // bins product smem
+  if (wide) return tlmm_wide_t5(t, yv_in, cy, out, os_t, os_c, s, dev_order);
   return tlmm_impl(t, yv_in, cy, out, os_t, os_c, s, dev_order, true);
 }
 

@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
   const int64_t base = ntiles / G, rem = ntiles % G;
   const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
   const int n = (int)(base + (blockIdx.x < rem ? 1 : 0));
+  double ra[64];   // fold warps: this lane's row of D, fp64
 
   if (warp == 0) {
     if (lane == 0) {
@@ -124,7 +125,6 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
   } else if (warp >= 8) {
     const int q4 = warp & 3, r = 32 * q4 + lane;   // q4 = 0, 1: rows 0..63 of D
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
-    double ra[64];
 #pragma unroll
     for (int j = 0; j < 64; j++) ra[j] = 0.0;
     const int nw = n > 0 ? (n - 1) / M5_FT + 1 : 0;
@@ -147,15 +147,17 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
       tc::fence_before();
       mbar_arrive(&acc_empty[b]);
     }
-    // all MMAs are complete (the last acc_full): stage 0 is free for the
-    // combine area acc[col][row] (fp64 64 x 64 = 32 KB)
-    double* acc = reinterpret_cast<double*>(sm);
+  }
+  tc::fence_before();
+  __syncthreads();   // every stage is idle: stage 0 becomes the combine area
+  tc::fence_after();
+  if (warp >= 8) {
+    const int r = 32 * (warp & 3) + lane;
+    double* acc = reinterpret_cast<double*>(sm);   // acc[col][row], fp64 64 x 64
 #pragma unroll
     for (int j = 0; j < 64; j++) acc[j * 64 + r] = ra[j];
   }
-  tc::fence_before();
   __syncthreads();
-  tc::fence_after();
   // (F^T Y)[i][c] = D[i][c] + D[32 + i][c] + D[i][32 + c]
   const double* acc = reinterpret_cast<const double*>(sm);
   double* out = part + (int64_t)blockIdx.x * pf * cy;
@@ -167,27 +169,76 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
   if (warp == 0) tc::dealloc(tmem, 128);
 }
 
-// YD[iperm[t]][c] = y(t, c) for a column-strided y view (rmm's x^T): each
-// block transposes 32 target rows through shared memory -- coalesced reads
-// along the columns of x, one 128-byte row write per device row
-__global__ void __launch_bounds__(256) k_ydev32_cols(YView yv, int cy, int64_t r_T,
-                                                     const int32_t* __restrict__ iperm,
-                                                     float* __restrict__ yd) {
-  __shared__ float tile[32][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t t0 = blockIdx.x * 32LL; t0 < r_T; t0 += gridDim.x * 32LL) {
-    const int64_t tr = t0 + lane;
-    for (int c = warp; c < 32; c += 8)
-      tile[lane][c] = (c < cy && tr < r_T) ? yv.at(tr, c) : 0.f;
-    __syncthreads();
-    for (int rr = warp; rr < 32; rr += 8) {
-      const int64_t t = t0 + rr;
-      if (t < r_T) {
-        const int64_t p = iperm ? (int64_t)iperm[t] : t;
-        yd[p * 32 + lane] = tile[rr][lane];
+// XT[t][c] = y(t, c) for a column-strided y view (rmm's x^T, element (t, c)
+// at base[c * sc + t], sr == 1): 128 target rows x 32 columns per block
+// step through shared memory, float4 reads along the columns of x and
+// float4 row writes, sequential on both sides; columns past c_y are zero
+__global__ void __launch_bounds__(256) k_xt32(YView yv, int cy, int64_t r_T,
+                                              float* __restrict__ xt) {
+  __shared__ float tile[32][128 + 4];   // [column][row]
+  const int tid = threadIdx.x;
+  for (int64_t t0 = blockIdx.x * 128LL; t0 < r_T; t0 += gridDim.x * 128LL) {
+    const bool full = t0 + 128 <= r_T && (((uintptr_t)(yv.base + t0) | (uintptr_t)yv.sc * 4) & 15) == 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {   // 32 columns x 32 float4 = 1024 loads
+      const int i = tid + 256 * k, c = i >> 5, q = i & 31;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < cy) {
+        if (full) {
+          v = __ldg(reinterpret_cast<const float4*>(yv.base + (int64_t)c * yv.sc + t0) + q);
+        } else {
+          const int64_t t = t0 + 4 * q;
+          v.x = t < r_T ? yv.at(t, c) : 0.f;
+          v.y = t + 1 < r_T ? yv.at(t + 1, c) : 0.f;
+          v.z = t + 2 < r_T ? yv.at(t + 2, c) : 0.f;
+          v.w = t + 3 < r_T ? yv.at(t + 3, c) : 0.f;
+        }
       }
+      *reinterpret_cast<float4*>(&tile[c][4 * q]) = v;
     }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {   // 128 rows x 8 float4
+      const int i = tid + 256 * k, row = i >> 3, c4 = i & 7;
+      const int64_t t = t0 + row;
+      if (t < r_T)
+        reinterpret_cast<float4*>(xt + t * 32)[c4] =
+            make_float4(tile[4 * c4][row], tile[4 * c4 + 1][row], tile[4 * c4 + 2][row],
+                        tile[4 * c4 + 3][row]);
+    }
+    __syncthreads();
+  }
+}
+
+// bins[j][c] = sum over the members of group j (ascending) of YD[p][c],
+// fp64 -- k_group_bins' order -- with a warp per group and lane = column
+// (YD rows are 128-byte device-order rows)
+__global__ void __launch_bounds__(256) k_group_bins32(const int64_t* __restrict__ grp_ptr,
+                                                      const int32_t* __restrict__ grp_rows,
+                                                      bool sorted, int64_t n_neg, int64_t rows,
+                                                      const float* __restrict__ yd, int cy,
+                                                      double* __restrict__ bins) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < rows;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t m0 = grp_ptr[j], m1 = grp_ptr[j + 1];
+    double s = 0.0;
+    int64_t m = m0;
+    for (; m + 8 <= m1; m += 8) {   // eight row loads in flight
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int64_t p = sorted ? n_neg + m + u : (int64_t)grp_rows[m + u];
+        v[u] = yd[p * 32 + lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) s += (double)v[u];
+    }
+    for (; m < m1; m++) {
+      const int64_t p = sorted ? n_neg + m : (int64_t)grp_rows[m];
+      s += (double)yd[p * 32 + lane];
+    }
+    if (lane < cy) bins[j * cy + lane] = s;
   }
 }
 

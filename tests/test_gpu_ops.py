@@ -314,10 +314,14 @@ def test_crossprod_tcgen05_gram_matches_simt(fl, monkeypatch, c_fact, dims):
     td = oracle.materialize(tab)
     h = fl.TargetHandle.factorized(ft)
     got = h.crossprod()
+    monkeypatch.setenv("FL_GRAM_M64", "1")   # M = 64 MMA shape (16-lane TMEM quadrants)
+    got64 = h.crossprod()
+    monkeypatch.delenv("FL_GRAM_M64")
     monkeypatch.setenv("FL_NO_GRAM_T5", "1")
     simt = h.crossprod()
     assert rel(got, td.T @ td) < RTOL
     assert rel(got, simt) < 4e-6
+    assert rel(got64, simt) < 4e-6
 
 
 @pytest.mark.parametrize("c_fact,dims,sort_fk", [(20, [(2000, 30)], False), (28, [], False),
