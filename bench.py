@@ -620,7 +620,11 @@ def main():
             torch.cuda.synchronize()
             ms_total = e0.elapsed_time(e1)
         else:       # L2-resident working set: flush between iterations, time each alone
-            ms_total = 0.0
+            # all steps are enqueued back to back (flush, event, iteration,
+            # event) and synchronized once: each pair of events brackets one
+            # iteration on the device, after a cold L2, without the host's
+            # launch latency of an idle stream inside the bracket
+            evs = []
             for _ in range(args.steps):
                 flush_buf.fill_(1.0)
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -628,8 +632,9 @@ def main():
                 e0.record(stream0)
                 run(1)
                 e1.record(stream0)
-                torch.cuda.synchronize()
-                ms_total += e0.elapsed_time(e1)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            ms_total = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     if dist is not None:
         t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

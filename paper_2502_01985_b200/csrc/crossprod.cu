@@ -146,6 +146,122 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nb, int ntile
   }
 }
 
+// k_gram for acols, bcols <= GF (the usual dimension widths): ONE tile
+// covers the whole output, so every CTA reads its rows of A and B once
+// (k_gram reads them once per 32 x 32 output tile and was latency-bound at
+// 1.1 ms for a 1M x 50 dimension Gram).  Rows staged 64 at a time with
+// float4 loads when the pitches allow; thread = 4 x 4 micro tile of the
+// output; fp32 over a staged tile, fp64 across tiles.
+constexpr int GF = 64;
+__global__ void __launch_bounds__(256) k_gram_full(const float* __restrict__ A, int pa, int acols,
+                                                   const float* __restrict__ B, int pb, int bcols,
+                                                   int64_t rows, int64_t rows_per_cta,
+                                                   const int64_t* __restrict__ wptr,
+                                                   double* __restrict__ part) {
+  __shared__ __align__(16) float As[GROWS][GF + 4];
+  __shared__ __align__(16) float Bs[GROWS][GF + 4];
+  const int tid = threadIdx.x;
+  const int ma = (acols + 3) / 4, mb = (bcols + 3) / 4;
+  const int micro = ma * mb;
+  const bool active = tid < micro;
+  const int i0 = (tid / mb) * 4, k0 = (tid % mb) * 4;
+  const int64_t r_begin = blockIdx.x * rows_per_cta;
+  const int64_t r_end = min64(rows, r_begin + rows_per_cta);
+  const int ac4 = (acols + 3) / 4, bc4 = (bcols + 3) / 4;
+  const bool vec = ((pa | pb) & 3) == 0;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int k = 0; k < 4; k++) acc[i][k] = 0.0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += GROWS) {
+    const int nr = (int)min64(GROWS, r_end - r0);
+    __syncthreads();
+    for (int e = tid; e < GROWS * (ac4 + bc4); e += 256) {
+      const int r = e / (ac4 + bc4), q = e - r * (ac4 + bc4);
+      const bool isa = q < ac4;
+      const int c4 = isa ? q : q - ac4;
+      const int cols = isa ? acols : bcols;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nr) {
+        const int64_t row = r0 + r;
+        const float* src = isa ? A + row * pa : B + row * pb;
+        if (vec && 4 * c4 + 3 < (isa ? pa : pb)) {
+          v = __ldg(reinterpret_cast<const float4*>(src) + c4);
+        } else {
+          v.x = 4 * c4 < cols ? src[4 * c4] : 0.f;
+          v.y = 4 * c4 + 1 < cols ? src[4 * c4 + 1] : 0.f;
+          v.z = 4 * c4 + 2 < cols ? src[4 * c4 + 2] : 0.f;
+          v.w = 4 * c4 + 3 < cols ? src[4 * c4 + 3] : 0.f;
+        }
+        // padding columns of a pitched source are zero; clip anyway
+        if (4 * c4 >= cols) v = make_float4(0.f, 0.f, 0.f, 0.f);
+        else {
+          if (4 * c4 + 1 >= cols) v.y = 0.f;
+          if (4 * c4 + 2 >= cols) v.z = 0.f;
+          if (4 * c4 + 3 >= cols) v.w = 0.f;
+        }
+        if (isa && wptr) {
+          const float wgt = (float)(wptr[row + 1] - wptr[row]);
+          v.x *= wgt; v.y *= wgt; v.z *= wgt; v.w *= wgt;
+        }
+      }
+      *reinterpret_cast<float4*>(isa ? &As[r][4 * c4] : &Bs[r][4 * c4]) = v;
+    }
+    __syncthreads();
+    if (active) {
+      float f[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) f[i][k] = 0.f;
+      for (int r = 0; r < nr; r++) {
+        const float4 a = *reinterpret_cast<const float4*>(&As[r][i0]);
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[r][k0]);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+          for (int k = 0; k < 4; k++) f[i][k] = fmaf(av[i], bv[k], f[i][k]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[i][k] += (double)f[i][k];
+    }
+  }
+  if (active) {
+    double* out = part + (int64_t)blockIdx.x * acols * bcols;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (i0 + i < acols && k0 + k < bcols) out[(i0 + i) * bcols + k0 + k] = acc[i][k];
+  }
+}
+
+// out[tcol_a[i], tcol_b[k]] += sum over CTAs (CTA order) of part[.][i * bcols + k]
+// (+ the mirrored entry for off-diagonal blocks)
+__global__ void k_gram_full_reduce(const double* __restrict__ part, int nb, int acols, int bcols,
+                                   const int32_t* __restrict__ tcol_a,
+                                   const int32_t* __restrict__ tcol_b, int c_T, bool mirror,
+                                   double* __restrict__ out) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)acols * bcols) return;
+  const int e = (int)w, i = e / bcols, k = e - i * bcols;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += part[(int64_t)b * acols * bcols + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int ta = tcol_a[i], tb = tcol_b[k];
+  if (lane == 0 && ta >= 0 && tb >= 0) {
+    out[(int64_t)ta * c_T + tb] += s;
+    if (mirror) out[(int64_t)tb * c_T + ta] += s;
+  }
+}
+
 struct PartnerSrc {   // a gathered source whose rows are summed into Y_de
   const float* S;
   const int32_t* fk;
@@ -156,6 +272,59 @@ struct Partners {
   PartnerSrc p[MAX_PARTNERS];
   int n;
 };
+
+// Z[j][0..pf) = sum over the members p of dimension row j of F[p][0..pf) for
+// a stream block of pf % 4 == 0, pf <= 32 columns and no gathered partners
+// (the common d x F block): warp per dimension row, lane = (row phase,
+// 16-byte chunk) -- RP = 32 / (pf / 4) member rows per warp load instead
+// of one, so the grouped read of F has enough bytes in flight to run at HBM
+// speed.  fp64 per row phase, phases summed in a fixed order (not the
+// strictly ascending order of k_group_rows_sum; same values to fp64
+// rounding), fp32 store.
+__global__ void __launch_bounds__(256) k_group_sum_f4(const int64_t* __restrict__ grp_ptr,
+                                                      const int32_t* __restrict__ grp_rows,
+                                                      bool sorted, int64_t n_neg, int64_t rows,
+                                                      const float* __restrict__ F, int pf,
+                                                      float* __restrict__ Z) {
+  const int lane = threadIdx.x & 31;
+  const int nc4 = pf >> 2, rp = 32 / nc4;
+  const int ph = lane / nc4, q = lane - ph * nc4;
+  const bool on = ph < rp;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < rows; j += nw) {
+    const int64_t m0 = grp_ptr[j], m1 = grp_ptr[j + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (on) {
+      int64_t m = m0 + ph;
+      for (; m + rp < m1; m += 2 * rp) {   // two member rows in flight per lane
+        const int64_t pa = sorted ? n_neg + m : (int64_t)grp_rows[m];
+        const int64_t pb = sorted ? n_neg + m + rp : (int64_t)grp_rows[m + rp];
+        const float4 a = __ldg(reinterpret_cast<const float4*>(F + pa * pf) + q);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(F + pb * pf) + q);
+        s0 += (double)a.x; s1 += (double)a.y; s2 += (double)a.z; s3 += (double)a.w;
+        s0 += (double)b.x; s1 += (double)b.y; s2 += (double)b.z; s3 += (double)b.w;
+      }
+      if (m < m1) {
+        const int64_t pa = sorted ? n_neg + m : (int64_t)grp_rows[m];
+        const float4 a = __ldg(reinterpret_cast<const float4*>(F + pa * pf) + q);
+        s0 += (double)a.x; s1 += (double)a.y; s2 += (double)a.z; s3 += (double)a.w;
+      }
+    }
+    // fixed-order sum over the row phases: lane (0, q) gathers phases 1.. in order
+    for (int k = 1; k < rp; k++) {
+      const int src = k * nc4 + q;
+      const double t0 = __shfl_sync(0xffffffffu, s0, src < 32 ? src : lane);
+      const double t1 = __shfl_sync(0xffffffffu, s1, src < 32 ? src : lane);
+      const double t2 = __shfl_sync(0xffffffffu, s2, src < 32 ? src : lane);
+      const double t3 = __shfl_sync(0xffffffffu, s3, src < 32 ? src : lane);
+      if (ph == 0) {
+        s0 += t0; s1 += t1; s2 += t2; s3 += t3;
+      }
+    }
+    if (ph == 0)
+      reinterpret_cast<float4*>(Z + j * pf)[q] = make_float4((float)s0, (float)s1, (float)s2, (float)s3);
+  }
+}
 
 // Z[j][0..w) = sum over members p of dimension row j (ascending order) of
 // [F[p][0..pf) | S_e[fk_e[p]] for every partner e]  (fp64 sums, fp32 store);
@@ -222,6 +391,21 @@ int gram(fl_table* t, const float* A, int pa, int acols, const float* B, int pb,
          int64_t rows, const int64_t* wptr, const int32_t* tcol_a, const int32_t* tcol_b,
          bool mirror, double* out, cudaStream_t s) {
   if (rows <= 0 || acols <= 0 || bcols <= 0) return FL_OK;
+  if (acols <= GF && bcols <= GF && !getenv("FL_NO_GRAM_FULL")) {
+    int64_t nb = std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 4 * GROWS),
+                                                        8 * (int64_t)t->sm_count));
+    const int64_t rpc = round_up(ceil_div(rows, nb), GROWS);
+    nb = ceil_div(rows, rpc);
+    double* part = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * acols * bcols * 8, s));
+    k_gram_full<<<(unsigned)nb, 256, 0, s>>>(A, pa, acols, B, pb, bcols, rows, rpc, wptr, part);
+    FL_CHECK_LAUNCH();
+    k_gram_full_reduce<<<(unsigned)ceil_div((int64_t)acols * bcols * 32, 256), 256, 0, s>>>(
+        part, (int)nb, acols, bcols, tcol_a, tcol_b, t->c_T, mirror, out);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaFreeAsync(part, s));
+    return FL_OK;
+  }
   const int nta = (acols + GT - 1) / GT, ntb = (bcols + GT - 1) / GT;
   const int ntiles = nta * ntb;
   // ~8 CTAs per SM over all tiles (the staged loop is latency-bound); row
@@ -315,15 +499,11 @@ extern "C" int fl_crossprod(fl_table* t, double* out, void* stream) {
     for (int e0 = d + 1, first = 1; first || e0 < ng; first = 0) {
       Partners pt{};
       int w = first ? t->pf : 0;
-      std::vector<int32_t> ztcol;
-      if (first)
-        for (int j = 0; j < t->pf; j++) ztcol.push_back(t->f_tcol[j]);
       int e = e0;
       for (; e < ng && pt.n < MAX_PARTNERS; e++) {
         const GatherSrc& ge = t->g[e];
         pt.p[pt.n++] = PartnerSrc{ge.S->as<float>(), ge.fk->as<int32_t>(), ge.pitch, ge.cols, w};
         w += ge.cols;
-        for (int c = 0; c < ge.cols; c++) ztcol.push_back(ge.tcol[c]);
       }
       e0 = e;
       if (w == 0 || g.rows == 0) continue;
@@ -331,19 +511,31 @@ extern "C" int fl_crossprod(fl_table* t, double* out, void* stream) {
       FL_CUDA(cudaMallocAsync((void**)&Z, (size_t)g.rows * w * 4 + 16, s));
       const unsigned nbz = (unsigned)std::min<int64_t>(ceil_div(g.rows * 32, 256),
                                                        32 * (int64_t)t->sm_count);
-      k_group_rows_sum<<<nbz, 256, 0, s>>>(g.grp_ptr->as<int64_t>(),
+      if (first && pt.n == 0 && t->pf % 4 == 0 && t->pf <= 32)
+        k_group_sum_f4<<<nbz, 256, 0, s>>>(g.grp_ptr->as<int64_t>(),
                                            g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr,
-                                           g.sorted, g.n_neg, g.rows, first ? F : nullptr,
-                                           first ? t->pf : 0, pt, w, Z);
+                                           g.sorted, g.n_neg, g.rows, F, t->pf, Z);
+      else
+        k_group_rows_sum<<<nbz, 256, 0, s>>>(g.grp_ptr->as<int64_t>(),
+                                             g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr,
+                                             g.sorted, g.n_neg, g.rows, first ? F : nullptr,
+                                             first ? t->pf : 0, pt, w, Z);
       FL_CHECK_LAUNCH();
+      // target columns of Z's columns, assembled on the device (no host
+      // buffer to keep alive, no stream sync between the passes)
       int32_t* dz = nullptr;
       FL_CUDA(cudaMallocAsync((void**)&dz, (size_t)w * 4, s));
-      FL_CUDA(cudaMemcpyAsync(dz, ztcol.data(), (size_t)w * 4, cudaMemcpyHostToDevice, s));
+      if (first && t->pf > 0)
+        FL_CUDA(cudaMemcpyAsync(dz, t->d_f_tcol->p, (size_t)t->pf * 4, cudaMemcpyDeviceToDevice, s));
+      for (int q = 0; q < pt.n; q++) {
+        const GatherSrc& ge = t->g[e - pt.n + q];
+        FL_CUDA(cudaMemcpyAsync(dz + pt.p[q].off, ge.d_tcol->p, (size_t)ge.cols * 4,
+                                cudaMemcpyDeviceToDevice, s));
+      }
       // d x (F | later dims), mirrored into (F | later dims) x d
       rc = gram(t, g.S->as<float>(), g.pitch, g.cols, Z, w, w, g.rows, nullptr, tcol_d, dz, true,
                 od, s);
       if (rc) return rc;
-      FL_CUDA(cudaStreamSynchronize(s));   // ztcol (host) must outlive the async copy
       FL_CUDA(cudaFreeAsync(dz, s));
       FL_CUDA(cudaFreeAsync(Z, s));
     }

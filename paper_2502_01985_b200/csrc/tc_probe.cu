@@ -97,9 +97,79 @@ __global__ void __launch_bounds__(128) k_tc_probe(int mode, const __grid_constan
   if (warp == 0) tc::dealloc(tmem, 256);
 }
 
+// Issue-rate probe: one thread per CTA issues `reps` chains of 16 kind::tf32
+// MMAs (M x N x 8, operands K-major SW128 or MN-major 128B/32-byte-atom,
+// content zero) back to back into one TMEM accumulator and waits for the
+// last; cycles / MMA from clock64 around the whole run.
+__global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b_mn, int reps,
+                                                   double* __restrict__ cyc) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 3 * 65536 / 16; i += blockDim.x)   // A: 64 KB, B: 128 KB
+    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+  }
+  tc::fence_smem_to_async();
+  if (warp == 0) tc::alloc(&tbase, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 65536);
+    const uint32_t id = tc::idesc_tf32(M, N, a_mn != 0, b_mn != 0);
+    auto desc = [&](uint32_t base, int rows, int mn, int kk) -> uint64_t {
+      return mn ? tc::smem_desc(base + kk * 1024, 16384, 512, tc::kSw128B32)
+                : tc::smem_desc(base + (kk >> 2) * rows * 128 + (kk & 3) * 32, 16, 1024, tc::kSw128);
+    };
+    const long long c0 = clock64();
+    for (int r = 0; r < reps; r++) {
+#pragma unroll
+      for (int kk = 0; kk < 16; kk++)
+        tc::mma_tf32(tmem, desc(a0, M, a_mn, kk), desc(b0, N, b_mn, kk), id, r > 0 || kk > 0);
+    }
+    tc::commit(&mbar);
+    mbar_wait(&mbar, 0);
+    const long long c1 = clock64();
+    cyc[blockIdx.x] = (double)(c1 - c0) / (16.0 * reps);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tmem, 256);
+}
+
 }  // namespace flb
 
 using namespace flb;
+
+// cycles per kind::tf32 MMA (mean over `ctas` concurrent CTAs, one per SM)
+extern "C" int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, int32_t reps,
+                            int32_t ctas, double* cycles) {
+  if ((M != 64 && M != 128) || N < 8 || N > 256 || (N & 7) || reps < 1 || ctas < 1 ||
+      ctas > 1024) {
+    set_error("fl_tc_timing: unsupported shape (M %d, N %d)", M, N);
+    return FL_ERR_ARG;
+  }
+  double* d = nullptr;
+  FL_CUDA(cudaMalloc(&d, (size_t)ctas * 8));
+  const size_t smem = 1024 + 3 * 65536;
+  FL_CUDA(cudaFuncSetAttribute(k_tc_timing, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_tc_timing<<<ctas, 128, smem>>>(M, N, a_mn, b_mn, reps, d);
+  FL_CHECK_LAUNCH();
+  FL_CUDA(cudaDeviceSynchronize());
+  std::vector<double> h((size_t)ctas);
+  FL_CUDA(cudaMemcpy(h.data(), d, (size_t)ctas * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  double sum = 0.0;
+  for (double v : h) sum += v;
+  *cycles = sum / ctas;
+  return FL_OK;
+}
 
 // params = {lbo, sbo, layout}; mode 0: A = the 32 x 32 tile, dump = 1024 floats
 extern "C" int fl_tc_probe(int32_t mode, const float* A, const float* B, float* D, float* dump,

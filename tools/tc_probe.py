@@ -55,7 +55,29 @@ def truncation():
           " rounded:", float(np.max(np.abs(D - tf32_round(A)))), flush=True)
 
 
+def timing():
+    """cycles per kind::tf32 MMA (M x N x 8) issued back to back, K-major vs
+    MN-major operands, 1 CTA and one CTA per SM"""
+    _lib.load()
+    print(f"{'M':>4} {'N':>4} {'A':>3} {'B':>3} {'1 CTA':>8} {'148 CTAs':>9}  cycles / MMA "
+          f"(floor max(M,128) N / 256 = {{}})", flush=True)
+    for M in (64, 128):
+        for N in (32, 64, 128, 256):
+            for a_mn, b_mn in ((0, 0), (1, 1), (1, 0), (0, 1)):
+                out = []
+                for ctas in (1, 148):
+                    c = C.c_double()
+                    _lib.call("fl_tc_timing", M, N, a_mn, b_mn, 200, ctas, C.byref(c))
+                    out.append(c.value)
+                lay = {0: "K", 1: "MN"}
+                print(f"{M:>4} {N:>4} {lay[a_mn]:>3} {lay[b_mn]:>3} {out[0]:8.1f} {out[1]:9.1f}"
+                      f"   floor {max(M, 128) * N / 256:.0f}", flush=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "timing":
+        timing()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         one(*(int(v) for v in sys.argv[2:8]))
         return
