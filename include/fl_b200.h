@@ -240,10 +240,10 @@ int fl_tc_selftest(int32_t mode, const float* A, const float* B, float* D, int32
 int fl_tc_probe(int32_t mode, const float* A, const float* B, float* D, float* dump, int32_t K,
                 int32_t N, const int32_t* params);
 // diagnostics: cycles per kind::tf32 tcgen05.mma (M x N x 8; a_mn / b_mn:
-// MN-major operands) issued back to back by one thread per CTA, mean over
-// `ctas` concurrent CTAs
+// MN-major operands) issued back to back by one thread per CTA, round-robin
+// over `nacc` accumulators, mean over `ctas` concurrent CTAs
 int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, int32_t reps, int32_t ctas,
-                 double* cycles);
+                 int32_t nacc, double* cycles);
 
 #ifdef __cplusplus
 }

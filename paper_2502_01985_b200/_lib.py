@@ -102,7 +102,7 @@ SIGNATURES = {
     "fl_kmeans_set_comm": [_P, _P],
     "fl_gnmf_set_comm": [_P, _P],
     "fl_tc_probe": [_I32, _P, _P, _P, _P, _I32, _I32, _P],
-    "fl_tc_timing": [_I32, _I32, _I32, _I32, _I32, _I32, _P],
+    "fl_tc_timing": [_I32, _I32, _I32, _I32, _I32, _I32, _I32, _P],
     "fl_tc_selftest": [_I32, _P, _P, _P, _I32, _I32, _P],
 }
 

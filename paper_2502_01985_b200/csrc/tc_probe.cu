@@ -99,10 +99,10 @@ __global__ void __launch_bounds__(128) k_tc_probe(int mode, const __grid_constan
 
 // Issue-rate probe: one thread per CTA issues `reps` chains of 16 kind::tf32
 // MMAs (M x N x 8, operands K-major SW128 or MN-major 128B/32-byte-atom,
-// content zero) back to back into one TMEM accumulator and waits for the
-// last; cycles / MMA from clock64 around the whole run.
+// content zero) back to back, round-robin over `nacc` TMEM accumulators,
+// and waits for the last; cycles / MMA from clock64 around the whole run.
 __global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b_mn, int reps,
-                                                   double* __restrict__ cyc) {
+                                                   int nacc, double* __restrict__ cyc) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t mbar;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b
     fence_mbar_init();
   }
   tc::fence_smem_to_async();
-  if (warp == 0) tc::alloc(&tbase, 256);
+  if (warp == 0) tc::alloc(&tbase, 512);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b
     for (int r = 0; r < reps; r++) {
 #pragma unroll
       for (int kk = 0; kk < 16; kk++)
-        tc::mma_tf32(tmem, desc(a0, M, a_mn, kk), desc(b0, N, b_mn, kk), id, r > 0 || kk > 0);
+        tc::mma_tf32(tmem + (uint32_t)(N * (kk % nacc)), desc(a0, M, a_mn, kk), desc(b0, N, b_mn, kk),
+                     id, r > 0 || kk >= nacc);
     }
     tc::commit(&mbar);
     mbar_wait(&mbar, 0);
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::dealloc(tmem, 256);
+  if (warp == 0) tc::dealloc(tmem, 512);
 }
 
 }  // namespace flb
@@ -149,9 +150,9 @@ using namespace flb;
 
 // cycles per kind::tf32 MMA (mean over `ctas` concurrent CTAs, one per SM)
 extern "C" int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, int32_t reps,
-                            int32_t ctas, double* cycles) {
+                            int32_t ctas, int32_t nacc, double* cycles) {
   if ((M != 64 && M != 128) || N < 8 || N > 256 || (N & 7) || reps < 1 || ctas < 1 ||
-      ctas > 1024) {
+      ctas > 1024 || nacc < 1 || nacc > 16 || N * nacc > 512 || 16 % nacc) {
     set_error("fl_tc_timing: unsupported shape (M %d, N %d)", M, N);
     return FL_ERR_ARG;
   }
@@ -159,7 +160,7 @@ extern "C" int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, in
   FL_CUDA(cudaMalloc(&d, (size_t)ctas * 8));
   const size_t smem = 1024 + 3 * 65536;
   FL_CUDA(cudaFuncSetAttribute(k_tc_timing, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_tc_timing<<<ctas, 128, smem>>>(M, N, a_mn, b_mn, reps, d);
+  k_tc_timing<<<ctas, 128, smem>>>(M, N, a_mn, b_mn, reps, nacc, d);
   FL_CHECK_LAUNCH();
   FL_CUDA(cudaDeviceSynchronize());
   std::vector<double> h((size_t)ctas);

@@ -57,21 +57,33 @@ def truncation():
 
 def timing():
     """cycles per kind::tf32 MMA (M x N x 8) issued back to back, K-major vs
-    MN-major operands, 1 CTA and one CTA per SM"""
+    MN-major operands, 1 CTA and one CTA per SM; then the same chain spread
+    round-robin over 1-8 independent accumulators"""
     _lib.load()
-    print(f"{'M':>4} {'N':>4} {'A':>3} {'B':>3} {'1 CTA':>8} {'148 CTAs':>9}  cycles / MMA "
-          f"(floor max(M,128) N / 256 = {{}})", flush=True)
+    print(f"{'M':>4} {'N':>4} {'A':>3} {'B':>3} {'1 CTA':>8} {'148 CTAs':>9}  cycles / MMA, one "
+          f"accumulator", flush=True)
+    lay = {0: "K", 1: "MN"}
     for M in (64, 128):
         for N in (32, 64, 128, 256):
             for a_mn, b_mn in ((0, 0), (1, 1), (1, 0), (0, 1)):
                 out = []
                 for ctas in (1, 148):
                     c = C.c_double()
-                    _lib.call("fl_tc_timing", M, N, a_mn, b_mn, 200, ctas, C.byref(c))
+                    _lib.call("fl_tc_timing", M, N, a_mn, b_mn, 200, ctas, 1, C.byref(c))
                     out.append(c.value)
-                lay = {0: "K", 1: "MN"}
                 print(f"{M:>4} {N:>4} {lay[a_mn]:>3} {lay[b_mn]:>3} {out[0]:8.1f} {out[1]:9.1f}"
-                      f"   floor {max(M, 128) * N / 256:.0f}", flush=True)
+                      f"   floor max(M,128) N / 256 = {max(M, 128) * N / 256:.0f}", flush=True)
+    print("independent accumulators (148 CTAs, MN-major A and B):", flush=True)
+    for M, N in ((64, 32), (128, 32), (128, 64), (128, 128)):
+        row = []
+        for nacc in (1, 2, 4, 8):
+            if N * nacc > 512:
+                row.append("   -")
+                continue
+            c = C.c_double()
+            _lib.call("fl_tc_timing", M, N, 1, 1, 200, 148, nacc, C.byref(c))
+            row.append(f"{c.value:6.1f}")
+        print(f" M {M:>3} N {N:>3}: nacc 1 / 2 / 4 / 8 -> " + " ".join(row), flush=True)
 
 
 def main():
