@@ -241,7 +241,8 @@ int fl_tc_probe(int32_t mode, const float* A, const float* B, float* D, float* d
                 int32_t N, const int32_t* params);
 // diagnostics: cycles per kind::tf32 tcgen05.mma (M x N x 8; a_mn / b_mn:
 // MN-major operands) issued back to back by one thread per CTA, round-robin
-// over `nacc` accumulators, mean over `ctas` concurrent CTAs
+// over `nacc` accumulators (nacc | 256: kind::f16 with bf16 operands, K = 16),
+// mean over `ctas` concurrent CTAs
 int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, int32_t reps, int32_t ctas,
                  int32_t nacc, double* cycles);
 

@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     }
   } else if (warp == 1) {
     // =================== MMA issuer ===================
-    if (lane == 0 && n > 0) {
+    // the whole warp walks the tiles (barrier waits); one elected lane issues
+    // the MMA chains and commits (tc05.cuh: a lane-0 branch costs a branch
+    // loop per UTC instruction)
+    if (n > 0) {
       const uint32_t id_qv = tc::idesc_tf32(128, 32, false, false);
       const uint32_t id_pg = tc::idesc_tf32(128, 64, true, true);
       const uint32_t c0 = smem_u32(cst);
@@ -173,25 +176,29 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         const uint32_t st = smem_u32(sm + (t % G5_NS) * gm.stage);
         const uint32_t lo = smem_u32(sm + gm.o_lo);
         const uint32_t tq = tmem + 64 * b;
-        for (int ks = 0; ks < kst; ks++) {   // Q = F H_F^T
-          const uint64_t ah = tc::smem_desc(st + gm.o_f + ks * 32, 16, 1024, tc::kSw128);
-          const uint64_t al = tc::smem_desc(lo + 16384 + ks * 32, 16, 1024, tc::kSw128);
-          const uint64_t bh = tc::smem_desc(c0 + ks * 1024, 512, 128, tc::kInterleave);
-          const uint64_t bl = tc::smem_desc(c0 + 4096 + ks * 1024, 512, 128, tc::kInterleave);
-          tc::mma_tf32(tq, ah, bh, id_qv, ks > 0);
-          tc::mma_tf32(tq, al, bh, id_qv, true);
-          tc::mma_tf32(tq, ah, bl, id_qv, true);
+        if (tc::elect_one()) {
+          for (int ks = 0; ks < kst; ks++) {   // Q = F H_F^T
+            const uint64_t ah = tc::smem_desc(st + gm.o_f + ks * 32, 16, 1024, tc::kSw128);
+            const uint64_t al = tc::smem_desc(lo + 16384 + ks * 32, 16, 1024, tc::kSw128);
+            const uint64_t bh = tc::smem_desc(c0 + ks * 1024, 512, 128, tc::kInterleave);
+            const uint64_t bl = tc::smem_desc(c0 + 4096 + ks * 1024, 512, 128, tc::kInterleave);
+            tc::mma_tf32(tq, ah, bh, id_qv, ks > 0);
+            tc::mma_tf32(tq, al, bh, id_qv, true);
+            tc::mma_tf32(tq, ah, bl, id_qv, true);
+          }
+#pragma unroll
+          for (int ks = 0; ks < 4; ks++) {     // V = W HH
+            const uint64_t ah = tc::smem_desc(st + ks * 32, 16, 1024, tc::kSw128);
+            const uint64_t al = tc::smem_desc(lo + ks * 32, 16, 1024, tc::kSw128);
+            const uint64_t bh = tc::smem_desc(c0 + 8192 + ks * 1024, 512, 128, tc::kInterleave);
+            const uint64_t bl = tc::smem_desc(c0 + 12288 + ks * 1024, 512, 128, tc::kInterleave);
+            tc::mma_tf32(tq + 32, ah, bh, id_qv, ks > 0);
+            tc::mma_tf32(tq + 32, al, bh, id_qv, true);
+            tc::mma_tf32(tq + 32, ah, bl, id_qv, true);
+          }
+          tc::commit(&qv_full[b]);
         }
-        for (int ks = 0; ks < 4; ks++) {     // V = W HH
-          const uint64_t ah = tc::smem_desc(st + ks * 32, 16, 1024, tc::kSw128);
-          const uint64_t al = tc::smem_desc(lo + ks * 32, 16, 1024, tc::kSw128);
-          const uint64_t bh = tc::smem_desc(c0 + 8192 + ks * 1024, 512, 128, tc::kInterleave);
-          const uint64_t bl = tc::smem_desc(c0 + 12288 + ks * 1024, 512, 128, tc::kInterleave);
-          tc::mma_tf32(tq + 32, ah, bh, id_qv, ks > 0);
-          tc::mma_tf32(tq + 32, al, bh, id_qv, true);
-          tc::mma_tf32(tq + 32, ah, bl, id_qv, true);
-        }
-        tc::commit(&qv_full[b]);
+        __syncwarp();
       };
       if (UPDATE) qv(0);
       for (int t = 0; t < n; t++) {
@@ -206,16 +213,19 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         // of 8 rows advances the start address by 1024 B (64 in the 16-byte
         // address field)
         const uint64_t ad0 = tc::smem_desc(ops, 16384, 512, tc::kSw128B32);
-        if (!(a.diag & 2)) {
+        if (tc::elect_one()) {
+          if (!(a.diag & 2)) {
 #pragma unroll
-          for (int kk = 0; kk < G5_TILE / 8; kk++) {
-            const uint64_t ad = ad0 + (uint64_t)(kk * 64);
-            tc::mma_tf32(tp, ad, ad, id_pg, !((t % G5_FT) == 0 && kk == 0));
+            for (int kk = 0; kk < G5_TILE / 8; kk++) {
+              const uint64_t ad = ad0 + (uint64_t)(kk * 64);
+              tc::mma_tf32(tp, ad, ad, id_pg, !((t % G5_FT) == 0 && kk == 0));
+            }
           }
+          tc::commit(&empty[s]);
+          tc::commit(&ops_free);
+          if ((t % G5_FT) == G5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
         }
-        tc::commit(&empty[s]);
-        tc::commit(&ops_free);
-        if ((t % G5_FT) == G5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
+        __syncwarp();
       }
     }
   } else {

@@ -100,14 +100,15 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n > 0) {
-      const uint32_t id = tc::idesc_tf32(m64 ? 64 : 128, 32, true, true);
-      for (int t = 0; t < n; t++) {
-        const int s = t % R5_NS, w = t / R5_FT, b = w & 1;
-        mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / R5_NS) & 1));
-        if ((t % R5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
-        tc::fence_after();
-        const uint64_t d0 = tc::smem_desc(smem_u32(sm + s * gm.stage), 16384, 512, tc::kSw128B32);
+    // the whole warp walks the tiles; one elected lane issues (tc05.cuh)
+    const uint32_t id = tc::idesc_tf32(m64 ? 64 : 128, 32, true, true);
+    for (int t = 0; t < n; t++) {
+      const int s = t % R5_NS, w = t / R5_FT, b = w & 1;
+      mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / R5_NS) & 1));
+      if ((t % R5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
+      tc::fence_after();
+      const uint64_t d0 = tc::smem_desc(smem_u32(sm + s * gm.stage), 16384, 512, tc::kSw128B32);
+      if (tc::elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < R5_TILE / 8; kk++) {
           const uint64_t d = d0 + (uint64_t)(kk * 64);
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(R5_THREADS, 1)
         tc::commit(&empty[s]);
         if ((t % R5_FT) == R5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
       }
+      __syncwarp();
     }
   } else if (warp >= 2 && warp < 6) {
     const int r = 32 * (warp & 3) + lane;

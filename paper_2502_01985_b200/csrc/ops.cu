@@ -644,6 +644,21 @@ static int tlmm_impl(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t
 static int tlmm_bins_product(fl_table* t, const GatherSrc& g, const double* bins, int cy,
                              double* out, int64_t os_t, int64_t os_c, cudaStream_t s) {
   if (g.rows <= 0 || g.cols <= 0) return FL_OK;
+  if (g.cols <= 64 && cy <= 32) {
+    int64_t nb = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.rows, 256), 16 * (int64_t)t->sm_count));
+    const int64_t rpc = round_up(ceil_div(g.rows, nb), 64);
+    nb = ceil_div(g.rows, rpc);
+    double* part = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * g.cols * cy * 8, s));
+    k_sbins<<<(unsigned)nb, 128, 0, s>>>(g.S->as<float>(), g.pitch, g.cols, bins, cy, g.rows, rpc,
+                                         part);
+    FL_CHECK_LAUNCH();
+    k_reduce_partials<<<gridn((int64_t)g.cols * cy * 32), 256, 0, s>>>(
+        part, (int)nb, g.cols, cy, g.d_tcol->as<int32_t>(), out, os_t, os_c);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaFreeAsync(part, s));
+    return FL_OK;
+  }
   int64_t nb = std::min<int64_t>(std::max<int64_t>(1, ceil_div(g.rows, 2048)), 4 * t->sm_count);
   const int64_t rpb = round_up(ceil_div(g.rows, nb), 32);
   nb = ceil_div(g.rows, rpb);

@@ -60,6 +60,20 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
                : "memory");
 }
 
+// one lane of a CONVERGED warp (elect.sync).  Issue tcgen05.mma / commit
+// chains inside `if (elect_one())` of a converged warp, not inside
+// `if (lane == 0)`: for a lane-0 branch the compiler cannot prove a single
+// active thread and wraps every UTC* instruction in its own ELECT / BRA.U.ANY
+// loop, which measured ~46 cycles per MMA (profiles/r02_tc_mma_timing.txt);
+// under elect.sync the MMAs are emitted back to back.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }

@@ -101,8 +101,22 @@ __global__ void __launch_bounds__(128) k_tc_probe(int mode, const __grid_constan
 // MMAs (M x N x 8, operands K-major SW128 or MN-major 128B/32-byte-atom,
 // content zero) back to back, round-robin over `nacc` TMEM accumulators,
 // and waits for the last; cycles / MMA from clock64 around the whole run.
-__global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b_mn, int reps,
-                                                   int nacc, double* __restrict__ cyc) {
+__device__ __forceinline__ void probe_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate ? 1u : 0u));
+}
+
+// kind 0: tf32 (K = 8 per MMA), 1: bf16 (K = 16).  Everything the issuing
+// lane computes per MMA is a compile-time offset from two base descriptors
+// (like the production kernels), so the loop measures the tensor core, not
+// the issuing thread.
+template <int KIND, bool AMN, bool BMN>
+__global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int reps, int nacc,
+                                                   double* __restrict__ cyc) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t mbar;
@@ -120,24 +134,39 @@ __global__ void __launch_bounds__(128) k_tc_timing(int M, int N, int a_mn, int b
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tbase;
-  if (tid == 0) {
+  if (warp == 0) {
     const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 65536);
-    const uint32_t id = tc::idesc_tf32(M, N, a_mn != 0, b_mn != 0);
-    auto desc = [&](uint32_t base, int rows, int mn, int kk) -> uint64_t {
-      return mn ? tc::smem_desc(base + kk * 1024, 16384, 512, tc::kSw128B32)
-                : tc::smem_desc(base + (kk >> 2) * rows * 128 + (kk & 3) * 32, 16, 1024, tc::kSw128);
-    };
+    const uint32_t id = KIND ? ((1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) |
+                                ((BMN ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) |
+                                ((uint32_t)(M >> 4) << 24))
+                             : tc::idesc_tf32(M, N, AMN, BMN);
+    // K steps advance by 1024 B (MN-major: 8 rows) or 32 B within a 4-step
+    // K-major chunk; the chunk stride is left at zero (content is zero)
+    const uint64_t da = AMN ? tc::smem_desc(a0, 16384, 512, tc::kSw128B32)
+                            : tc::smem_desc(a0, 16, 1024, tc::kSw128);
+    const uint64_t db = BMN ? tc::smem_desc(b0, 16384, 512, tc::kSw128B32)
+                            : tc::smem_desc(b0, 16, 1024, tc::kSw128);
+    const uint32_t sa = AMN ? 64 : 2, sb = BMN ? 64 : 2;
+    __syncwarp();
     const long long c0 = clock64();
-    for (int r = 0; r < reps; r++) {
+    if (tc::elect_one()) {
+      for (int r = 0; r < reps; r++) {
 #pragma unroll
-      for (int kk = 0; kk < 16; kk++)
-        tc::mma_tf32(tmem + (uint32_t)(N * (kk % nacc)), desc(a0, M, a_mn, kk), desc(b0, N, b_mn, kk),
-                     id, r > 0 || kk >= nacc);
+        for (int kk = 0; kk < 16; kk++) {
+          const uint32_t acc = tmem + (uint32_t)(N * (kk % nacc));
+          const uint64_t a = da + (uint64_t)((AMN ? kk : (kk & 3)) * sa);
+          const uint64_t b = db + (uint64_t)((BMN ? kk : (kk & 3)) * sb);
+          if (KIND) probe_mma_bf16(acc, a, b, id, r > 0 || kk >= nacc);
+          else tc::mma_tf32(acc, a, b, id, r > 0 || kk >= nacc);
+        }
+      }
+      tc::commit(&mbar);
     }
-    tc::commit(&mbar);
+    __syncwarp();
     mbar_wait(&mbar, 0);
     const long long c1 = clock64();
-    cyc[blockIdx.x] = (double)(c1 - c0) / (16.0 * reps);
+    if (tc::elect_one()) cyc[blockIdx.x] = (double)(c1 - c0) / (16.0 * reps);
+    __syncwarp();
   }
   tc::fence_before();
   __syncthreads();
@@ -151,6 +180,8 @@ using namespace flb;
 // cycles per kind::tf32 MMA (mean over `ctas` concurrent CTAs, one per SM)
 extern "C" int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, int32_t reps,
                             int32_t ctas, int32_t nacc, double* cycles) {
+  const int kind = (nacc >> 8) & 1;   // nacc | 256: kind::f16 with bf16 operands
+  nacc &= 255;
   if ((M != 64 && M != 128) || N < 8 || N > 256 || (N & 7) || reps < 1 || ctas < 1 ||
       ctas > 1024 || nacc < 1 || nacc > 16 || N * nacc > 512 || 16 % nacc) {
     set_error("fl_tc_timing: unsupported shape (M %d, N %d)", M, N);
@@ -159,8 +190,24 @@ extern "C" int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, in
   double* d = nullptr;
   FL_CUDA(cudaMalloc(&d, (size_t)ctas * 8));
   const size_t smem = 1024 + 3 * 65536;
-  FL_CUDA(cudaFuncSetAttribute(k_tc_timing, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_tc_timing<<<ctas, 128, smem>>>(M, N, a_mn, b_mn, reps, nacc, d);
+  auto go = [&](auto kern) -> int {
+    FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<ctas, 128, smem>>>(M, N, reps, nacc, d);
+    return FL_OK;
+  };
+  int rc;
+  const int sel = kind * 4 + (a_mn ? 2 : 0) + (b_mn ? 1 : 0);
+  switch (sel) {
+    case 0: rc = go(k_tc_timing<0, false, false>); break;
+    case 1: rc = go(k_tc_timing<0, false, true>); break;
+    case 2: rc = go(k_tc_timing<0, true, false>); break;
+    case 3: rc = go(k_tc_timing<0, true, true>); break;
+    case 4: rc = go(k_tc_timing<1, false, false>); break;
+    case 5: rc = go(k_tc_timing<1, false, true>); break;
+    case 6: rc = go(k_tc_timing<1, true, false>); break;
+    default: rc = go(k_tc_timing<1, true, true>); break;
+  }
+  if (rc) return rc;
   FL_CHECK_LAUNCH();
   FL_CUDA(cudaDeviceSynchronize());
   std::vector<double> h((size_t)ctas);

@@ -82,16 +82,17 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n > 0) {
-      const uint32_t id = tc::idesc_tf32(128, 64, true, true);
-      for (int t = 0; t < n; t++) {
-        const int s = t % M5_NS, w = t / M5_FT, b = w & 1;
-        mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / M5_NS) & 1));
-        if ((t % M5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
-        tc::fence_after();
-        const uint32_t st = smem_u32(sm + s * M5_STAGE);
-        const uint64_t a0 = tc::smem_desc(st, 16384, 512, tc::kSw128B32);
-        const uint64_t b0 = tc::smem_desc(st + 32768, 16384, 512, tc::kSw128B32);
+    // the whole warp walks the tiles; one elected lane issues (tc05.cuh)
+    const uint32_t id = tc::idesc_tf32(128, 64, true, true);
+    for (int t = 0; t < n; t++) {
+      const int s = t % M5_NS, w = t / M5_FT, b = w & 1;
+      mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / M5_NS) & 1));
+      if ((t % M5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
+      tc::fence_after();
+      const uint32_t st = smem_u32(sm + s * M5_STAGE);
+      const uint64_t a0 = tc::smem_desc(st, 16384, 512, tc::kSw128B32);
+      const uint64_t b0 = tc::smem_desc(st + 32768, 16384, 512, tc::kSw128B32);
+      if (tc::elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < M5_TILE / 8; kk++)
           tc::mma_tf32(tmem + 64 * b, a0 + (uint64_t)(kk * 64), b0 + (uint64_t)(kk * 64), id,
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
         tc::commit(&empty[s]);
         if ((t % M5_FT) == M5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
       }
+      __syncwarp();
     }
   } else if (warp >= 2 && warp < 6) {
     const int r = 32 * (warp & 3) + lane;
@@ -252,5 +254,91 @@ __global__ void __launch_bounds__(256) k_ydev32_rows(YView yv, int cy, int64_t r
        p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t tr = perm ? (int64_t)perm[p] : p;
     yd[p * 32 + lane] = lane < cy ? yv.at(tr, lane) : 0.f;
+  }
+}
+
+// part[cta][i * cy + c] = sum over the CTA's dimension rows r of
+// S[r][i] * bins[r][c] (bins fp64, used as fp32 like k_tmm_partial) for
+// <= 64 dimension columns and <= 32 operand columns: 64 rows staged with
+// float4 / double2 loads, thread = 4 x 4 micro tile, fp32 over a staged
+// tile, fp64 across tiles.  (k_tmm_partial's generic staging took 1.7 ms
+// for C2's 1M x 50 dimension at 32 columns.)
+__global__ void __launch_bounds__(128) k_sbins(const float* __restrict__ S, int pitch, int cols,
+                                               const double* __restrict__ bins, int cy,
+                                               int64_t rows, int64_t rows_per_cta,
+                                               double* __restrict__ part) {
+  __shared__ __align__(16) float Ss[64][64 + 4];
+  __shared__ __align__(16) float Bs[64][32 + 4];
+  const int tid = threadIdx.x;
+  const int ma = (cols + 3) / 4, mb = (cy + 3) / 4;
+  const bool active = tid < ma * mb;
+  const int i0 = (tid / mb) * 4, k0 = (tid % mb) * 4;
+  const int64_t r_begin = blockIdx.x * rows_per_cta;
+  const int64_t r_end = min64(rows, r_begin + rows_per_cta);
+  const bool vec = (pitch & 3) == 0;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int k = 0; k < 4; k++) acc[i][k] = 0.0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += 64) {
+    const int nr = (int)min64(64, r_end - r0);
+    __syncthreads();
+    for (int e = tid; e < 64 * ma; e += 128) {
+      const int r = e / ma, c4 = e - r * ma;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nr) {
+        const float* src = S + (r0 + r) * pitch;
+        if (vec && 4 * c4 + 3 < pitch) v = __ldg(reinterpret_cast<const float4*>(src) + c4);
+        else {
+          v.x = 4 * c4 < cols ? src[4 * c4] : 0.f;
+          v.y = 4 * c4 + 1 < cols ? src[4 * c4 + 1] : 0.f;
+          v.z = 4 * c4 + 2 < cols ? src[4 * c4 + 2] : 0.f;
+          v.w = 4 * c4 + 3 < cols ? src[4 * c4 + 3] : 0.f;
+        }
+        if (4 * c4 + 1 >= cols) v.y = 0.f;
+        if (4 * c4 + 2 >= cols) v.z = 0.f;
+        if (4 * c4 + 3 >= cols) v.w = 0.f;
+      }
+      *reinterpret_cast<float4*>(&Ss[r][4 * c4]) = v;
+    }
+    for (int e = tid; e < 64 * cy; e += 128) {
+      const int r = e / cy, c = e - r * cy;
+      Bs[r][c] = r < nr ? (float)bins[(r0 + r) * cy + c] : 0.f;
+    }
+    for (int e = tid; e < 64 * (4 * mb - cy); e += 128) {   // pad columns of the last quad
+      const int w = 4 * mb - cy, r = e / w;
+      Bs[r][cy + e - r * w] = 0.f;
+    }
+    __syncthreads();
+    if (active) {
+      float f[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) f[i][k] = 0.f;
+      for (int r = 0; r < nr; r++) {
+        const float4 a = *reinterpret_cast<const float4*>(&Ss[r][i0]);
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[r][k0]);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+          for (int k = 0; k < 4; k++) f[i][k] = fmaf(av[i], bv[k], f[i][k]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[i][k] += (double)f[i][k];
+    }
+  }
+  if (active) {
+    double* out = part + (int64_t)blockIdx.x * cols * cy;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (i0 + i < cols && k0 + k < cy) out[(i0 + i) * cy + k0 + k] = acc[i][k];
   }
 }

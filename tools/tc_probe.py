@@ -84,6 +84,14 @@ def timing():
             _lib.call("fl_tc_timing", M, N, 1, 1, 200, 148, nacc, C.byref(c))
             row.append(f"{c.value:6.1f}")
         print(f" M {M:>3} N {N:>3}: nacc 1 / 2 / 4 / 8 -> " + " ".join(row), flush=True)
+    print("kind::f16 (bf16 operands, K = 16 per MMA), 148 CTAs, one accumulator:", flush=True)
+    for M in (64, 128):
+        row = []
+        for N in (32, 64, 96, 128, 256):
+            c = C.c_double()
+            _lib.call("fl_tc_timing", M, N, 0, 0, 200, 148, 1 | 256, C.byref(c))
+            row.append(f"N {N}: {c.value:6.1f}")
+        print(f" M {M:>3}: " + "  ".join(row), flush=True)
 
 
 def main():
