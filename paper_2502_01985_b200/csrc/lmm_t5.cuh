@@ -27,6 +27,8 @@ struct LmT5Args {
   const int32_t* f_tcol;
   const int32_t* perm;              // device row -> target row
   float* out;
+  int dev_rows;                     // 1: out rows in device order
+  int o_pitch, o_col0;              // out row pitch / first column
 };
 
 struct L5Geom {
@@ -107,16 +109,17 @@ __global__ void __launch_bounds__(L5_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n > 0) {
-      const uint32_t idq = tc::idesc_tf32(128, 32, false, false);
-      const uint32_t c0 = smem_u32(cst);
-      const int kst = (pf + 7) / 8;
-      for (int t = 0; t < n; t++) {
-        const int b = t & 1;
-        mbar_wait_sleep(&lo_ready[b], (uint32_t)((t >> 1) & 1));   // (implies the stage landed)
-        tc::fence_after();
-        const uint32_t st = smem_u32(sm + (t % L5_NS) * gm.stage);
-        const uint32_t lo = smem_u32(sm + gm.o_lo + b * 16384);
+    // the whole warp walks the tiles; one elected lane issues (tc05.cuh)
+    const uint32_t idq = tc::idesc_tf32(128, 32, false, false);
+    const uint32_t c0 = smem_u32(cst);
+    const int kst = (pf + 7) / 8;
+    for (int t = 0; t < n; t++) {
+      const int b = t & 1;
+      mbar_wait_sleep(&lo_ready[b], (uint32_t)((t >> 1) & 1));   // (implies the stage landed)
+      tc::fence_after();
+      const uint32_t st = smem_u32(sm + (t % L5_NS) * gm.stage);
+      const uint32_t lo = smem_u32(sm + gm.o_lo + b * 16384);
+      if (tc::elect_one()) {
         for (int ks = 0; ks < kst; ks++) {
           const uint64_t ah = tc::smem_desc(st + ks * 32, 16, 1024, tc::kSw128);
           const uint64_t al = tc::smem_desc(lo + ks * 32, 16, 1024, tc::kSw128);
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(L5_THREADS, 1)
         }
         tc::commit(&q_full[b]);
       }
+      __syncwarp();
     }
   } else {
     const int ew = warp - 2, h = ew >> 2, q4 = warp & 3;
@@ -189,7 +193,8 @@ __global__ void __launch_bounds__(L5_THREADS, 1)
       for (int rr = ew * 16; rr < ew * 16 + 16; rr++) {
         const int64_t pr = (t0 + t) * L5_TILE + rr;
         if (pr < a.r_T && lane < a.ncol)
-          a.out[(int64_t)a.perm[pr] * a.c_x + a.col0 + lane] = stg[rr * 33 + lane];
+          a.out[(a.dev_rows ? pr : (int64_t)a.perm[pr]) * a.o_pitch + a.o_col0 + lane] =
+              stg[rr * 33 + lane];
       }
       (void)valid;
     }

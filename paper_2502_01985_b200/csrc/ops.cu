@@ -555,10 +555,29 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
         la.x = x_dev;
         la.f_tcol = t->d_f_tcol->as<int32_t>();
         la.perm = t->perm->as<int32_t>();
-        la.out = out_dev;
+        // FL_LMM_T5=2: device-order rows (sequential) + a row gather into
+        // target order, instead of scattered row writes
+        const bool devrows = atoi(on5) == 2;
+        float* dst = out_dev;
+        la.o_pitch = c_x;
+        la.o_col0 = col0;
+        if (devrows) {
+          FL_CUDA(cudaMallocAsync((void**)&dst, (size_t)t->r_T * ncol * 4 + 16, s));
+          la.o_pitch = ncol;
+          la.o_col0 = 0;
+          la.dev_rows = 1;
+        }
+        la.out = dst;
         const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(la.ntiles, t->sm_count));
         k_lmm_t5<<<nb, L5_THREADS, g5.total + 1024, s>>>(tm, la, g5);
         FL_CHECK_LAUNCH();
+        if (devrows) {
+          const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(t->r_T, 8), 16 * (int64_t)t->sm_count);
+          k_rows_unperm<<<gb, 256, 0, s>>>(dst, ncol, t->iperm->as<int32_t>(), t->r_T, c_x, col0,
+                                           out_dev);
+          FL_CHECK_LAUNCH();
+          FL_CUDA(cudaFreeAsync(dst, s));
+        }
         for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
         continue;
       }

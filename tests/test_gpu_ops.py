@@ -302,6 +302,9 @@ def test_lmm_tcgen05_vs_oracle(fl, monkeypatch, c_fact, dims):
         x = rng.random((ft.c_T, cx)).astype(np.float32)
         got = h.lmm(x)
         assert rel(got, oracle.lmm(tab, x)) < RTOL, cx
+        monkeypatch.setenv("FL_LMM_T5", "2")   # device-order rows + row gather: same values
+        assert np.array_equal(h.lmm(x), got), cx
+        monkeypatch.setenv("FL_LMM_T5", "1")
 
 
 @pytest.mark.parametrize("c_fact,dims", [(20, [(2000, 30)]), (28, []), (3, [(500, 7), (40, 3)])])
