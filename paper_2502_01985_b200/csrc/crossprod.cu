@@ -429,8 +429,29 @@ int gram(fl_table* t, const float* A, int pa, int acols, const float* B, int pb,
 
 #include "gram_t5.cuh"
 
-// F^T F through k_fgram_t5 (stream block <= 28 columns)
+// F^T F through k_fgram_t5l (bulk-copied tiles; pf % 4 == 0) or k_fgram_t5
+// (2-D TMA tiles; FL_GRAM_TMA=1 forces it), stream block <= 28 columns
 int fgram_t5(fl_table* t, double* out, cudaStream_t s) {
+  if (t->pf % 4 == 0 && !getenv("FL_GRAM_TMA")) {
+    const R5LGeom gl = r5l_geom(t->pf);
+    static bool attr_l = false;
+    if (!attr_l) {
+      FL_CUDA(cudaFuncSetAttribute(k_fgram_t5l, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(r5l_geom(28).total + 1024)));
+      attr_l = true;
+    }
+    const int64_t ntiles = t->r_pad / R5_TILE;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
+    double* part = nullptr;
+    FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * t->pf * t->pf * 8, s));
+    k_fgram_t5l<<<nb, R5_THREADS, gl.total + 1024, s>>>(t->F->as<float>(), t->pf, ntiles, gl, part);
+    FL_CHECK_LAUNCH();
+    k_fgram_reduce<<<(unsigned)ceil_div((int64_t)t->pf * t->pf * 32, 256), 256, 0, s>>>(
+        part, nb, t->pf, t->d_f_tcol->as<int32_t>(), t->c_T, out);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaFreeAsync(part, s));
+    return FL_OK;
+  }
   const R5Geom gm = r5_geom();
   CUtensorMap tm;
   int rc = make_tmap_2d(&tm, t->F->p, (uint64_t)t->r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,

@@ -317,9 +317,13 @@ def test_crossprod_tcgen05_gram_matches_simt(fl, monkeypatch, c_fact, dims):
     td = oracle.materialize(tab)
     h = fl.TargetHandle.factorized(ft)
     got = h.crossprod()
+    monkeypatch.setenv("FL_GRAM_TMA", "1")   # 2-D TMA tiles instead of bulk-copied rows
     monkeypatch.setenv("FL_GRAM_M64", "1")   # M = 64 MMA shape (16-lane TMEM quadrants)
     got64 = h.crossprod()
     monkeypatch.delenv("FL_GRAM_M64")
+    got_tma = h.crossprod()
+    monkeypatch.delenv("FL_GRAM_TMA")
+    assert rel(got, got_tma) < 4e-6
     monkeypatch.setenv("FL_NO_GRAM_T5", "1")
     simt = h.crossprod()
     assert rel(got, td.T @ td) < RTOL
