@@ -729,12 +729,7 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
     k_ydev32_rows<<<gb, 256, 0, s>>>(yv, cy, r_T, perm, yd);
   }
   FL_CHECK_LAUNCH();
-  CUtensorMap tmF, tmY;
-  int rc = make_tmap_2d(&tmF, t->F->p, (uint64_t)r_pad, (uint64_t)t->pf, (uint64_t)t->pf * 4,
-                        M5_TILE, 32, kSwz128Atom32);
-  if (rc) return rc;
-  rc = make_tmap_2d(&tmY, yd, (uint64_t)r_pad, 32, 128, M5_TILE, 32, kSwz128Atom32);
-  if (rc) return rc;
+  int rc = FL_OK;
   static bool attr = false;
   if (!attr) {
     FL_CUDA(cudaFuncSetAttribute(k_tmm_t5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M5_SMEM));
@@ -744,7 +739,7 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
   double* part = nullptr;
   FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * t->pf * cy * 8, s));
-  k_tmm_t5<<<nb, M5_THREADS, M5_SMEM, s>>>(tmF, tmY, t->pf, cy, ntiles, part);
+  k_tmm_t5<<<nb, M5_THREADS, M5_SMEM, s>>>(t->F->as<float>(), yd, t->pf, cy, ntiles, part);
   FL_CHECK_LAUNCH();
   k_reduce_partials<<<gridn((int64_t)t->pf * cy * 32), 256, 0, s>>>(
       part, nb, t->pf, cy, t->d_f_tcol->as<int32_t>(), out, os_t, os_c);
@@ -777,7 +772,8 @@ static int tmm_t5_min_cols() {
 // generic T^T y with strided y view and strided fp64 output
 int do_tlmm(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t, int64_t os_c,
             cudaStream_t s, bool dev_order) {
-  bool wide = t->pf > 0 && t->pf <= 28 && cy >= tmm_t5_min_cols() && cy <= 32 && t->r_T > 0 &&
+  bool wide = t->pf > 0 && t->pf <= 28 && t->pf % 4 == 0 && cy >= tmm_t5_min_cols() && cy <= 32 &&
+              t->r_T > 0 &&
               t->r_T <= (int64_t)INT32_MAX - M5_TILE && !getenv("FL_NO_TMM_T5");
   for (const auto& g : t->g)
     if ((size_t)g.cols * cy * 8 > 190 * 1024) wide = false;   // bins product smem

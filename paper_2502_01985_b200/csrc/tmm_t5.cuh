@@ -1,34 +1,39 @@
 // Stream-block part of a WIDE T^T y on the 5th-generation tensor cores
 // (included inside namespace flb by ops.cu): F^T Y for stream blocks of
-// <= 28 columns and 3..32 operand columns -- the op-level transpose_lmm
-// (reference ops.py:237-253) and rmm = (T^T x^T)^T (ops.py:219-235 via the
-// strided view), which before took one F pass per pair of operand columns.
+// <= 28 columns (pitch a multiple of 4) and 6..32 operand columns -- the
+// op-level transpose_lmm (reference ops.py:237-253) and rmm = (T^T x^T)^T
+// (ops.py:219-235 via the strided view), which before took one F pass per
+// pair of operand columns.
 //
 // Y is first laid out as YD[r_pad x 32] fp32 in DEVICE row order (operand
-// columns past c_y and the padding rows are zero; k_ydev32_*).  Then per
-// 128-row tile ONE M = 128, N = 64 MMA chain over the tile's rows computes
+// columns past c_y and the padding rows are zero; k_ydev32_*).  Per 128-row
+// tile the F rows and the YD rows are each ONE contiguous block: a 1-D bulk
+// copy apiece lands them in a linear stage (a 2-D TMA box of narrow rows is
+// one request per row -- the crossprod Gram ran 1.6x faster on bulk
+// copies), and the split warps write the MMA operands [F | F_lo | Y | Y_lo]
+// (MN-major 128B / 32-byte-atom swizzle, descriptor layout 1, tc05.cuh) into
+// a two-slot ring.  ONE M = 128, N = 64 MMA chain over the tile's rows then
+// computes
 //     D = [F | F_lo | Y | Y_lo]^T [Y | Y_lo]
-// with both operands read MN-major straight from the row-major TMA tiles
-// (128B / 32-byte-atom swizzle, descriptor layout 1, tc05.cuh); the tiles are
-// their own tf32 hi parts (the tensor core truncates), the lo parts are
-// written next to them by the split warps, and
 //     F^T Y = D[F][Y] + D[F_lo][Y] + D[F][Y_lo]          (3xTF32)
 // (rows 64..127 of D -- Y^T Y -- are a by-product of the M = 128 shape and
 // unused).  TMEM accumulates two tiles (256 rows) in fp32; dedicated fold
 // warps move them into fp64 registers; per-CTA partials are reduced in CTA
 // order by k_reduce_partials.  Bytes: F (4 pf) + YD (128) per row, read once.
 //
-//   warp 0     producer (TMA of the F and Y tiles)
-//   warp 1     MMA issuer (one thread)
-//   warps 2-5  split: F_lo and Y_lo of each tile (thread = tile row)
+//   warp 0     producer (bulk copies of the F and Y blocks)
+//   warp 1     MMA issuer (elected lane)
+//   warps 2-5  split: thread = tile row, hi / lo operand rows
 //   warps 8-9  fold: TMEM lanes 0..63 (the F / F_lo rows of D)
-//   warps 6-7  idle (TMEM lane quadrants 2, 3 hold the unused Y rows of D)
+//   warps 6-7  idle
 constexpr int M5_TILE = 128;
-constexpr int M5_NS = 3;
+constexpr int M5_NS = 3;                     // linear stages (F block | Y block)
+constexpr int M5_NO = 2;                     // operand ring slots
 constexpr int M5_FT = 2;
 constexpr int M5_THREADS = 320;
-constexpr uint32_t M5_STAGE = 65536;   // F | F_lo | Y | Y_lo, 16 KB each
-constexpr uint32_t M5_SMEM = M5_NS * M5_STAGE + 1024;
+constexpr uint32_t M5_SLOT = 65536;          // F | F_lo | Y | Y_lo, 16 KB each
+constexpr uint32_t M5_LIN = 14336 + 16384;   // F block (<= 128 x 28 fp32) | Y block
+constexpr uint32_t M5_SMEM = M5_NO * M5_SLOT + M5_NS * M5_LIN + 1024;
 
 __device__ __forceinline__ uint32_t m5_b32(int row, int c4) {
   return (uint32_t)(row * 128 + (((c4 >> 1) ^ (row & 3)) << 5) + ((c4 & 1) << 4));
@@ -36,21 +41,32 @@ __device__ __forceinline__ uint32_t m5_b32(int row, int c4) {
 __device__ __forceinline__ float m5_lo(float v) {
   return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u);
 }
+__device__ __forceinline__ float4 m5_lo4(float4 v) {
+  return make_float4(m5_lo(v.x), m5_lo(v.y), m5_lo(v.z), m5_lo(v.w));
+}
 
 // part[cta][i * cy + c] = sum over the CTA's rows of F[r][i] Y[r][c]
 __global__ void __launch_bounds__(M5_THREADS, 1)
-    k_tmm_t5(const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmY,
-             int pf, int cy, int64_t ntiles, double* __restrict__ part) {
+    k_tmm_t5(const float* __restrict__ F, const float* __restrict__ Y, int pf, int cy,
+             int64_t ntiles, double* __restrict__ part) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[M5_NS], empty[M5_NS], lo_ready[M5_NS], acc_full[2], acc_empty[2];
+  __shared__ uint64_t lin_full[M5_NS], lin_empty[M5_NS], op_ready[M5_NO], op_free[M5_NO];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  char* lin0 = sm + M5_NO * M5_SLOT;
+  // F operand chunks past pf are never written: zero the ring once
+  for (int i = tid; i < M5_NO * (M5_SLOT / 16); i += blockDim.x)
+    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (tid == 0) {
     for (int s = 0; s < M5_NS; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      mbar_init(&lo_ready[s], 128);
+      mbar_init(&lin_full[s], 1);
+      mbar_init(&lin_empty[s], 128);   // the split threads
+    }
+    for (int l = 0; l < M5_NO; l++) {
+      mbar_init(&op_ready[l], 128);
+      mbar_init(&op_free[l], 1);
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&acc_full[b], 1);
@@ -58,6 +74,7 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
     }
     fence_mbar_init();
   }
+  tc::fence_smem_to_async();
   if (warp == 0) tc::alloc(&tbase, 128);
   tc::fence_before();
   __syncthreads();
@@ -67,65 +84,83 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
   const int64_t base = ntiles / G, rem = ntiles % G;
   const int64_t t0 = blockIdx.x * base + min64(blockIdx.x, rem);
   const int n = (int)(base + (blockIdx.x < rem ? 1 : 0));
+  const uint32_t fbytes = 128u * pf * 4u;
   double ra[64];   // fold warps: this lane's row of D, fp64
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol = l2_policy_evict_first();
-      for (int i = 0; i < n; i++) {
-        const int s = i % M5_NS;
-        if (i >= M5_NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / M5_NS) - 1) & 1));
-        char* st = sm + s * M5_STAGE;
-        mbar_arrive_expect_tx(&full[s], 32768u);
-        tma_load_2d_hint(st, &tmF, 0, (int)((t0 + i) * M5_TILE), &full[s], pol);
-        tma_load_2d_hint(st + 32768, &tmY, 0, (int)((t0 + i) * M5_TILE), &full[s], pol);
+    const uint64_t pol = l2_policy_evict_first();
+    for (int i = 0; i < n; i++) {
+      const int s = i % M5_NS;
+      if (i >= M5_NS) mbar_wait_sleep(&lin_empty[s], (uint32_t)(((i / M5_NS) - 1) & 1));
+      if (tc::elect_one()) {
+        char* st = lin0 + s * M5_LIN;
+        mbar_arrive_expect_tx(&lin_full[s], fbytes + 16384u);
+        bulk_g2s_hint(st, F + (t0 + i) * M5_TILE * pf, fbytes, &lin_full[s], pol);
+        bulk_g2s_hint(st + 14336, Y + (t0 + i) * M5_TILE * 32, 16384u, &lin_full[s], pol);
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // the whole warp walks the tiles; one elected lane issues (tc05.cuh)
     const uint32_t id = tc::idesc_tf32(128, 64, true, true);
     for (int t = 0; t < n; t++) {
-      const int s = t % M5_NS, w = t / M5_FT, b = w & 1;
-      mbar_wait_sleep(&lo_ready[s], (uint32_t)((t / M5_NS) & 1));
+      const int l = t % M5_NO, w = t / M5_FT, b = w & 1;
+      mbar_wait_sleep(&op_ready[l], (uint32_t)((t / M5_NO) & 1));
       if ((t % M5_FT) == 0 && w >= 2) mbar_wait_sleep(&acc_empty[b], (uint32_t)(((w >> 1) - 1) & 1));
       tc::fence_after();
-      const uint32_t st = smem_u32(sm + s * M5_STAGE);
-      const uint64_t a0 = tc::smem_desc(st, 16384, 512, tc::kSw128B32);
-      const uint64_t b0 = tc::smem_desc(st + 32768, 16384, 512, tc::kSw128B32);
+      const uint32_t op = smem_u32(sm + l * M5_SLOT);
+      const uint64_t a0 = tc::smem_desc(op, 16384, 512, tc::kSw128B32);
+      const uint64_t b0 = tc::smem_desc(op + 32768, 16384, 512, tc::kSw128B32);
       if (tc::elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < M5_TILE / 8; kk++)
           tc::mma_tf32(tmem + 64 * b, a0 + (uint64_t)(kk * 64), b0 + (uint64_t)(kk * 64), id,
                        !((t % M5_FT) == 0 && kk == 0));
-        tc::commit(&empty[s]);
+        tc::commit(&op_free[l]);
         if ((t % M5_FT) == M5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
       }
       __syncwarp();
     }
   } else if (warp >= 2 && warp < 6) {
     const int r = 32 * (warp & 3) + lane;
-    const int sw = (r >> 2) & 1;   // rows r, r + 4 share a granule: swap chunk halves
+    const int nc4 = pf >> 2;
     for (int t = 0; t < n; t++) {
-      const int s = t % M5_NS;
-      char* st = sm + s * M5_STAGE;
-      mbar_wait_sleep(&full[s], (uint32_t)((t / M5_NS) & 1));
+      const int s = t % M5_NS, l = t % M5_NO;
+      const char* st = lin0 + s * M5_LIN;
+      char* op = sm + l * M5_SLOT;
+      mbar_wait_sleep(&lin_full[s], (uint32_t)((t / M5_NS) & 1));
+      float4 f[7], y[8];
+      const float4* fr = reinterpret_cast<const float4*>(st + r * pf * 4);
+      const float4* yr = reinterpret_cast<const float4*>(st + 14336 + r * 128);
 #pragma unroll
-      for (int h = 0; h < 2; h++) {   // F, then Y
-        char* src = st + h * 32768;
+      for (int c = 0; c < 7; c++)
+        if (c < nc4) f[c] = fr[c];
+      // y[c] holds chunk (c + r) % 8 of the row: the rotation makes both the
+      // linear reads and the swizzled writes of a store phase conflict-free
 #pragma unroll
-        for (int c = 0; c < 8; c++) {
-          const uint32_t o = m5_b32(r, c ^ sw);
-          const float4 v = *reinterpret_cast<const float4*>(src + o);
-          *reinterpret_cast<float4*>(src + 16384 + o) =
-              make_float4(m5_lo(v.x), m5_lo(v.y), m5_lo(v.z), m5_lo(v.w));
+      for (int c = 0; c < 8; c++) y[c] = yr[(c + r) & 7];
+      mbar_arrive(&lin_empty[s]);   // the linear stage is consumed
+      if (t >= M5_NO) mbar_wait_sleep(&op_free[l], (uint32_t)(((t / M5_NO) - 1) & 1));
+#pragma unroll
+      for (int c = 0; c < 7; c++) {
+        if (c < nc4) {
+          const uint32_t o = m5_b32(r, c);
+          *reinterpret_cast<float4*>(op + o) = f[c];
+          *reinterpret_cast<float4*>(op + 16384 + o) = m5_lo4(f[c]);
         }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const uint32_t o = m5_b32(r, (c + r) & 7);
+        *reinterpret_cast<float4*>(op + 32768 + o) = y[c];
+        *reinterpret_cast<float4*>(op + 49152 + o) = m5_lo4(y[c]);
       }
       fence_proxy_async();
       tc::fence_before();
-      mbar_arrive(&lo_ready[s]);
+      mbar_arrive(&op_ready[l]);
     }
   } else if (warp >= 8) {
-    const int q4 = warp & 3, r = 32 * q4 + lane;   // q4 = 0, 1: rows 0..63 of D
+    const int q4 = warp & 3;   // q4 = 0, 1: rows 0..63 of D
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
 #pragma unroll
     for (int j = 0; j < 64; j++) ra[j] = 0.0;
@@ -151,7 +186,7 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
     }
   }
   tc::fence_before();
-  __syncthreads();   // every stage is idle: stage 0 becomes the combine area
+  __syncthreads();   // everything is idle: the operand ring becomes the combine area
   tc::fence_after();
   if (warp >= 8) {
     const int r = 32 * (warp & 3) + lane;
