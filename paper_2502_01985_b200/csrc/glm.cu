@@ -25,6 +25,7 @@
 
 #include "internal.h"
 #include "reduce.cuh"
+#include "tc05.cuh"
 
 namespace flb {
 

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
       }
     }
     __syncwarp();
-    if (lane == 0 && i + a.nst < cnt) {
+    if (i + a.nst < cnt && tc::elect_one()) {   // converged warp: no per-instruction ELECT loop
       fence_proxy_async();
       issue(s, u0 + i + a.nst);
     }

@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(KM_WARPS * 32, (NT <= 2 && KC <= 4) ? 2 : 1)
       }
     }
     __syncwarp();
-    if (lane == 0 && i + a.nst < cnt) {
+    if (i + a.nst < cnt && tc::elect_one()) {   // converged warp: no per-instruction ELECT loop
       fence_proxy_async();
       issue(s, u0 + i + a.nst);
     }
