@@ -708,27 +708,47 @@ static int tlmm_bins_product(fl_table* t, const GatherSrc& g, const double* bins
 static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t, int64_t os_c,
                         cudaStream_t s, bool dev_order) {
   const int64_t r_T = t->r_T, r_pad = t->r_pad;
-  float* yd = nullptr;
-  FL_CUDA(cudaMallocAsync((void**)&yd, (size_t)r_pad * 32 * 4, s));
-  if (r_pad > r_T) FL_CUDA(cudaMemsetAsync(yd + r_T * 32, 0, (size_t)(r_pad - r_T) * 32 * 4, s));
   const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(r_T, 32), 16 * (int64_t)t->sm_count);
   const int32_t* perm = dev_order ? nullptr : t->perm->as<int32_t>();
-  if (yv.sc > yv.sr && yv.sr == 1) {
-    // column-strided (rmm's x^T): transpose in target order, then gather rows
-    float* xt = yd;
-    if (perm) FL_CUDA(cudaMallocAsync((void**)&xt, (size_t)r_T * 32 * 4, s));
-    k_xt32<<<(unsigned)std::min<int64_t>(ceil_div(r_T, 128), 8 * (int64_t)t->sm_count), 256, 0, s>>>(
-        yv, cy, r_T, xt);
-    FL_CHECK_LAUNCH();
-    if (perm) {
-      k_ydev32_rows<<<gb, 256, 0, s>>>(YView{xt, 32, 1}, 32, r_T, perm, yd);
-      FL_CHECK_LAUNCH();
-      FL_CUDA(cudaFreeAsync(xt, s));
-    }
+  // y's rows are read where they lie (target order, through perm) by the
+  // pass and by the group sums: a row-major y with 16-byte rows directly,
+  // any other view (rmm's column-strided x^T) after one sequential copy into
+  // 32-column target-order rows.  Wider than 16 columns (or FL_TMM_YD=1): y
+  // is laid out in device order first (YD) and bulk-copied per tile.
+  // (measured at C2 size: gathering wins up to 16 columns -- k = 8 / 16
+  // transpose_lmm 9.3 / 9.6 ms vs 11.1 / 11.2 with YD -- and loses at 32:
+  // 14.7 vs 11.3 ms)
+  const char* yde = getenv("FL_TMM_YD");
+  const bool use_yd = yde ? atoi(yde) != 0 : cy > 16;
+  float* tmp = nullptr;
+  const float* yg = nullptr;
+  int yp = 32;
+  if (!use_yd && yv.sc == 1 && yv.sr == cy && cy % 4 == 0 && ((uintptr_t)yv.base & 15) == 0) {
+    yg = yv.base;
+    yp = cy;
   } else {
-    k_ydev32_rows<<<gb, 256, 0, s>>>(yv, cy, r_T, perm, yd);
+    FL_CUDA(cudaMallocAsync((void**)&tmp, (size_t)r_pad * 32 * 4, s));
+    if (r_pad > r_T) FL_CUDA(cudaMemsetAsync(tmp + r_T * 32, 0, (size_t)(r_pad - r_T) * 32 * 4, s));
+    if (yv.sc > yv.sr && yv.sr == 1) {
+      // column-strided (rmm's x^T): transpose in target order, sequential both ways
+      float* xt = tmp;
+      if (use_yd && perm) FL_CUDA(cudaMallocAsync((void**)&xt, (size_t)r_T * 32 * 4, s));
+      k_xt32<<<(unsigned)std::min<int64_t>(ceil_div(r_T, 128), 8 * (int64_t)t->sm_count), 256, 0,
+               s>>>(yv, cy, r_T, xt);
+      FL_CHECK_LAUNCH();
+      if (use_yd && perm) {
+        k_ydev32_rows<<<gb, 256, 0, s>>>(YView{xt, 32, 1}, 32, r_T, perm, tmp);
+        FL_CHECK_LAUNCH();
+        FL_CUDA(cudaFreeAsync(xt, s));
+      }
+    } else {
+      k_ydev32_rows<<<gb, 256, 0, s>>>(yv, cy, r_T, use_yd ? perm : nullptr, tmp);
+      FL_CHECK_LAUNCH();
+    }
+    yg = tmp;
   }
-  FL_CHECK_LAUNCH();
+  // the rows of yg are in device order when YD was built (or y is already)
+  const int32_t* yperm = (use_yd || dev_order) ? nullptr : perm;
   int rc = FL_OK;
   static bool attr = false;
   if (!attr) {
@@ -739,7 +759,12 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
   double* part = nullptr;
   FL_CUDA(cudaMallocAsync((void**)&part, (size_t)nb * t->pf * cy * 8, s));
-  k_tmm_t5<<<nb, M5_THREADS, M5_SMEM, s>>>(t->F->as<float>(), yd, t->pf, cy, ntiles, part);
+  if (use_yd)   // YD: one bulk copy per tile
+    k_tmm_t5<<<nb, M5_THREADS, M5_SMEM, s>>>(t->F->as<float>(), yg, t->pf, cy, ntiles, part,
+                                             nullptr, 0, nullptr, r_T);
+  else          // rows gathered in the pass
+    k_tmm_t5<<<nb, M5_THREADS, M5_SMEM, s>>>(t->F->as<float>(), nullptr, t->pf, cy, ntiles, part,
+                                             yg, yp, yperm, r_T);
   FL_CHECK_LAUNCH();
   k_reduce_partials<<<gridn((int64_t)t->pf * cy * 32), 256, 0, s>>>(
       part, nb, t->pf, cy, t->d_f_tcol->as<int32_t>(), out, os_t, os_c);
@@ -751,13 +776,13 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
     k_group_bins32<<<(unsigned)std::min<int64_t>(ceil_div(g.rows, 8), 32 * (int64_t)t->sm_count),
                      256, 0, s>>>(g.grp_ptr->as<int64_t>(),
                                   g.grp_rows ? g.grp_rows->as<int32_t>() : nullptr, g.sorted,
-                                  g.n_neg, g.rows, yd, cy, bins);
+                                  g.n_neg, g.rows, yg, yp, yperm, cy, bins);
     FL_CHECK_LAUNCH();
     rc = tlmm_bins_product(t, g, bins, cy, out, os_t, os_c, s);
     if (rc) return rc;
     FL_CUDA(cudaFreeAsync(bins, s));
   }
-  FL_CUDA(cudaFreeAsync(yd, s));
+  if (tmp) FL_CUDA(cudaFreeAsync(tmp, s));
   return FL_OK;
 }
 

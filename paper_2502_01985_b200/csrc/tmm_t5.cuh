@@ -48,7 +48,8 @@ __device__ __forceinline__ float4 m5_lo4(float4 v) {
 // part[cta][i * cy + c] = sum over the CTA's rows of F[r][i] Y[r][c]
 __global__ void __launch_bounds__(M5_THREADS, 1)
     k_tmm_t5(const float* __restrict__ F, const float* __restrict__ Y, int pf, int cy,
-             int64_t ntiles, double* __restrict__ part) {
+             int64_t ntiles, double* __restrict__ part, const float* __restrict__ Yg, int yp,
+             const int32_t* __restrict__ perm, int64_t r_T) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t lin_full[M5_NS], lin_empty[M5_NS], op_ready[M5_NO], op_free[M5_NO];
@@ -94,9 +95,9 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
       if (i >= M5_NS) mbar_wait_sleep(&lin_empty[s], (uint32_t)(((i / M5_NS) - 1) & 1));
       if (tc::elect_one()) {
         char* st = lin0 + s * M5_LIN;
-        mbar_arrive_expect_tx(&lin_full[s], fbytes + 16384u);
+        mbar_arrive_expect_tx(&lin_full[s], fbytes + (Yg ? 0u : 16384u));
         bulk_g2s_hint(st, F + (t0 + i) * M5_TILE * pf, fbytes, &lin_full[s], pol);
-        bulk_g2s_hint(st + 14336, Y + (t0 + i) * M5_TILE * 32, 16384u, &lin_full[s], pol);
+        if (!Yg) bulk_g2s_hint(st + 14336, Y + (t0 + i) * M5_TILE * 32, 16384u, &lin_full[s], pol);
       }
       __syncwarp();
     }
@@ -124,10 +125,39 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
   } else if (warp >= 2 && warp < 6) {
     const int r = 32 * (warp & 3) + lane;
     const int nc4 = pf >> 2;
+    const int ych = (cy + 3) >> 2;   // 16-byte chunks of a gathered y row
+    // gather mode: this thread's own y row of tile t lands in the Y block of
+    // linear stage t % M5_NS by async copies issued two tiles ahead (only
+    // this thread reads it: no barrier, no proxy fence).  (A warp-
+    // cooperative variant -- one copy instruction per 4 rows -- measured
+    // 1.4-3x slower.)
+    auto gather = [&](int t) {
+      if (Yg && t < n) {
+        char* yr = lin0 + (t % M5_NS) * M5_LIN + 14336 + r * 128;
+        const int64_t p = (t0 + t) * M5_TILE + r;
+        if (p < r_T) {
+          const float* src = Yg + (perm ? (int64_t)perm[p] : p) * yp;
+#pragma unroll
+          for (int k = 0; k < 8; k++) {   // rotated chunk order: conflict-free phases
+            const int c = (k + r) & 7;
+            if (c < ych) cp_async16(yr + 16 * c, src + 4 * c);
+            else *reinterpret_cast<float4*>(yr + 16 * c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+          for (int c = 0; c < 8; c++)
+            *reinterpret_cast<float4*>(yr + 16 * c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      cp_async_commit();
+    };
+    gather(0);
+    gather(1);
     for (int t = 0; t < n; t++) {
       const int s = t % M5_NS, l = t % M5_NO;
       const char* st = lin0 + s * M5_LIN;
       char* op = sm + l * M5_SLOT;
+      gather(t + 2);
+      cp_async_wait_group<2>();   // tile t's row (groups t + 1, t + 2 may be in flight)
       mbar_wait_sleep(&lin_full[s], (uint32_t)((t / M5_NS) & 1));
       float4 f[7], y[8];
       const float4* fr = reinterpret_cast<const float4*>(st + r * pf * 4);
@@ -247,15 +277,17 @@ __global__ void __launch_bounds__(256) k_xt32(YView yv, int cy, int64_t r_T,
   }
 }
 
-// bins[j][c] = sum over the members of group j (ascending) of YD[p][c],
-// fp64 -- k_group_bins' order -- with a warp per group and lane = column
-// (YD rows are 128-byte device-order rows)
+// bins[j][c] = sum over the members p of group j (ascending) of y's row at
+// device row p -- y[(perm ? perm[p] : p) * yp + c] -- in fp64 (k_group_bins'
+// order), warp per group, lane = column
 __global__ void __launch_bounds__(256) k_group_bins32(const int64_t* __restrict__ grp_ptr,
                                                       const int32_t* __restrict__ grp_rows,
                                                       bool sorted, int64_t n_neg, int64_t rows,
-                                                      const float* __restrict__ yd, int cy,
+                                                      const float* __restrict__ y, int yp,
+                                                      const int32_t* __restrict__ perm, int cy,
                                                       double* __restrict__ bins) {
   const int lane = threadIdx.x & 31;
+  const int ln = lane < cy ? lane : 0;
   for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < rows;
        j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t m0 = grp_ptr[j], m1 = grp_ptr[j + 1];
@@ -266,14 +298,16 @@ __global__ void __launch_bounds__(256) k_group_bins32(const int64_t* __restrict_
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         const int64_t p = sorted ? n_neg + m + u : (int64_t)grp_rows[m + u];
-        v[u] = yd[p * 32 + lane];
+        const int64_t row = perm ? (int64_t)perm[p] : p;
+        v[u] = y[row * yp + ln];
       }
 #pragma unroll
       for (int u = 0; u < 8; u++) s += (double)v[u];
     }
     for (; m < m1; m++) {
       const int64_t p = sorted ? n_neg + m : (int64_t)grp_rows[m];
-      s += (double)yd[p * 32 + lane];
+      const int64_t row = perm ? (int64_t)perm[p] : p;
+      s += (double)y[row * yp + ln];
     }
     if (lane < cy) bins[j * cy + lane] = s;
   }
