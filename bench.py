@@ -725,7 +725,10 @@ def main():
                                      {"gnmf": 2}.get(wl["model"], 3))
     if world == 1 and not args.no_e2e:
         sess.close()
-        out["e2e"] = bench_e2e(torch, fl, wl, sh, hyper, args)
+        try:
+            out["e2e"] = bench_e2e(torch, fl, wl, sh, hyper, args)
+        except Exception as ex:   # keep the line: report why there is no e2e number
+            out["e2e"] = {"value": None, "error": f"{type(ex).__name__}: {ex}"[:300]}
     elif world > 1 and not args.no_e2e and wl["model"] in ("linreg", "logreg"):
         sess.close()
         out["e2e"] = bench_e2e_sharded(torch, fl, wl, sh, hyper, args, dist, dev)

@@ -35,7 +35,15 @@ if [ "$what" = full ] || [ "$what" = all ]; then
 fi
 ls -la $out
 if [ "$what" = ops ]; then
+  timeout 900 python tools/op_probe.py --crossprod c2 > $out/op_crossprod.txt 2>&1
+  OP_KS=8,16,32 timeout 900 python tools/op_probe.py --wide c2 > $out/op_wide.txt 2>&1
+  timeout 900 $NCU --metrics gpu__time_duration.sum --csv --log-file $out/launches_crossprod.csv \
+    python tools/op_probe.py --crossprod c2 > /dev/null 2>&1
+  OP_KS=32 timeout 900 $NCU --metrics gpu__time_duration.sum --csv --log-file $out/launches_wide32.csv \
+    python tools/op_probe.py --wide c2 > /dev/null 2>&1
   timeout 900 $NCU --set full --import-source on -k regex:k_fgram_t5 -s 1 -c 1 -o $out/full_fgram \
     python tools/op_probe.py --crossprod c2 > /dev/null 2>&1
+  OP_KS=32 timeout 900 $NCU --set full --import-source on -k regex:k_tmm_t5 -c 1 -o $out/full_tmm \
+    python tools/op_probe.py --wide c2 > /dev/null 2>&1
   ls -la $out
 fi
