@@ -557,12 +557,14 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
         la.perm = t->perm->as<int32_t>();
         // FL_LMM_T5=2: device-order rows (sequential) + a row gather into
         // target order, instead of scattered row writes
-        const bool devrows = atoi(on5) == 2;
+        const bool devrows = atoi(on5) >= 2;
+        const bool plain = atoi(on5) == 3;   // experiment: cudaMalloc'd row buffer (page size)
         float* dst = out_dev;
         la.o_pitch = c_x;
         la.o_col0 = col0;
         if (devrows) {
-          FL_CUDA(cudaMallocAsync((void**)&dst, (size_t)t->r_T * ncol * 4 + 16, s));
+          if (plain) FL_CUDA(cudaMalloc((void**)&dst, (size_t)t->r_T * ncol * 4 + 16));
+          else FL_CUDA(cudaMallocAsync((void**)&dst, (size_t)t->r_T * ncol * 4 + 16, s));
           la.o_pitch = ncol;
           la.o_col0 = 0;
           la.dev_rows = 1;
@@ -576,7 +578,12 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
           k_rows_unperm<<<gb, 256, 0, s>>>(dst, ncol, t->iperm->as<int32_t>(), t->r_T, c_x, col0,
                                            out_dev);
           FL_CHECK_LAUNCH();
-          FL_CUDA(cudaFreeAsync(dst, s));
+          if (plain) {
+            FL_CUDA(cudaStreamSynchronize(s));
+            FL_CUDA(cudaFree(dst));
+          } else {
+            FL_CUDA(cudaFreeAsync(dst, s));
+          }
         }
         for (float* q : qs) FL_CUDA(cudaFreeAsync(q, s));
         continue;

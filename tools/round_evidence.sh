@@ -33,6 +33,18 @@ if [ "$what" = full ] || [ "$what" = all ]; then
   timeout 900 $NCU --set full --import-source on -k regex:k_gnmf_t5 -s 4 -c 1 -o $out/full_c4_fact \
     python bench.py --workload c4 --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity > /dev/null 2>&1
 fi
+# .ncu-rep files are too large to bring back (gpurun merges <= 64 MiB):
+# summarise them here and keep the text
+summarise() {
+  for f in $out/full_*.ncu-rep; do
+    [ -f "$f" ] || continue
+    b=${f%.ncu-rep}
+    python tools/ncu_summary.py report "$f" > "$b.txt" 2>&1
+    python tools/ncu_source.py "$f" 40 >> "$b.txt" 2>&1
+    rm -f "$f"
+  done
+}
+summarise
 ls -la $out
 if [ "$what" = ops ]; then
   timeout 900 python tools/op_probe.py --crossprod c2 > $out/op_crossprod.txt 2>&1
@@ -45,5 +57,6 @@ if [ "$what" = ops ]; then
     python tools/op_probe.py --crossprod c2 > /dev/null 2>&1
   OP_KS=32 timeout 900 $NCU --set full --import-source on -k regex:k_tmm_t5 -c 1 -o $out/full_tmm \
     python tools/op_probe.py --wide c2 > /dev/null 2>&1
+  summarise
   ls -la $out
 fi
