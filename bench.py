@@ -589,9 +589,16 @@ def main():
     h = build_handle(fl, wl, sh)
     sess, hyper = make_session(torch, fl, wl, h, sh, dist)
     stream0 = torch.cuda.default_stream(dev)
-    flush_buf = None
+    flush_buf = flush_rd = None
     if args.workload == "c1":
         flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB
+        # FL_BENCH_FLUSH=dirty: the write alone (round-2 protocol).  Default:
+        # the write, then a read of a second 256 MB buffer, so the L2 the
+        # iteration starts from holds no workload data AND no dirty lines
+        # (otherwise every line the iteration brings in first writes back a
+        # dirty flush line: up to 88 MB of extra HBM writes charged to C1)
+        flush_clean = os.environ.get("FL_BENCH_FLUSH", "clean") != "dirty"
+        flush_rd = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=dev) if flush_clean else None
 
     # NCCL: the library's own communicator, the all-reduce captured in the
     # session's CUDA graphs (gloo: host-driven loop through torch.distributed)
@@ -627,6 +634,8 @@ def main():
             evs = []
             for _ in range(args.steps):
                 flush_buf.fill_(1.0)
+                if flush_rd is not None:
+                    flush_rd.sum()
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream0)
@@ -692,7 +701,10 @@ def main():
         "config": {
             "workload": wl["desc"], "fact_rows": wl["rows"],
             "dims": [list(d) for d in wl["dims"]], "c_T": h.shape[1], **hyper,
-            "l2": ("working set < L2: 256 MB L2 flush between iterations, each timed alone"
+            "l2": (("working set < L2: L2 flushed between iterations (256 MB written, then 256 MB "
+                    "of other clean lines read: no workload data and no dirty lines left), each "
+                    "timed alone" if flush_rd is not None else
+                    "working set < L2: 256 MB L2 flush (write) between iterations, each timed alone")
                    if flush_buf is not None else "inputs >> L2 126 MB (no flush needed)"),
             "parallelism": (f"dp{world}: fact rows sharded by FK range of the largest "
                             "dimension; one all-reduce of the reduce buffer per iteration"

@@ -1328,8 +1328,18 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
       int span = 0;
       FL_CUDA(cudaMemcpyAsync(&span, s->solo_span.p, 4, cudaMemcpyDeviceToHost, st));
       FL_CUDA(cudaStreamSynchronize(st));
-      const size_t extra = (size_t)FW_QCAP * 4 + (size_t)FW_WARPS * FW_LCAP * sizeof(SoloRec) +
-                           (size_t)FW_WARPS * FW_SOLO_PITCH * 8;
+      // q staging sized to the measured span (not FW_QCAP): the solo kernel
+      // must keep 2 CTAs per SM at C1 (112 KB of stages each)
+      const int qcap = (int)std::min<int64_t>(FW_QCAP, round_up((int64_t)std::max(span, 1), 4));
+      size_t extra = (size_t)qcap * 4 + (size_t)FW_WARPS * FW_LCAP * sizeof(SoloRec) +
+                     (size_t)FW_WARPS * FW_SOLO_PITCH * 8;
+      // the CTA's S_d span staged in shared memory when it is short (C1:
+      // ~35 rows = 7 KB): one bulk copy before the PDL wait replaces the
+      // prologue's and the gradient records' dependent L2 / HBM row reads
+      const size_t s0_bytes = (size_t)span * t->g[0].pitch * 4;
+      const char* e0 = getenv("FL_GLM_SOLO_S0");
+      const bool s0_on = (!e0 || atoi(e0) != 0) && span > 0 && s0_bytes <= 32 * 1024;
+      if (s0_on) extra += round_up((int64_t)s0_bytes, 16);
       const size_t smem_solo = s->smem_fw + extra;
       // a CTA stages its q rows before streaming: worth it while that
       // prologue is short (C1: 34 rows per CTA, one kernel instead of three);
@@ -1342,6 +1352,8 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         if ((rc = s->solo_part.alloc((size_t)s->nblk_fw * t->g[0].pitch * 8))) return rc;
         GlmFactWArgs& fw = s->fw;
         fw.solo = 1;
+        fw.s0_rows = s0_on ? span : 0;
+        fw.qcap = qcap;
         fw.S0 = t->g[0].S->as<float>();
         fw.pitch0 = t->g[0].pitch;
         fw.w0d = da.w[0];

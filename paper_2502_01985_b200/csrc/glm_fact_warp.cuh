@@ -101,6 +101,10 @@ struct GlmFactWArgs {
   const UpdateArgs* up;      // the session's update arguments (device copy: no param copies)
   int* gcnt;                 // per-group arrival counters (zeroed; reset by each group's last CTA)
   double* gpart;             // groups x (pf + 1 + pitch0): first-level partial sums
+  int qcap;                  // q entries staged per CTA (a multiple of 4, <= FW_QCAP)
+  int s0_rows;               // > 0: the CTA's S_d row span (<= s0_rows rows) is bulk-copied
+                             // into shared memory before the PDL wait and serves both the
+                             // q prologue and the gradient records (0: read through L2)
 };
 
 struct SoloRec {
@@ -167,8 +171,37 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
              &wbar[s]);
     if (has_sort) bulk_g2s(st + a.off_fk, fks + unit * RW, RW * 4, &wbar[s]);
   };
-  // F, labels and FKs are immutable: the warp's first stages stream in before
-  // the dependency wait (PDL), overlapping the previous kernel's tail
+  // solo: this CTA's dimension-row span [k_lo, k_lo + nq) (keys are sorted)
+  char* solo_sm = smem + (size_t)FW_WARPS * a.nst * a.stage_bytes;
+  float* q_s = reinterpret_cast<float*>(solo_sm);
+  SoloRec* rec = reinterpret_cast<SoloRec*>(q_s + a.qcap) + warp * FW_LCAP;
+  double* gsd_all = reinterpret_cast<double*>(reinterpret_cast<SoloRec*>(q_s + a.qcap) +
+                                              FW_WARPS * FW_LCAP);
+  float* S0_s = reinterpret_cast<float*>(gsd_all + FW_WARPS * FW_SOLO_PITCH);
+  __shared__ int span_s[2];
+  __shared__ uint64_t s0bar;
+  // F, labels, FKs and S_d are immutable: the warp's first stages (and the
+  // CTA's S_d span) stream in before the dependency wait (PDL), overlapping
+  // the previous kernel's tail
+  if (a.solo && threadIdx.x == 0) {
+    const int64_t cw0 = (int64_t)blockIdx.x * FW_WARPS, cw1 = cw0 + FW_WARPS;
+    const int64_t cu0 = cw0 * base + min64(cw0, rem), cu1 = cw1 * base + min64(cw1, rem);
+    const int64_t rlo = max64(cu0 * RW, a.n_neg0), rhi = min64(cu1 * RW, a.r_T) - 1;
+    int klo = 0, nq = 0;
+    if (rlo <= rhi) {
+      klo = __ldg(fks + rlo);
+      nq = __ldg(fks + rhi) - klo + 1;
+    }
+    span_s[0] = klo;
+    span_s[1] = nq;
+    if (a.s0_rows > 0 && nq > 0) {
+      mbar_init(&s0bar, 1);
+      fence_mbar_init();
+      const uint32_t bytes = (uint32_t)nq * (uint32_t)a.pitch0 * 4u;
+      mbar_arrive_expect_tx(&s0bar, bytes);
+      bulk_g2s(S0_s, a.S0 + (int64_t)klo * a.pitch0, bytes, &s0bar);
+    }
+  }
   if (lane == 0) {
     lsum[warp] = 0.0;
     for (int s = 0; s < a.nst; s++) mbar_init(&wbar[s], 1);
@@ -181,23 +214,18 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
   for (int j = threadIdx.x; j < C4; j += blockDim.x)
     w_s[j] = reinterpret_cast<const float4*>(a.wF)[j];
   // solo: q_d of the dimension rows this CTA's rows reference
-  char* solo_sm = smem + (size_t)FW_WARPS * a.nst * a.stage_bytes;
-  float* q_s = reinterpret_cast<float*>(solo_sm);
-  SoloRec* rec = reinterpret_cast<SoloRec*>(q_s + FW_QCAP) + warp * FW_LCAP;
   int k_lo = 0;
+  const bool s0_smem = a.solo && a.s0_rows > 0;
   if (a.solo) {
-    const int64_t cw0 = (int64_t)blockIdx.x * FW_WARPS, cw1 = cw0 + FW_WARPS;
-    const int64_t cu0 = cw0 * base + min64(cw0, rem), cu1 = cw1 * base + min64(cw1, rem);
-    const int64_t rlo = max64(cu0 * RW, a.n_neg0), rhi = min64(cu1 * RW, a.r_T) - 1;
-    int nq = 0;
-    if (rlo <= rhi) {
-      k_lo = fks[rlo];
-      nq = fks[rhi] - k_lo + 1;
-    }
+    __syncthreads();   // span_s
+    k_lo = span_s[0];
+    const int nq = span_s[1];
     const int p4 = a.pitch0 / 4;
     const float4* w04 = reinterpret_cast<const float4*>(a.w0d);
+    if (s0_smem && nq > 0) mbar_wait(&s0bar, 0);
+    const float* S0b = s0_smem ? S0_s : a.S0 + (int64_t)k_lo * a.pitch0;
     for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-      const float4* sr = reinterpret_cast<const float4*>(a.S0 + (int64_t)(k_lo + i) * a.pitch0);
+      const float4* sr = reinterpret_cast<const float4*>(S0b + (int64_t)i * a.pitch0);
       float z = 0.f;
       for (int j = 0; j < p4; j++) {
         const float4 v = sr[j], ww = w04[j];
@@ -217,11 +245,20 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
     __syncwarp();
     for (int e = 0; e < ln; e++) {
       const SoloRec rr = rec[e];
-      const float* sr = a.S0 + (int64_t)rr.key * a.pitch0;
+      if (s0_smem) {
+        const float* sr = S0_s + (rr.key - k_lo) * a.pitch0;
 #pragma unroll
-      for (int m = 0; m < FW_SOLO_PITCH / 32; m++) {
-        const int c = lane + 32 * m;
-        if (c < a.pitch0) gd[m] += (double)rr.v * (double)__ldg(sr + c);
+        for (int m = 0; m < FW_SOLO_PITCH / 32; m++) {
+          const int c = lane + 32 * m;
+          if (c < a.pitch0) gd[m] += (double)rr.v * (double)sr[c];
+        }
+      } else {
+        const float* sr = a.S0 + (int64_t)rr.key * a.pitch0;
+#pragma unroll
+        for (int m = 0; m < FW_SOLO_PITCH / 32; m++) {
+          const int c = lane + 32 * m;
+          if (c < a.pitch0) gd[m] += (double)rr.v * (double)__ldg(sr + c);
+        }
       }
     }
     __syncwarp();
@@ -440,7 +477,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
     out[t] = sum;
   }
   if (a.solo) {
-    double* gsd = reinterpret_cast<double*>(rec + FW_LCAP * (FW_WARPS - warp));   // past all lists
+    double* gsd = gsd_all;   // past all lists
 #pragma unroll
     for (int m = 0; m < FW_SOLO_PITCH / 32; m++) {
       const int c = lane + 32 * m;
