@@ -436,8 +436,7 @@ int fgram_t5(fl_table* t, double* out, cudaStream_t s) {
     const R5LGeom gl = r5l_geom(t->pf);
     static bool attr_l = false;
     if (!attr_l) {
-      FL_CUDA(cudaFuncSetAttribute(k_fgram_t5l, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(r5l_geom(28).total + 1024)));
+      FL_CUDA(raise_smem_limit(k_fgram_t5l, (int)(r5l_geom(28).total + 1024)));
       attr_l = true;
     }
     const int64_t ntiles = t->r_pad / R5_TILE;
@@ -459,8 +458,7 @@ int fgram_t5(fl_table* t, double* out, cudaStream_t s) {
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    FL_CUDA(cudaFuncSetAttribute(k_fgram_t5, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(gm.total + 1024)));
+    FL_CUDA(raise_smem_limit(k_fgram_t5, (int)(gm.total + 1024)));
     attr = true;
   }
   const int64_t ntiles = t->r_pad / R5_TILE;

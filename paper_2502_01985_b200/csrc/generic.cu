@@ -242,8 +242,7 @@ int kmg_create(fl_table* t, int k, const double* c0, cudaStream_t st, KmGen** ou
   const size_t cf_bytes = (size_t)t->pf * s->KPAD * 4;
   s->stage_cf = cf_bytes <= 96 * 1024 ? 1 : 0;
   if (s->stage_cf)
-    FL_CUDA(cudaFuncSetAttribute(k_kg_fact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(cf_bytes, 16)));
+    FL_CUDA(raise_smem_limit(k_kg_fact, (int)std::max<size_t>(cf_bytes, 16)));
   FL_CUDA(cudaStreamSynchronize(st));
   *out = guard.release();
   return FL_OK;
@@ -546,11 +545,10 @@ int gng_create(fl_table* t, int rank, const double* w0, const double* h0, double
     set_error("GNMF: rank %d too large for the Gram tiles", rank);
     return FL_ERR_OP;
   }
-  FL_CUDA(cudaFuncSetAttribute(k_gg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)((size_t)32 * R * 4)));
+  FL_CUDA(raise_smem_limit(k_gg_gram, (int)((size_t)32 * R * 4)));
   s->stage_hh = (size_t)R * R * 4 + (size_t)8 * R * 4 <= 160 * 1024 ? 1 : 0;
   s->smem_w = (s->stage_hh ? (size_t)R * R * 4 : 0) + (size_t)8 * R * 4;
-  FL_CUDA(cudaFuncSetAttribute(k_gg_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_w));
+  FL_CUDA(raise_smem_limit(k_gg_w, (int)s->smem_w));
   FL_CUDA(cudaStreamSynchronize(st));
   *out = guard.release();
   return FL_OK;

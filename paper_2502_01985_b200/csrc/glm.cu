@@ -1061,7 +1061,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     return FL_ERR_OP;
   }
   auto kf = model == FL_MODEL_LINREG ? (const void*)k_glm_fact<0> : (const void*)k_glm_fact<1>;
-  FL_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_fact));
+  FL_CUDA(raise_smem_limit(kf, (int)s->smem_fact));
   int occ = 1;
   FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, NTHREADS, s->smem_fact));
   occ = std::max(1, std::min(occ, 2));
@@ -1134,8 +1134,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     s->smem_fw = (size_t)FW_WARPS * fw.nst * fw.stage_bytes;
     if (s->smem_fw <= 220 * 1024) {
       const void* kfw = fw_kernel(model, c4);
-      FL_CUDA(cudaFuncSetAttribute(kfw, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)s->smem_fw));
+      FL_CUDA(raise_smem_limit(kfw, (int)s->smem_fw));
       int occw = 1;
       FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occw, kfw, FW_WARPS * 32, s->smem_fw));
       occw = std::max(1, occw);
@@ -1210,8 +1209,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         s->smem_csr = ((size_t)round_up(t->pf, 4) + (size_t)FW_WARPS * 32 * (t->pf | 1)) * 4;
         for (int m = 0; m < 2; m++) {
           const void* kc = m == 0 ? (const void*)k_glm_fact_csr<0> : (const void*)k_glm_fact_csr<1>;
-          FL_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)s->smem_csr));
+          FL_CUDA(raise_smem_limit(kc, (int)s->smem_csr));
         }
         int occc = 1;
         FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -1245,10 +1243,8 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
     set_error("fused GLM: gathered source too wide");
     return FL_ERR_OP;
   }
-  FL_CUDA(cudaFuncSetAttribute(k_glm_dim_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->smem_dim));
-  FL_CUDA(cudaFuncSetAttribute(k_glm_dim_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->smem_dim));
+  FL_CUDA(raise_smem_limit(k_glm_dim_q, (int)s->smem_dim));
+  FL_CUDA(raise_smem_limit(k_glm_dim_t, (int)s->smem_dim));
   int occd = 1;
   FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, k_glm_dim_t, NTHREADS, s->smem_dim));
   occd = std::max(1, occd);
@@ -1347,8 +1343,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
       const int span_max = e ? FW_QCAP : 512;   // FL_GLM_SOLO=1 forces up to FW_QCAP
       if (span <= span_max && smem_solo <= 227 * 1024) {
         const void* kfw = fw_kernel(model, c4);
-        FL_CUDA(cudaFuncSetAttribute(kfw, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_solo));
+        FL_CUDA(raise_smem_limit(kfw, (int)smem_solo));
         if ((rc = s->solo_part.alloc((size_t)s->nblk_fw * t->g[0].pitch * 8))) return rc;
         GlmFactWArgs& fw = s->fw;
         fw.solo = 1;
@@ -1457,11 +1452,23 @@ int fl_glm_run(fl_glm* s, int32_t iterations, void* stream) {
     return FL_OK;
   };
   int rc;
-  if (!s->graph && (rc = capture(1, &s->graph))) return rc;
+  // FL_GLM_DIRECT=1: the remainder iterations as plain stream launches
+  // instead of the one-iteration graph (launch-latency experiment)
+  static const bool direct = [] {
+    const char* e = getenv("FL_GLM_DIRECT");
+    return e && atoi(e) != 0;
+  }();
+  if (!direct && !s->graph && (rc = capture(1, &s->graph))) return rc;
   const int nbig = iterations / kGlmGraphIters;
   if (nbig > 0 && !s->graph_n && (rc = capture(kGlmGraphIters, &s->graph_n))) return rc;
   for (int i = 0; i < nbig; i++) FL_CUDA(cudaGraphLaunch(s->graph_n, st));
-  for (int i = nbig * kGlmGraphIters; i < iterations; i++) FL_CUDA(cudaGraphLaunch(s->graph, st));
+  for (int i = nbig * kGlmGraphIters; i < iterations; i++) {
+    if (direct) {
+      if ((rc = glm_iteration(s, st))) return rc;
+    } else {
+      FL_CUDA(cudaGraphLaunch(s->graph, st));
+    }
+  }
   return FL_OK;
 }
 

@@ -115,7 +115,9 @@ struct SoloRec {
 // the last CTA of a solo iteration: red = the fixed-order sum of the group
 // partials [grad_F | loss | grad_d], then the update.  Arguments are plain
 // pointers / scalars and the update arguments live in global memory: nothing
-// forces a local copy of a kernel parameter struct.
+// forces a local copy of a kernel parameter struct.  (A variant that first
+// staged every partial in shared memory with one round of independent loads
+// measured 1.7 us slower per C1 step: profiles/r02_s2_experiments.txt.)
 __device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, int ngroups, int pf,
                                             int pitch0, int sort_g, int fuse_update,
                                             const UpdateArgs* u) {

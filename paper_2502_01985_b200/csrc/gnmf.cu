@@ -981,8 +981,7 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
   int occ = 1;
   for (int u = 0; u < 2; u++) {
     const void* kf = gn_fact_ptr(NR, KC, u == 0);
-    FL_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)s->smem_fact));
+    FL_CUDA(raise_smem_limit(kf, (int)s->smem_fact));
     if (u == 0)
       FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, GN_WARPS * 32,
                                                             s->smem_fact));
@@ -1027,10 +1026,8 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
       ta.f_tcol = fa.f_tcol;
       if ((rc = s->scratch.alloc((size_t)s->nblk_fact * GT_TILE * 32 * 8))) return rc;
       ta.scratch = s->scratch.as<double>();
-      FL_CUDA(cudaFuncSetAttribute(k_gnmf_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(gm.total + 1024)));
-      FL_CUDA(cudaFuncSetAttribute(k_gnmf_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(gm.total + 1024)));
+      FL_CUDA(raise_smem_limit(k_gnmf_tc<true>, (int)(gm.total + 1024)));
+      FL_CUDA(raise_smem_limit(k_gnmf_tc<false>, (int)(gm.total + 1024)));
     }
   }
   // default: the tcgen05 pass with MN-major row-contraction operands
@@ -1071,11 +1068,13 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
       ga.f_tcol = fa.f_tcol;
       ga.scratch = s->scratch5.as<double>();
       if (const char* dg = getenv("FL_GN5_DIAG")) ga.diag = atoi(dg);   // timing experiments
+      {
+        const char* gp = getenv("FL_GN5_GPRE");
+        ga.gpre = (gp && atoi(gp) == 0) ? 0 : 1;
+      }
       const size_t smem5 = g5.total + 1024;
-      FL_CUDA(cudaFuncSetAttribute(k_gnmf_t5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem5));
-      FL_CUDA(cudaFuncSetAttribute(k_gnmf_t5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem5));
+      FL_CUDA(raise_smem_limit(k_gnmf_t5<true>, (int)smem5));
+      FL_CUDA(raise_smem_limit(k_gnmf_t5<false>, (int)smem5));
     }
   }
   const size_t WP = (size_t)MR * 16 * (SC + R);
@@ -1139,8 +1138,7 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
   {
     const void* fg0 = R == 8 ? (const void*)k_gnmf_dim_g<8> : R == 16 ? (const void*)k_gnmf_dim_g<16>
                                                                      : (const void*)k_gnmf_dim_g<32>;
-    FL_CUDA(cudaFuncSetAttribute(fg0, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(s->smem_g, 16)));
+    FL_CUDA(raise_smem_limit(fg0, (int)std::max<size_t>(s->smem_g, 16)));
     int occ_g = 2;
     FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, fg0, 256, s->smem_g));
     occ_g = std::max(1, std::min(occ_g, 8));
@@ -1161,8 +1159,7 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
   {
     const void* fg = R == 8 ? (const void*)k_gnmf_dim_g<8> : R == 16 ? (const void*)k_gnmf_dim_g<16>
                                                                     : (const void*)k_gnmf_dim_g<32>;
-    FL_CUDA(cudaFuncSetAttribute(fg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(s->smem_g, 16)));
+    FL_CUDA(raise_smem_limit(fg, (int)std::max<size_t>(s->smem_g, 16)));
   }
   {
     std::vector<RedDesc> dv;
@@ -1209,8 +1206,7 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
     set_error("fused GNMF: rank x columns too large for the H update");
     return FL_ERR_OP;
   }
-  FL_CUDA(cudaFuncSetAttribute(k_gnmf_h, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->smem_h));
+  FL_CUDA(raise_smem_limit(k_gnmf_h, (int)s->smem_h));
   FL_CUDA(cudaStreamSynchronize(st));
   *out = guard.release();
   return FL_OK;

@@ -36,6 +36,7 @@ struct GnT5Args {
   int64_t r_T, ntiles;
   int ng;                          // 0 or 1 (the sort source)
   int diag;                        // timing experiments only (FL_GN5_DIAG): 1 no Z sums, 2 no PG MMA
+  int gpre;                        // G_d rows gathered one tile ahead (FL_GN5_GPRE=0: at use)
   const int32_t* fk;
   const float* Gd;                 // r_d x 32
   double* Z;                       // r_d x 32
@@ -287,26 +288,40 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
       tc::fence_before();
       mbar_arrive(&lo_ready[t & 1]);
     };
-    if (UPDATE && n > 0) split(0);
+    // G_d[fk] rows of tile t (L2 gathers), loaded one tile ahead: issued
+    // right after the tile's stage is known to have landed (split), consumed
+    // a tile later, so their latency hides behind this tile's epilogue
+    float4 gl_next[NU];
+    auto gload = [&](int tt) {
+#pragma unroll
+      for (int u = 0; u < NU; u++) gl_next[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!a.ng) return;
+      const int32_t* fk_t = reinterpret_cast<const int32_t*>(sm + (tt % G5_NS) * gm.stage + gm.o_fk);
+      const int f = fk_t[r];
+      if (f >= 0) {
+        const float4* gr = reinterpret_cast<const float4*>(a.Gd + (int64_t)f * 32 + G5_CPT * h);
+#pragma unroll
+        for (int u = 0; u < NU; u++) gl_next[u] = __ldg(gr + u);
+      }
+    };
+    if (UPDATE && n > 0) {
+      split(0);
+      if (a.gpre) gload(0);
+    }
     for (int t = 0; t < n; t++) {
       const int s = t % G5_NS;
       char* st = sm + s * gm.stage;
       mbar_wait_sleep(&full[s], (uint32_t)((t / G5_NS) & 1));
       const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
-      const int fk = a.ng ? fks[r] : -1;
       float w[G5_CPT], x[G5_CPT];
       float4 flo[NU];
 #pragma unroll
       for (int u = 0; u < NU; u++) flo[u] = flo_next[u];
       if (UPDATE) {
+        if (!a.gpre) gload(t);
         float4 gl[NU];
 #pragma unroll
-        for (int u = 0; u < NU; u++) gl[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (fk >= 0) {
-          const float4* gr = reinterpret_cast<const float4*>(a.Gd + (int64_t)fk * 32 + G5_CPT * h);
-#pragma unroll
-          for (int u = 0; u < NU; u++) gl[u] = __ldg(gr + u);
-        }
+        for (int u = 0; u < NU; u++) gl[u] = gl_next[u];
         mbar_wait_sleep(&qv_full[t & 1], (uint32_t)((t >> 1) & 1));
         tc::fence_after();
         uint32_t qq[G5_CPT], vv[G5_CPT];
@@ -318,7 +333,10 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         // software pipeline: Q / V(t) are done with the lo buffer, so the
         // next tile's lo parts go out now and its MMAs overlap the rest of
         // this tile's epilogue
-        if (t + 1 < n) split(t + 1);
+        if (t + 1 < n) {
+          split(t + 1);
+          if (a.gpre) gload(t + 1);
+        }
         load_row(t, w, x);
         // W' = W o (Q + G_d[fk]) / (V + eps)   (k_gnmf_fact's expression)
 #pragma unroll

@@ -44,6 +44,15 @@ constexpr int MAX_GATHER = 8;      // gathered sources handled by the fused kern
 void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per kernel and
+// device: sessions only ever RAISE it (a later session with a smaller plan
+// must not invalidate the launches of one still alive)
+cudaError_t raise_smem_limit_ptr(const void* fn, int bytes);
+template <typename F>
+inline cudaError_t raise_smem_limit(F* fn, int bytes) {
+  return raise_smem_limit_ptr(reinterpret_cast<const void*>(fn), bytes);
+}
+
 #define FL_CUDA(call)                                                        \
   do {                                                                       \
     cudaError_t e__ = (call);                                                \

@@ -1093,8 +1093,7 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
   // the stage area starts right after the fixed area (kernel computes the
   // same offsets); pad the fixed area so stages stay 128-byte aligned
   const void* kf = km_fact_ptr(NT, KC);
-  FL_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->smem_fact));
+  FL_CUDA(raise_smem_limit(kf, (int)s->smem_fact));
   int occ = 1;
   FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, KM_WARPS * 32, s->smem_fact));
   occ = std::max(1, occ);
@@ -1128,7 +1127,7 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
       return FL_ERR_OP;
     }
     const void* kt = KP == 16 ? (const void*)k_km_tc<16> : (const void*)k_km_tc<32>;
-    FL_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tc));
+    FL_CUDA(raise_smem_limit(kt, (int)s->smem_tc));
     s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
     KmTcArgs& ta = s->ta;
     ta.Fblk = s->Fblk.as<float>();
@@ -1161,7 +1160,7 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
                            (uint64_t)t->pf * 4, K5_TILE, 32, 128)))
       return rc;
     const void* k5 = KP == 16 ? (const void*)k_km_t5<16> : (const void*)k_km_t5<32>;
-    FL_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+    FL_CUDA(raise_smem_limit(k5, (int)smem5));
     const int64_t ntiles = t->r_pad / K5_TILE;
     s->nblk_fact = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, t->sm_count));
     KmT5Args& ta = s->t5a;
@@ -1255,8 +1254,7 @@ static int km_create_fused(fl_table* t, int32_t k, const double* centroids0, fl_
   {
     const void* fe = KP == 8 ? (const void*)k_km_dim_e<8> : KP == 16 ? (const void*)k_km_dim_e<16>
                                                                      : (const void*)k_km_dim_e<32>;
-    FL_CUDA(cudaFuncSetAttribute(fe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(s->smem_e, 16)));
+    FL_CUDA(raise_smem_limit(fe, (int)std::max<size_t>(s->smem_e, 16)));
   }
 
   KmUpdateArgs& ua = s->ua;

@@ -536,8 +536,7 @@ int do_lmm(fl_table* t, const float* x_dev, int c_x, float* out_dev, cudaStream_
         if (rc) return rc;
         static bool attr_set = false;
         if (!attr_set) {
-          FL_CUDA(cudaFuncSetAttribute(k_lmm_t5, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(l5_geom(MAX_GATHER).total + 1024)));
+          FL_CUDA(raise_smem_limit(k_lmm_t5, (int)(l5_geom(MAX_GATHER).total + 1024)));
           attr_set = true;
         }
         LmT5Args la{};
@@ -692,8 +691,7 @@ static int tlmm_bins_product(fl_table* t, const GatherSrc& g, const double* bins
   const size_t sm = (size_t)npair * 8;
   double* part = nullptr;
   FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
-  FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sm));
+  FL_CUDA(raise_smem_limit(k_tmm_partial<true>, (int)sm));
   k_tmm_partial<true><<<(unsigned)nb, 256, sm, s>>>(g.S->as<float>(), g.pitch, g.cols, g.rows,
                                                     YView{nullptr, 0, 0}, nullptr, bins, cy, rpb,
                                                     part);
@@ -759,7 +757,7 @@ static int tlmm_wide_t5(fl_table* t, YView yv, int cy, double* out, int64_t os_t
   int rc = FL_OK;
   static bool attr = false;
   if (!attr) {
-    FL_CUDA(cudaFuncSetAttribute(k_tmm_t5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M5_SMEM));
+    FL_CUDA(raise_smem_limit(k_tmm_t5, (int)M5_SMEM));
     attr = true;
   }
   const int64_t ntiles = r_pad / M5_TILE;
@@ -897,13 +895,11 @@ static int tlmm_impl(fl_table* t, YView yv_in, int cy, double* out, int64_t os_t
     double* part = nullptr;
     FL_CUDA(cudaMallocAsync((void**)&part, nb * npair * 8, s));
     if (bins) {
-      FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sm));
+      FL_CUDA(raise_smem_limit(k_tmm_partial<true>, (int)sm));
       k_tmm_partial<true><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv, nullptr, bins,
                                                         cy, rpb, part);
     } else {
-      FL_CUDA(cudaFuncSetAttribute(k_tmm_partial<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      FL_CUDA(raise_smem_limit(k_tmm_partial<false>, (int)sm));
       k_tmm_partial<false><<<(unsigned)nb, 256, sm, s>>>(A, pitch, acols, rows, yv,
                                                          yperm, nullptr, cy, rpb,
                                                          part);

@@ -25,6 +25,25 @@ void set_error(const char* fmt, ...) {
   g_last_error = buf;
 }
 
+cudaError_t raise_smem_limit_ptr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> set;   // (device, kernel) -> bytes
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& kv : set)
+    if (kv.first.first == dev && kv.first.second == fn) {
+      if (bytes <= kv.second) return cudaSuccess;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) kv.second = bytes;
+      return e;
+    }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) set.push_back({{dev, fn}, bytes});
+  return e;
+}
+
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   set_error("CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e), cudaGetErrorString(e),
             what, file, line);

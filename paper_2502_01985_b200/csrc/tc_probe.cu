@@ -191,7 +191,7 @@ extern "C" int fl_tc_timing(int32_t M, int32_t N, int32_t a_mn, int32_t b_mn, in
   FL_CUDA(cudaMalloc(&d, (size_t)ctas * 8));
   const size_t smem = 1024 + 3 * 65536;
   auto go = [&](auto kern) -> int {
-    FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FL_CUDA(raise_smem_limit(kern, (int)smem));
     kern<<<ctas, 128, smem>>>(M, N, reps, nacc, d);
     return FL_OK;
   };
@@ -255,7 +255,7 @@ extern "C" int fl_tc_probe(int32_t mode, const float* A, const float* B, float* 
   }
   if (rc) return rc;
   const size_t smem = 1024 + 65536 + 65536;
-  FL_CUDA(cudaFuncSetAttribute(k_tc_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  FL_CUDA(raise_smem_limit(k_tc_probe, (int)smem));
   k_tc_probe<<<1, 128, smem>>>(mode, tm, dA, dB, dD, dT, K, N, params ? params[0] : 16,
                                params ? params[1] : 1024, params ? params[2] : 1);
   FL_CHECK_LAUNCH();

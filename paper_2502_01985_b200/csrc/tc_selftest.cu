@@ -103,7 +103,7 @@ extern "C" int fl_tc_selftest(int32_t mode, const float* A, const float* B, floa
   FL_CUDA(cudaMemcpy(dA, A, 128 * K * 4, cudaMemcpyDefault));
   FL_CUDA(cudaMemcpy(dB, B, (size_t)K * N * 4, cudaMemcpyDefault));
   const size_t smem = 1024 + 128 * 128 * 4 + 128 * 256 * 4;
-  FL_CUDA(cudaFuncSetAttribute(k_tc_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  FL_CUDA(raise_smem_limit(k_tc_selftest, (int)smem));
   int ov[4] = {-1, -1, -1, -1};
   if (lbo_sbo)
     for (int i = 0; i < 4; i++) ov[i] = lbo_sbo[i];

@@ -1,0 +1,55 @@
+"""Several sessions alive on one table with different launch plans (the solo
+one-kernel GLM iteration with its shared-memory plan, and the three-kernel
+iteration): creating the second must not break the first's launches (the
+per-kernel dynamic shared-memory limit is process-wide and only raised), and
+every variant of the solo tail reaches the same weights."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import star_table
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fl():
+    import paper_2502_01985_b200 as fl
+    return fl
+
+
+def _session(fl, h, y, env):
+    from paper_2502_01985_b200.trainers import GlmSession
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return GlmSession(h, "linreg", y, 1e-7)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_sessions_with_different_plans_coexist(fl):
+    # C1-like shape: one sort-source dimension, fanout 100 -> the solo path
+    ft = star_table(5, 200_000, [(2000, 50)], 20)
+    h = fl.TargetHandle.factorized(ft)
+    y = np.random.default_rng(0).random(200_000).astype(np.float32)
+    variants = [{}, {"FL_GLM_SOLO_S0": "0"}, {"FL_GLM_SOLO": "0"}]
+    sess = [_session(fl, h, y, v) for v in variants]
+    assert sess[0].path[0] == "solo" and sess[2].path[0] != "solo"
+    out = []
+    for s in sess:   # the first sessions launch after the later ones were planned
+        s.run(7)
+        s.kernel_times(2)   # direct (non-graph) launches
+        out.append(s.result(7))
+    w0, l0 = out[0]
+    w1, l1 = out[1]   # S_d span from shared memory or L2: same sums, identical results
+    assert np.array_equal(w1, w0) and np.array_equal(l1, l0)
+    w3, l3 = out[2]
+    assert np.max(np.abs(w3 - w0)) <= 1e-5 * np.max(np.abs(w0))
+    assert np.max(np.abs(l3 - l0) / np.abs(l0)) <= 1e-5
