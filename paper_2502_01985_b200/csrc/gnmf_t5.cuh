@@ -160,10 +160,11 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     }
   } else if (warp == 1) {
     // =================== MMA issuer ===================
-    // the whole warp walks the tiles (barrier waits); one elected lane issues
-    // the MMA chains and commits (tc05.cuh: a lane-0 branch costs a branch
-    // loop per UTC instruction)
-    if (n > 0) {
+    // lane 0 walks the tiles and issues the MMA chains and commits.  (The
+    // converged-warp form with elect.sync issues the UTC instructions back to
+    // back but measured 4% slower here: 6.47 vs 6.23 ms per C4 step,
+    // profiles/r02_s2_experiments.txt)
+    if (lane == 0 && n > 0) {
       const uint32_t id_qv = tc::idesc_tf32(128, 32, false, false);
       const uint32_t id_pg = tc::idesc_tf32(128, 64, true, true);
       const uint32_t c0 = smem_u32(cst);
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         const uint32_t st = smem_u32(sm + (t % G5_NS) * gm.stage);
         const uint32_t lo = smem_u32(sm + gm.o_lo);
         const uint32_t tq = tmem + 64 * b;
-        if (tc::elect_one()) {
+        {
           for (int ks = 0; ks < kst; ks++) {   // Q = F H_F^T
             const uint64_t ah = tc::smem_desc(st + gm.o_f + ks * 32, 16, 1024, tc::kSw128);
             const uint64_t al = tc::smem_desc(lo + 16384 + ks * 32, 16, 1024, tc::kSw128);
@@ -199,7 +200,6 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
           }
           tc::commit(&qv_full[b]);
         }
-        __syncwarp();
       };
       if (UPDATE) qv(0);
       for (int t = 0; t < n; t++) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
         // of 8 rows advances the start address by 1024 B (64 in the 16-byte
         // address field)
         const uint64_t ad0 = tc::smem_desc(ops, 16384, 512, tc::kSw128B32);
-        if (tc::elect_one()) {
+        {
           if (!(a.diag & 2)) {
 #pragma unroll
             for (int kk = 0; kk < G5_TILE / 8; kk++) {
@@ -226,7 +226,6 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
           tc::commit(&ops_free);
           if ((t % G5_FT) == G5_FT - 1 || t == n - 1) tc::commit(&acc_full[b]);
         }
-        __syncwarp();
       }
     }
   } else {
