@@ -1349,10 +1349,6 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         fw.solo = 1;
         fw.s0_rows = s0_on ? span : 0;
         fw.qcap = qcap;
-        {
-          const char* ef = getenv("FL_GLM_SOLO_FIN");
-          fw.solo_fin = ef ? atoi(ef) : 1;
-        }
         fw.S0 = t->g[0].S->as<float>();
         fw.pitch0 = t->g[0].pitch;
         fw.w0d = da.w[0];

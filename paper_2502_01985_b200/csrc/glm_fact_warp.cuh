@@ -101,7 +101,6 @@ struct GlmFactWArgs {
   const UpdateArgs* up;      // the session's update arguments (device copy: no param copies)
   int* gcnt;                 // per-group arrival counters (zeroed; reset by each group's last CTA)
   double* gpart;             // groups x (pf + 1 + pitch0): first-level partial sums
-  int solo_fin;              // FL_GLM_SOLO_FIN=2: the latency-shaped final (A/B)
   int qcap;                  // q entries staged per CTA (a multiple of 4, <= FW_QCAP)
   int s0_rows;               // > 0: the CTA's S_d row span (<= s0_rows rows) is bulk-copied
                              // into shared memory before the PDL wait and serves both the
@@ -116,9 +115,9 @@ struct SoloRec {
 // the last CTA of a solo iteration: red = the fixed-order sum of the group
 // partials [grad_F | loss | grad_d], then the update.  Arguments are plain
 // pointers / scalars and the update arguments live in global memory: nothing
-// forces a local copy of a kernel parameter struct.  (A variant that first
-// staged every partial in shared memory with one round of independent loads
-// measured 1.7 us slower per C1 step: profiles/r02_s2_experiments.txt.)
+// forces a local copy of a kernel parameter struct.  (Variants that staged
+// the partials, red and w in shared memory with up-front independent loads
+// measured 1.2-1.7 us slower per C1 step: profiles/r02_s2_experiments.txt.)
 __device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, int ngroups, int pf,
                                             int pitch0, int sort_g, int fuse_update,
                                             const UpdateArgs* u) {
@@ -136,60 +135,6 @@ __device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, in
   }
   __syncthreads();
   if (fuse_update) glm_apply_update(*u);
-}
-
-// solo final, latency-shaped (FL_GLM_SOLO_FIN=2, A/B): every update field,
-// the mapping arrays, w and the group partials are loaded up front with
-// independent loads, then the same fixed-order sums; red and the new w stay
-// in shared memory for the fp32 copies (no global read-backs).  Only for
-// the sort source as the single gathered source (index 0), as solo requires.
-__device__ __noinline__ void glm_solo_final2(const double* __restrict__ gpart, int ngroups, int pf,
-                                             int pitch0, int fuse_update,
-                                             const UpdateArgs* __restrict__ u, char* smem) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int c_T = u->c_T;
-  const double lr = u->lr;
-  const int32_t* f_tcol = u->f_tcol;
-  const int32_t* dt = u->d_tcol[0];
-  float* wF = u->wF;
-  float* wd0 = u->wd[0];
-  double* w64 = u->w64;
-  double* red = u->red;
-  double* loss_hist = u->loss_hist;
-  const int loss_cap = u->loss_cap;
-  GlmState* state = u->state;
-  const int ne = pf + 1 + pitch0;
-  double* red_s = reinterpret_cast<double*>(smem);   // c_T + 1
-  double* w_s = red_s + c_T + 1;                     // c_T
-  const int it = fuse_update ? state->it : 0;
-  for (int c = tid; c < c_T; c += nt) w_s[c] = w64[c];
-  for (int c = tid; c <= c_T; c += nt) red_s[c] = 0.0;
-  __syncthreads();
-  for (int e = tid; e < ne; e += nt) {
-    const int dst = e < pf ? f_tcol[e] : e == pf ? c_T : dt[e - pf - 1];
-    double v = 0.0;
-    for (int g = 0; g < ngroups; g++) v += __ldcg(gpart + (int64_t)g * ne + e);
-    if (dst >= 0) red_s[dst] = v;
-  }
-  __syncthreads();
-  for (int c = tid; c <= c_T; c += nt) red[c] = red_s[c];
-  if (!fuse_update) return;
-  if (tid == 0 && it < loss_cap) loss_hist[it] = red_s[c_T];
-  for (int c = tid; c < c_T; c += nt) {
-    const double w = w_s[c] - lr * red_s[c];
-    w64[c] = w;
-    w_s[c] = w;
-  }
-  __syncthreads();
-  for (int j = tid; j < pf; j += nt) {
-    const int tc = f_tcol[j];
-    wF[j] = tc >= 0 ? (float)w_s[tc] : 0.f;
-  }
-  for (int c = tid; c < pitch0; c += nt) {
-    const int tc = dt[c];
-    wd0[c] = tc >= 0 ? (float)w_s[tc] : 0.f;
-  }
-  if (tid == 0) state->it = it + 1;
 }
 
 template <int MODEL, int C4, int RPL>
@@ -575,10 +520,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    if (a.solo_fin == 2)
-      glm_solo_final2(a.gpart, ngroups, pf, a.pitch0, a.fuse_update, a.up, smem);
-    else
-      glm_solo_final(a.gpart, ngroups, pf, a.pitch0, a.sort_g, a.fuse_update, a.up);
+    glm_solo_final(a.gpart, ngroups, pf, a.pitch0, a.sort_g, a.fuse_update, a.up);
     if (threadIdx.x == 0) a.state->done_fact = 0;
     return;
   }
