@@ -1349,6 +1349,7 @@ int fl_glm_create(fl_table* t, int32_t model, const void* y, double learning_rat
         fw.solo = 1;
         fw.s0_rows = s0_on ? span : 0;
         fw.qcap = qcap;
+        if (const char* dg = getenv("FL_GLM_SOLO_DIAG")) fw.diag = atoi(dg);   // timing only
         fw.S0 = t->g[0].S->as<float>();
         fw.pitch0 = t->g[0].pitch;
         fw.w0d = da.w[0];

@@ -101,6 +101,9 @@ struct GlmFactWArgs {
   const UpdateArgs* up;      // the session's update arguments (device copy: no param copies)
   int* gcnt;                 // per-group arrival counters (zeroed; reset by each group's last CTA)
   double* gpart;             // groups x (pf + 1 + pitch0): first-level partial sums
+  int diag;                  // FL_GLM_SOLO_DIAG (timing experiments only): 1 no tail, 2 no final
+                             // level, 4 no update, 16 final CTA elected but idle, 32 final sums
+                             // with one load per group step (the round-2 loop)
   int qcap;                  // q entries staged per CTA (a multiple of 4, <= FW_QCAP)
   int s0_rows;               // > 0: the CTA's S_d row span (<= s0_rows rows) is bulk-copied
                              // into shared memory before the PDL wait and serves both the
@@ -120,7 +123,7 @@ struct SoloRec {
 // measured 1.2-1.7 us slower per C1 step: profiles/r02_s2_experiments.txt.)
 __device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, int ngroups, int pf,
                                             int pitch0, int sort_g, int fuse_update,
-                                            const UpdateArgs* u) {
+                                            const UpdateArgs* u, int batched) {
   const int tid = threadIdx.x;
   const int c_T = u->c_T, ne = pf + 1 + pitch0;
   double* red = u->red;
@@ -129,7 +132,24 @@ __device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, in
   const int32_t* dt = u->d_tcol[sort_g];
   for (int e = tid; e < ne; e += blockDim.x) {
     double v = 0.0;
-    for (int g = 0; g < ngroups; g++) v += __ldcg(gpart + (int64_t)g * ne + e);
+    if (batched == 2) {
+      v = (double)ngroups;   // timing experiment only: no partial loads
+    } else if (batched) {
+      // every group partial of the element in flight at once (the plain loop
+      // issues one dependent L2 round trip per group: ~4.8 us of the C1
+      // step, profiles/r02_s2_experiments.txt), summed in the same order
+      for (int g0 = 0; g0 < ngroups; g0 += 32) {
+        double tv[32];
+#pragma unroll
+        for (int q = 0; q < 32; q++)
+          tv[q] = g0 + q < ngroups ? __ldcg(gpart + (int64_t)(g0 + q) * ne + e) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 32; q++)
+          if (g0 + q < ngroups) v += tv[q];
+      }
+    } else {
+      for (int g = 0; g < ngroups; g++) v += __ldcg(gpart + (int64_t)g * ne + e);
+    }
     const int dst = e < pf ? u->f_tcol[e] : e == pf ? c_T : dt[e - pf - 1];
     if (dst >= 0) red[dst] = v;
   }
@@ -492,8 +512,16 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
       a.part_d[(int64_t)blockIdx.x * a.pitch0 + c] = sum;
     }
   }
-  __threadfence();
+  // solo: release / acquire arrivals instead of __threadfence (MEMBAR.SC.GPU
+  // + L1 invalidate, ~1 us each on the two-die B200, three of them on the
+  // critical path of the tail): the CTA's partial stores are ordered before
+  // thread 0's release by the barrier, the last arriver's acquire before its
+  // CTA's reads by the barrier after it, and the reads go to L2 (__ldcg).
+  // FL_GLM_SOLO_DIAG bit 128 restores the fences (A/B).
+  const bool sc = !a.solo || (a.diag & 128);
+  if (sc) __threadfence();
   __syncthreads();
+  if (a.solo && (a.diag & 1)) return;   // timing experiment only: no tail (wrong results)
   if (a.solo) {
     // two-level fixed-order reduction: the last CTA of each group of
     // FW_GROUP CTAs sums the group's partials, the last group the groups'
@@ -502,10 +530,10 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
     const int g = blockIdx.x / FW_GROUP, g0 = g * FW_GROUP;
     const int g1 = min((int)gridDim.x, g0 + FW_GROUP);
     const int ngroups = (gridDim.x + FW_GROUP - 1) / FW_GROUP;
-    if (threadIdx.x == 0) is_last = atomicAdd(&a.gcnt[g], 1) == g1 - g0 - 1;
+    if (threadIdx.x == 0) is_last = atomic_add_acq_rel_gpu(&a.gcnt[g], 1) == g1 - g0 - 1;
     __syncthreads();
     if (!is_last) return;
-    __threadfence();
+    if (sc) __threadfence();
     for (int e = threadIdx.x; e < ne; e += blockDim.x) {
       double sum = 0.0;
       for (int b = g0; b < g1; b++)
@@ -514,13 +542,16 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
       a.gpart[(int64_t)g * ne + e] = sum;
     }
     if (threadIdx.x == 0) a.gcnt[g] = 0;
-    __threadfence();
+    if (sc) __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) is_last = atomicAdd(&a.state->done_fact, 1) == ngroups - 1;
+    if (a.diag & 2) return;   // timing experiment only: no final level
+    if (threadIdx.x == 0) is_last = atomic_add_acq_rel_gpu(&a.state->done_fact, 1) == ngroups - 1;
     __syncthreads();
     if (!is_last) return;
-    __threadfence();
-    glm_solo_final(a.gpart, ngroups, pf, a.pitch0, a.sort_g, a.fuse_update, a.up);
+    if (sc) __threadfence();
+    if (a.diag & 16) return;   // timing experiment only: the final CTA does nothing
+    glm_solo_final(a.gpart, ngroups, pf, a.pitch0, a.sort_g, (a.diag & 4) ? 0 : a.fuse_update, a.up,
+                   (a.diag & 64) ? 2 : !(a.diag & 32));
     if (threadIdx.x == 0) a.state->done_fact = 0;
     return;
   }

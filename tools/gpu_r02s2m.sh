@@ -1,0 +1,4 @@
+out=gpurun_out/s2m; mkdir -p $out
+timeout 600 python -m pytest tests/test_gpu_sessions.py tests/test_gpu_trainers.py tests/test_gpu_configs.py -x -q > $out/pytest.txt 2>&1; echo "exit $?" >> $out/pytest.txt
+timeout 900 python tools/ab_sessions.py --workload c1 --rounds 7 --steps 40 --variants "batched:;stepwise:FL_GLM_SOLO_TAILB=0;notail:FL_GLM_SOLO_DIAG=1" > $out/ab_c1.txt 2>&1
+tail -2 $out/pytest.txt; grep c1 $out/ab_c1.txt | cut -c1-70
