@@ -103,7 +103,8 @@ struct GlmFactWArgs {
   double* gpart;             // groups x (pf + 1 + pitch0): first-level partial sums
   int diag;                  // FL_GLM_SOLO_DIAG (timing experiments only): 1 no tail, 2 no final
                              // level, 4 no update, 16 final CTA elected but idle, 32 final sums
-                             // with one load per group step (the round-2 loop)
+                             // with every group load in flight (measured slower), 64 final sums
+                             // without loads, 128 __threadfence instead of acq_rel arrivals
   int qcap;                  // q entries staged per CTA (a multiple of 4, <= FW_QCAP)
   int s0_rows;               // > 0: the CTA's S_d row span (<= s0_rows rows) is bulk-copied
                              // into shared memory before the PDL wait and serves both the
@@ -135,9 +136,9 @@ __device__ __noinline__ void glm_solo_final(const double* __restrict__ gpart, in
     if (batched == 2) {
       v = (double)ngroups;   // timing experiment only: no partial loads
     } else if (batched) {
-      // every group partial of the element in flight at once (the plain loop
-      // issues one dependent L2 round trip per group: ~4.8 us of the C1
-      // step, profiles/r02_s2_experiments.txt), summed in the same order
+      // A/B only: every group partial of the element in flight at once,
+      // summed in the same order (measured 0.8 us slower per C1 step than
+      // the loop below, profiles/r02_s2_experiments.txt)
       for (int g0 = 0; g0 < ngroups; g0 += 32) {
         double tv[32];
 #pragma unroll
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
     if (sc) __threadfence();
     if (a.diag & 16) return;   // timing experiment only: the final CTA does nothing
     glm_solo_final(a.gpart, ngroups, pf, a.pitch0, a.sort_g, (a.diag & 4) ? 0 : a.fuse_update, a.up,
-                   (a.diag & 64) ? 2 : !(a.diag & 32));
+                   (a.diag & 64) ? 2 : (a.diag & 32) ? 1 : 0);
     if (threadIdx.x == 0) a.state->done_fact = 0;
     return;
   }
