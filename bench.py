@@ -936,9 +936,9 @@ def bench_e2e(torch, fl, wl, sh, hyper, args):
         elif wl["model"] == "gnmf":
             # t_sq through the public API (square, row_sum) as gaussian_nmf
             # does; W_0 / H_0 are inputs (pinned fp64, counted in h2d)
-            from paper_2502_01985_b200.sparse import as_dense
+            from paper_2502_01985_b200.trainers import _rows_total
             sq = h2.elementwise("square", traced=False)
-            t_sq = float(as_dense(sq.row_sum(traced=False)).sum())
+            t_sq = _rows_total(sq)
             del sq
             s2 = GnmfSession(h2, wl["rank"], w0_h.numpy(), h0_h.numpy(), t_sq)
             torch.cuda.synchronize()

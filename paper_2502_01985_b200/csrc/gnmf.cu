@@ -1424,7 +1424,8 @@ int fl_gnmf_result(fl_gnmf* s, double* w, double* h, double* loss, int32_t n, in
     k_gnmf_w_out<<<(unsigned)ceil_div(t->r_T * s->rank, 256), 256, 0, st>>>(
         s->W.as<float>(), t->perm->as<int32_t>(), t->r_T, s->rank, s->R, tmp);
     FL_CHECK_LAUNCH();
-    FL_CUDA(cudaMemcpyAsync(w, tmp, (size_t)t->r_T * s->rank * 8, cudaMemcpyDefault, st));
+    int rc = d2h_copy(w, tmp, (size_t)t->r_T * s->rank * 8, st);
+    if (rc) return rc;
     FL_CUDA(cudaFreeAsync(tmp, st));
   }
   if (h) FL_CUDA(cudaMemcpyAsync(h, s->H.p, (size_t)s->rank * t->c_T * 8, cudaMemcpyDefault, st));

@@ -310,7 +310,9 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     for (int t = 0; t < n; t++) {
       const int s = t % G5_NS;
       char* st = sm + s * gm.stage;
-      mbar_wait_sleep(&full[s], (uint32_t)((t / G5_NS) & 1));
+      // with UPDATE the tile's split (one iteration earlier) already waited
+      // for this stage
+      if (!UPDATE) mbar_wait_sleep(&full[s], (uint32_t)((t / G5_NS) & 1));
       const int32_t* fks = reinterpret_cast<const int32_t*>(st + gm.o_fk);
       float w[G5_CPT], x[G5_CPT];
       float4 flo[NU];

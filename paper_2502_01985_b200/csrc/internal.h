@@ -241,10 +241,17 @@ inline int out_buffer(T* p, size_t n, cudaStream_t s, T** dev, bool* owned) {
   return FL_OK;
 }
 
+// device -> host copy that returns once `dst` holds the data.  Large copies
+// into pageable host memory go through a pinned two-buffer ring (DMA of
+// chunk i overlaps a multi-threaded host memcpy of chunk i - 1): the
+// driver's pageable path measured ~4.5 GB/s for the 12.8 GB GNMF W readback.
+int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 template <class T>
 inline int finish_out(T* user, T* dev, bool owned, size_t n, cudaStream_t s) {
   if (owned) {
-    FL_CUDA(cudaMemcpyAsync(user, dev, n * sizeof(T), cudaMemcpyDefault, s));
+    int rc = d2h_copy(user, dev, n * sizeof(T), s);
+    if (rc) return rc;
     FL_CUDA(cudaFreeAsync(dev, s));
     FL_CUDA(cudaStreamSynchronize(s));
   }

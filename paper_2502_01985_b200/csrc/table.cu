@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <algorithm>
 
 #include "internal.h"
 
@@ -42,6 +44,57 @@ cudaError_t raise_smem_limit_ptr(const void* fn, int bytes) {
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) set.push_back({{dev, fn}, bytes});
   return e;
+}
+
+int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = (size_t)64 << 20;
+  cudaPointerAttributes pa{};
+  const bool pageable = cudaPointerGetAttributes(&pa, dst) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeUnregistered;
+  (void)cudaGetLastError();
+  if (!pageable || bytes < 2 * kChunk || std::getenv("FL_NO_STAGED_D2H")) {
+    FL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    return FL_OK;
+  }
+  // one pinned ring per process (serialised: concurrent callers take turns)
+  static std::mutex mu;
+  static char* ring[2] = {nullptr, nullptr};
+  static cudaEvent_t ev[2];
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ring[0]) {
+    for (int i = 0; i < 2; i++) {
+      FL_CUDA(cudaHostAlloc((void**)&ring[i], kChunk, cudaHostAllocPortable));
+      FL_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  auto host_copy = [&](char* d, const char* from, size_t n) {
+    std::vector<std::thread> th;
+    const size_t per = (n + nthr - 1) / nthr;
+    for (unsigned k = 0; k < nthr; k++) {
+      const size_t o = k * per;
+      if (o >= n) break;
+      th.emplace_back([=] { std::memcpy(d + o, from + o, std::min(per, n - o)); });
+    }
+    for (auto& x : th) x.join();
+  };
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  for (size_t i = 0; i <= nch; i++) {
+    if (i < nch) {   // issue chunk i (its buffer was drained in iteration i - 1)
+      const size_t n = std::min(kChunk, bytes - i * kChunk);
+      FL_CUDA(cudaMemcpyAsync(ring[i & 1], sp + i * kChunk, n, cudaMemcpyDeviceToHost, s));
+      FL_CUDA(cudaEventRecord(ev[i & 1], s));
+    }
+    if (i > 0) {     // drain chunk i - 1 while chunk i is in flight
+      const size_t j = i - 1, n = std::min(kChunk, bytes - j * kChunk);
+      FL_CUDA(cudaEventSynchronize(ev[j & 1]));
+      host_copy(dp + j * kChunk, ring[j & 1], n);
+    }
+  }
+  return FL_OK;
 }
 
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {

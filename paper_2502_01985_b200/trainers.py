@@ -588,6 +588,23 @@ class GnmfSession:
         self.close()
 
 
+def _rows_total(t: TargetHandle) -> float:
+    """sum(rowSum(T)) as the reference forms it (trainers.py:264-279): the
+    fp32 device row sums added in fp64.  The row sums stay on the device
+    (a CUDA tensor handed to fl_row_sum) and are summed there; building the
+    r_T-entry SparseMatrix on the host cost 2 s at 50M rows."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            rs = torch.empty(t.shape[0], dtype=torch.float32, device=f"cuda:{t.device}")
+            _lib.call("fl_row_sum", t._dev.ptr, C.c_void_p(rs.data_ptr()), C.c_void_p(0))
+            torch.cuda.synchronize(rs.device)
+            return float(rs.double().sum().item())
+    except ImportError:
+        pass
+    return float(as_dense(t.row_sum(traced=False)).sum())
+
+
 def gaussian_nmf(t: TargetHandle, cfg: TrainConfig) -> TrainResult:
     """Multiplicative-update NMF under Frobenius loss (trainers.py:256-307).
 
@@ -600,13 +617,13 @@ def gaussian_nmf(t: TargetHandle, cfg: TrainConfig) -> TrainResult:
         raise ConfigError(f"rank = {r} exceeds min(shape) = {min(r_t, c_t)}")
     if _nonneg_min(t) < 0.0:
         raise ConfigError("gaussian_nmf requires a non-negative target")
-    total = float(as_dense(t.row_sum(traced=False)).sum())
+    total = _rows_total(t)
     scale = total / (r_t * c_t) if total > 0 else 1.0
     rng = np.random.default_rng(cfg.seed)
     w0 = rng.random((r_t, r)) * scale
     h0 = rng.random((r, c_t)) * scale
     sq = t.elementwise("square", traced=False)
-    t_sq = float(as_dense(sq.row_sum(traced=False)).sum())
+    t_sq = _rows_total(sq)
     del sq
     s = GnmfSession(t, r, w0, h0, t_sq)
     try:
