@@ -917,7 +917,7 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
   {
     double* w0d = nullptr;
     FL_CUDA(cudaMallocAsync((void**)&w0d, (size_t)t->r_T * rank * 8 + 16, st));
-    FL_CUDA(cudaMemcpyAsync(w0d, w0, (size_t)t->r_T * rank * 8, cudaMemcpyDefault, st));
+    if (int rc = h2d_copy(w0d, w0, (size_t)t->r_T * rank * 8, st)) return rc;
     k_gnmf_w_in<<<(unsigned)ceil_div(t->r_pad * R, 256), 256, 0, st>>>(
         w0d, t->perm->as<int32_t>(), t->r_pad, rank, R, s->W.as<float>());
     FL_CHECK_LAUNCH();

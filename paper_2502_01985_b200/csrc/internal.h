@@ -246,6 +246,10 @@ inline int out_buffer(T* p, size_t n, cudaStream_t s, T** dev, bool* owned) {
 // chunk i overlaps a multi-threaded host memcpy of chunk i - 1): the
 // driver's pageable path measured ~4.5 GB/s for the 12.8 GB GNMF W readback.
 int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// host -> device counterpart (multi-threaded memcpy into the pinned ring,
+// DMA of chunk i overlapping the memcpy of chunk i + 1); returns once `src`
+// may be reused
+int h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 template <class T>
 inline int finish_out(T* user, T* dev, bool owned, size_t n, cudaStream_t s) {

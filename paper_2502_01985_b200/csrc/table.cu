@@ -46,39 +46,76 @@ cudaError_t raise_smem_limit_ptr(const void* fn, int bytes) {
   return e;
 }
 
-int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  constexpr size_t kChunk = (size_t)64 << 20;
-  cudaPointerAttributes pa{};
-  const bool pageable = cudaPointerGetAttributes(&pa, dst) == cudaSuccess &&
-                        pa.type == cudaMemoryTypeUnregistered;
-  (void)cudaGetLastError();
-  if (!pageable || bytes < 2 * kChunk || std::getenv("FL_NO_STAGED_D2H")) {
-    FL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
-    FL_CUDA(cudaStreamSynchronize(s));
-    return FL_OK;
-  }
-  // one pinned ring per process (serialised: concurrent callers take turns)
-  static std::mutex mu;
+// pinned two-buffer staging ring shared by d2h_copy / h2d_copy (one per
+// process, serialised by g_ring_mu: concurrent callers take turns)
+static constexpr size_t kChunk = (size_t)64 << 20;
+static std::mutex g_ring_mu;
+static int staging_ring(char*** ring_out, cudaEvent_t** ev_out) {
   static char* ring[2] = {nullptr, nullptr};
   static cudaEvent_t ev[2];
-  std::lock_guard<std::mutex> lk(mu);
   if (!ring[0]) {
     for (int i = 0; i < 2; i++) {
       FL_CUDA(cudaHostAlloc((void**)&ring[i], kChunk, cudaHostAllocPortable));
       FL_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     }
   }
+  *ring_out = ring;
+  *ev_out = ev;
+  return FL_OK;
+}
+static void host_copy(char* d, const char* from, size_t n) {   // 8-thread memcpy
   const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  auto host_copy = [&](char* d, const char* from, size_t n) {
-    std::vector<std::thread> th;
-    const size_t per = (n + nthr - 1) / nthr;
-    for (unsigned k = 0; k < nthr; k++) {
-      const size_t o = k * per;
-      if (o >= n) break;
-      th.emplace_back([=] { std::memcpy(d + o, from + o, std::min(per, n - o)); });
-    }
-    for (auto& x : th) x.join();
-  };
+  std::vector<std::thread> th;
+  const size_t per = (n + nthr - 1) / nthr;
+  for (unsigned k = 0; k < nthr; k++) {
+    const size_t o = k * per;
+    if (o >= n) break;
+    th.emplace_back([=] { std::memcpy(d + o, from + o, std::min(per, n - o)); });
+  }
+  for (auto& x : th) x.join();
+}
+static bool staged_host(const void* host, size_t bytes) {
+  cudaPointerAttributes pa{};
+  const bool pageable = cudaPointerGetAttributes(&pa, host) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeUnregistered;
+  (void)cudaGetLastError();
+  return pageable && bytes >= 2 * kChunk && !std::getenv("FL_NO_STAGED_COPY");
+}
+
+int h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!staged_host(src, bytes)) {
+    FL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    return FL_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  char** ring;
+  cudaEvent_t* ev;
+  if (int rc = staging_ring(&ring, &ev)) return rc;
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  for (size_t i = 0; i < nch; i++) {
+    const size_t n = std::min(kChunk, bytes - i * kChunk);
+    if (i >= 2) FL_CUDA(cudaEventSynchronize(ev[i & 1]));   // the DMA of chunk i - 2 is done
+    host_copy(ring[i & 1], sp + i * kChunk, n);
+    FL_CUDA(cudaMemcpyAsync(dp + i * kChunk, ring[i & 1], n, cudaMemcpyHostToDevice, s));
+    FL_CUDA(cudaEventRecord(ev[i & 1], s));
+  }
+  FL_CUDA(cudaStreamSynchronize(s));
+  return FL_OK;
+}
+
+int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!staged_host(dst, bytes)) {
+    FL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    return FL_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  char** ring;
+  cudaEvent_t* ev;
+  if (int rc = staging_ring(&ring, &ev)) return rc;
   const size_t nch = (bytes + kChunk - 1) / kChunk;
   const char* sp = static_cast<const char*>(src);
   char* dp = static_cast<char*>(dst);

@@ -53,3 +53,40 @@ def test_sessions_with_different_plans_coexist(fl):
     w3, l3 = out[2]
     assert np.max(np.abs(w3 - w0)) <= 1e-5 * np.max(np.abs(w0))
     assert np.max(np.abs(l3 - l0) / np.abs(l0)) <= 1e-5
+
+
+def test_staged_host_copies_match_direct(fl):
+    """Pageable host buffers of >= 128 MB go through the pinned staging ring
+    (GNMF W_0 upload, W read-back): bit-identical to the driver's copies."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from conftest import star_table
+import paper_2502_01985_b200 as fl
+from paper_2502_01985_b200.trainers import GnmfSession
+ft = star_table(9, 1_100_000, [(11_000, 12)], 20)
+h = fl.TargetHandle.factorized(ft)
+rng = np.random.default_rng(4)
+w0 = rng.random((1_100_000, 32)) * 0.1     # 282 MB, pageable
+h0 = rng.random((32, 32)) * 0.1
+s = GnmfSession(h, 32, w0, h0, 1.0)
+s.run(2)
+w, hh, loss = s.result(2)
+np.save(sys.argv[1], w)
+'''
+    import os
+    import tempfile
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for env in ({}, {"FL_NO_STAGED_COPY": "1"}):
+            p = os.path.join(td, f"w{len(outs)}.npy")
+            e = dict(os.environ, **env)
+            r = subprocess.run([sys.executable, "-c", code, p], cwd=here, env=e,
+                               capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(p))
+    assert outs[0].shape == (1_100_000, 32)
+    assert np.array_equal(outs[0], outs[1])
