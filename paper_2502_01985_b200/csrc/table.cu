@@ -730,6 +730,17 @@ int fl_table_finalize(fl_table* t, void* stream) {
     }
   };
   int nissued = 0;
+  // pageable host values (a drop-in caller's numpy arrays) cross through the
+  // pinned staging ring: an 8-thread memcpy into pinned buffer i & 1, then
+  // the DMA (the driver's own pageable path is several times slower)
+  std::unique_lock<std::mutex> pin_lock(g_ring_mu, std::defer_lock);
+  char** pin_ring = nullptr;
+  cudaEvent_t* pin_ev = nullptr;
+  int npinned = 0;
+  std::vector<char> pageable(n, 0);
+  for (int k = 0; k < n; k++)
+    pageable[k] = t->staged[k].h_vals &&
+                  staged_host(t->staged[k].h_vals, (size_t)t->staged[k].rows * t->staged[k].cols * 4);
   auto issue_chunk = [&](int c) -> int {
     const Chunk& ch = chunks[c];
     const Staged& st = t->staged[ch.k];
@@ -739,8 +750,21 @@ int fl_table_finalize(fl_table* t, void* stream) {
     }
     char* slot = ring->as<char>() + (size_t)(c % ring_n) * slot_bytes;
     if (c >= ring_n) FL_CUDA(cudaStreamWaitEvent(cv, (cudaEvent_t)ev_free[c - ring_n].get(), 0));
-    FL_CUDA(cudaMemcpyAsync(slot, st.h_vals + ch.r0 * st.cols, (size_t)ch.nrows * st.cols * 4,
-                            cudaMemcpyHostToDevice, cv));
+    const size_t nb = (size_t)ch.nrows * st.cols * 4;
+    if (pageable[ch.k] && nb <= kChunk) {
+      if (!pin_lock.owns_lock()) {
+        pin_lock.lock();
+        if (int rc2 = staging_ring(&pin_ring, &pin_ev)) return rc2;
+      }
+      const int b = npinned & 1;
+      if (npinned >= 2) FL_CUDA(cudaEventSynchronize(pin_ev[b]));   // its previous DMA is done
+      host_copy(pin_ring[b], reinterpret_cast<const char*>(st.h_vals + ch.r0 * st.cols), nb);
+      FL_CUDA(cudaMemcpyAsync(slot, pin_ring[b], nb, cudaMemcpyHostToDevice, cv));
+      FL_CUDA(cudaEventRecord(pin_ev[b], cv));
+      npinned++;
+    } else {
+      FL_CUDA(cudaMemcpyAsync(slot, st.h_vals + ch.r0 * st.cols, nb, cudaMemcpyHostToDevice, cv));
+    }
     FL_CUDA(cudaEventRecord((cudaEvent_t)ev_ready[c].get(), cv));
     nissued = c + 1;
     return FL_OK;
@@ -909,6 +933,10 @@ int fl_table_finalize(fl_table* t, void* stream) {
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaEventRecord((cudaEvent_t)ev_free[c].get(), s));
     if (c + ring_n < nch && (rc = issue_chunk(c + ring_n))) return rc;
+  }
+  if (pin_lock.owns_lock()) {   // the pinned buffers are free again before the ring is released
+    for (int b = 0; b < 2 && b < npinned; b++) FL_CUDA(cudaEventSynchronize(pin_ev[b]));
+    pin_lock.unlock();
   }
   mark("scatter chunks issued");
   // 4. gathered sources

@@ -90,3 +90,18 @@ np.save(sys.argv[1], w)
             outs.append(np.load(p))
     assert outs[0].shape == (1_100_000, 32)
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_pageable_table_upload_staged_bit_exact(fl):
+    """A >= 128 MB pageable fact block is uploaded through the pinned staging
+    ring (fl_table_finalize): the join is still bit-exact."""
+    rng = np.random.default_rng(12)
+    r, cf, rd, cd = 2_000_000, 20, 20_000, 6
+    fact = rng.random((r, cf), dtype=np.float32)          # 160 MB, numpy-owned (pageable)
+    dim = rng.random((rd, cd), dtype=np.float32)
+    fk = rng.permutation(np.arange(r) % rd).astype(np.int32)
+    maps = [np.arange(cf, dtype=np.int32), cf + np.arange(cd, dtype=np.int32)]
+    h = fl.TargetHandle.from_arrays([fact, dim], [None, fk], maps, r, cf + cd)
+    got = h.materialize_dense()
+    assert np.array_equal(got[:, :cf], fact)
+    assert np.array_equal(got[:, cf:], dim[fk])

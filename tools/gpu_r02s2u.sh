@@ -1,0 +1,6 @@
+out=gpurun_out/s2u; mkdir -p $out
+timeout 1200 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.txt 2>&1; echo "exit $?" >> $out/pytest_gpu.txt
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.txt 2>&1; echo "exit $?" >> $out/smoke.txt
+rm -rf gpurun_out/ev
+bash tools/round_evidence.sh all > $out/evidence.log 2>&1
+tail -2 $out/pytest_gpu.txt; tail -2 $out/smoke.txt; ls gpurun_out/ev

@@ -1,5 +1,5 @@
 """Phase timing of the C2 table upload from pinned host buffers (what bounds
-bench.py's e2e).  Run with FL_TRACE_UPLOAD=1 for the library's own
+bench.py's e2e; PROBE_PAGEABLE=1: from plain numpy memory, a drop-in user's case).  Run with FL_TRACE_UPLOAD=1 for the library's own
 finalize-phase timestamps."""
 import os
 import sys
@@ -19,6 +19,8 @@ def main():
     maps, c_t = bench.col_maps(wl)
 
     def pinned(t):
+        if os.environ.get("PROBE_PAGEABLE"):   # plain numpy-owned (pageable) host memory
+            return torch.from_numpy(t.cpu().numpy().copy())
         p = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         p.copy_(t)
         return p
