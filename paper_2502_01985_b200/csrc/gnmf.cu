@@ -1071,6 +1071,8 @@ static int gn_create_fused(fl_table* t, int32_t rank, const double* w0, const do
       {
         const char* gp = getenv("FL_GN5_GPRE");
         ga.gpre = (gp && atoi(gp) == 0) ? 0 : 1;
+        const char* pd = getenv("FL_GN5_PD");
+        ga.pd = pd ? atoi(pd) : G5_PD;
       }
       const size_t smem5 = g5.total + 1024;
       FL_CUDA(raise_smem_limit(k_gnmf_t5<true>, (int)smem5));

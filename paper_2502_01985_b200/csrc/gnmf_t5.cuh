@@ -37,6 +37,7 @@ struct GnT5Args {
   int ng;                          // 0 or 1 (the sort source)
   int diag;                        // timing experiments only (FL_GN5_DIAG): 1 no Z sums, 2 no PG MMA
   int gpre;                        // G_d rows gathered one tile ahead (FL_GN5_GPRE=0: at use)
+  int pd;                          // tiles prefetched into L2 ahead of the TMA loads (FL_GN5_PD)
   const int32_t* fk;
   const float* Gd;                 // r_d x 32
   double* Z;                       // r_d x 32
@@ -138,16 +139,17 @@ __global__ void __launch_bounds__(G5_THREADS, 1)
     // =================== producer ===================
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
-      for (int i = 0; i < G5_PD && i < n; i++) {
+      const int pd = a.pd;
+      for (int i = 0; i < pd && i < n; i++) {
         tma_prefetch_2d(&tmW, 0, (int)((t0 + i) * G5_TILE));
         tma_prefetch_2d(&tmF, 0, (int)((t0 + i) * G5_TILE));
       }
       for (int i = 0; i < n; i++) {
         const int s = i % G5_NS;
-        if (i + G5_PD < n) {
-          tma_prefetch_2d(&tmW, 0, (int)((t0 + i + G5_PD) * G5_TILE));
-          tma_prefetch_2d(&tmF, 0, (int)((t0 + i + G5_PD) * G5_TILE));
-          if (a.ng) bulk_prefetch_l2(a.fk + (t0 + i + G5_PD) * G5_TILE, 512);
+        if (pd > 0 && i + pd < n) {
+          tma_prefetch_2d(&tmW, 0, (int)((t0 + i + pd) * G5_TILE));
+          tma_prefetch_2d(&tmF, 0, (int)((t0 + i + pd) * G5_TILE));
+          if (a.ng) bulk_prefetch_l2(a.fk + (t0 + i + pd) * G5_TILE, 512);
         }
         if (i >= G5_NS) mbar_wait_sleep(&empty[s], (uint32_t)(((i / G5_NS) - 1) & 1));
         char* st = sm + s * gm.stage;
