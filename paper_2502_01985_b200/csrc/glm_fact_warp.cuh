@@ -104,7 +104,8 @@ struct GlmFactWArgs {
   int diag;                  // FL_GLM_SOLO_DIAG (timing experiments only): 1 no tail, 2 no final
                              // level, 4 no update, 16 final CTA elected but idle, 32 final sums
                              // with every group load in flight (measured slower), 64 final sums
-                             // without loads, 128 __threadfence instead of acq_rel arrivals
+                             // without loads, 128 __threadfence instead of acq_rel arrivals,
+                             // 256 no L2 prefetch of the tail's operands
   int qcap;                  // q entries staged per CTA (a multiple of 4, <= FW_QCAP)
   int s0_rows;               // > 0: the CTA's S_d row span (<= s0_rows rows) is bulk-copied
                              // into shared memory before the PDL wait and serves both the
@@ -230,6 +231,24 @@ __global__ void __launch_bounds__(FW_WARPS * 32, (C4 <= 7 ? 2 : 1))
     for (int s = 0; s < a.nst; s++) mbar_init(&wbar[s], 1);
     fence_mbar_init();
     for (int s = 0; s < a.nst && s < cnt; s++) issue(s, u0 + s);
+  }
+  // solo: the tail's small operands (update arguments, column maps, w, red,
+  // the arrival counters, the fp32 w copies) are pulled into L2 while the
+  // fact rows stream: after a cold L2 each of the tail's dependent accesses
+  // would otherwise be an HBM round trip.  FL_GLM_SOLO_DIAG bit 256: off.
+  if (a.solo && blockIdx.x == 0 && threadIdx.x == 32 && !(a.diag & 256)) {
+    const UpdateArgs* u = a.up;
+    auto r16 = [](int64_t b) { return (uint32_t)((b + 15) & ~(int64_t)15); };
+    bulk_prefetch_l2(u, r16(sizeof(UpdateArgs)));
+    const int c_T = u->c_T;
+    bulk_prefetch_l2(u->f_tcol, r16((int64_t)u->pf * 4));
+    bulk_prefetch_l2(u->d_tcol[0], r16((int64_t)a.pitch0 * 4));
+    bulk_prefetch_l2(u->w64, r16((int64_t)c_T * 8));
+    bulk_prefetch_l2(u->red, r16((int64_t)(c_T + 1) * 8));
+    bulk_prefetch_l2(u->wF, r16((int64_t)u->pf * 4));
+    bulk_prefetch_l2(u->wd[0], r16((int64_t)a.pitch0 * 4));
+    bulk_prefetch_l2(u->state, 16);
+    bulk_prefetch_l2(a.gcnt, r16(((int64_t)gridDim.x + FW_GROUP - 1) / FW_GROUP * 4));
   }
   for (int j = lane; j < C4 * 4; j += 32) gsum[warp][j] = 0.0;
   pdl_wait();      // w (previous update) and q (this iteration's dim_q) are final
