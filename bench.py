@@ -11,8 +11,10 @@ larger than L2 (126 MB), so no L2 flush is needed between steps.
 
 Other workloads (`--workload`):
   c1  configs[0]: fact 1M x 20 + dim 10K x 50, linear regression.  The
-      working set (92 MB) fits in L2, so L2 is flushed (256 MB write) between
-      iterations and each iteration is timed alone.
+      working set (92 MB) fits in L2, so L2 is flushed between iterations
+      (256 MB written, then 256 MB of other clean lines read, so no workload
+      data and no dirty lines remain; FL_BENCH_FLUSH=dirty: the write alone)
+      and each iteration is timed alone.
   c3  configs[2]: fact 10M x 20 + dims 100K x 60 and 10K x 5 (TR 100 / 1000),
       K-means k = 16 on planted clusters (noise 0.01).
   c4  configs[3]: fact 50M x 20 + dim 500K x 50 (TR 100), GNMF rank 32.
