@@ -242,38 +242,52 @@ __global__ void __launch_bounds__(M5_THREADS, 1)
 // float4 row writes, sequential on both sides; columns past c_y are zero
 __global__ void __launch_bounds__(256) k_xt32(YView yv, int cy, int64_t r_T,
                                               float* __restrict__ xt) {
-  __shared__ float tile[32][128 + 4];   // [column][row]
+  // software-pipelined: the next tile's column reads are issued before this
+  // tile's row writes (twice the bytes in flight), and the tile alternates
+  // between two shared buffers (one barrier per tile)
+  __shared__ float tile[2][32][128 + 4];   // [buffer][column][row]
   const int tid = threadIdx.x;
-  for (int64_t t0 = blockIdx.x * 128LL; t0 < r_T; t0 += gridDim.x * 128LL) {
+  auto load = [&](int64_t t0, float4 (&v)[4]) {
     const bool full = t0 + 128 <= r_T && (((uintptr_t)(yv.base + t0) | (uintptr_t)yv.sc * 4) & 15) == 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) {   // 32 columns x 32 float4 = 1024 loads
       const int i = tid + 256 * k, c = i >> 5, q = i & 31;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (c < cy) {
         if (full) {
-          v = __ldg(reinterpret_cast<const float4*>(yv.base + (int64_t)c * yv.sc + t0) + q);
+          v[k] = __ldg(reinterpret_cast<const float4*>(yv.base + (int64_t)c * yv.sc + t0) + q);
         } else {
           const int64_t t = t0 + 4 * q;
-          v.x = t < r_T ? yv.at(t, c) : 0.f;
-          v.y = t + 1 < r_T ? yv.at(t + 1, c) : 0.f;
-          v.z = t + 2 < r_T ? yv.at(t + 2, c) : 0.f;
-          v.w = t + 3 < r_T ? yv.at(t + 3, c) : 0.f;
+          v[k].x = t < r_T ? yv.at(t, c) : 0.f;
+          v[k].y = t + 1 < r_T ? yv.at(t + 1, c) : 0.f;
+          v[k].z = t + 2 < r_T ? yv.at(t + 2, c) : 0.f;
+          v[k].w = t + 3 < r_T ? yv.at(t + 3, c) : 0.f;
         }
       }
-      *reinterpret_cast<float4*>(&tile[c][4 * q]) = v;
+    }
+  };
+  const int64_t step = gridDim.x * 128LL;
+  int64_t t0 = blockIdx.x * 128LL;
+  if (t0 >= r_T) return;
+  float4 v[4];
+  load(t0, v);
+  for (int b = 0; t0 < r_T; t0 += step, b ^= 1) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int i = tid + 256 * k, c = i >> 5, q = i & 31;
+      *reinterpret_cast<float4*>(&tile[b][c][4 * q]) = v[k];
     }
     __syncthreads();
+    if (t0 + step < r_T) load(t0 + step, v);   // in flight during the writes below
 #pragma unroll
     for (int k = 0; k < 4; k++) {   // 128 rows x 8 float4
       const int i = tid + 256 * k, row = i >> 3, c4 = i & 7;
       const int64_t t = t0 + row;
       if (t < r_T)
         reinterpret_cast<float4*>(xt + t * 32)[c4] =
-            make_float4(tile[4 * c4][row], tile[4 * c4 + 1][row], tile[4 * c4 + 2][row],
-                        tile[4 * c4 + 3][row]);
+            make_float4(tile[b][4 * c4][row], tile[b][4 * c4 + 1][row], tile[b][4 * c4 + 2][row],
+                        tile[b][4 * c4 + 3][row]);
     }
-    __syncthreads();
   }
 }
 
